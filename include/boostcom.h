@@ -1,0 +1,197 @@
+/*
+ * boostcom.h -- C ABI of libboostcom.so, the B200-native hot path of BoostCom
+ * (arXiv 2407.07308): BGV word-wise encrypted comparison over non-power-of-two
+ * cyclotomic rings, batched over RNS ciphertexts, hand-written for sm_100a.
+ *
+ * Citations: P:<n> = PAPER.md line n (section named alongside); R<k> = reading k
+ * in DESIGN.md §3 (where the paper is silent).
+ *
+ * Problem statement (§1): "compares pairs of encrypted data to generate an
+ * encrypted result that indicates whether they are equivalent, less than, or
+ * greater than"; the result "returns encrypted '1' when a<b or encrypted '0'
+ * otherwise" (§2.1).
+ *
+ * Conventions
+ * -----------
+ *  - All pointers named `d_*` or carried in bc_ct are DEVICE pointers on the
+ *    context's device; `h_*` are HOST pointers.  Nothing is retained past
+ *    return except by *_async calls until their event completes.
+ *  - Ciphertext batches are caller-owned device memory with layout
+ *    u64[batch][parts][level][n], limb-major, canonical residues in [0, q_i),
+ *    in EVALUATION form: E[k] = a(omega_i^{z_k}), z_k the k-th element of Z_m^*
+ *    in ascending order (§2.2, Listing 2; R3).
+ *    `level` = number of ciphertext primes present (1 .. n_cipher).
+ *  - Workspace: caller-owned device memory of at least bc_workspace_bytes().
+ *  - Every call returns a bc_status; no partial output is valid on error;
+ *    bc_last_error() gives a thread-local message.
+ *  - ctx and keys are immutable after creation: concurrent calls on distinct
+ *    streams with distinct workspaces are safe.
+ *  - There is no CPU fallback: every arithmetic step runs in CUDA kernels.
+ */
+#ifndef BOOSTCOM_H
+#define BOOSTCOM_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BC_OK = 0,
+    BC_E_ARG = 1,       /* bad argument (null, size mismatch)                   */
+    BC_E_PARAM = 2,     /* parameters unusable (NotEnoughPrimes, non-cyclic ...) */
+    BC_E_RANGE = 3,     /* word out of range for (d, l, base)  (SPEC OutOfRange) */
+    BC_E_LEVEL = 4,     /* level mismatch / out of levels                        */
+    BC_E_KEY = 5,       /* missing Galois key                                    */
+    BC_E_NOISE = 6,     /* noise budget exhausted (reported by probes)           */
+    BC_E_CONSUMED = 7,  /* non-blocking handle already waited on                 */
+    BC_E_CUDA = 8,      /* CUDA runtime failure                                  */
+    BC_E_OOM = 9,       /* workspace too small                                   */
+    BC_E_INTERNAL = 10
+} bc_status;
+
+/* Parameter set (Table 3; readings R1, R5, R6, R8).  The chain
+ * q_0..q_{n_cipher-1} is the n_cipher smallest primes >= 2^(cipher_bits-1) with
+ * q = 1 mod lcm(p, m, M), M = 2^ceil(log2(2m-1)); the n_special special
+ * primes continue the same ascending search.  Key switching is hybrid with
+ * digits of `alpha` consecutive primes (R8, R14).  circuit: 'U' univariate
+ * (digits in [0,(p-1)/2], base (p+1)/2) or 'B' bivariate (digits in [0,p)).
+ * d digits per F_{p^D} slot, l slots per word (Table 3 "(d l)", F1). */
+typedef struct {
+    uint32_t p, m;
+    char circuit;
+    uint32_t d, l;
+    uint32_t n_cipher, cipher_bits;
+    uint32_t n_special, special_bits;
+    uint32_t alpha;
+    uint32_t compact_span;   /* slot compaction offsets |delta| <= span blocks (0 -> 3), R17 */
+} bc_params;
+
+typedef struct {
+    uint32_t n, m, M, D, S, ints_per_ct, n_cipher, n_special, dnum, g;
+    uint32_t base;           /* digit base: p ('B') or (p+1)/2 ('U')      */
+    uint32_t n_galois;       /* number of Galois keys keygen generates    */
+} bc_info;
+
+typedef struct bc_ctx bc_ctx;     /* params + device tables; immutable after create */
+typedef struct bc_keys bc_keys;   /* pk, relin key, Galois keys (device-resident)   */
+typedef struct bc_sk bc_sk;       /* secret key (host copy + device eval form)      */
+typedef struct { void *data; uint32_t batch, level; } bc_ct;  /* VIEW, 2 parts */
+typedef struct { void *event; void *stream; int consumed; } bc_handle;
+
+/* ---- context ------------------------------------------------------------- */
+bc_status bc_ctx_create(const bc_params *prm, int device, bc_ctx **out);
+void bc_ctx_destroy(bc_ctx *ctx);
+bc_status bc_ctx_info(const bc_ctx *ctx, bc_info *out);
+/* h_out[n_cipher + n_special] = the moduli; h_omega[...] = omega_i (R2). */
+bc_status bc_ctx_moduli(const bc_ctx *ctx, uint64_t *h_out, uint64_t *h_omega);
+/* slot algebra (R5): h_G[D+1] field polynomial, h_zeta[D], h_t[S] slot exponents */
+bc_status bc_ctx_slots(const bc_ctx *ctx, int64_t *h_G, int64_t *h_zeta, int64_t *h_t);
+/* Galois elements keygen generates keys for (Frobenius p^k, rotations) */
+bc_status bc_ctx_galois(const bc_ctx *ctx, uint32_t *h_out);
+size_t bc_ct_bytes(const bc_ctx *ctx, uint32_t batch, uint32_t level);
+/* device workspace needed by compare/min/max/select/compact on `batch` pairs
+ * (computed by a dry run of the schedule; a smaller workspace makes the
+ * library process the batch in chunks, never fail, down to 1 pair). */
+size_t bc_workspace_bytes(bc_ctx *ctx, uint32_t batch);
+
+/* ---- keys (R7, R8) --------------------------------------------------------- */
+bc_status bc_keygen(bc_ctx *ctx, uint64_t seed, bc_sk **sk, bc_keys **keys);
+void bc_sk_destroy(bc_sk *sk);
+void bc_keys_destroy(bc_keys *keys);
+
+/* ---- encode / encrypt / decrypt (R6, R9, R10) -------------------------------- */
+/* words[batch * ints_per_ct] (little-endian digits) -> batch
+ * ciphertexts at the top level.  ct_index0 = global index of the first
+ * ciphertext (drives the counter-based sampler, R7). */
+bc_status bc_encrypt(bc_ctx *ctx, const bc_keys *keys, const uint64_t *h_words, uint32_t batch,
+                     uint64_t seed, uint64_t ct_index0, bc_ct out, void *d_ws, size_t ws_bytes,
+                     void *stream);
+/* slot form: h_slots[batch][S][D] F_p coefficients (int16) -> ciphertexts */
+bc_status bc_encrypt_slots(bc_ctx *ctx, const bc_keys *keys, const int16_t *h_slots,
+                           uint32_t batch, uint64_t seed, uint64_t ct_index0, bc_ct out,
+                           void *d_ws, size_t ws_bytes, void *stream);
+/* decrypt to slot values h_slots[batch][S][D] (int16, canonical in [0,p)) */
+bc_status bc_decrypt_slots(bc_ctx *ctx, const bc_sk *sk, bc_ct in, int16_t *h_slots,
+                           void *d_ws, size_t ws_bytes, void *stream);
+/* decrypt words (as_bits = 0) or result bits from block slot 0 (as_bits = 1):
+ * h_out[batch * ints_per_ct] */
+bc_status bc_decrypt(bc_ctx *ctx, const bc_sk *sk, bc_ct in, uint64_t *h_out, int as_bits,
+                     void *d_ws, size_t ws_bytes, void *stream);
+/* plaintext polynomial (coefficients mod p) of a ciphertext: h_out[batch][n] */
+bc_status bc_decrypt_poly(bc_ctx *ctx, const bc_sk *sk, bc_ct in, int64_t *h_out,
+                          void *d_ws, size_t ws_bytes, void *stream);
+
+/* ---- comparison (§8(a) a7-a9) ---------------------------------------- */
+bc_status bc_compare(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct lt_out,
+                     bc_ct eq_out, void *d_ws, size_t ws_bytes, void *stream);
+bc_status bc_compare_lt(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out,
+                        void *d_ws, size_t ws_bytes, void *stream);
+bc_status bc_compare_eq(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out,
+                        void *d_ws, size_t ws_bytes, void *stream);
+/* out = x2 + bcast(cond) * (x1 - x2)  (Listing 4 straightlining) */
+bc_status bc_select(bc_ctx *ctx, const bc_keys *keys, bc_ct cond, bc_ct x1, bc_ct x2, bc_ct out,
+                    void *d_ws, size_t ws_bytes, void *stream);
+bc_status bc_min(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out, void *d_ws,
+                 size_t ws_bytes, void *stream);
+bc_status bc_max(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out, void *d_ws,
+                 size_t ws_bytes, void *stream);
+/* output level of compare_lt / select for an input level (for sizing outputs) */
+uint32_t bc_compare_out_level(bc_ctx *ctx, uint32_t level, int which /*0 lt, 1 eq, 2 min*/);
+
+/* ---- non-blocking comparison (a11, Listing 5) ------------------------- */
+bc_status bc_compare_lt_async(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out,
+                              void *d_ws, size_t ws_bytes, void *side_stream, bc_handle *h);
+bc_status bc_wait(bc_handle *h, void *joiner_stream);   /* BC_E_CONSUMED on 2nd wait */
+
+/* ---- primitives (each a §8(a) row; used by the parity tests) ---------------------- */
+/* a1/a2: batched Bluestein NTT over `npoly` polynomials of `nlimb` limbs each,
+ * limb i mapped to modulus index prime0 + i; layout u64[npoly][nlimb][n]. */
+bc_status bc_ntt_fwd(bc_ctx *ctx, const void *d_in, void *d_out, uint32_t npoly, uint32_t nlimb,
+                     uint32_t prime0, void *d_ws, size_t ws_bytes, void *stream);
+bc_status bc_ntt_inv(bc_ctx *ctx, const void *d_in, void *d_out, uint32_t npoly, uint32_t nlimb,
+                     uint32_t prime0, void *d_ws, size_t ws_bytes, void *stream);
+/* a3: tensor product, out = 3-part u64[batch][3][level][n] */
+bc_status bc_tensor(bc_ctx *ctx, bc_ct a, bc_ct b, void *d_out, void *stream);
+/* a4: automorphism sigma_t on both parts (no key switch) */
+bc_status bc_automorph(bc_ctx *ctx, bc_ct a, uint32_t t, bc_ct out, void *stream);
+/* a5: key switch of one polynomial batch d[batch][level][n] (eval) with the key
+ * for Galois element t (t = 0: relinearisation key); out u64[batch][2][level][n] */
+bc_status bc_keyswitch(bc_ctx *ctx, const bc_keys *keys, const void *d_poly, uint32_t batch,
+                       uint32_t level, uint32_t t, void *d_out, void *d_ws, size_t ws_bytes,
+                       void *stream);
+/* a6: modulus switch of a 2-part batch from level to level-1 */
+bc_status bc_modswitch(bc_ctx *ctx, bc_ct a, bc_ct out, void *d_ws, size_t ws_bytes, void *stream);
+/* a3+a5+a6: out = modswitch(relin(tensor(a, b))) */
+bc_status bc_mul(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out, void *d_ws,
+                 size_t ws_bytes, void *stream);
+/* a4+a5: rotation (slot s receives slot s+k) and Frobenius sigma_{p^k} */
+bc_status bc_rotate(bc_ctx *ctx, const bc_keys *keys, bc_ct a, int32_t k, bc_ct out, void *d_ws,
+                    size_t ws_bytes, void *stream);
+bc_status bc_frobenius(bc_ctx *ctx, const bc_keys *keys, bc_ct a, uint32_t k, bc_ct out,
+                       void *d_ws, size_t ws_bytes, void *stream);
+/* a8: digit extraction: out = d digit ciphertexts u64[batch][d][2][level][n] */
+bc_status bc_extract(bc_ctx *ctx, const bc_keys *keys, bc_ct a, void *d_out, void *d_ws,
+                     size_t ws_bytes, void *stream);
+
+/* ---- slot compaction (a10, Fig. 7) ------------------------------------- */
+/* h_useful[n_in * ints_per_ct] (1 = block holds a useful word).  The R17 greedy plan
+ * packs the useful blocks into as few ciphertexts as the offsets |delta| <= compact_span
+ * allow (= ceil(useful / ints_per_ct) for the Fig. 7 strided pattern), one plaintext
+ * mask product + rotation per (input, output, offset) group, then one modulus switch.
+ * out has capacity n_in cts at level in.level - 1; *n_out is set; h_dest[n_in * ints]
+ * receives the destination block (out_ct * ints_per_ct + block) of every useful block,
+ * -1 elsewhere. */
+bc_status bc_compact(bc_ctx *ctx, const bc_keys *keys, bc_ct in, const uint8_t *h_useful,
+                     bc_ct out, uint32_t *n_out, int32_t *h_dest, void *d_ws, size_t ws_bytes,
+                     void *stream);
+
+/* number of CUDA kernel launches issued by this thread since the last reset */
+uint64_t bc_launch_count(int reset);
+const char *bc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,520 @@
+"""Comparison circuits for the oracle (TEST INFRASTRUCTURE ONLY).
+
+P:71, P:77 (§1): digit LT/EQ, 3p-5 multiplications [Tan]; bivariate vs univariate (PS).
+P:282-290 (§2.1): decomposition -> mod extract -> digit EQ/LT -> lexicographic combination
+  (first within each block of d digits, then across the l slots: ShiftMul / ShiftAdd).
+P:490-506 (§5.3, Fig. 7): slot compaction.  P:557-573 (Listings 3-5): select by straightlining.
+Readings: R16 schedules (the exact expression trees below are the contract both
+sides follow; only ct x ct products, key switches and modulus switches can change bits),
+R17 select/min/max/compaction.
+
+Schedules are written once against an evaluator interface and run either on the oracle BGV
+(OracleEval) or on plaintext slot values (PlainEval, used to pin the schedules).
+Values are either ciphertext objects or python ints (plaintext constants in F_p).
+"""
+import math
+
+import numpy as np
+
+from . import bgv
+
+
+# ----------------------------------------------------------------------------------------
+# digit polynomials over F_p (definitions by interpolation)
+# ----------------------------------------------------------------------------------------
+def _binom_row(n, p):
+    row = [1]
+    for k in range(1, n + 1):
+        row.append(row[-1] * (n - k + 1) // k)
+    return [r % p for r in row]
+
+
+def indicator_poly(p, target):
+    """Lagrange interpolation over F_p: f(z) = sum_v target(v) (1 - (z - v)^{p-1}).
+    Returns coefficients c_0..c_{p-1}."""
+    c = [0] * p
+    row = _binom_row(p - 1, p)
+    for v in range(p):
+        if target(v):
+            c[0] = (c[0] + 1) % p
+            # (z - v)^{p-1} = sum_k C(p-1,k) z^k (-v)^{p-1-k}
+            for k in range(p):
+                c[k] = (c[k] - row[k] * pow(-v, p - 1 - k, p)) % p
+    return c
+
+
+def lt_univariate_coeffs(p):
+    """LT_U(z) = 1 iff z in {-1, ..., -(p-1)/2} (i.e. a_i < b_i with digits <= (p-1)/2)."""
+    h = (p - 1) // 2
+    return indicator_poly(p, lambda v: (p - h) <= v <= p - 1)
+
+
+def eq_coeffs(p):
+    return indicator_poly(p, lambda v: v == 0)
+
+
+def lt_bivariate_coeffs(p):
+    """LT_B(x, y) = [x < y] on [0,p)^2 by 2-D Lagrange interpolation, rewritten in
+    (Y = y, Z = x - y): returns c[j][k] with LT = sum_{j,k} c[j][k] Y^j Z^k."""
+    # f(x, y) = sum_{u<v} (1 - (x-u)^{p-1}) (1 - (y-v)^{p-1})
+    fx = {}
+    for u in range(p):
+        fx[u] = indicator_poly(p, lambda t, u=u: t == u)
+    C = [[0] * p for _ in range(p)]          # C[a][b] coefficient of x^a y^b
+    for u in range(p):
+        for v in range(u + 1, p):
+            for a_ in range(p):
+                if fx[u][a_]:
+                    for b_ in range(p):
+                        if fx[v][b_]:
+                            C[a_][b_] = (C[a_][b_] + fx[u][a_] * fx[v][b_]) % p
+    # substitute x = Z + Y: x^a = sum_r C(a, r) Z^r Y^(a-r)
+    out = [[0] * (2 * p) for _ in range(2 * p)]   # out[j][k]: Y^j Z^k
+    for a_ in range(p):
+        row = _binom_row(a_, p) if a_ else [1]
+        for b_ in range(p):
+            c = C[a_][b_]
+            if c:
+                for r in range(a_ + 1):
+                    out[(a_ - r) + b_][r] = (out[(a_ - r) + b_][r] + c * row[r]) % p
+    return out
+
+
+def eval_poly_fp(c, z, p):
+    return sum(ci * pow(z, i, p) for i, ci in enumerate(c)) % p
+
+
+# ----------------------------------------------------------------------------------------
+# value helpers: python ints are plaintext constants
+# ----------------------------------------------------------------------------------------
+def is_const(x):
+    return isinstance(x, (int, np.integer))
+
+
+def vmul(ev, a, b):
+    if is_const(a) and is_const(b):
+        return int(a) * int(b) % ev.p
+    if is_const(a):
+        return ev.scalar(b, a)
+    if is_const(b):
+        return ev.scalar(a, b)
+    return ev.mul(a, b)
+
+
+def vadd(ev, a, b):
+    if is_const(a) and is_const(b):
+        return (int(a) + int(b)) % ev.p
+    if is_const(a):
+        return ev.add_const(b, a)
+    if is_const(b):
+        return ev.add_const(a, b)
+    return ev.add(a, b)
+
+
+def lincomb(ev, terms, const):
+    """sum of c * x over terms with c != 0 (in the listed order) plus const (skipped if 0).
+    R16: zero coefficients are dropped; a combination with no ciphertext term is a constant."""
+    acc = None
+    for c, x in terms:
+        c %= ev.p
+        if c == 0:
+            continue
+        t = vmul(ev, x, c)
+        acc = t if acc is None else vadd(ev, acc, t)
+    const %= ev.p
+    if acc is None:
+        return const
+    if const:
+        acc = vadd(ev, acc, const)
+    return acc
+
+
+class Powers:
+    """R16 power rule: x^1 given; x^j (j >= 2) = x^a * x^(j-a), a = largest power of two < j."""
+
+    def __init__(self, ev, x):
+        self.ev = ev
+        self.pw = {1: x}
+
+    def __call__(self, j):
+        if j not in self.pw:
+            a = 1 << ((j - 1).bit_length() - 1)
+            self.pw[j] = vmul(self.ev, self(a), self(j - a))
+        return self.pw[j]
+
+
+# ----------------------------------------------------------------------------------------
+# digit circuits (a7)
+# ----------------------------------------------------------------------------------------
+def univariate_lt_eq(ev, z, p):
+    """R16 univariate: W = z^2; e = (p-3)/2; LT = z*g(W) + ((p+1)/2) W^{e+1}, EQ = 1 - W^{e+1}
+    (both read off the interpolated LT_U / EQ coefficients).  g(W) = sum_k c_{2k+1} W^k is
+    evaluated Paterson-Stockmeyer style: baby step k0 = 2^ceil(log2 sqrt(e+1)), powers W^1..W^k0
+    built in increasing order, chunks B_i = sum_{j<k0} c_{2(i k0 + j)+1} W^j, recursive split
+    g[lo,hi) = g[lo,lo+h) + W^{k0 h} * g[lo+h,hi), h = largest power of two < hi-lo."""
+    c = lt_univariate_coeffs(p)
+    e = (p - 3) // 2
+    assert all(c[2 * k] == 0 for k in range(1, (p - 1) // 2)) and c[0] == 0
+    g = [c[2 * k + 1] for k in range(e + 1)]
+    top = c[p - 1]
+    W = vmul(ev, z, z)
+    pw = Powers(ev, W)
+    k0 = 1
+    while k0 * k0 < e + 1:      # k0 = 2^ceil(log2 sqrt(e+1)): smallest power of two with k0^2 >= e+1
+        k0 *= 2
+    for j in range(2, k0 + 1):
+        pw(j)
+    nchunks = -(-(e + 1) // k0)
+
+    def chunk(i):
+        terms = [(g[i * k0 + j], pw(j)) for j in range(1, k0) if i * k0 + j <= e]
+        return lincomb(ev, terms, g[i * k0])
+
+    def ps(lo, hi):
+        if hi - lo == 1:
+            return chunk(lo)
+        h = 1 << ((hi - lo - 1).bit_length() - 1)
+        low = ps(lo, lo + h)
+        high = ps(lo + h, hi)
+        return vadd(ev, low, vmul(ev, pw(k0 * h), high))
+
+    gval = ps(0, nchunks)
+    We = pw(e + 1)
+    lt = vadd(ev, vmul(ev, z, gval), vmul(ev, We, top))
+    eq = vadd(ev, vmul(ev, We, -1), 1)
+    return lt, eq
+
+
+def bivariate_lt_eq(ev, x, y, p):
+    """R16 bivariate: Z = x - y; powers Z^2..Z^{p-1} then Y^2..Y^{p-1} by the power rule;
+    LT = sum_{j=1}^{p-1} Y^j * R_j(Z), R_j = sum_k c_{jk} Z^k; EQ = 1 - Z^{p-1}."""
+    c = lt_bivariate_coeffs(p)
+    assert all(c[0][k] == 0 for k in range(len(c[0]))), "LT_B has a Y^0 term"
+    Z = vadd(ev, x, vmul(ev, y, -1))
+    zp = Powers(ev, Z)
+    for j in range(2, p):
+        zp(j)
+    yp = Powers(ev, y)
+    for j in range(2, p):
+        yp(j)
+    lt = None
+    for j in range(1, p):
+        terms = [(c[j][k], zp(k)) for k in range(1, p)]
+        R = lincomb(ev, terms, c[j][0])
+        if is_const(R) and R == 0:
+            continue
+        t = vmul(ev, yp(j), R)
+        lt = t if lt is None else vadd(ev, lt, t)
+    eq = vadd(ev, vmul(ev, zp(p - 1), -1), 1)
+    return lt, eq
+
+
+# ----------------------------------------------------------------------------------------
+# extraction (a8), lexicographic combination (a9), compare
+# ----------------------------------------------------------------------------------------
+def kappa_slots(alg, i, k):
+    """kappa_{i,k} = mu_i^{p^k} in every slot (mu = trace-dual basis of {X^i})."""
+    mu = alg.dual_basis()[i]
+    v = alg.gf.pow(mu, alg.p ** k)
+    return np.tile(v, (alg.S, 1))
+
+
+def extract_digits(ev, ct, d):
+    """digit_i = sum_{k<D} kappa_{i,k} (.) sigma_{p^k}(ct), i < d  ("mod extract")."""
+    D = ev.alg.D
+    F = [ct] + [ev.frobenius(ct, k) for k in range(1, D)]
+    out = []
+    for i in range(d):
+        acc = None
+        for k in range(D):
+            t = ev.ptmul(F[k], kappa_slots(ev.alg, i, k))
+            acc = t if acc is None else ev.add(acc, t)
+        out.append(acc)
+    return out
+
+
+def lex_tree(ev, lts, eqs):
+    """Within a slot: merge adjacent pairs (hi = 2i+1, lo = 2i): LT = LT_hi + EQ_hi LT_lo,
+    EQ = EQ_hi EQ_lo; an unpaired most-significant element passes through."""
+    lts, eqs = list(lts), list(eqs)
+    while len(lts) > 1:
+        nl, ne = [], []
+        for i in range(0, len(lts) - 1, 2):
+            nl.append(vadd(ev, lts[i + 1], vmul(ev, eqs[i + 1], lts[i])))
+            ne.append(vmul(ev, eqs[i + 1], eqs[i]))
+        if len(lts) % 2:
+            nl.append(lts[-1])
+            ne.append(eqs[-1])
+        lts, eqs = nl, ne
+    return lts[0], eqs[0]
+
+
+def block_mask(alg, l, ints, pred):
+    m = np.zeros((alg.S, alg.D), dtype=np.int64)
+    for s in range(alg.S):
+        if s < ints * l and pred(s % l):
+            m[s, 0] = 1
+    return m
+
+
+def lex_slots(ev, lt, eq, l, ints):
+    """Across slots (ShiftMul/ShiftAdd), Kogge-Stone: round r, shift 2^r:
+    mask[s] = [(s mod l) + 2^r < l]; hiLT = mask (.) rot(LT); hiEQ = mask (.) rot(EQ) + (1-mask);
+    LT = hiLT + hiEQ * LT; EQ = hiEQ * EQ.  Result in slot 0 of each block."""
+    r = 0
+    while (1 << r) < l:
+        sh = 1 << r
+        mask = block_mask(ev.alg, l, ints, lambda t: t + sh < l)
+        inv = (1 - mask) % ev.p
+        inv[:, 1:] = 0
+        hi_lt = ev.ptmul(ev.rotate(lt, sh), mask)
+        hi_eq = ev.add_pt(ev.ptmul(ev.rotate(eq, sh), mask), inv)
+        lt = vadd(ev, hi_lt, vmul(ev, hi_eq, lt))
+        eq = vmul(ev, hi_eq, eq)
+        r += 1
+    return lt, eq
+
+
+def compare(ev, a, b, circuit, d, l, ints):
+    """(LT, EQ) of the words packed in a and b (block slot 0 holds the result)."""
+    p = ev.p
+    if circuit == "U":
+        z = ev.add(a, ev.scalar(b, -1))
+        digs = extract_digits(ev, z, d)
+        res = [univariate_lt_eq(ev, x, p) for x in digs]
+    else:
+        da = extract_digits(ev, a, d)
+        db = extract_digits(ev, b, d)
+        res = [bivariate_lt_eq(ev, x, y, p) for x, y in zip(da, db)]
+    lt, eq = lex_tree(ev, [r[0] for r in res], [r[1] for r in res])
+    if l > 1:
+        lt, eq = lex_slots(ev, lt, eq, l, ints)
+    return lt, eq
+
+
+def broadcast(ev, c, l, ints):
+    """Copy block slot 0 to every slot of its block: c = mask0 (.) c, then for r:
+    c = c + [(s mod l) >= 2^r] (.) rot_{-2^r}(c)."""
+    c = ev.ptmul(c, block_mask(ev.alg, l, ints, lambda t: t == 0))
+    r = 0
+    while (1 << r) < l:
+        sh = 1 << r
+        c = ev.add(c, ev.ptmul(ev.rotate(c, -sh), block_mask(ev.alg, l, ints, lambda t: t >= sh)))
+        r += 1
+    return c
+
+
+def select(ev, cond, x1, x2, l, ints):
+    """x2 + bcast(cond) * (x1 - x2)  (Listing 4 straightlining)."""
+    bc = broadcast(ev, cond, l, ints)
+    diff = ev.add(x1, ev.scalar(x2, -1))
+    return ev.add(x2, ev.mul(bc, diff))
+
+
+def vmin(ev, a, b, circuit, d, l, ints):
+    lt, _ = compare(ev, a, b, circuit, d, l, ints)
+    return select(ev, lt, a, b, l, ints)
+
+
+def vmax(ev, a, b, circuit, d, l, ints):
+    lt, _ = compare(ev, a, b, circuit, d, l, ints)
+    return select(ev, lt, b, a, l, ints)
+
+
+# ----------------------------------------------------------------------------------------
+# evaluators
+# ----------------------------------------------------------------------------------------
+class OracleEval:
+    """Evaluator over the oracle BGV (bgv.py)."""
+
+    def __init__(self, P, K):
+        self.P, self.K = P, K
+        self.p = P.p
+        self.alg = P.alg
+        self._pt = {}
+        self.counts = {"mul": 0, "ks": 0}
+
+    def _encode(self, slots):
+        key = np.asarray(slots, dtype=np.int64).tobytes()
+        if key not in self._pt:
+            self._pt[key] = self.alg.encode(slots)
+        return self._pt[key]
+
+    def mul(self, a, b):
+        self.counts["mul"] += 1
+        self.counts["ks"] += 1
+        return bgv.mul(self.P, self.K, a, b)
+
+    def add(self, a, b):
+        return bgv.add(self.P, a, b)
+
+    def scalar(self, a, c):
+        return bgv.mul_scalar(self.P, a, c)
+
+    def add_const(self, a, c):
+        return bgv.add_const(self.P, a, c)
+
+    def ptmul(self, a, slots):
+        return bgv.mul_plain(self.P, a, self._encode(slots))
+
+    def add_pt(self, a, slots):
+        return bgv.add_plain(self.P, a, self._encode(slots))
+
+    def rotate(self, a, k):
+        self.counts["ks"] += 1
+        return bgv.rotate(self.P, self.K, a, k)
+
+    def frobenius(self, a, k):
+        self.counts["ks"] += 1
+        return bgv.frobenius(self.P, self.K, a, k)
+
+    def modswitch(self, a):
+        return bgv.modswitch(self.P, a)
+
+
+class PlainValue:
+    def __init__(self, v, depth=0):
+        self.v = np.asarray(v, dtype=np.int64)
+        self.depth = depth
+
+
+class PlainEval:
+    """Evaluator over plaintext slot values in F_{p^D} (pins the schedules; depth = number of
+    ct x ct multiplications on the longest path)."""
+
+    def __init__(self, alg):
+        self.alg = alg
+        self.p = alg.p
+        self.gf = alg.gf
+        self.counts = {"mul": 0, "ks": 0}
+
+    def mul(self, a, b):
+        self.counts["mul"] += 1
+        return PlainValue(self.gf.mul(a.v, b.v), max(a.depth, b.depth) + 1)
+
+    def add(self, a, b):
+        return PlainValue((a.v + b.v) % self.p, max(a.depth, b.depth))
+
+    def scalar(self, a, c):
+        return PlainValue(a.v * int(c) % self.p, a.depth)
+
+    def add_const(self, a, c):
+        v = a.v.copy()
+        v[..., 0] = (v[..., 0] + int(c)) % self.p
+        return PlainValue(v, a.depth)
+
+    def ptmul(self, a, slots):
+        return PlainValue(self.gf.mul(a.v, slots), a.depth)
+
+    def add_pt(self, a, slots):
+        return PlainValue((a.v + slots) % self.p, a.depth)
+
+    def _rot_map(self, k):
+        """slot s of sigma_{g^k}(a) is a(zeta^{g^k t_s}) = beta_{s'}^{p^j} with g^k t_s = t_{s'} p^j."""
+        key = k % (self.alg.m * self.alg.S)
+        if not hasattr(self, "_rm"):
+            self._rm = {}
+        if key not in self._rm:
+            alg = self.alg
+            t = pow(alg.g, k, alg.m)
+            ppow = {pow(alg.p, j, alg.m): j for j in range(alg.D)}
+            tindex = {ts: s for s, ts in enumerate(alg.t)}
+            src, fj = [], []
+            for s in range(alg.S):
+                target = t * alg.t[s] % alg.m
+                for jm, j in ppow.items():
+                    cand = target * pow(jm, -1, alg.m) % alg.m
+                    if cand in tindex:
+                        src.append(tindex[cand])
+                        fj.append(j)
+                        break
+            self._rm[key] = (np.array(src), np.array(fj))
+        return self._rm[key]
+
+    def rotate(self, a, k):
+        src, fj = self._rot_map(k)
+        out = a.v[src].copy()
+        for j in set(fj.tolist()):
+            if j:
+                sel = fj == j
+                out[sel] = self.gf.pow(out[sel], self.alg.p ** j)
+        return PlainValue(out, a.depth)
+
+    def frobenius(self, a, k):
+        return PlainValue(self.gf.pow(a.v, self.p ** k), a.depth)
+
+    def modswitch(self, a):
+        return PlainValue(a.v, a.depth + 1)
+
+
+# ----------------------------------------------------------------------------------------
+# slot compaction (a10, Fig. 7; R17)
+# ----------------------------------------------------------------------------------------
+def compaction_offsets(span):
+    """candidate block offsets in preference order: 0, 1, -1, 2, -2, ..., span, -span."""
+    out = [0]
+    for k in range(1, span + 1):
+        out += [k, -k]
+    return out
+
+
+def plan_compaction(useful, ints, span):
+    """R17 greedy plan.  useful[c] = sorted useful block indices of input ct c.  For each input
+    in order, repeatedly pick (existing output c', offset delta) placing the most remaining blocks
+    b at free blocks b - delta of c' (first maximum in the order outputs ascending x offsets
+    0, 1, -1, ...); if nothing fits anywhere, open a new output with delta = 0.
+    Returns (groups [(c, c', delta, blocks)], n_out, dest {(c, b): (c', b')})."""
+    occ = []
+    groups = []
+    dest = {}
+    for c, blocks in enumerate(useful):
+        rem = list(blocks)
+        while rem:
+            best, best_cnt = None, 0
+            for cp in range(len(occ)):
+                for dl in compaction_offsets(span):
+                    cnt = sum(1 for b in rem if 0 <= b - dl < ints and (b - dl) not in occ[cp])
+                    if cnt > best_cnt:
+                        best, best_cnt = (cp, dl), cnt
+            if best is None:
+                occ.append(set())
+                best = (len(occ) - 1, 0)
+            cp, dl = best
+            moved = [b for b in rem if 0 <= b - dl < ints and (b - dl) not in occ[cp]]
+            for b in moved:
+                occ[cp].add(b - dl)
+                dest[(c, b)] = (cp, b - dl)
+            groups.append((c, cp, dl, moved))
+            rem = [b for b in rem if b not in set(moved)]
+    return groups, len(occ), dest
+
+
+def compaction_galois(alg, l, span):
+    """rotation elements g^{+-delta l}, delta in [1, span]."""
+    return sorted({pow(alg.g, s * k * l, alg.m) for k in range(1, span + 1) for s in (1, -1)})
+
+
+def compact(ev, cts, useful, l, ints, span, modswitch=True):
+    """out_{c'} = sum over groups (c, c', delta) of rot_{delta l}(cts[c] (.) mask(blocks)), then one
+    modulus switch per output (R17).  Blocks of an output not written by any group are zero."""
+    groups, n_out, dest = plan_compaction(useful, ints, span)
+    outs = [None] * n_out
+    for c, cp, dl, blocks in groups:
+        if not blocks:
+            continue
+        bs = set(blocks)
+        mask = block_mask_sets(ev.alg, l, bs)
+        t = ev.ptmul(cts[c], mask)
+        if dl:
+            t = ev.rotate(t, dl * l)
+        outs[cp] = t if outs[cp] is None else ev.add(outs[cp], t)
+    if modswitch:
+        outs = [ev.modswitch(o) for o in outs]
+    return outs, dest
+
+
+def block_mask_sets(alg, l, blocks):
+    m = np.zeros((alg.S, alg.D), dtype=np.int64)
+    for b in blocks:
+        m[b * l:(b + 1) * l, 0] = 1
+    return m

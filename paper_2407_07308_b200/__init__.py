@@ -1,0 +1,408 @@
+"""paper_2407_07308_b200 -- B200-native BoostCom hot path (BGV word-wise comparison).
+
+Thin Python binding over the C ABI of ``libboostcom.so`` (include/boostcom.h): argument
+marshalling only.  Every arithmetic step runs in the library's sm_100a kernels; PyTorch
+provides device memory (ciphertexts, workspaces) and streams.  There is no CPU fallback:
+importing this package fails if the extension is missing, and every call raises if the
+library reports an error.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libboostcom.so")
+
+if not os.path.exists(_SO):
+    raise ImportError("libboostcom.so not built: run __graft_entry__.build() "
+                      "(python paper_2407_07308_b200/_build.py)")
+
+_lib = ctypes.CDLL(_SO)
+
+
+class bc_params(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_uint32), ("m", ctypes.c_uint32), ("circuit", ctypes.c_char),
+                ("d", ctypes.c_uint32), ("l", ctypes.c_uint32),
+                ("n_cipher", ctypes.c_uint32), ("cipher_bits", ctypes.c_uint32),
+                ("n_special", ctypes.c_uint32), ("special_bits", ctypes.c_uint32),
+                ("alpha", ctypes.c_uint32), ("compact_span", ctypes.c_uint32)]
+
+
+class bc_info(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in
+                ("n", "m", "M", "D", "S", "ints_per_ct", "n_cipher", "n_special", "dnum", "g",
+                 "base", "n_galois")]
+
+
+class bc_ct(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("batch", ctypes.c_uint32), ("level", ctypes.c_uint32)]
+
+
+class bc_handle(ctypes.Structure):
+    _fields_ = [("event", ctypes.c_void_p), ("stream", ctypes.c_void_p), ("consumed", ctypes.c_int)]
+
+
+_vp, _u32, _u64, _sz = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_size_t
+_st = ctypes.c_int
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("bc_ctx_create", _st, ctypes.POINTER(bc_params), ctypes.c_int, ctypes.POINTER(_vp))
+_sig("bc_ctx_destroy", None, _vp)
+_sig("bc_ctx_info", _st, _vp, ctypes.POINTER(bc_info))
+_sig("bc_ctx_moduli", _st, _vp, _vp, _vp)
+_sig("bc_ctx_slots", _st, _vp, _vp, _vp, _vp)
+_sig("bc_ctx_galois", _st, _vp, _vp)
+_sig("bc_ct_bytes", _sz, _vp, _u32, _u32)
+_sig("bc_workspace_bytes", _sz, _vp, _u32)
+_sig("bc_keygen", _st, _vp, _u64, ctypes.POINTER(_vp), ctypes.POINTER(_vp))
+_sig("bc_sk_destroy", None, _vp)
+_sig("bc_keys_destroy", None, _vp)
+_sig("bc_encrypt", _st, _vp, _vp, _vp, _u32, _u64, _u64, bc_ct, _vp, _sz, _vp)
+_sig("bc_encrypt_slots", _st, _vp, _vp, _vp, _u32, _u64, _u64, bc_ct, _vp, _sz, _vp)
+_sig("bc_decrypt_slots", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
+_sig("bc_decrypt", _st, _vp, _vp, bc_ct, _vp, ctypes.c_int, _vp, _sz, _vp)
+_sig("bc_decrypt_poly", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
+_sig("bc_compare", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_compare_lt", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_compare_eq", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_select", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_min", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_max", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_compare_out_level", _u32, _vp, _u32, ctypes.c_int)
+_sig("bc_compare_lt_async", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp, ctypes.POINTER(bc_handle))
+_sig("bc_wait", _st, ctypes.POINTER(bc_handle), _vp)
+_sig("bc_ntt_fwd", _st, _vp, _vp, _vp, _u32, _u32, _u32, _vp, _sz, _vp)
+_sig("bc_ntt_inv", _st, _vp, _vp, _vp, _u32, _u32, _u32, _vp, _sz, _vp)
+_sig("bc_tensor", _st, _vp, bc_ct, bc_ct, _vp, _vp)
+_sig("bc_automorph", _st, _vp, bc_ct, _u32, bc_ct, _vp)
+_sig("bc_keyswitch", _st, _vp, _vp, _vp, _u32, _u32, _u32, _vp, _vp, _sz, _vp)
+_sig("bc_modswitch", _st, _vp, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_mul", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
+_sig("bc_rotate", _st, _vp, _vp, bc_ct, ctypes.c_int32, bc_ct, _vp, _sz, _vp)
+_sig("bc_frobenius", _st, _vp, _vp, bc_ct, _u32, bc_ct, _vp, _sz, _vp)
+_sig("bc_extract", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
+_sig("bc_launch_count", _u64, ctypes.c_int)
+_sig("bc_last_error", ctypes.c_char_p)
+_sig("bc_compact", _st, _vp, _vp, bc_ct, _vp, bc_ct, ctypes.POINTER(_u32), _vp, _vp, _sz, _vp)
+
+EXPORTS = [n for n in dir(_lib) if n.startswith("bc_")]
+
+
+class BoostComError(RuntimeError):
+    pass
+
+
+def _check(status, what):
+    if status != 0:
+        msg = _lib.bc_last_error()
+        raise BoostComError("%s failed (status %d): %s" % (what, status, msg.decode() if msg else ""))
+
+
+def launch_count(reset=False):
+    return int(_lib.bc_launch_count(1 if reset else 0))
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Keys:
+    def __init__(self, ctx, sk, keys):
+        self.ctx, self.sk, self.keys = ctx, sk, keys
+
+    def __del__(self):
+        try:
+            _lib.bc_sk_destroy(self.sk)
+            _lib.bc_keys_destroy(self.keys)
+        except Exception:
+            pass
+
+
+class Context:
+    """One parameter set on one CUDA device (R1-R17 of DESIGN.md)."""
+
+    def __init__(self, cfg, device=0):
+        torch = _torch()
+        self.device = torch.device("cuda", device)
+        prm = bc_params(int(cfg["p"]), int(cfg["m"]), cfg.get("circuit", "U").encode(), int(cfg["d"]),
+                        int(cfg["l"]), int(cfg["n_cipher"]), int(cfg["cipher_bits"]),
+                        int(cfg["n_special"]), int(cfg["special_bits"]), int(cfg["alpha"]),
+                        int(cfg.get("compact_span", 3)))
+        h = _vp()
+        with torch.cuda.device(self.device):
+            _check(_lib.bc_ctx_create(ctypes.byref(prm), device, ctypes.byref(h)), "bc_ctx_create")
+        self._h = h
+        info = bc_info()
+        _check(_lib.bc_ctx_info(h, ctypes.byref(info)), "bc_ctx_info")
+        self.info = {k: getattr(info, k) for k, _ in bc_info._fields_}
+        for k, v in self.info.items():
+            setattr(self, k, v)
+        self.cfg = dict(cfg)
+        self.p = int(cfg["p"])
+        self.d, self.l = int(cfg["d"]), int(cfg["l"])
+        self._ws = None
+
+    def __del__(self):
+        try:
+            _lib.bc_ctx_destroy(self._h)
+        except Exception:
+            pass
+
+    # ---- tables ----
+    def moduli(self):
+        k = self.n_cipher + self.n_special
+        a = np.zeros(k, dtype=np.uint64)
+        w = np.zeros(k, dtype=np.uint64)
+        _check(_lib.bc_ctx_moduli(self._h, a.ctypes.data, w.ctypes.data), "bc_ctx_moduli")
+        return [int(x) for x in a], [int(x) for x in w]
+
+    def slots(self):
+        G = np.zeros(self.D + 1, dtype=np.int64)
+        z = np.zeros(self.D, dtype=np.int64)
+        t = np.zeros(self.S, dtype=np.int64)
+        _check(_lib.bc_ctx_slots(self._h, G.ctypes.data, z.ctypes.data, t.ctypes.data), "bc_ctx_slots")
+        return G, z, t
+
+    def galois(self):
+        g = np.zeros(self.n_galois, dtype=np.uint32)
+        _check(_lib.bc_ctx_galois(self._h, g.ctypes.data), "bc_ctx_galois")
+        return [int(x) for x in g]
+
+    # ---- memory ----
+    def ct_empty(self, batch, level, parts=2):
+        torch = _torch()
+        return torch.empty((batch, parts, level, self.n), dtype=torch.int64, device=self.device)
+
+    def workspace(self, nbytes):
+        torch = _torch()
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = None
+            self._ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def default_ws(self, batch=1):
+        need = _lib.bc_workspace_bytes(self._h, batch)
+        return self.workspace(max(need, 1 << 26))
+
+    def _wsargs(self, ws):
+        if ws is None:
+            ws = self._ws if self._ws is not None else self.default_ws(1)
+        return _ptr(ws), ws.numel()
+
+    @staticmethod
+    def view(t):
+        assert t.dtype.itemsize == 8 and t.is_contiguous() and t.dim() == 4 and t.shape[1] == 2
+        return bc_ct(t.data_ptr(), t.shape[0], t.shape[2])
+
+    def workspace_bytes(self, batch):
+        return int(_lib.bc_workspace_bytes(self._h, batch))
+
+    def out_level(self, level, which=0):
+        return int(_lib.bc_compare_out_level(self._h, level, which))
+
+    # ---- keys / encryption ----
+    def keygen(self, seed):
+        sk, k = _vp(), _vp()
+        _check(_lib.bc_keygen(self._h, seed, ctypes.byref(sk), ctypes.byref(k)), "bc_keygen")
+        return Keys(self, sk, k)
+
+    def encrypt(self, keys, words, seed, ct_index0=0, ws=None):
+        words = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1, self.ints_per_ct)
+        B = words.shape[0]
+        out = self.ct_empty(B, self.n_cipher)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_encrypt(self._h, keys.keys, words.ctypes.data, B, seed, ct_index0, self.view(out), w, wb,
+                               _stream()), "bc_encrypt")
+        return out
+
+    def encrypt_slots(self, keys, slots, seed, ct_index0=0, ws=None):
+        slots = np.ascontiguousarray(slots, dtype=np.int16).reshape(-1, self.S, self.D)
+        B = slots.shape[0]
+        out = self.ct_empty(B, self.n_cipher)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_encrypt_slots(self._h, keys.keys, slots.ctypes.data, B, seed, ct_index0, self.view(out), w,
+                                     wb, _stream()), "bc_encrypt_slots")
+        return out
+
+    def decrypt(self, keys, ct, as_bits=False, ws=None):
+        B = ct.shape[0]
+        out = np.zeros((B, self.ints_per_ct), dtype=np.uint64)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_decrypt(self._h, keys.sk, self.view(ct), out.ctypes.data, 1 if as_bits else 0, w, wb,
+                               _stream()), "bc_decrypt")
+        return out
+
+    def decrypt_slots(self, keys, ct, ws=None):
+        B = ct.shape[0]
+        out = np.zeros((B, self.S, self.D), dtype=np.int16)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_decrypt_slots(self._h, keys.sk, self.view(ct), out.ctypes.data, w, wb, _stream()),
+               "bc_decrypt_slots")
+        return out
+
+    def decrypt_poly(self, keys, ct, ws=None):
+        B = ct.shape[0]
+        out = np.zeros((B, self.n), dtype=np.int64)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_decrypt_poly(self._h, keys.sk, self.view(ct), out.ctypes.data, w, wb, _stream()),
+               "bc_decrypt_poly")
+        return out
+
+    # ---- comparison ----
+    def _cmp(self, fn, keys, a, b, which, ws):
+        lvl = self.out_level(min(a.shape[2], b.shape[2]), which)
+        out = self.ct_empty(a.shape[0], lvl)
+        w, wb = self._wsargs(ws)
+        _check(fn(self._h, keys.keys, self.view(a), self.view(b), self.view(out), w, wb, _stream()), fn.__name__)
+        return out
+
+    def compare_lt(self, keys, a, b, ws=None):
+        return self._cmp(_lib.bc_compare_lt, keys, a, b, 0, ws)
+
+    def compare_eq(self, keys, a, b, ws=None):
+        return self._cmp(_lib.bc_compare_eq, keys, a, b, 1, ws)
+
+    def min(self, keys, a, b, ws=None):
+        return self._cmp(_lib.bc_min, keys, a, b, 2, ws)
+
+    def max(self, keys, a, b, ws=None):
+        return self._cmp(_lib.bc_max, keys, a, b, 2, ws)
+
+    def compare(self, keys, a, b, ws=None):
+        lvl = min(a.shape[2], b.shape[2])
+        lt = self.ct_empty(a.shape[0], self.out_level(lvl, 0))
+        eq = self.ct_empty(a.shape[0], self.out_level(lvl, 1))
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_compare(self._h, keys.keys, self.view(a), self.view(b), self.view(lt), self.view(eq), w, wb,
+                               _stream()), "bc_compare")
+        return lt, eq
+
+    def compare_lt_async(self, keys, a, b, out, side_stream, ws):
+        h = bc_handle()
+        _check(_lib.bc_compare_lt_async(self._h, keys.keys, self.view(a), self.view(b), self.view(out), _ptr(ws),
+                                        ws.numel(), ctypes.c_void_p(side_stream.cuda_stream), ctypes.byref(h)),
+               "bc_compare_lt_async")
+        return h
+
+    @staticmethod
+    def wait(h, joiner_stream):
+        return _lib.bc_wait(ctypes.byref(h), ctypes.c_void_p(joiner_stream.cuda_stream))
+
+    def select(self, keys, cond, x1, x2, ws=None):
+        torch = _torch()
+        # output level: mul(bcast(cond), diff) -> min level - 1
+        lvl = min(cond.shape[2], x1.shape[2], x2.shape[2]) - 1
+        out = self.ct_empty(x1.shape[0], lvl)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_select(self._h, keys.keys, self.view(cond), self.view(x1), self.view(x2), self.view(out), w,
+                              wb, _stream()), "bc_select")
+        del torch
+        return out
+
+    # ---- primitives (parity tests) ----
+    def ntt_fwd(self, x, prime0=0, ws=None):
+        """x: int64 tensor [npoly, nlimb, n] (coefficient residues) -> evaluation form."""
+        out = x.new_empty(x.shape)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_ntt_fwd(self._h, _ptr(x), _ptr(out), x.shape[0], x.shape[1], prime0, w, wb, _stream()),
+               "bc_ntt_fwd")
+        return out
+
+    def ntt_inv(self, x, prime0=0, ws=None):
+        out = x.new_empty(x.shape)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_ntt_inv(self._h, _ptr(x), _ptr(out), x.shape[0], x.shape[1], prime0, w, wb, _stream()),
+               "bc_ntt_inv")
+        return out
+
+    def tensor(self, a, b):
+        torch = _torch()
+        out = torch.empty((a.shape[0], 3, a.shape[2], self.n), dtype=torch.int64, device=self.device)
+        _check(_lib.bc_tensor(self._h, self.view(a), self.view(b), _ptr(out), _stream()), "bc_tensor")
+        return out
+
+    def automorph(self, a, t):
+        out = a.new_empty(a.shape)
+        _check(_lib.bc_automorph(self._h, self.view(a), t, self.view(out), _stream()), "bc_automorph")
+        return out
+
+    def keyswitch(self, keys, d, t, ws=None):
+        """d: [B, level, n] evaluation form -> (u0, u1) as [B, 2, level, n]."""
+        torch = _torch()
+        B, lvl = d.shape[0], d.shape[1]
+        out = torch.empty((B, 2, lvl, self.n), dtype=torch.int64, device=self.device)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_keyswitch(self._h, keys.keys, _ptr(d), B, lvl, t, _ptr(out), w, wb, _stream()),
+               "bc_keyswitch")
+        return out
+
+    def modswitch(self, a, ws=None):
+        out = self.ct_empty(a.shape[0], a.shape[2] - 1)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_modswitch(self._h, self.view(a), self.view(out), w, wb, _stream()), "bc_modswitch")
+        return out
+
+    def mul(self, keys, a, b, ws=None):
+        out = self.ct_empty(a.shape[0], min(a.shape[2], b.shape[2]) - 1)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_mul(self._h, keys.keys, self.view(a), self.view(b), self.view(out), w, wb, _stream()),
+               "bc_mul")
+        return out
+
+    def rotate(self, keys, a, k, ws=None):
+        out = a.new_empty(a.shape)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_rotate(self._h, keys.keys, self.view(a), k, self.view(out), w, wb, _stream()), "bc_rotate")
+        return out
+
+    def frobenius(self, keys, a, k, ws=None):
+        out = a.new_empty(a.shape)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_frobenius(self._h, keys.keys, self.view(a), k, self.view(out), w, wb, _stream()),
+               "bc_frobenius")
+        return out
+
+    def extract(self, keys, a, ws=None):
+        torch = _torch()
+        out = torch.empty((a.shape[0], self.d, 2, a.shape[2], self.n), dtype=torch.int64, device=self.device)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_extract(self._h, keys.keys, self.view(a), _ptr(out), w, wb, _stream()), "bc_extract")
+        return out
+
+    def compact(self, keys, cts, useful, ws=None):
+        """-> (compacted cts at level-1, dest[n_in, ints] destination block or -1)."""
+        useful = np.ascontiguousarray(useful, dtype=np.uint8).reshape(cts.shape[0], self.ints_per_ct)
+        out = self.ct_empty(cts.shape[0], cts.shape[2] - 1)
+        nout = _u32(0)
+        dest = np.zeros(useful.shape, dtype=np.int32)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_compact(self._h, keys.keys, self.view(cts), useful.ctypes.data, self.view(out),
+                               ctypes.byref(nout), dest.ctypes.data, w, wb, _stream()), "bc_compact")
+        return out[: nout.value], dest
+
+
+def load_params(name_or_path):
+    import json
+    path = name_or_path
+    if not os.path.exists(path):
+        path = os.path.join(_HERE, "..", "params", name_or_path + ".json")
+    with open(path) as f:
+        return json.load(f)

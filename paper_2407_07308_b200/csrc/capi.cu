@@ -1,0 +1,406 @@
+// capi.cu -- extern "C" boundary of libboostcom.so (include/boostcom.h).
+#include <algorithm>
+#include <cstring>
+
+#include "engine.h"
+
+using namespace bc;
+
+#define API_BEGIN try {
+#define API_END                                   \
+    }                                             \
+    catch (BcError & e) {                         \
+        last_error() = e.msg;                     \
+        return e.st;                              \
+    }                                             \
+    catch (std::exception & e) {                  \
+        last_error() = e.what();                  \
+        return BC_E_INTERNAL;                     \
+    }                                             \
+    return BC_OK;
+
+static cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+static void check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) BC_THROW(BC_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+extern "C" {
+
+const char *bc_last_error(void) { return last_error().c_str(); }
+uint64_t bc_launch_count(int reset) {
+    uint64_t c = launch_counter();
+    if (reset) launch_counter() = 0;
+    return c;
+}
+
+bc_status bc_ctx_create(const bc_params *prm, int device, bc_ctx **out) {
+    API_BEGIN
+    if (!prm || !out) BC_THROW(BC_E_ARG, "null argument");
+    bc_ctx *X = new bc_ctx();
+    X->prm = *prm;
+    X->device = device;
+    try {
+        ctx_build(X);
+    } catch (...) {
+        ctx_free(X);
+        delete X;
+        throw;
+    }
+    *out = X;
+    API_END
+}
+
+void bc_ctx_destroy(bc_ctx *ctx) {
+    if (!ctx) return;
+    ctx_free(ctx);
+    delete ctx;
+}
+
+bc_status bc_ctx_info(const bc_ctx *X, bc_info *o) {
+    API_BEGIN
+    if (!X || !o) BC_THROW(BC_E_ARG, "null argument");
+    o->n = X->n; o->m = X->m; o->M = X->M; o->D = X->alg.D; o->S = X->alg.S;
+    o->ints_per_ct = X->ints; o->n_cipher = X->L1; o->n_special = X->K; o->dnum = X->dnum;
+    o->g = X->alg.g; o->base = X->base; o->n_galois = (uint32_t)X->galois.size();
+    API_END
+}
+
+bc_status bc_ctx_moduli(const bc_ctx *X, uint64_t *h_out, uint64_t *h_omega) {
+    API_BEGIN
+    if (!X) BC_THROW(BC_E_ARG, "null ctx");
+    if (h_out) std::copy(X->moduli.begin(), X->moduli.end(), h_out);
+    if (h_omega) std::copy(X->omega.begin(), X->omega.end(), h_omega);
+    API_END
+}
+
+bc_status bc_ctx_slots(const bc_ctx *X, int64_t *h_G, int64_t *h_zeta, int64_t *h_t) {
+    API_BEGIN
+    if (!X) BC_THROW(BC_E_ARG, "null ctx");
+    if (h_G) std::copy(X->alg.gf.G.begin(), X->alg.gf.G.end(), h_G);
+    if (h_zeta) std::copy(X->alg.zeta.begin(), X->alg.zeta.end(), h_zeta);
+    if (h_t) for (size_t s = 0; s < X->alg.t.size(); ++s) h_t[s] = X->alg.t[s];
+    API_END
+}
+
+bc_status bc_ctx_galois(const bc_ctx *X, uint32_t *h_out) {
+    API_BEGIN
+    if (!X || !h_out) BC_THROW(BC_E_ARG, "null argument");
+    std::copy(X->galois.begin(), X->galois.end(), h_out);
+    API_END
+}
+
+size_t bc_ct_bytes(const bc_ctx *X, uint32_t batch, uint32_t level) {
+    return X ? (size_t)batch * 2 * level * X->n * 8 : 0;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ dry-run sizing
+template <class F>
+static size_t dry_peak(bc_ctx *X, const bc_keys *keys, F fn) {
+    Arena A;
+    A.init(nullptr, (size_t)1 << 62, true);
+    Eng E{X, keys, &A, 0};
+    fn(E);
+    return A.peak;
+}
+
+static size_t compare_peak(bc_ctx *X, const bc_keys *keys, uint32_t B, uint32_t lvl, int which) {
+    return dry_peak(X, keys, [&](Eng &E) {
+        CT a = E.view((uint64_t *)(uintptr_t)256, B, lvl), b = E.view((uint64_t *)(uintptr_t)256, B, lvl);
+        CT lt, eq;
+        if (which == 2) {
+            compare_batch(E, a, b, &lt, nullptr);
+            CT o = select_batch(E, lt, a, b);
+        } else {
+            compare_batch(E, a, b, &lt, which == 1 ? &eq : nullptr);
+        }
+    });
+}
+
+extern "C" size_t bc_workspace_bytes(bc_ctx *X, uint32_t batch) {
+    try {
+        return compare_peak(X, nullptr, batch, X->L1, 2) + (1u << 20);
+    } catch (...) {
+        return 0;
+    }
+}
+
+extern "C" uint32_t bc_compare_out_level(bc_ctx *X, uint32_t level, int which) {
+    try {
+        uint32_t out = 0;
+        Arena A;
+        A.init(nullptr, (size_t)1 << 62, true);
+        Eng E{X, nullptr, &A, 0};
+        CT a = E.view((uint64_t *)(uintptr_t)256, 1, level), b = a;
+        CT lt, eq;
+        if (which == 2) {
+            compare_batch(E, a, b, &lt, nullptr);
+            out = select_batch(E, lt, a, b).lvl;
+        } else {
+            compare_batch(E, a, b, &lt, which == 1 ? &eq : nullptr);
+            out = which == 1 ? eq.lvl : lt.lvl;
+        }
+        return out;
+    } catch (...) {
+        return 0;
+    }
+}
+
+// choose the largest chunk whose dry-run peak fits the workspace
+static uint32_t choose_chunk(bc_ctx *X, const bc_keys *keys, uint32_t B, uint32_t lvl, int which, size_t ws) {
+    size_t p1 = compare_peak(X, keys, 1, lvl, which);
+    if (p1 > ws) BC_THROW(BC_E_OOM, "workspace smaller than one pair needs (" + std::to_string(p1) + " bytes)");
+    if (B == 1) return 1;
+    size_t p2 = compare_peak(X, keys, 2, lvl, which);
+    size_t per = p2 > p1 ? p2 - p1 : p1;
+    uint64_t c = 1 + (ws - p1) / per;
+    uint32_t chunk = (uint32_t)std::min<uint64_t>(B, c);
+    while (chunk > 1 && compare_peak(X, keys, chunk, lvl, which) > ws) chunk = chunk * 7 / 8;
+    return std::max<uint32_t>(chunk, 1);
+}
+
+static void out_copy(Eng &E, const CT &src, const bc_ct &dst, uint32_t b0) {
+    if (src.lvl != dst.level) BC_THROW(BC_E_LEVEL, "output level " + std::to_string(dst.level) + " != computed " + std::to_string(src.lvl));
+    uint64_t *d = (uint64_t *)dst.data + (uint64_t)b0 * 2 * dst.level * E.X->n;
+    CK(cudaMemcpyAsync(d, src.d, (size_t)src.B * src.bstride * 8, cudaMemcpyDeviceToDevice, E.st));
+}
+
+static void check_ct(const bc_ctx *X, const bc_ct &c, const char *nm) {
+    if (!c.data || c.batch == 0) BC_THROW(BC_E_ARG, std::string(nm) + ": empty ciphertext view");
+    if (c.level < 1 || c.level > X->L1) BC_THROW(BC_E_LEVEL, std::string(nm) + ": bad level");
+}
+
+// which: 0 lt, 1 lt+eq, 3 eq only, 2 min, 4 max
+static bc_status run_compare(bc_ctx *X, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct o1, bc_ct o2, void *ws,
+                             size_t wsb, void *st, int which) {
+    API_BEGIN
+    if (!X || !keys) BC_THROW(BC_E_ARG, "null ctx/keys");
+    check_ct(X, a, "a");
+    check_ct(X, b, "b");
+    if (a.batch != b.batch) BC_THROW(BC_E_ARG, "batch mismatch");
+    const uint32_t lvl = std::min(a.level, b.level);
+    const int pk = (which == 2 || which == 4) ? 2 : (which == 0 ? 0 : 1);
+    const uint32_t chunk = choose_chunk(X, keys, a.batch, lvl, pk, wsb);
+    for (uint32_t b0 = 0; b0 < a.batch; b0 += chunk) {
+        const uint32_t nb = std::min(chunk, a.batch - b0);
+        Arena A;
+        A.init(ws, wsb, false);
+        Eng E{X, keys, &A, S(st)};
+        CT av = E.view((uint64_t *)a.data + (uint64_t)b0 * 2 * a.level * X->n, nb, a.level);
+        CT bv = E.view((uint64_t *)b.data + (uint64_t)b0 * 2 * b.level * X->n, nb, b.level);
+        CT lt, eq;
+        if (which == 2 || which == 4) {
+            compare_batch(E, av, bv, &lt, nullptr);
+            CT r = which == 2 ? select_batch(E, lt, av, bv) : select_batch(E, lt, bv, av);
+            out_copy(E, r, o1, b0);
+        } else {
+            compare_batch(E, av, bv, &lt, which ? &eq : nullptr);
+            if (which == 0 || which == 1) out_copy(E, lt, o1, b0);
+            if (which == 1 && o2.data) out_copy(E, eq, o2, b0);
+            if (which == 3) out_copy(E, eq, o1, b0);
+        }
+        check_launch();
+        // the arena is reused by the next chunk: make sure the stream has consumed this one
+        if (b0 + nb < a.batch) CK(cudaStreamSynchronize(S(st)));
+    }
+    API_END
+}
+
+extern "C" {
+
+bc_status bc_compare(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct lt, bc_ct eq, void *ws, size_t wsb, void *st) {
+    return run_compare(X, k, a, b, lt, eq, ws, wsb, st, 1);
+}
+bc_status bc_compare_lt(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void *ws, size_t wsb, void *st) {
+    bc_ct none{nullptr, 0, 0};
+    return run_compare(X, k, a, b, out, none, ws, wsb, st, 0);
+}
+bc_status bc_compare_eq(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void *ws, size_t wsb, void *st) {
+    bc_ct none{nullptr, 0, 0};
+    return run_compare(X, k, a, b, out, none, ws, wsb, st, 3);
+}
+bc_status bc_min(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void *ws, size_t wsb, void *st) {
+    bc_ct none{nullptr, 0, 0};
+    return run_compare(X, k, a, b, out, none, ws, wsb, st, 2);
+}
+bc_status bc_max(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void *ws, size_t wsb, void *st) {
+    bc_ct none{nullptr, 0, 0};
+    return run_compare(X, k, a, b, out, none, ws, wsb, st, 4);
+}
+
+bc_status bc_select(bc_ctx *X, const bc_keys *k, bc_ct cond, bc_ct x1, bc_ct x2, bc_ct out, void *ws, size_t wsb,
+                    void *st) {
+    API_BEGIN
+    if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
+    check_ct(X, cond, "cond"); check_ct(X, x1, "x1"); check_ct(X, x2, "x2");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    CT r = select_batch(E, E.view((uint64_t *)cond.data, cond.batch, cond.level),
+                        E.view((uint64_t *)x1.data, x1.batch, x1.level), E.view((uint64_t *)x2.data, x2.batch, x2.level));
+    out_copy(E, r, out, 0);
+    check_launch();
+    API_END
+}
+
+// ------------------------------------------------------------------ non-blocking (a11)
+bc_status bc_compare_lt_async(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void *ws, size_t wsb,
+                              void *side, bc_handle *h) {
+    if (!h) { last_error() = "null handle"; return BC_E_ARG; }
+    bc_status s = bc_compare_lt(X, k, a, b, out, ws, wsb, side);
+    if (s != BC_OK) return s;
+    API_BEGIN
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, S(side)));
+    h->event = ev;
+    h->stream = side;
+    h->consumed = 0;
+    API_END
+}
+
+bc_status bc_wait(bc_handle *h, void *joiner) {
+    API_BEGIN
+    if (!h || !h->event) BC_THROW(BC_E_ARG, "null handle");
+    if (h->consumed) BC_THROW(BC_E_CONSUMED, "handle already waited on");
+    CK(cudaStreamWaitEvent(S(joiner), (cudaEvent_t)h->event, 0));
+    CK(cudaEventDestroy((cudaEvent_t)h->event));
+    h->consumed = 1;
+    API_END
+}
+
+// ------------------------------------------------------------------ primitives
+bc_status bc_ntt_fwd(bc_ctx *X, const void *in, void *out, uint32_t npoly, uint32_t nlimb, uint32_t prime0, void *ws,
+                     size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !in || !out) BC_THROW(BC_E_ARG, "null argument");
+    if (prime0 + nlimb > X->L1 + X->K) BC_THROW(BC_E_ARG, "limbs out of range");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, nullptr, &A, S(st)};
+    E.ntt_fwd((const uint64_t *)in, (uint64_t *)out, npoly, limbmap_plain(nlimb, prime0), (uint64_t)nlimb * X->n,
+              (uint64_t)nlimb * X->n);
+    check_launch();
+    API_END
+}
+bc_status bc_ntt_inv(bc_ctx *X, const void *in, void *out, uint32_t npoly, uint32_t nlimb, uint32_t prime0, void *ws,
+                     size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !in || !out) BC_THROW(BC_E_ARG, "null argument");
+    if (prime0 + nlimb > X->L1 + X->K) BC_THROW(BC_E_ARG, "limbs out of range");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, nullptr, &A, S(st)};
+    E.ntt_inv((const uint64_t *)in, (uint64_t *)out, npoly, limbmap_plain(nlimb, prime0), (uint64_t)nlimb * X->n,
+              (uint64_t)nlimb * X->n);
+    check_launch();
+    API_END
+}
+
+bc_status bc_tensor(bc_ctx *X, bc_ct a, bc_ct b, void *out, void *st) {
+    API_BEGIN
+    if (!X || !out) BC_THROW(BC_E_ARG, "null argument");
+    check_ct(X, a, "a"); check_ct(X, b, "b");
+    if (a.level != b.level || a.batch != b.batch) BC_THROW(BC_E_LEVEL, "tensor: shape mismatch");
+    ew_tensor(X->d_mods, (uint64_t *)a.data, (uint64_t *)b.data, (uint64_t *)out, a.batch, a.level, X->n, S(st));
+    check_launch();
+    API_END
+}
+
+bc_status bc_automorph(bc_ctx *X, bc_ct a, uint32_t t, bc_ct out, void *st) {
+    API_BEGIN
+    if (!X) BC_THROW(BC_E_ARG, "null ctx");
+    check_ct(X, a, "a");
+    if (gcd_u64(t, X->m) != 1) BC_THROW(BC_E_ARG, "t not in Z_m^*");
+    ew_automorph(X->T, (uint64_t *)a.data, (uint64_t *)out.data, a.batch, 2, a.level, t % X->m, S(st));
+    check_launch();
+    API_END
+}
+
+bc_status bc_keyswitch(bc_ctx *X, const bc_keys *k, const void *poly, uint32_t batch, uint32_t level, uint32_t t,
+                       void *out, void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !k || !poly || !out) BC_THROW(BC_E_ARG, "null argument");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    CT u = E.keyswitch((const uint64_t *)poly, (uint64_t)level * X->n, batch, level, t);
+    CK(cudaMemcpyAsync(out, u.d, (size_t)batch * u.bstride * 8, cudaMemcpyDeviceToDevice, S(st)));
+    check_launch();
+    API_END
+}
+
+bc_status bc_modswitch(bc_ctx *X, bc_ct a, bc_ct out, void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X) BC_THROW(BC_E_ARG, "null ctx");
+    check_ct(X, a, "a");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, nullptr, &A, S(st)};
+    CT r = E.modswitch(E.view((uint64_t *)a.data, a.batch, a.level));
+    out_copy(E, r, out, 0);
+    check_launch();
+    API_END
+}
+
+bc_status bc_mul(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
+    check_ct(X, a, "a"); check_ct(X, b, "b");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    CT r = E.mul(E.view((uint64_t *)a.data, a.batch, a.level), E.view((uint64_t *)b.data, b.batch, b.level));
+    out_copy(E, r, out, 0);
+    check_launch();
+    API_END
+}
+
+bc_status bc_rotate(bc_ctx *X, const bc_keys *k, bc_ct a, int32_t r, bc_ct out, void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
+    check_ct(X, a, "a");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    CT res = E.rotate(E.view((uint64_t *)a.data, a.batch, a.level), r);
+    out_copy(E, res, out, 0);
+    check_launch();
+    API_END
+}
+
+bc_status bc_frobenius(bc_ctx *X, const bc_keys *k, bc_ct a, uint32_t r, bc_ct out, void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
+    check_ct(X, a, "a");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    CT res = E.frobenius(E.view((uint64_t *)a.data, a.batch, a.level), r);
+    out_copy(E, res, out, 0);
+    check_launch();
+    API_END
+}
+
+bc_status bc_extract(bc_ctx *X, const bc_keys *k, bc_ct a, void *out, void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !k || !out) BC_THROW(BC_E_ARG, "null argument");
+    check_ct(X, a, "a");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    std::vector<CT> digs = extract_batch(E, E.view((uint64_t *)a.data, a.batch, a.level));
+    // digits form one batch [d][B]; the ABI layout is [B][d]
+    const uint64_t cw = (uint64_t)2 * a.level * X->n;
+    for (uint32_t i = 0; i < digs.size(); ++i)
+        for (uint32_t b = 0; b < a.batch; ++b)
+            CK(cudaMemcpyAsync((uint64_t *)out + ((uint64_t)b * digs.size() + i) * cw, digs[i].d + (uint64_t)b * cw, cw * 8,
+                               cudaMemcpyDeviceToDevice, S(st)));
+    check_launch();
+    API_END
+}
+
+}  // extern "C"

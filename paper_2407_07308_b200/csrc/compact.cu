@@ -1,0 +1,135 @@
+// compact.cu -- slot compaction (§8(a) a10; §5.3, Fig. 7) with the R17 greedy plan:
+// offsets bucketed so that each (input, output, offset) group costs one plaintext mask product
+// and one rotation; one modulus switch per output at the end.
+#include <algorithm>
+#include <set>
+
+#include "engine.h"
+
+using namespace bc;
+
+namespace bc {
+
+struct Group {
+    uint32_t c, cp;
+    int32_t dl;
+    std::vector<uint32_t> blocks;
+};
+
+static std::vector<int32_t> offsets(uint32_t span) {
+    std::vector<int32_t> o{0};
+    for (int32_t k = 1; k <= (int32_t)span; ++k) { o.push_back(k); o.push_back(-k); }
+    return o;
+}
+
+// mirrors oracle/circuits.py plan_compaction (independent implementation of R17)
+static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful, uint32_t ints, uint32_t span,
+                               uint32_t *n_out) {
+    std::vector<std::set<int64_t>> occ;
+    std::vector<Group> groups;
+    const std::vector<int32_t> offs = offsets(span);
+    for (uint32_t c = 0; c < useful.size(); ++c) {
+        std::vector<uint32_t> rem = useful[c];
+        while (!rem.empty()) {
+            int best_cp = -1, best_dl = 0;
+            size_t best_cnt = 0;
+            for (uint32_t cp = 0; cp < occ.size(); ++cp)
+                for (int32_t dl : offs) {
+                    size_t cnt = 0;
+                    for (uint32_t b : rem) {
+                        int64_t t = (int64_t)b - dl;
+                        if (t >= 0 && t < (int64_t)ints && !occ[cp].count(t)) ++cnt;
+                    }
+                    if (cnt > best_cnt) { best_cnt = cnt; best_cp = (int)cp; best_dl = dl; }
+                }
+            if (best_cp < 0) { occ.emplace_back(); best_cp = (int)occ.size() - 1; best_dl = 0; }
+            Group g{c, (uint32_t)best_cp, best_dl, {}};
+            std::vector<uint32_t> left;
+            for (uint32_t b : rem) {
+                int64_t t = (int64_t)b - best_dl;
+                if (t >= 0 && t < (int64_t)ints && !occ[best_cp].count(t)) {
+                    occ[best_cp].insert(t);
+                    g.blocks.push_back(b);
+                } else {
+                    left.push_back(b);
+                }
+            }
+            groups.push_back(g);
+            rem.swap(left);
+        }
+    }
+    *n_out = (uint32_t)occ.size();
+    return groups;
+}
+
+// encode a 0/1 block mask into an evaluation-form plaintext inside the workspace
+static BufP encode_mask(Eng &E, const std::vector<uint32_t> &blocks) {
+    bc_ctx *X = E.X;
+    const uint32_t S = X->alg.S, D = X->alg.D, n = X->n, L1 = X->L1, l = X->l;
+    std::vector<int16_t> sl((size_t)S * D, 0);
+    for (uint32_t b : blocks)
+        for (uint32_t s = b * l; s < (b + 1) * l; ++s) sl[(size_t)s * D] = 1;
+    BufP s16(new Buf{E.A, E.A->alloc(sl.size() * 2), sl.size() * 2});
+    BufP c16(new Buf{E.A, E.A->alloc((size_t)n * 2), (size_t)n * 2});
+    BufP pt = E.alloc_words((uint64_t)L1 * n);
+    if (!E.dry()) CK(cudaMemcpyAsync(s16->p, sl.data(), sl.size() * 2, cudaMemcpyHostToDevice, E.st));
+    encode_slots_dev(X, (int16_t *)s16->p, 1, (int16_t *)c16->p, E.A, E.st);
+    if (!E.dry()) s16_to_rns(X->d_mods, (int16_t *)c16->p, (uint64_t *)pt->p, 1, L1, n, E.st);
+    E.ntt_fwd((uint64_t *)pt->p, (uint64_t *)pt->p, 1, limbmap_plain(L1, 0), (uint64_t)L1 * n, (uint64_t)L1 * n);
+    if (!E.dry()) CK(cudaStreamSynchronize(E.st));   // the host mask vector dies here
+    return pt;
+}
+
+}  // namespace bc
+
+extern "C" bc_status bc_compact(bc_ctx *X, const bc_keys *keys, bc_ct in, const uint8_t *h_useful, bc_ct out,
+                                uint32_t *n_out, int32_t *h_dest, void *ws, size_t wsb, void *stv) {
+    try {
+        if (!X || !keys || !in.data || !out.data || !h_useful || !n_out) BC_THROW(BC_E_ARG, "null argument");
+        if (in.level < 2) BC_THROW(BC_E_LEVEL, "compaction needs one level");
+        if (out.level != in.level - 1) BC_THROW(BC_E_LEVEL, "output level must be input level - 1");
+        const uint32_t ints = X->ints, nin = in.batch;
+        std::vector<std::vector<uint32_t>> useful(nin);
+        for (uint32_t c = 0; c < nin; ++c)
+            for (uint32_t b = 0; b < ints; ++b)
+                if (h_useful[(size_t)c * ints + b]) useful[c].push_back(b);
+        uint32_t nout = 0;
+        const uint32_t span = X->prm.compact_span ? X->prm.compact_span : 3;
+        std::vector<Group> groups = plan(useful, ints, span, &nout);
+        if (nout > out.batch) BC_THROW(BC_E_ARG, "output capacity too small");
+        if (h_dest) {
+            for (size_t i = 0; i < (size_t)nin * ints; ++i) h_dest[i] = -1;
+            for (const Group &g : groups)
+                for (uint32_t b : g.blocks) h_dest[(size_t)g.c * ints + b] = (int32_t)(g.cp * ints + (uint32_t)((int64_t)b - g.dl));
+        }
+        Arena A;
+        A.init(ws, wsb, false);
+        Eng E{X, keys, &A, (cudaStream_t)stv};
+        const uint64_t cw = (uint64_t)2 * in.level * X->n;
+        std::vector<CT> acc(nout);
+        std::vector<bool> have(nout, false);
+        for (const Group &g : groups) {
+            if (g.blocks.empty()) continue;
+            BufP mk = encode_mask(E, g.blocks);
+            CT src = E.view((uint64_t *)in.data + (uint64_t)g.c * cw, 1, in.level);
+            CT t = E.ptmul(src, (uint64_t *)mk->p);
+            if (g.dl) t = E.rotate(t, (int64_t)g.dl * X->l);
+            acc[g.cp] = have[g.cp] ? E.add(acc[g.cp], t) : t;
+            have[g.cp] = true;
+        }
+        const uint64_t ow = (uint64_t)2 * out.level * X->n;
+        for (uint32_t cp = 0; cp < nout; ++cp) {
+            CT r = E.modswitch(acc[cp]);
+            CK(cudaMemcpyAsync((uint64_t *)out.data + (uint64_t)cp * ow, r.d, ow * 8, cudaMemcpyDeviceToDevice, E.st));
+        }
+        CK(cudaGetLastError());
+        *n_out = nout;
+    } catch (BcError &e) {
+        last_error() = e.msg;
+        return e.st;
+    } catch (std::exception &e) {
+        last_error() = e.what();
+        return BC_E_INTERNAL;
+    }
+    return BC_OK;
+}

@@ -1,0 +1,968 @@
+// engine.cu -- context construction, batched BGV operations and the comparison schedule.
+//
+// Every arithmetic step runs in the kernels of kernels.cu; this file only builds tables (once
+// per context), allocates from the caller's workspace and enqueues kernels on the caller's
+// stream.  Readings R1-R17 are listed in DESIGN.md §3.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+
+#include "engine.h"
+
+namespace bc {
+
+std::string &last_error() {
+    static thread_local std::string e;
+    return e;
+}
+
+// =====================================================================================
+// arena
+// =====================================================================================
+static const size_t ALIGN = 256;
+void Arena::init(void *b, size_t c, bool dry_) {
+    base = (char *)b;
+    cap = c;
+    dry = dry_;
+    used = peak = 0;
+    freel.clear();
+    if (dry) base = (char *)(uintptr_t)4096;
+    freel[0] = cap;
+}
+char *Arena::alloc(size_t bytes) {
+    bytes = (bytes + ALIGN - 1) / ALIGN * ALIGN;
+    if (bytes == 0) bytes = ALIGN;
+    for (auto it = freel.begin(); it != freel.end(); ++it) {
+        if (it->second >= bytes) {
+            size_t off = it->first, sz = it->second;
+            freel.erase(it);
+            if (sz > bytes) freel[off + bytes] = sz - bytes;
+            used += bytes;
+            peak = std::max(peak, used);
+            return base + off;
+        }
+    }
+    BC_THROW(BC_E_OOM, "workspace exhausted (" + std::to_string(bytes) + " bytes requested, " +
+                           std::to_string(cap - used) + " free, fragmented)");
+}
+void Arena::release(char *p, size_t bytes) {
+    bytes = (bytes + ALIGN - 1) / ALIGN * ALIGN;
+    if (bytes == 0) bytes = ALIGN;
+    size_t off = (size_t)(p - base);
+    used -= bytes;
+    auto it = freel.emplace(off, bytes).first;
+    auto nx = std::next(it);
+    if (nx != freel.end() && off + it->second == nx->first) {
+        it->second += nx->second;
+        freel.erase(nx);
+    }
+    if (it != freel.begin()) {
+        auto pv = std::prev(it);
+        if (pv->first + pv->second == it->first) {
+            pv->second += it->second;
+            freel.erase(it);
+        }
+    }
+}
+
+// =====================================================================================
+// context tables
+// =====================================================================================
+static uint64_t shoup(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+static u64x2 sh2(uint64_t w, uint64_t q) { return u64x2{w, shoup(w, q)}; }
+
+template <class Tp>
+static Tp *dev_upload(bc_ctx *X, const std::vector<Tp> &v) {
+    void *p = nullptr;
+    size_t bytes = std::max<size_t>(v.size() * sizeof(Tp), 16);
+    CK(cudaMalloc(&p, bytes));
+    if (!v.empty()) CK(cudaMemcpy(p, v.data(), v.size() * sizeof(Tp), cudaMemcpyHostToDevice));
+    X->owned.push_back(p);
+    return (Tp *)p;
+}
+
+static void host_ntt(std::vector<uint64_t> &a, uint64_t w, uint64_t q) {  // natural in/out, root w
+    size_t N = a.size();
+    for (size_t i = 1, j = 0; i < N; ++i) {
+        size_t bit = N >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= N; len <<= 1) {
+        uint64_t wl = powmod_h(w, N / len, q);
+        for (size_t i = 0; i < N; i += len) {
+            uint64_t x = 1;
+            for (size_t j = 0; j < len / 2; ++j) {
+                uint64_t u = a[i + j], v = mulmod_h(a[i + j + len / 2], x, q);
+                a[i + j] = (u + v) % q;
+                a[i + j + len / 2] = (u + q - v) % q;
+                x = mulmod_h(x, wl, q);
+            }
+        }
+    }
+}
+
+static uint32_t brev_h(uint32_t x, uint32_t bits) {
+    uint32_t r = 0;
+    for (uint32_t i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
+    return r;
+}
+
+static uint64_t mod_of(uint64_t tgt_is_p, uint64_t v, uint64_t T) { (void)tgt_is_p; return v % T; }
+
+// lift plan blob (see kernels.cu k_lift)
+static std::vector<uint64_t> build_plan(const bc_ctx *X, const std::vector<uint32_t> &src,
+                                        const std::vector<int64_t> &tgt /* prime idx or -1 for p */) {
+    const uint32_t ns = (uint32_t)src.size(), nt = (uint32_t)tgt.size();
+    std::vector<uint64_t> qs(ns);
+    for (uint32_t k = 0; k < ns; ++k) qs[k] = X->moduli[src[k]];
+    std::vector<uint64_t> inv(ns), invs(ns), qm((size_t)ns * ns, 0), half(ns);
+    for (uint32_t k = 0; k < ns; ++k) {
+        uint64_t pre = 1;
+        for (uint32_t j = 0; j < k; ++j) pre = mulmod_h(pre, qs[j] % qs[k], qs[k]);
+        inv[k] = k ? invmod_h(pre, qs[k]) : 1;
+        invs[k] = shoup(inv[k], qs[k]);
+        for (uint32_t j = 0; j < k; ++j) qm[(size_t)k * ns + j] = qs[j] % qs[k];
+    }
+    // mixed-radix digits of (Q-1)/2: its residues are (q_k - 1)/2 (Q = 0 mod q_k, Q odd)
+    for (uint32_t k = 0; k < ns; ++k) {
+        uint64_t r = (qs[k] - 1) / 2;
+        if (k == 0) { half[0] = r; continue; }
+        uint64_t acc = half[k - 1] % qs[k];
+        for (int j = (int)k - 2; j >= 0; --j) acc = (mulmod_h(acc, qm[(size_t)k * ns + j], qs[k]) + half[j] % qs[k]) % qs[k];
+        half[k] = mulmod_h((r + qs[k] - acc) % qs[k], inv[k], qs[k]);
+    }
+    std::vector<uint64_t> blob;
+    blob.push_back(ns);
+    blob.push_back(nt);
+    for (uint32_t k = 0; k < ns; ++k) blob.push_back(src[k]);
+    blob.insert(blob.end(), inv.begin(), inv.end());
+    blob.insert(blob.end(), invs.begin(), invs.end());
+    blob.insert(blob.end(), qm.begin(), qm.end());
+    blob.insert(blob.end(), half.begin(), half.end());
+    for (uint32_t t = 0; t < nt; ++t) blob.push_back(tgt[t] < 0 ? ~0ull : (uint64_t)tgt[t]);
+    std::vector<uint64_t> Qm(nt);
+    for (uint32_t t = 0; t < nt; ++t) {
+        uint64_t T = tgt[t] < 0 ? X->p : X->moduli[tgt[t]];
+        uint64_t pre = 1 % T;
+        for (uint32_t k = 0; k < ns; ++k) {
+            blob.push_back(pre);
+            pre = mulmod_h(pre, qs[k] % T, T);
+        }
+        Qm[t] = pre;
+    }
+    blob.insert(blob.end(), Qm.begin(), Qm.end());
+    (void)mod_of;
+    return blob;
+}
+
+
+// F_p interpolation: coefficients c with sum_k c_k v^k = f(v) for all v in F_p (Vandermonde solve)
+static std::vector<int64_t> interp_fp(int64_t p, const std::function<int64_t(int64_t)> &f) {
+    std::vector<std::vector<int64_t>> A(p, std::vector<int64_t>(p + 1));
+    for (int64_t v = 0; v < p; ++v) {
+        int64_t x = 1;
+        for (int64_t k = 0; k < p; ++k) { A[v][k] = x; x = x * v % p; }
+        A[v][p] = ((f(v) % p) + p) % p;
+    }
+    for (int64_t c = 0; c < p; ++c) {
+        int64_t piv = c;
+        while (A[piv][c] == 0) ++piv;
+        std::swap(A[piv], A[c]);
+        int64_t inv = (int64_t)powmod_h((uint64_t)A[c][c], p - 2, p);
+        for (auto &x : A[c]) x = x * inv % p;
+        for (int64_t r = 0; r < p; ++r) {
+            if (r == c || !A[r][c]) continue;
+            int64_t fct = A[r][c];
+            for (int64_t k = 0; k <= p; ++k) A[r][k] = ((A[r][k] - fct * A[c][k]) % p + p) % p;
+        }
+    }
+    std::vector<int64_t> c(p);
+    for (int64_t k = 0; k < p; ++k) c[k] = A[k][p];
+    return c;
+}
+
+// bivariate LT(x,y) = [x<y] = sum_u d_u(x) sum_{v>u} d_v(y), d_u = indicator of u, rewritten in
+// (Y = y, Z = x - y): out[j][k] coefficient of Y^j Z^k.
+static std::vector<std::vector<int64_t>> lt_bivariate(int64_t p) {
+    std::vector<std::vector<int64_t>> dl(p);
+    for (int64_t u = 0; u < p; ++u) dl[u] = interp_fp(p, [u](int64_t v) { return v == u ? 1 : 0; });
+    // binomials mod p
+    std::vector<std::vector<int64_t>> Cb(p, std::vector<int64_t>(p, 0));
+    for (int64_t a = 0; a < p; ++a) {
+        Cb[a][0] = 1;
+        for (int64_t r = 1; r <= a; ++r) Cb[a][r] = (Cb[a - 1][r - 1] + (r < a ? Cb[a - 1][r] : 0)) % p;
+    }
+    std::vector<std::vector<int64_t>> out(2 * p, std::vector<int64_t>(2 * p, 0));
+    for (int64_t u = 0; u < p; ++u) {
+        std::vector<int64_t> G(p, 0);   // sum_{v>u} d_v(Y)
+        for (int64_t v = u + 1; v < p; ++v)
+            for (int64_t b = 0; b < p; ++b) G[b] = (G[b] + dl[v][b]) % p;
+        for (int64_t a = 0; a < p; ++a) {
+            if (!dl[u][a]) continue;
+            for (int64_t r = 0; r <= a; ++r) {          // x^a = (Y+Z)^a = sum C(a,r) Z^r Y^{a-r}
+                int64_t cz = dl[u][a] * Cb[a][r] % p;
+                if (!cz) continue;
+                for (int64_t b = 0; b < p; ++b) {
+                    if (!G[b]) continue;
+                    int64_t &o = out[(a - r) + b][r];
+                    o = (o + cz * G[b]) % p;
+                }
+            }
+        }
+    }
+    return out;
+}
+
+static bool is_prime_small(uint32_t m) {
+    if (m < 2) return false;
+    for (uint32_t d = 2; d * d <= m; ++d) if (m % d == 0) return false;
+    return true;
+}
+
+void ctx_build(bc_ctx *X) {
+    const bc_params &P = X->prm;
+    if (P.p < 3 || P.m < 3 || (P.m % 2) == 0 || gcd_u64(P.p, P.m) != 1) BC_THROW(BC_E_PARAM, "need odd p >= 3, odd m, gcd = 1");
+    if (P.circuit != 'U' && P.circuit != 'B') BC_THROW(BC_E_PARAM, "circuit must be 'U' or 'B'");
+    if (P.n_cipher < 1 || P.n_cipher > 60 || P.n_special < 1 || P.n_special > 16 || P.alpha < 1 || P.alpha > 16)
+        BC_THROW(BC_E_PARAM, "chain sizes out of range");
+    if (P.alpha > P.n_special) BC_THROW(BC_E_PARAM, "need n_special >= alpha (P > Q_j, R8)");
+    X->p = P.p; X->m = P.m; X->d = P.d; X->l = P.l;
+    X->M = 1;
+    while (X->M < 2 * X->m - 1) X->M <<= 1;
+    uint32_t lg = 0;
+    while ((1u << lg) < X->M) ++lg;
+    X->logR = lg / 2; X->logC = lg - X->logR;
+    X->R = 1u << X->logR; X->C = 1u << X->logC;
+    X->phi = cyclotomic(X->m);
+    X->n = (uint32_t)X->phi.size() - 1;
+    X->prime_m = is_prime_small(X->m);
+    // primes (R1)
+    uint64_t L = X->p;
+    auto lcm = [](uint64_t a, uint64_t b) { return a / gcd_u64(a, b) * b; };
+    L = lcm(lcm(L, X->m), X->M);
+    try {
+        auto qs = prime_chain(L, (int)P.cipher_bits, (int)P.n_cipher, 0, X->p);
+        auto ps = prime_chain(L, (int)P.special_bits, (int)P.n_special, *std::max_element(qs.begin(), qs.end()), X->p);
+        X->moduli = qs;
+        X->moduli.insert(X->moduli.end(), ps.begin(), ps.end());
+    } catch (std::exception &e) {
+        BC_THROW(BC_E_PARAM, e.what());
+    }
+    X->L1 = P.n_cipher; X->K = P.n_special; X->alpha = P.alpha;
+    X->dnum = (X->L1 + X->alpha - 1) / X->alpha;
+    const uint32_t NP = X->L1 + X->K;
+    X->omega.resize(NP);
+    for (uint32_t i = 0; i < NP; ++i) X->omega[i] = root_of_order(X->m, X->moduli[i]);
+    // slot algebra (R5)
+    if (!X->alg.build(X->p, X->m, X->phi, std::min<uint32_t>(P.d, (uint32_t)mult_order(X->p, X->m))))
+        BC_THROW(BC_E_PARAM, X->alg.error);
+    if (P.d > X->alg.D || P.d < 1 || P.l < 1 || P.l > X->alg.S) BC_THROW(BC_E_PARAM, "(d, l) incompatible with the ring");
+    X->base = P.circuit == 'B' ? X->p : (X->p + 1) / 2;
+    X->ints = X->alg.S / P.l;
+    // circuit coefficients (R16)
+    {
+        const int64_t p = X->p, h = (p - 1) / 2;
+        X->lt_u = interp_fp(p, [p, h](int64_t v) { return (v >= p - h && v <= p - 1) ? 1 : 0; });
+        X->eq_u = interp_fp(p, [](int64_t v) { return v == 0 ? 1 : 0; });
+        if (P.circuit == 'B') X->lt_b = lt_bivariate(p);
+    }
+    // Galois elements: Frobenius p^k (k < D), rotations g^{+-2^r} (r < ceil log2 l)
+    {
+        std::vector<uint32_t> gl;
+        for (uint32_t k = 1; k < X->alg.D; ++k) gl.push_back((uint32_t)powmod_h(X->p, k, X->m));
+        const uint64_t ginv = invmod_h_any(X->alg.g, X->m);
+        for (uint32_t sh = 1; sh < P.l; sh <<= 1) {
+            gl.push_back((uint32_t)powmod_h(X->alg.g, sh, X->m));
+            gl.push_back((uint32_t)powmod_h(ginv, sh, X->m));
+        }
+        // slot compaction offsets +-delta*l, delta <= span (R17)
+        const uint32_t span = P.compact_span ? P.compact_span : 3;
+        for (uint32_t k = 1; k <= span; ++k) {
+            gl.push_back((uint32_t)powmod_h(X->alg.g, (uint64_t)k * P.l, X->m));
+            gl.push_back((uint32_t)powmod_h(ginv, (uint64_t)k * P.l, X->m));
+        }
+        std::sort(gl.begin(), gl.end());
+        gl.erase(std::unique(gl.begin(), gl.end()), gl.end());
+        X->galois = gl;
+    }
+
+    // ---------------- device tables ----------------
+    CK(cudaSetDevice(X->device));
+    const uint32_t m = X->m, n = X->n, M = X->M;
+    std::vector<Mod> mods(NP);
+    for (uint32_t i = 0; i < NP; ++i) {
+        uint64_t q = X->moduli[i];
+        uint32_t b = 64 - __builtin_clzll(q);
+        u128 num = (u128)1 << (2 * b);
+        mods[i] = Mod{q, (uint64_t)(num / q), b, 0};
+    }
+    X->d_mods = dev_upload(X, mods);
+    std::vector<u64x2> psi((size_t)NP * M), tf1((size_t)NP * m), tf1i((size_t)NP * m), tfo((size_t)NP * m),
+        tfoi((size_t)NP * m), dhf((size_t)NP * M), dhi((size_t)NP * M);
+    const uint64_t h = (m + 1) / 2;   // 2^{-1} mod m
+    for (uint32_t i = 0; i < NP; ++i) {
+        const uint64_t q = X->moduli[i], w = X->omega[i], wi = invmod_h(w, q);
+        const uint64_t ps = root_of_order(M, q);
+        uint64_t x = 1;
+        for (uint32_t e = 0; e < M; ++e) { psi[(size_t)i * M + e] = sh2(x, q); x = mulmod_h(x, ps, q); }
+        const uint64_t Minv = invmod_h(M % q, q), minv = invmod_h(m % q, q);
+        std::vector<uint64_t> wp(m), wip(m);
+        x = 1;
+        for (uint32_t e = 0; e < m; ++e) { wp[e] = x; x = mulmod_h(x, w, q); }
+        x = 1;
+        for (uint32_t e = 0; e < m; ++e) { wip[e] = x; x = mulmod_h(x, wi, q); }
+        std::vector<uint64_t> Df(M, 0), Di(M, 0);
+        for (uint64_t j = 0; j < m; ++j) {
+            const uint64_t e = h * (j * j % m) % m;
+            tf1[(size_t)i * m + j] = sh2(wp[e], q);
+            tf1i[(size_t)i * m + j] = sh2(wip[e], q);
+            tfo[(size_t)i * m + j] = sh2(mulmod_h(wp[e], Minv, q), q);
+            tfoi[(size_t)i * m + j] = sh2(mulmod_h(mulmod_h(wip[e], Minv, q), minv, q), q);
+            // forward: D_t = w^{-h t^2}; inverse (root w^{-1}): D'_t = w^{+h t^2}
+            Df[j] = wip[e];
+            Di[j] = wp[e];
+            if (j) { Df[M - j] = wip[e]; Di[M - j] = wp[e]; }
+        }
+        host_ntt(Df, ps, q);
+        host_ntt(Di, ps, q);
+        for (uint32_t rp = 0; rp < X->R; ++rp)
+            for (uint32_t cp = 0; cp < X->C; ++cp) {
+                uint32_t k = brev_h(rp, X->logR) + X->R * brev_h(cp, X->logC);
+                dhf[(size_t)i * M + (size_t)rp * X->C + cp] = sh2(Df[k], q);
+                dhi[(size_t)i * M + (size_t)rp * X->C + cp] = sh2(Di[k], q);
+            }
+    }
+    std::vector<int32_t> pos(m, -1), z;
+    for (uint32_t t = 0; t < m; ++t)
+        if (gcd_u64(t, m) == 1) { pos[t] = (int32_t)z.size(); z.push_back((int32_t)t); }
+    std::vector<int8_t> phi8(n + 1);
+    for (uint32_t j = 0; j <= n; ++j) {
+        if (X->phi[j] < -127 || X->phi[j] > 127) BC_THROW(BC_E_PARAM, "Phi_m coefficient out of int8 range");
+        phi8[j] = (int8_t)X->phi[j];
+    }
+    NttTables &T = X->T;
+    T.psi = dev_upload(X, psi); T.tf1 = dev_upload(X, tf1); T.tf1i = dev_upload(X, tf1i);
+    T.tfo = dev_upload(X, tfo); T.tfoi = dev_upload(X, tfoi); T.dhf = dev_upload(X, dhf); T.dhi = dev_upload(X, dhi);
+    T.pos = dev_upload(X, pos); T.z = dev_upload(X, z); T.phi = dev_upload(X, phi8); T.mods = X->d_mods;
+    T.m = m; T.n = n; T.M = M; T.R = X->R; T.C = X->C; T.logR = X->logR; T.logC = X->logC;
+    T.prime_m = X->prime_m ? 1 : 0;
+
+    // ---------------- lift plans ----------------
+    std::vector<uint64_t> blob;
+    auto add_plan = [&](const std::string &k, const std::vector<uint32_t> &src, const std::vector<int64_t> &tgt) {
+        X->plan_off[k] = blob.size();
+        auto b = build_plan(X, src, tgt);
+        blob.insert(blob.end(), b.begin(), b.end());
+    };
+    for (uint32_t lv = 1; lv <= X->L1; ++lv) {
+        for (uint32_t j = 0; j * X->alpha < lv; ++j) {
+            uint32_t g0 = j * X->alpha, g1 = std::min(lv, (j + 1) * X->alpha);
+            std::vector<uint32_t> src;
+            for (uint32_t i = g0; i < g1; ++i) src.push_back(i);
+            std::vector<int64_t> tgt;
+            for (uint32_t i = 0; i < lv; ++i) if (i < g0 || i >= g1) tgt.push_back(i);
+            for (uint32_t k = 0; k < X->K; ++k) tgt.push_back(X->L1 + k);
+            add_plan("up:" + std::to_string(lv) + ":" + std::to_string(j), src, tgt);
+        }
+        {
+            std::vector<uint32_t> src;
+            for (uint32_t k = 0; k < X->K; ++k) src.push_back(X->L1 + k);
+            std::vector<int64_t> tgt;
+            for (uint32_t i = 0; i < lv; ++i) tgt.push_back(i);
+            tgt.push_back(-1);
+            add_plan("down:" + std::to_string(lv), src, tgt);
+        }
+        if (lv >= 2) {
+            std::vector<int64_t> tgt;
+            for (uint32_t i = 0; i + 1 < lv; ++i) tgt.push_back(i);
+            tgt.push_back(-1);
+            add_plan("ms:" + std::to_string(lv), {lv - 1}, tgt);
+        }
+        {
+            std::vector<uint32_t> src;
+            for (uint32_t i = 0; i < lv; ++i) src.push_back(i);
+            add_plan("dec:" + std::to_string(lv), src, {-1});
+        }
+    }
+    X->d_plans = dev_upload(X, blob);
+    // ModDown / modswitch scaling constants
+    {
+        std::vector<u64x2> ip(X->L1), iq((size_t)(X->L1 + 1) * X->L1, u64x2{0, 0});
+        for (uint32_t i = 0; i < X->L1; ++i) {
+            uint64_t q = X->moduli[i], P = 1;
+            for (uint32_t k = 0; k < X->K; ++k) P = mulmod_h(P, X->moduli[X->L1 + k] % q, q);
+            ip[i] = sh2(invmod_h(P, q), q);
+        }
+        for (uint32_t lv = 2; lv <= X->L1; ++lv)
+            for (uint32_t i = 0; i + 1 < lv; ++i) {
+                uint64_t q = X->moduli[i];
+                iq[(size_t)lv * X->L1 + i] = sh2(invmod_h(X->moduli[lv - 1] % q, q), q);
+            }
+        X->d_invP = dev_upload(X, ip);
+        X->d_invq = dev_upload(X, iq);
+    }
+    // ---------------- encode / decode matrices ----------------
+    {
+        const uint32_t D = X->alg.D, S = X->alg.S;
+        std::vector<int16_t> E0((size_t)D * m, 0), zp((size_t)m * D);
+        for (uint32_t i = 0; i < D; ++i)
+            for (uint32_t e = 0; e < n; ++e) E0[(size_t)i * m + e] = (int16_t)X->alg.E0[i][e];
+        for (size_t e = 0; e < (size_t)m * D; ++e) zp[e] = (int16_t)X->alg.zpow[e];
+        X->d_E0 = dev_upload(X, E0);
+        X->d_zpow = dev_upload(X, zp);
+        X->d_ts = dev_upload(X, X->alg.t);
+        if (!X->prime_m) {
+            // rows x^k mod Phi_m (k = n .. m-1) over Z
+            std::vector<int8_t> red((size_t)(m - n) * n);
+            std::vector<int64_t> cur(n, 0);
+            // x^n = -sum_{j<n} phi_j x^j
+            for (uint32_t j = 0; j < n; ++j) cur[j] = -X->phi[j];
+            for (uint32_t k = n; k < m; ++k) {
+                for (uint32_t j = 0; j < n; ++j) {
+                    if (cur[j] < -127 || cur[j] > 127) BC_THROW(BC_E_PARAM, "reduction row out of int8 range");
+                    red[(size_t)(k - n) * n + j] = (int8_t)cur[j];
+                }
+                int64_t top = cur[n - 1];
+                for (int j = (int)n - 1; j > 0; --j) cur[j] = cur[j - 1] - top * X->phi[j];
+                cur[0] = -top * X->phi[0];
+            }
+            X->d_red = dev_upload(X, red);
+        }
+        void *em = nullptr, *dm = nullptr;
+        CK(cudaMalloc(&em, (size_t)n * n));
+        CK(cudaMalloc(&dm, (size_t)n * n));
+        X->owned.push_back(em);
+        X->owned.push_back(dm);
+        X->d_Em = (int8_t *)em;
+        X->d_Dm = (int8_t *)dm;
+        build_encode_matrix(X->d_E0, X->d_ts, X->d_red, X->d_Em, n, m, D, S, (int32_t)X->p, 0);
+        build_decode_matrix(X->d_zpow, X->d_ts, X->d_Dm, n, m, D, S, (int32_t)X->p, 0);
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+    }
+}
+
+void ctx_free(bc_ctx *X) {
+    for (void *p : X->owned) cudaFree(p);
+    X->owned.clear();
+    for (auto &kv : X->pt) cudaFree(kv.second);
+    X->pt.clear();
+}
+
+// =====================================================================================
+// plaintext encoding
+// =====================================================================================
+void encode_slots_dev(bc_ctx *X, const int16_t *d_slots, uint32_t B, int16_t *d_coef, Arena *A, cudaStream_t st) {
+    const uint32_t n = X->n;
+    BufP a8(new Buf{A, A->alloc((size_t)B * n), (size_t)B * n});
+    BufP c32(new Buf{A, A->alloc((size_t)B * n * 4), (size_t)B * n * 4});
+    if (A->dry) return;
+    s16_to_s8(d_slots, (int8_t *)a8->p, (uint64_t)B * n, (int32_t)X->p, st);
+    gemm_s8((int8_t *)a8->p, X->d_Em, (int32_t *)c32->p, B, n, n, st);
+    mod_p_center((int32_t *)c32->p, d_coef, (uint64_t)B * n, (int32_t)X->p, st);
+}
+
+uint64_t *ctx_pt(bc_ctx *X, const std::string &key, const std::vector<int16_t> &slots, cudaStream_t st) {
+    auto it = X->pt.find(key);
+    if (it != X->pt.end()) return it->second;
+    const uint32_t n = X->n, L1 = X->L1;
+    uint64_t *out = nullptr;
+    CK(cudaMalloc(&out, (size_t)L1 * n * 8));
+    // temporary workspace
+    size_t need = (size_t)n * 2 + (size_t)n * (1 + 4 + 2) + (size_t)L1 * X->M * 8 + 4096 * 4;
+    void *ws = nullptr;
+    CK(cudaMalloc(&ws, need));
+    Arena A;
+    A.init(ws, need, false);
+    {
+        BufP s16(new Buf{&A, A.alloc(slots.size() * 2), slots.size() * 2});
+        BufP c16(new Buf{&A, A.alloc((size_t)n * 2), (size_t)n * 2});
+        CK(cudaMemcpyAsync(s16->p, slots.data(), slots.size() * 2, cudaMemcpyHostToDevice, st));
+        encode_slots_dev(X, (int16_t *)s16->p, 1, (int16_t *)c16->p, &A, st);
+        s16_to_rns(X->d_mods, (int16_t *)c16->p, out, 1, L1, n, st);
+        BufP scr(new Buf{&A, A.alloc((size_t)L1 * X->M * 8), (size_t)L1 * X->M * 8});
+        ntt_forward(X->T, out, out, 1, limbmap_plain(L1, 0), (uint64_t)L1 * n, (uint64_t)L1 * n, (uint64_t *)scr->p, st);
+        CK(cudaStreamSynchronize(st));
+    }
+    cudaFree(ws);
+    X->pt[key] = out;
+    return out;
+}
+
+// =====================================================================================
+// engine ops
+// =====================================================================================
+BufP Eng::alloc_words(uint64_t words) {
+    size_t bytes = (size_t)words * 8;
+    return BufP(new Buf{A, A->alloc(bytes), bytes});
+}
+CT Eng::ct_alloc(uint32_t B, uint32_t lvl, uint32_t parts) {
+    CT c;
+    c.B = B; c.lvl = lvl; c.parts = parts;
+    c.bstride = (uint64_t)parts * lvl * X->n;
+    c.keep = alloc_words((uint64_t)B * c.bstride);
+    c.d = (uint64_t *)c.keep->p;
+    return c;
+}
+CT Eng::view(uint64_t *d, uint32_t B, uint32_t lvl, uint32_t parts) {
+    CT c;
+    c.d = d; c.B = B; c.lvl = lvl; c.parts = parts;
+    c.bstride = (uint64_t)parts * lvl * X->n;
+    return c;
+}
+CT Eng::sub(const CT &a, uint32_t b0, uint32_t nb) {
+    CT c = a;
+    c.d = a.d + (uint64_t)b0 * a.bstride;
+    c.B = nb;
+    return c;
+}
+
+void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
+    // bound the scratch: at most ~1 GiB (or the whole batch if smaller) per launch group
+    const uint64_t per = (uint64_t)lm.njl * X->M;
+    uint32_t chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(npoly, (1ull << 27) / per));
+    BufP scr = alloc_words((uint64_t)chunk * per);
+    if (dry()) return;
+    for (uint32_t p0 = 0; p0 < npoly; p0 += chunk) {
+        uint32_t np = std::min(chunk, npoly - p0);
+        ntt_forward(X->T, in + (uint64_t)p0 * ips, out + (uint64_t)p0 * ops, np, lm, ips, ops, (uint64_t *)scr->p, st);
+    }
+}
+void Eng::ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
+    const uint64_t per = (uint64_t)lm.njl * X->M;
+    uint32_t chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(npoly, (1ull << 27) / per));
+    BufP scr = alloc_words((uint64_t)chunk * per);
+    if (dry()) return;
+    for (uint32_t p0 = 0; p0 < npoly; p0 += chunk) {
+        uint32_t np = std::min(chunk, npoly - p0);
+        ntt_inverse(X->T, in + (uint64_t)p0 * ips, out + (uint64_t)p0 * ops, np, lm, ips, ops, (uint64_t *)scr->p, st);
+    }
+}
+
+// R13: c'_i = (c_i - delta) q^{-1}, delta = r + q [-r]_p, r = [c]_q (last prime)
+CT Eng::modswitch(const CT &a) {
+    if (a.lvl < 2) BC_THROW(BC_E_LEVEL, "modswitch: out of levels");
+    const uint32_t n = X->n, lv = a.lvl, np = a.B * a.parts;
+    CT out = ct_alloc(a.B, lv - 1, a.parts);
+    BufP last = alloc_words((uint64_t)np * n);
+    BufP delta = alloc_words((uint64_t)np * (lv - 1) * n);
+    // poly (b, k) at a.d + b*bstride + k*lv*n; flatten requires bstride == parts*lv*n
+    if (a.bstride != (uint64_t)a.parts * lv * n) BC_THROW(BC_E_INTERNAL, "modswitch: strided batch");
+    ntt_inv(a.d + (uint64_t)(lv - 1) * n, (uint64_t *)last->p, np, limbmap_plain(1, lv - 1), (uint64_t)lv * n, n);
+    if (!dry())
+        lift(X->plan("ms:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)last->p, n, (uint64_t *)delta->p,
+             (uint64_t)(lv - 1) * n, nullptr, np, n, 0, 0, 1, st);
+    ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, np, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
+            (uint64_t)(lv - 1) * n);
+    if (!dry())
+        ew_scale_sub(X->d_mods, a.d, (uint64_t)lv * n, (uint64_t *)delta->p, X->d_invq + (size_t)lv * X->L1, out.d, np,
+                     lv - 1, n, st);
+    return out;
+}
+
+CT Eng::modswitch_to(const CT &a, uint32_t lvl) {
+    CT c = a;
+    while (c.lvl > lvl) c = modswitch(c);
+    return c;
+}
+
+CT Eng::add(const CT &a0, const CT &b0) {
+    CT a = a0, b = b0;
+    const uint32_t lv = std::min(a.lvl, b.lvl);
+    a = modswitch_to(a, lv);
+    b = modswitch_to(b, lv);
+    if (a.parts != b.parts || a.B != b.B) BC_THROW(BC_E_INTERNAL, "add: shape mismatch");
+    CT o = ct_alloc(a.B, lv, a.parts);
+    if (!dry()) {
+        if (a.bstride == o.bstride && b.bstride == o.bstride) {
+            ew_add(X->d_mods, a.d, b.d, o.d, a.B, a.parts, lv, X->n, 0, st);
+        } else {
+            for (uint32_t i = 0; i < a.B; ++i)
+                ew_add(X->d_mods, a.d + i * a.bstride, b.d + i * b.bstride, o.d + i * o.bstride, 1, a.parts, lv, X->n, 0, st);
+        }
+    }
+    return o;
+}
+
+static int64_t centered_p(int64_t c, int64_t p) {
+    int64_t r = ((c % p) + p) % p;
+    return r > p / 2 ? r - p : r;
+}
+
+CT Eng::scalar(const CT &a, int64_t c) {
+    CT o = ct_alloc(a.B, a.lvl, a.parts);
+    if (!dry()) ew_scalar(X->d_mods, a.d, centered_p(c, X->p), o.d, a.B, a.parts, a.lvl, X->n, st);
+    return o;
+}
+CT Eng::add_const(const CT &a, int64_t c) {
+    CT o = ct_alloc(a.B, a.lvl, a.parts);
+    if (!dry()) ew_add_const(X->d_mods, a.d, centered_p(c, X->p), o.d, a.B, a.parts, a.lvl, X->n, st);
+    return o;
+}
+CT Eng::ptmul(const CT &a, const uint64_t *pt) {
+    CT o = ct_alloc(a.B, a.lvl, a.parts);
+    if (!dry()) ew_ptmul(X->d_mods, a.d, pt, o.d, a.B, a.parts, a.lvl, X->n, st);
+    return o;
+}
+CT Eng::add_pt(const CT &a, const uint64_t *pt) {
+    CT o = ct_alloc(a.B, a.lvl, a.parts);
+    if (!dry()) ew_add_pt(X->d_mods, a.d, pt, o.d, a.B, a.parts, a.lvl, X->n, st);
+    return o;
+}
+
+// R14 hybrid key switching: ModUp (exact lift per digit + NTT), KIP, ModDown.
+CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
+    const uint64_t *kptr = nullptr;
+    if (keys) {
+        auto kit = keys->ksk.find(key_id);
+        if (kit == keys->ksk.end()) BC_THROW(BC_E_KEY, "missing Galois key for t=" + std::to_string(key_id));
+        kptr = kit->second;
+    } else if (!dry()) {
+        BC_THROW(BC_E_ARG, "keyswitch without keys");
+    }
+    const uint32_t n = X->n, K = X->K, L1 = X->L1, al = X->alpha, nl = lvl + K;
+    const uint32_t ndig = (lvl + al - 1) / al;
+    BufP dc = alloc_words((uint64_t)B * lvl * n);
+    ntt_inv(d, (uint64_t *)dc->p, B, limbmap_plain(lvl, 0), dps, (uint64_t)lvl * n);
+    BufP ext = alloc_words((uint64_t)B * ndig * nl * n);
+    uint64_t *E = (uint64_t *)ext->p;
+    const uint64_t eps = (uint64_t)ndig * nl * n;
+    for (uint32_t j = 0; j < ndig; ++j) {
+        const uint32_t g0 = j * al, g1 = std::min(lvl, (j + 1) * al);
+        if (!dry())
+            lift(X->plan("up:" + std::to_string(lvl) + ":" + std::to_string(j)), X->d_mods, X->p,
+                 (uint64_t *)dc->p + (uint64_t)g0 * n, (uint64_t)lvl * n, E + (uint64_t)j * nl * n, eps, nullptr, B, n, g0,
+                 g1 - g0, 0, st);
+        LimbMap lm{nl - (g1 - g0), g0, g1 - g0, lvl, 0, L1};
+        ntt_fwd(E + (uint64_t)j * nl * n, E + (uint64_t)j * nl * n, B, lm, eps, eps);
+    }
+    BufP u = alloc_words((uint64_t)B * 2 * nl * n);
+    if (!dry()) {
+        if (dps == (uint64_t)lvl * n)
+            ks_kip(X->d_mods, d, E, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig, n, st);
+        else
+            BC_THROW(BC_E_INTERNAL, "keyswitch: strided input must be compacted first");
+    }
+    dc.reset();
+    ext.reset();
+    // ModDown of both parts: 2B polys with stride nl*n
+    BufP sp = alloc_words((uint64_t)2 * B * K * n);
+    ntt_inv((uint64_t *)u->p + (uint64_t)lvl * n, (uint64_t *)sp->p, 2 * B, LimbMap{K, K, 0, 0, 0, L1}, (uint64_t)nl * n,
+            (uint64_t)K * n);
+    BufP delta = alloc_words((uint64_t)2 * B * lvl * n);
+    if (!dry())
+        lift(X->plan("down:" + std::to_string(lvl)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)K * n,
+             (uint64_t *)delta->p, (uint64_t)lvl * n, nullptr, 2 * B, n, 0, 0, 1, st);
+    sp.reset();
+    ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lvl, 0), (uint64_t)lvl * n, (uint64_t)lvl * n);
+    CT o = ct_alloc(B, lvl, 2);
+    if (!dry())
+        ew_scale_sub(X->d_mods, (uint64_t *)u->p, (uint64_t)nl * n, (uint64_t *)delta->p, X->d_invP, o.d, 2 * B, lvl, n, st);
+    return o;
+}
+
+CT Eng::mul(const CT &a0, const CT &b0) {
+    const uint32_t lv = std::min(a0.lvl, b0.lvl);
+    CT a = modswitch_to(a0, lv), b = modswitch_to(b0, lv);
+    const uint32_t n = X->n, B = a.B;
+    if (a.bstride != (uint64_t)2 * lv * n || b.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "mul: strided");
+    BufP t = alloc_words((uint64_t)B * 3 * lv * n);
+    if (!dry()) ew_tensor(X->d_mods, a.d, b.d, (uint64_t *)t->p, B, lv, n, st);
+    // d2 compacted to [B][lv][n]
+    BufP d2 = alloc_words((uint64_t)B * lv * n);
+    if (!dry()) ew_copy_parts((uint64_t *)t->p, (uint64_t *)d2->p, B, 3, 2, 1, lv, lv, n, 1, 0, st);
+    CT u = keyswitch((uint64_t *)d2->p, (uint64_t)lv * n, B, lv, 0);
+    d2.reset();
+    // u += (d0, d1)
+    {
+        BufP t01 = alloc_words((uint64_t)B * 2 * lv * n);
+        if (!dry()) {
+            ew_copy_parts((uint64_t *)t->p, (uint64_t *)t01->p, B, 3, 0, 2, lv, lv, n, 2, 0, st);
+            ew_add(X->d_mods, u.d, (uint64_t *)t01->p, u.d, B, 2, lv, n, 0, st);
+        }
+    }
+    t.reset();
+    return modswitch(u);
+}
+
+CT Eng::automorph(const CT &a, uint32_t t) {
+    const uint32_t n = X->n, lv = a.lvl, B = a.B;
+    if (a.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "automorph: strided");
+    CT pm = ct_alloc(B, lv, 2);
+    if (!dry()) ew_automorph(X->T, a.d, pm.d, B, 2, lv, t, st);
+    BufP c1 = alloc_words((uint64_t)B * lv * n);
+    if (!dry()) ew_copy_parts(pm.d, (uint64_t *)c1->p, B, 2, 1, 1, lv, lv, n, 1, 0, st);
+    CT u = keyswitch((uint64_t *)c1->p, (uint64_t)lv * n, B, lv, t);
+    c1.reset();
+    {
+        // u part 0 += pm part 0 (pm part 1 is replaced by the key-switch output)
+        BufP c0 = alloc_words((uint64_t)B * 2 * lv * n);
+        if (!dry()) {
+            CK(cudaMemsetAsync(c0->p, 0, (size_t)B * 2 * lv * n * 8, st));
+            ew_copy_parts(pm.d, (uint64_t *)c0->p, B, 2, 0, 1, lv, lv, n, 2, 0, st);
+            ew_add(X->d_mods, u.d, (uint64_t *)c0->p, u.d, B, 2, lv, n, 0, st);
+        }
+    }
+    return u;
+}
+
+CT Eng::rotate(const CT &a, int64_t k) {
+    const int64_t m = X->m;
+    int64_t kk = k;
+    uint64_t g = X->alg.g;
+    uint64_t t;
+    if (kk >= 0) t = powmod_h(g, (uint64_t)kk, m);
+    else t = powmod_h(invmod_h_any(g, m), (uint64_t)(-kk), m);
+    return automorph(a, (uint32_t)t);
+}
+CT Eng::frobenius(const CT &a, uint32_t k) { return automorph(a, (uint32_t)powmod_h(X->p, k, X->m)); }
+
+void Eng::copy_into(const CT &src, uint64_t *dst) {
+    if (dry()) return;
+    CK(cudaMemcpyAsync(dst, src.d, (size_t)src.B * src.bstride * 8, cudaMemcpyDeviceToDevice, st));
+}
+
+// =====================================================================================
+// comparison schedule (R16) -- mirrors oracle/circuits.py operation by operation
+// =====================================================================================
+struct Val {
+    bool isc = false;
+    int64_t c = 0;
+    CT ct;
+};
+static Val VC(int64_t c) { Val v; v.isc = true; v.c = c; return v; }
+static Val VT(const CT &t) { Val v; v.ct = t; return v; }
+
+static Val vmul(Eng &E, const Val &a, const Val &b) {
+    const int64_t p = E.X->p;
+    if (a.isc && b.isc) return VC(((a.c * b.c) % p + p) % p);
+    if (a.isc) return VT(E.scalar(b.ct, a.c));
+    if (b.isc) return VT(E.scalar(a.ct, b.c));
+    return VT(E.mul(a.ct, b.ct));
+}
+static Val vadd(Eng &E, const Val &a, const Val &b) {
+    const int64_t p = E.X->p;
+    if (a.isc && b.isc) return VC(((a.c + b.c) % p + p) % p);
+    if (a.isc) return VT(E.add_const(b.ct, a.c));
+    if (b.isc) return VT(E.add_const(a.ct, b.c));
+    return VT(E.add(a.ct, b.ct));
+}
+static Val lincomb(Eng &E, const std::vector<std::pair<int64_t, std::function<Val()>>> &terms, int64_t cst) {
+    const int64_t p = E.X->p;
+    bool have = false;
+    Val acc;
+    for (auto &t : terms) {
+        int64_t c = ((t.first % p) + p) % p;
+        if (!c) continue;
+        Val v = vmul(E, t.second(), VC(c));
+        acc = have ? vadd(E, acc, v) : v;
+        have = true;
+    }
+    cst = ((cst % p) + p) % p;
+    if (!have) return VC(cst);
+    if (cst) acc = vadd(E, acc, VC(cst));
+    return acc;
+}
+
+struct Powers {
+    Eng &E;
+    std::map<int, Val> pw;
+    Powers(Eng &e, const Val &x) : E(e) { pw[1] = x; }
+    Val get(int j) {
+        auto it = pw.find(j);
+        if (it != pw.end()) return it->second;
+        int a = 1;
+        while (a * 2 < j) a *= 2;   // largest power of two < j
+        Val x = get(a), y = get(j - a);
+        Val r = vmul(E, x, y);
+        pw[j] = r;
+        return r;
+    }
+};
+
+static void univariate(Eng &E, const Val &z, Val *lt, Val *eq) {
+    const int64_t p = E.X->p;
+    const std::vector<int64_t> &c = E.X->lt_u;
+    const int e = (int)(p - 3) / 2;
+    std::vector<int64_t> g(e + 1);
+    for (int k = 0; k <= e; ++k) g[k] = c[2 * k + 1];
+    const int64_t top = c[p - 1];
+    Val W = vmul(E, z, z);
+    Powers pw(E, W);
+    int k0 = 1;
+    while ((int64_t)k0 * k0 < e + 1) k0 *= 2;   // smallest 2^a with 4^a >= e+1
+    for (int j = 2; j <= k0; ++j) pw.get(j);
+    const int nch = (e + 1 + k0 - 1) / k0;
+    auto chunk = [&](int i) {
+        std::vector<std::pair<int64_t, std::function<Val()>>> terms;
+        for (int j = 1; j < k0; ++j)
+            if (i * k0 + j <= e) terms.push_back({g[i * k0 + j], [&pw, j]() { return pw.get(j); }});
+        return lincomb(E, terms, g[i * k0]);
+    };
+    std::function<Val(int, int)> ps = [&](int lo, int hi) -> Val {
+        if (hi - lo == 1) return chunk(lo);
+        int h = 1;
+        while (h * 2 < hi - lo) h *= 2;
+        Val low = ps(lo, lo + h);
+        Val high = ps(lo + h, hi);
+        Val gk = pw.get(k0 * h);
+        return vadd(E, low, vmul(E, gk, high));
+    };
+    Val gval = ps(0, nch);
+    Val We = pw.get(e + 1);
+    *lt = vadd(E, vmul(E, z, gval), vmul(E, We, VC(top)));
+    if (eq) *eq = vadd(E, vmul(E, We, VC(-1)), VC(1));
+}
+
+static void bivariate(Eng &E, const Val &x, const Val &y, Val *lt, Val *eq) {
+    const int64_t p = E.X->p;
+    const auto &c = E.X->lt_b;
+    Val Z = vadd(E, x, vmul(E, y, VC(-1)));
+    Powers zp(E, Z);
+    for (int j = 2; j < p; ++j) zp.get(j);
+    Powers yp(E, y);
+    for (int j = 2; j < p; ++j) yp.get(j);
+    bool have = false;
+    Val acc;
+    for (int j = 1; j < p; ++j) {
+        std::vector<std::pair<int64_t, std::function<Val()>>> terms;
+        for (int k = 1; k < p; ++k) terms.push_back({c[j][k], [&zp, k]() { return zp.get(k); }});
+        Val R = lincomb(E, terms, c[j][0]);
+        if (R.isc && R.c == 0) continue;
+        Val t = vmul(E, yp.get(j), R);
+        acc = have ? vadd(E, acc, t) : t;
+        have = true;
+    }
+    *lt = acc;
+    if (eq) *eq = vadd(E, vmul(E, zp.get((int)p - 1), VC(-1)), VC(1));
+}
+
+static std::vector<int16_t> block_mask(bc_ctx *X, const std::function<bool(uint32_t)> &pred) {
+    const uint32_t S = X->alg.S, D = X->alg.D;
+    std::vector<int16_t> m((size_t)S * D, 0);
+    for (uint32_t s = 0; s < S; ++s)
+        if (s < X->ints * X->l && pred(s % X->l)) m[(size_t)s * D] = 1;
+    return m;
+}
+
+// digit extraction (a8): digit_i = sum_k kappa_{i,k} (.) sigma_{p^k}(ct); returns d views of one batch
+std::vector<CT> extract_batch(Eng &E, const CT &a) {
+    bc_ctx *X = E.X;
+    const uint32_t D = X->alg.D, d = X->d, S = X->alg.S;
+    std::vector<CT> F{a};
+    for (uint32_t k = 1; k < D; ++k) F.push_back(E.frobenius(a, k));
+    CT all = E.ct_alloc(a.B * d, a.lvl, 2);
+    std::vector<CT> out;
+    for (uint32_t i = 0; i < d; ++i) {
+        CT acc;
+        bool have = false;
+        for (uint32_t k = 0; k < D; ++k) {
+            std::vector<int16_t> sl((size_t)S * D);
+            const auto &kap = X->alg.kappa[(size_t)i * D + k];
+            for (uint32_t s = 0; s < S; ++s)
+                for (uint32_t j = 0; j < D; ++j) sl[(size_t)s * D + j] = (int16_t)kap[j];
+            const uint64_t *pt = ctx_pt(X, "kappa:" + std::to_string(i) + ":" + std::to_string(k), sl, E.st);
+            CT t = E.ptmul(F[k], pt);
+            acc = have ? E.add(acc, t) : t;
+            have = true;
+        }
+        CT dst = E.sub(all, i * a.B, a.B);
+        if (!E.dry()) CK(cudaMemcpyAsync(dst.d, acc.d, (size_t)acc.B * acc.bstride * 8, cudaMemcpyDeviceToDevice, E.st));
+        out.push_back(dst);
+    }
+    return out;
+}
+
+static void lex_tree(Eng &E, std::vector<Val> lts, std::vector<Val> eqs, Val *lt, Val *eq, bool need_eq) {
+    while (lts.size() > 1) {
+        std::vector<Val> nl, ne;
+        for (size_t i = 0; i + 1 < lts.size(); i += 2) {
+            nl.push_back(vadd(E, lts[i + 1], vmul(E, eqs[i + 1], lts[i])));
+            bool last_round = lts.size() <= 2;
+            if (need_eq || !last_round) ne.push_back(vmul(E, eqs[i + 1], eqs[i]));
+            else ne.push_back(VC(0));
+        }
+        if (lts.size() % 2) { nl.push_back(lts.back()); ne.push_back(eqs.back()); }
+        lts.swap(nl);
+        eqs.swap(ne);
+    }
+    *lt = lts[0];
+    *eq = eqs[0];
+}
+
+static void lex_slots(Eng &E, Val *lt, Val *eq, bool need_eq) {
+    bc_ctx *X = E.X;
+    const uint32_t l = X->l;
+    for (uint32_t sh = 1; sh < l; sh <<= 1) {
+        const bool last = (sh << 1) >= l;
+        const uint64_t *mask = ctx_pt(X, "ksm:" + std::to_string(sh), block_mask(X, [sh, l](uint32_t t) { return t + sh < l; }), E.st);
+        std::vector<int16_t> im = block_mask(X, [sh, l](uint32_t t) { return t + sh < l; });
+        for (size_t s = 0; s < X->alg.S; ++s) im[s * X->alg.D] = (int16_t)(1 - im[s * X->alg.D]);
+        const uint64_t *inv = ctx_pt(X, "ksi:" + std::to_string(sh), im, E.st);   // 1 - mask, every slot
+        CT hi_lt = E.ptmul(E.rotate(lt->ct, sh), mask);
+        CT hi_eq = E.add_pt(E.ptmul(E.rotate(eq->ct, sh), mask), inv);
+        Val nlt = vadd(E, VT(hi_lt), vmul(E, VT(hi_eq), *lt));
+        if (need_eq || !last) *eq = vmul(E, VT(hi_eq), *eq);
+        *lt = nlt;
+    }
+}
+
+void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
+    bc_ctx *X = E.X;
+    const uint32_t d = X->d, B = a.B;
+    std::vector<Val> lts, eqs;
+    const bool need_eq = eq != nullptr;
+    if (X->prm.circuit == 'U') {
+        CT z = E.add(a, E.scalar(b, -1));
+        std::vector<CT> digs = extract_batch(E, z);
+        // all d digits form one contiguous batch of d*B ciphertexts
+        CT all = digs[0];
+        all.B = d * B;
+        Val L, Q;
+        univariate(E, VT(all), &L, &Q);
+        for (uint32_t i = 0; i < d; ++i) {
+            lts.push_back(VT(E.sub(L.ct, i * B, B)));
+            eqs.push_back(VT(E.sub(Q.ct, i * B, B)));
+        }
+    } else {
+        std::vector<CT> da = extract_batch(E, a);
+        std::vector<CT> db = extract_batch(E, b);
+        CT xa = da[0], xb = db[0];
+        xa.B = d * B;
+        xb.B = d * B;
+        Val L, Q;
+        bivariate(E, VT(xa), VT(xb), &L, &Q);
+        for (uint32_t i = 0; i < d; ++i) {
+            lts.push_back(VT(E.sub(L.ct, i * B, B)));
+            eqs.push_back(VT(E.sub(Q.ct, i * B, B)));
+        }
+    }
+    Val LT, EQ;
+    lex_tree(E, lts, eqs, &LT, &EQ, need_eq || X->l > 1);
+    if (X->l > 1) lex_slots(E, &LT, &EQ, need_eq);
+    *lt = LT.ct;
+    if (eq) *eq = EQ.ct;
+}
+
+CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2) {
+    bc_ctx *X = E.X;
+    const uint32_t l = X->l;
+    CT c = E.ptmul(cond, ctx_pt(X, "bm0", block_mask(X, [](uint32_t t) { return t == 0; }), E.st));
+    for (uint32_t sh = 1; sh < l; sh <<= 1) {
+        const uint64_t *mk = ctx_pt(X, "bmr:" + std::to_string(sh), block_mask(X, [sh](uint32_t t) { return t >= sh; }), E.st);
+        c = E.add(c, E.ptmul(E.rotate(c, -(int64_t)sh), mk));
+    }
+    CT diff = E.add(x1, E.scalar(x2, -1));
+    return E.add(x2, E.mul(c, diff));
+}
+
+}  // namespace bc
+
+const uint64_t *bc_ctx::plan(const std::string &k) const {
+    auto it = plan_off.find(k);
+    if (it == plan_off.end()) BC_THROW(BC_E_INTERNAL, "missing lift plan " + k);
+    return d_plans + it->second;
+}

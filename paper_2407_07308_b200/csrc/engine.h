@@ -1,0 +1,146 @@
+// engine.h -- host orchestration of the batched BGV comparison path (product side).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/boostcom.h"
+#include "host_math.h"
+#include "kernels.h"
+
+namespace bc {
+
+std::string &last_error();
+
+struct BcError {
+    bc_status st;
+    std::string msg;
+};
+#define BC_THROW(code, m) throw ::bc::BcError{code, m}
+#define CK(x)                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess) BC_THROW(BC_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------- workspace arena
+struct Arena {
+    char *base = nullptr;
+    size_t cap = 0;
+    bool dry = false;
+    size_t used = 0, peak = 0;
+    std::map<size_t, size_t> freel;  // offset -> size
+    void init(void *b, size_t c, bool dry_);
+    char *alloc(size_t bytes);
+    void release(char *p, size_t bytes);
+};
+struct Buf {
+    Arena *a;
+    char *p;
+    size_t sz;
+    ~Buf() { if (a && p) a->release(p, sz); }
+};
+typedef std::shared_ptr<Buf> BufP;
+
+// a batch of ciphertexts: u64[B][parts][lvl][n] (possibly a view into a larger buffer)
+struct CT {
+    BufP keep;
+    uint64_t *d = nullptr;
+    uint32_t B = 0, lvl = 0, parts = 2;
+    uint64_t bstride = 0;  // words between consecutive ciphertexts
+};
+
+}  // namespace bc
+
+// ---------------------------------------------------------------- context
+struct bc_ctx {
+    bc_params prm;
+    int device = 0;
+    uint32_t p, m, n, M, R, C, logR, logC, L1, K, alpha, dnum, d, l, base, ints;
+    bool prime_m;
+    std::vector<uint64_t> moduli, omega;
+    std::vector<int64_t> phi;
+    bc::SlotAlgebra alg;
+    std::vector<uint32_t> galois;     // Galois elements with keys (besides relin)
+    // device
+    std::vector<void *> owned;
+    bc::Mod *d_mods = nullptr;
+    bc::NttTables T;
+    uint64_t *d_plans = nullptr;
+    std::map<std::string, size_t> plan_off;
+    bc::u64x2 *d_invP = nullptr;                // [L1] P^{-1} mod q_i
+    bc::u64x2 *d_invq = nullptr;                // [L1+1][L1] q_{l-1}^{-1} mod q_i (row l)
+    int8_t *d_Em = nullptr, *d_Dm = nullptr;    // encode / decode matrices (n x n)
+    int16_t *d_E0 = nullptr, *d_zpow = nullptr;
+    uint32_t *d_ts = nullptr;
+    int8_t *d_red = nullptr;
+    std::map<std::string, uint64_t *> pt;       // encoded plaintext constants, eval [L1][n]
+    // circuit coefficients
+    std::vector<int64_t> lt_u, eq_u;            // univariate LT / EQ coefficients
+    std::vector<std::vector<int64_t>> lt_b;     // bivariate c[j][k] (Y^j Z^k)
+    const uint64_t *plan(const std::string &k) const;
+};
+
+struct bc_sk {
+    std::vector<int64_t> s;    // ternary coefficients
+    uint64_t *d_s = nullptr;   // eval form [L1+K][n]
+};
+
+struct bc_keys {
+    std::map<uint32_t, uint64_t *> ksk;  // t -> [dnum][2][L1+K][n] eval (t = 0 relin)
+    uint64_t *d_pk = nullptr;            // [2][L1][n] (b, a) eval
+    std::vector<void *> owned;
+};
+
+namespace bc {
+
+void ctx_build(bc_ctx *X);
+void ctx_free(bc_ctx *X);
+
+// engine: batched BGV ops on one stream over a workspace arena
+struct Eng {
+    bc_ctx *X;
+    const bc_keys *keys;
+    Arena *A;
+    cudaStream_t st;
+    bool dry() const { return A->dry; }
+
+    BufP alloc_words(uint64_t words);
+    CT ct_alloc(uint32_t B, uint32_t lvl, uint32_t parts = 2);
+    CT view(uint64_t *d, uint32_t B, uint32_t lvl, uint32_t parts = 2);
+    CT sub(const CT &a, uint32_t b0, uint32_t nb);  // sub-batch view
+
+    // transforms / element-wise
+    void ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops);
+    void ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops);
+
+    CT modswitch(const CT &a);
+    CT modswitch_to(const CT &a, uint32_t lvl);
+    CT add(const CT &a, const CT &b);
+    CT scalar(const CT &a, int64_t c);       // c in F_p (centered)
+    CT add_const(const CT &a, int64_t c);
+    CT ptmul(const CT &a, const uint64_t *pt);
+    CT add_pt(const CT &a, const uint64_t *pt);
+    // key switch of polys d (ct b at d + b*dps, lvl limbs, eval) -> [B][2][lvl][n]
+    CT keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);
+    CT mul(const CT &a, const CT &b);
+    CT automorph(const CT &a, uint32_t t);
+    CT rotate(const CT &a, int64_t k);
+    CT frobenius(const CT &a, uint32_t k);
+    void copy_into(const CT &src, uint64_t *dst);
+};
+
+// plaintext constants
+uint64_t *ctx_pt(bc_ctx *X, const std::string &key, const std::vector<int16_t> &slots, cudaStream_t st);
+void encode_slots_dev(bc_ctx *X, const int16_t *d_slots, uint32_t B, int16_t *d_coef, Arena *A,
+                      cudaStream_t st);
+
+// comparison schedule (R16) and friends
+void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq);
+CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2);
+std::vector<CT> extract_batch(Eng &E, const CT &a);
+
+}  // namespace bc

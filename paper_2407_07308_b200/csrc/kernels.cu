@@ -1,0 +1,817 @@
+// kernels.cu -- sm_100a kernels of the BoostCom BGV comparison hot path.
+//
+// a1/a2  Bluestein NTT (§2.2): chirp (TF1), size-M cyclic convolution with D_pad by a
+//        four-step NTT (M = R x C: column pass, row pass with the pointwise D^ product fused
+//        between the forward and inverse row transforms, inverse column pass), output chirp
+//        and the Z_m^* filter of Listing 2 as a branch-free gather via pos[].
+// a3     element-wise ring ops (§5.2): tensor, add, plaintext / scalar products.
+// a4     automorphisms as an evaluation-index permutation.
+// a5/a6  exact centered CRT lifts (Garner) for ModUp / ModDown / modulus switching.
+// R7     counter-based sampler.  Encode/decode as exact int8 GEMMs over F_p.
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace bc {
+
+uint64_t &launch_counter() {
+    static thread_local uint64_t c = 0;
+    return c;
+}
+#define LAUNCHED() (++launch_counter())
+
+static inline unsigned grid_for(uint64_t total, unsigned threads, unsigned cap = 148u * 32u) {
+    uint64_t g = (total + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// =====================================================================================
+// NTT building blocks (shared memory, radix-2)
+// =====================================================================================
+// cnt transforms of length len; element (a, i) at s[a*sa + i*si].
+// COLT: consecutive threads take consecutive transforms a (column tiles, sa == 1);
+// otherwise consecutive threads take consecutive butterflies (row tiles, si == 1).
+template <bool COLT>
+__device__ __forceinline__ void smem_dif(uint64_t *s, int lcnt, int llen, int sa, int si,
+                                         const u64x2 *__restrict__ psi, uint32_t M, uint64_t q) {
+    const int cnt = 1 << lcnt, halfn = 1 << (llen - 1);
+    const int nb = cnt * halfn;
+    for (int lh = llen - 1; lh >= 0; --lh) {
+        const int h = 1 << lh;
+        const uint32_t tstep = M >> (lh + 1);
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+            int a, b;
+            if (COLT) { a = t & (cnt - 1); b = t >> lcnt; }
+            else { a = t >> (llen - 1); b = t & (halfn - 1); }
+            const int blk = b >> lh, jj = b & (h - 1);
+            const int i0 = (blk << (lh + 1)) + jj, i1 = i0 + h;
+            uint64_t *p0 = s + a * sa + i0 * si, *p1 = s + a * sa + i1 * si;
+            const uint64_t x = *p0, y = *p1;
+            *p0 = add_mod(x, y, q);
+            const u64x2 w = psi[jj * tstep];
+            *p1 = mul_shoup(sub_mod(x, y, q), w.w, w.ws, q);
+        }
+        __syncthreads();
+    }
+}
+
+template <bool COLT>
+__device__ __forceinline__ void smem_dit_inv(uint64_t *s, int lcnt, int llen, int sa, int si,
+                                             const u64x2 *__restrict__ psi, uint32_t M, uint64_t q) {
+    const int cnt = 1 << lcnt, halfn = 1 << (llen - 1);
+    const int nb = cnt * halfn;
+    for (int lh = 0; lh < llen; ++lh) {
+        const int h = 1 << lh;
+        const uint32_t tstep = M >> (lh + 1);
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+            int a, b;
+            if (COLT) { a = t & (cnt - 1); b = t >> lcnt; }
+            else { a = t >> (llen - 1); b = t & (halfn - 1); }
+            const int blk = b >> lh, jj = b & (h - 1);
+            const int i0 = (blk << (lh + 1)) + jj, i1 = i0 + h;
+            uint64_t *p0 = s + a * sa + i0 * si, *p1 = s + a * sa + i1 * si;
+            const uint64_t x = *p0;
+            const u64x2 w = psi[(M - jj * tstep) & (M - 1)];
+            const uint64_t y = mul_shoup(*p1, w.w, w.ws, q);
+            *p0 = add_mod(x, y, q);
+            *p1 = sub_mod(x, y, q);
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ uint32_t brev(uint32_t x, uint32_t bits) {
+    return bits ? (__brev(x) >> (32 - bits)) : 0;
+}
+
+struct JobInfo {
+    uint32_t poly, lb, pr;
+};
+__device__ __forceinline__ JobInfo job_info(const LimbMap &lm, uint32_t job) {
+    JobInfo j;
+    j.poly = job / lm.njl;
+    uint32_t jl = job - j.poly * lm.njl;
+    j.lb = lm.limb(jl);
+    j.pr = lm.prime(j.lb);
+    return j;
+}
+
+// ---- pass A: chirp-multiply input, column DIF (length R), twiddle psi^(c*k1), store ----
+template <int INV>
+__global__ void __launch_bounds__(256) k_passA(NttTables T, const uint64_t *__restrict__ in,
+                                               uint64_t in_pstride, LimbMap lm, uint64_t job0,
+                                               uint64_t *__restrict__ scratch, int lTC) {
+    extern __shared__ uint64_t sm[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobInfo J = job_info(lm, job);
+    const uint64_t q = T.mods[J.pr].q;
+    const uint64_t *src = in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
+    const int TC = 1 << lTC;
+    const uint32_t c0 = blockIdx.x << lTC;
+    const u64x2 *tf = (INV ? T.tf1i : T.tf1) + (uint64_t)J.pr * T.m;
+    const u64x2 *psi = T.psi + (uint64_t)J.pr * T.M;
+    const int tot = T.R << lTC;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int r = e >> lTC, c = e & (TC - 1);
+        const uint32_t t = r * T.C + c0 + c;
+        uint64_t v = 0;
+        if (!INV) {
+            if (t < T.n) { const u64x2 w = tf[t]; v = mul_shoup(src[t], w.w, w.ws, q); }
+        } else {
+            if (t < T.m) {
+                const int ps = T.pos[t];
+                if (ps >= 0) { const u64x2 w = tf[t]; v = mul_shoup(src[ps], w.w, w.ws, q); }
+            }
+        }
+        sm[e] = v;
+    }
+    __syncthreads();
+    smem_dif<true>(sm, lTC, T.logR, 1, TC, psi, T.M, q);
+    uint64_t *dst = scratch + (uint64_t)blockIdx.y * T.M;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int rp = e >> lTC, c = e & (TC - 1);
+        const uint32_t k1 = brev(rp, T.logR);
+        const u64x2 w = psi[((c0 + c) * k1) & (T.M - 1)];
+        dst[rp * T.C + c0 + c] = mul_shoup(sm[e], w.w, w.ws, q);
+    }
+}
+
+// ---- pass B: row DIF (length C), x D^, row inverse DIT, twiddle psi^(-c*k1) ----
+template <int INV>
+__global__ void __launch_bounds__(256) k_passB(NttTables T, LimbMap lm, uint64_t job0,
+                                               uint64_t *__restrict__ scratch, int lTR) {
+    extern __shared__ uint64_t sm[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobInfo J = job_info(lm, job);
+    const uint64_t q = T.mods[J.pr].q;
+    const u64x2 *psi = T.psi + (uint64_t)J.pr * T.M;
+    const u64x2 *dh = (INV ? T.dhi : T.dhf) + (uint64_t)J.pr * T.M;
+    const int TR = 1 << lTR;
+    const uint32_t r0 = blockIdx.x << lTR;
+    uint64_t *row = scratch + (uint64_t)blockIdx.y * T.M + (uint64_t)r0 * T.C;
+    const int tot = TR << T.logC;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) sm[e] = row[e];
+    __syncthreads();
+    smem_dif<false>(sm, lTR, T.logC, T.C, 1, psi, T.M, q);
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const u64x2 w = dh[(uint64_t)r0 * T.C + e];
+        sm[e] = mul_shoup(sm[e], w.w, w.ws, q);
+    }
+    __syncthreads();
+    smem_dit_inv<false>(sm, lTR, T.logC, T.C, 1, psi, T.M, q);
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int a = e >> T.logC, c = e & (T.C - 1);
+        const uint32_t k1 = brev(r0 + a, T.logR);
+        const u64x2 w = psi[(T.M - c * k1) & (T.M - 1)];
+        row[e] = mul_shoup(sm[e], w.w, w.ws, q);
+    }
+}
+
+// ---- pass C: column inverse DIT (length R) -> natural t, output chirp, filter / store ----
+template <int INV>
+__global__ void __launch_bounds__(256) k_passC(NttTables T, uint64_t *__restrict__ out,
+                                               uint64_t out_pstride, LimbMap lm, uint64_t job0,
+                                               uint64_t *__restrict__ scratch, int lTC) {
+    extern __shared__ uint64_t sm[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobInfo J = job_info(lm, job);
+    const uint64_t q = T.mods[J.pr].q;
+    const u64x2 *psi = T.psi + (uint64_t)J.pr * T.M;
+    const int TC = 1 << lTC;
+    const uint32_t c0 = blockIdx.x << lTC;
+    uint64_t *scr = scratch + (uint64_t)blockIdx.y * T.M;
+    const int tot = T.R << lTC;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int rp = e >> lTC, c = e & (TC - 1);
+        sm[e] = scr[rp * T.C + c0 + c];
+    }
+    __syncthreads();
+    smem_dit_inv<true>(sm, lTC, T.logR, 1, TC, psi, T.M, q);
+    const u64x2 *tfo = (INV ? T.tfoi : T.tfo) + (uint64_t)J.pr * T.m;
+    uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int r = e >> lTC, c = e & (TC - 1);
+        const uint32_t t = r * T.C + c0 + c;
+        if (t >= T.m) continue;
+        const u64x2 w = tfo[t];
+        const uint64_t v = mul_shoup(sm[e], w.w, w.ws, q);
+        if (!INV) {
+            const int ps = T.pos[t];
+            if (ps >= 0) dst[ps] = v;
+        } else {
+            scr[t] = v;    // A_t, t < m (reduced mod Phi_m by k_reduce_phi)
+        }
+    }
+}
+
+// ---- inverse epilogue: reduce A (length m) modulo Phi_m ----
+__global__ void k_reduce_prime(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride,
+                               LimbMap lm, uint64_t job0, uint32_t njobs,
+                               const uint64_t *__restrict__ scratch) {
+    const uint64_t total = (uint64_t)njobs * T.n;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t jr = (uint32_t)(i / T.n), x = (uint32_t)(i - (uint64_t)jr * T.n);
+        const JobInfo J = job_info(lm, (uint32_t)(job0 + jr));
+        const uint64_t q = T.mods[J.pr].q;
+        const uint64_t *A = scratch + (uint64_t)jr * T.M;
+        out[(uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n + x] = sub_mod(A[x], A[T.m - 1], q);
+    }
+}
+
+// composite m: long division by Phi_m (one CTA per job, m - n sequential steps)
+__global__ void k_reduce_composite(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride,
+                                   LimbMap lm, uint64_t job0, uint64_t *__restrict__ scratch) {
+    const JobInfo J = job_info(lm, (uint32_t)(job0 + blockIdx.x));
+    const uint64_t q = T.mods[J.pr].q;
+    uint64_t *A = scratch + (uint64_t)blockIdx.x * T.M;
+    for (int k = (int)T.m - 1; k >= (int)T.n; --k) {
+        const uint64_t c = A[k];
+        __syncthreads();
+        for (int j = threadIdx.x; j < (int)T.n; j += blockDim.x) {
+            const int f = T.phi[j];
+            uint64_t *d = &A[k - T.n + j];
+            if (f == 1) *d = sub_mod(*d, c, q);
+            else if (f == -1) *d = add_mod(*d, c, q);
+            else if (f != 0) {
+                const uint64_t fm = from_signed(f, q);
+                *d = sub_mod(*d, mul_mod(c, fm, T.mods[J.pr]), q);
+            }
+        }
+        __syncthreads();
+    }
+    uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
+    for (int j = threadIdx.x; j < (int)T.n; j += blockDim.x) dst[j] = A[j];
+}
+
+static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                       uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st,
+                       int inv) {
+    const uint64_t jobs = (uint64_t)npoly * lm.njl;
+    if (!jobs) return;
+    const int lTC = T.logC < 4 ? (int)T.logC : 4;
+    const int lTR = T.logR < 3 ? (int)T.logR : 3;
+    const size_t smA = ((size_t)T.R << lTC) * 8, smB = ((size_t)T.C << lTR) * 8;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_passA<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_passA<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_passB<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_passB<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_passC<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_passC<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        attr_set = true;
+    }
+    const uint64_t chunk = 65535;
+    for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
+        const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
+        dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
+        if (!inv) {
+            k_passA<0><<<gA, 256, smA, st>>>(T, in, in_pstride, lm, j0, scratch, lTC);
+            k_passB<0><<<gB, 256, smB, st>>>(T, lm, j0, scratch, lTR);
+            k_passC<0><<<gA, 256, smA, st>>>(T, out, out_pstride, lm, j0, scratch, lTC);
+            launch_counter() += 3;
+        } else {
+            k_passA<1><<<gA, 256, smA, st>>>(T, in, in_pstride, lm, j0, scratch, lTC);
+            k_passB<1><<<gB, 256, smB, st>>>(T, lm, j0, scratch, lTR);
+            k_passC<1><<<gA, 256, smA, st>>>(T, out, out_pstride, lm, j0, scratch, lTC);
+            if (T.prime_m)
+                k_reduce_prime<<<grid_for((uint64_t)nj * T.n, 256), 256, 0, st>>>(T, out, out_pstride, lm, j0,
+                                                                                 nj, scratch);
+            else
+                k_reduce_composite<<<nj, 256, 0, st>>>(T, out, out_pstride, lm, j0, scratch);
+            launch_counter() += 4;
+        }
+    }
+}
+
+void ntt_forward(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                 uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st) {
+    ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 0);
+}
+void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                 uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st) {
+    ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 1);
+}
+
+// =====================================================================================
+// element-wise kernels, layout [B][parts][lvl][n]; limb i -> prime i
+// =====================================================================================
+#define GRID_LOOP(i, total) \
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (total); i += (uint64_t)gridDim.x * blockDim.x)
+
+__global__ void k_add(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
+                      uint64_t *__restrict__ o, uint64_t total, uint32_t lvl, uint32_t n, int sub) {
+    GRID_LOOP(i, total) {
+        const uint32_t limb = (uint32_t)((i / n) % lvl);
+        const uint64_t q = mods[limb].q;
+        o[i] = sub ? sub_mod(a[i], b[i], q) : add_mod(a[i], b[i], q);
+    }
+}
+void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t parts,
+            uint32_t lvl, uint32_t n, int sub, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * n;
+    k_add<<<grid_for(total, 256), 256, 0, st>>>(mods, a, b, o, total, lvl, n, sub);
+    LAUNCHED();
+}
+
+__global__ void k_neg(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, uint64_t *__restrict__ o,
+                      uint64_t total, uint32_t lvl, uint32_t n) {
+    GRID_LOOP(i, total) {
+        const uint32_t limb = (uint32_t)((i / n) % lvl);
+        o[i] = neg_mod(a[i], mods[limb].q);
+    }
+}
+void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
+            uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * n;
+    k_neg<<<grid_for(total, 256), 256, 0, st>>>(mods, a, o, total, lvl, n);
+    LAUNCHED();
+}
+
+__global__ void k_scalar(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, int64_t c,
+                         uint64_t *__restrict__ o, uint64_t total, uint32_t lvl, uint32_t n) {
+    GRID_LOOP(i, total) {
+        const uint32_t limb = (uint32_t)((i / n) % lvl);
+        const Mod M = mods[limb];
+        o[i] = mul_mod(a[i], from_signed(c, M.q), M);
+    }
+}
+void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
+               uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * n;
+    k_scalar<<<grid_for(total, 256), 256, 0, st>>>(mods, a, c, o, total, lvl, n);
+    LAUNCHED();
+}
+
+__global__ void k_add_const(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, int64_t c,
+                            uint64_t *__restrict__ o, uint64_t total, uint32_t parts, uint32_t lvl, uint32_t n) {
+    GRID_LOOP(i, total) {
+        const uint64_t r = i / n;
+        const uint32_t limb = (uint32_t)(r % lvl);
+        const uint32_t part = (uint32_t)((r / lvl) % parts);
+        const uint64_t q = mods[limb].q;
+        o[i] = part == 0 ? add_mod(a[i], from_signed(c, q), q) : a[i];
+    }
+}
+void ew_add_const(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
+                  uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * n;
+    k_add_const<<<grid_for(total, 256), 256, 0, st>>>(mods, a, c, o, total, parts, lvl, n);
+    LAUNCHED();
+}
+
+__global__ void k_ptmul(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
+                        const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint64_t total,
+                        uint32_t lvl, uint32_t n) {
+    GRID_LOOP(i, total) {
+        const uint64_t r = i / n;
+        const uint32_t x = (uint32_t)(i - r * n);
+        const uint32_t limb = (uint32_t)(r % lvl);
+        o[i] = mul_mod(a[i], pt[(uint64_t)limb * n + x], mods[limb]);
+    }
+}
+void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B, uint32_t parts,
+              uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * n;
+    k_ptmul<<<grid_for(total, 256), 256, 0, st>>>(mods, a, pt, o, total, lvl, n);
+    LAUNCHED();
+}
+
+__global__ void k_add_pt(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
+                         const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint64_t total,
+                         uint32_t parts, uint32_t lvl, uint32_t n) {
+    GRID_LOOP(i, total) {
+        const uint64_t r = i / n;
+        const uint32_t x = (uint32_t)(i - r * n);
+        const uint32_t limb = (uint32_t)(r % lvl);
+        const uint32_t part = (uint32_t)((r / lvl) % parts);
+        o[i] = part == 0 ? add_mod(a[i], pt[(uint64_t)limb * n + x], mods[limb].q) : a[i];
+    }
+}
+void ew_add_pt(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B, uint32_t parts,
+               uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * n;
+    k_add_pt<<<grid_for(total, 256), 256, 0, st>>>(mods, a, pt, o, total, parts, lvl, n);
+    LAUNCHED();
+}
+
+// tensor: (a0 b0, a0 b1 + a1 b0, a1 b1)
+__global__ void k_tensor(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
+                         const uint64_t *__restrict__ b, uint64_t *__restrict__ o, uint64_t total,
+                         uint32_t lvl, uint32_t n) {
+    const uint64_t ln = (uint64_t)lvl * n;
+    GRID_LOOP(i, total) {   // i over B * lvl * n
+        const uint64_t bi = i / ln, r = i - bi * ln;
+        const uint32_t limb = (uint32_t)(r / n);
+        const Mod M = mods[limb];
+        const uint64_t a0 = a[bi * 2 * ln + r], a1 = a[bi * 2 * ln + ln + r];
+        const uint64_t b0 = b[bi * 2 * ln + r], b1 = b[bi * 2 * ln + ln + r];
+        uint64_t *ob = o + bi * 3 * ln + r;
+        ob[0] = mul_mod(a0, b0, M);
+        ob[ln] = add_mod(mul_mod(a0, b1, M), mul_mod(a1, b0, M), M.q);
+        ob[2 * ln] = mul_mod(a1, b1, M);
+    }
+}
+void ew_tensor(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t lvl,
+               uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * lvl * n;
+    k_tensor<<<grid_for(total, 256), 256, 0, st>>>(mods, a, b, o, total, lvl, n);
+    LAUNCHED();
+}
+
+// automorphism sigma_t in evaluation form: E'[k] = E[pos[t z_k mod m]]
+__global__ void k_automorph(NttTables T, const uint64_t *__restrict__ a, uint64_t *__restrict__ o,
+                            uint64_t total, uint32_t t) {
+    GRID_LOOP(i, total) {
+        const uint64_t r = i / T.n;
+        const uint32_t x = (uint32_t)(i - r * T.n);
+        const uint32_t src = (uint32_t)T.pos[(uint32_t)(((uint64_t)t * (uint32_t)T.z[x]) % T.m)];
+        o[i] = a[r * T.n + src];
+    }
+}
+void ew_automorph(const NttTables &T, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
+                  uint32_t t, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * parts * lvl * T.n;
+    k_automorph<<<grid_for(total, 256), 256, 0, st>>>(T, a, o, total, t);
+    LAUNCHED();
+}
+
+// copy parts [part0, part0+nparts) of a [B][parts_in][lvl_in][n] (first lvl_out limbs) into
+// o [B][parts_out][lvl_out][n] at part opart0
+__global__ void k_copy_parts(const uint64_t *__restrict__ a, uint64_t *__restrict__ o, uint64_t total,
+                             uint32_t parts_in, uint32_t part0, uint32_t nparts, uint32_t lvl_in,
+                             uint32_t lvl_out, uint32_t n, uint32_t parts_out, uint32_t opart0) {
+    GRID_LOOP(i, total) {   // over B * nparts * lvl_out * n
+        uint64_t r = i / n;
+        const uint32_t x = (uint32_t)(i - r * n);
+        const uint32_t limb = (uint32_t)(r % lvl_out);
+        r /= lvl_out;
+        const uint32_t k = (uint32_t)(r % nparts);
+        const uint64_t b = r / nparts;
+        o[((b * parts_out + opart0 + k) * lvl_out + limb) * n + x] =
+            a[((b * parts_in + part0 + k) * lvl_in + limb) * n + x];
+    }
+}
+void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in, uint32_t part0, uint32_t nparts,
+                   uint32_t lvl_in, uint32_t lvl_out, uint32_t n, uint32_t parts_out, uint32_t opart0,
+                   cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * nparts * lvl_out * n;
+    k_copy_parts<<<grid_for(total, 256), 256, 0, st>>>(a, o, total, parts_in, part0, nparts, lvl_in, lvl_out, n,
+                                                      parts_out, opart0);
+    LAUNCHED();
+}
+
+// =====================================================================================
+// key switching: KIP and ModDown scaling
+// =====================================================================================
+__global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__ d,
+                      const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
+                      uint64_t *__restrict__ u, uint64_t total, uint32_t lvl, uint32_t K, uint32_t L1,
+                      uint32_t alpha, uint32_t ndig, uint32_t n) {
+    const uint32_t nl = lvl + K;
+    const uint64_t ln = (uint64_t)nl * n;
+    GRID_LOOP(i, total) {   // over B * nl * n
+        const uint64_t b = i / ln, rr = i - b * ln;
+        const uint32_t r = (uint32_t)(rr / n), x = (uint32_t)(rr - (uint64_t)r * n);
+        const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
+        const Mod M = mods[kl];
+        const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
+        uint64_t s0 = 0, s1 = 0;
+        for (uint32_t j = 0; j < ndig; ++j) {
+            const uint64_t dig = (j == jr) ? d[(b * lvl + r) * n + x] : ext[((b * ndig + j) * nl + r) * n + x];
+            const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
+            s0 = add_mod(s0, mul_mod(dig, kj[(uint64_t)kl * n + x], M), M.q);
+            s1 = add_mod(s1, mul_mod(dig, kj[(uint64_t)(L1 + K + kl) * n + x], M), M.q);
+        }
+        u[(b * 2 + 0) * ln + rr] = s0;
+        u[(b * 2 + 1) * ln + rr] = s1;
+    }
+}
+void ks_kip(const Mod *mods, const uint64_t *d, const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B,
+            uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * (lvl + K) * n;
+    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, ext, key, u, total, lvl, K, L1, alpha, ndig, n);
+    LAUNCHED();
+}
+
+__global__ void k_scale_sub(const Mod *__restrict__ mods, const uint64_t *__restrict__ u, uint64_t u_pstride,
+                            const uint64_t *__restrict__ delta, const u64x2 *__restrict__ inv,
+                            uint64_t *__restrict__ o, uint64_t total, uint32_t lvl, uint32_t n) {
+    const uint64_t ln = (uint64_t)lvl * n;
+    GRID_LOOP(i, total) {
+        const uint64_t pidx = i / ln, rr = i - pidx * ln;
+        const uint32_t limb = (uint32_t)(rr / n);
+        const uint64_t q = mods[limb].q;
+        const uint64_t v = sub_mod(u[pidx * u_pstride + rr], delta[i], q);
+        const u64x2 w = inv[limb];
+        o[i] = mul_shoup(v, w.w, w.ws, q);
+    }
+}
+void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *delta, const u64x2 *inv,
+                  uint64_t *o, uint32_t npoly, uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)npoly * lvl * n;
+    k_scale_sub<<<grid_for(total, 256), 256, 0, st>>>(mods, u, u_pstride, delta, inv, o, total, lvl, n);
+    LAUNCHED();
+}
+
+// =====================================================================================
+// exact centered CRT lift (Garner mixed radix + lexicographic sign test)
+// plan blob (u64 words): [0]=ns [1]=nt, then
+//   src[ns] inv[ns] invs[ns] qm[ns*ns] half[ns] tgt[nt] Bt[nt*ns] Qm[nt]
+// tgt[t] = prime index, or ~0 for the plaintext modulus p.
+// =====================================================================================
+template <int MAXS>
+__global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict__ mods, uint32_t p,
+                       const uint64_t *__restrict__ src, uint64_t src_pstride, uint64_t *__restrict__ out,
+                       uint64_t out_pstride, int16_t *__restrict__ out16, uint64_t total, uint32_t n,
+                       uint32_t skip0, uint32_t skipn, int mode) {
+    const uint32_t ns = (uint32_t)plan[0], nt = (uint32_t)plan[1];
+    const uint64_t *P_src = plan + 2, *P_inv = P_src + ns, *P_invs = P_inv + ns, *P_qm = P_invs + ns;
+    const uint64_t *P_half = P_qm + ns * ns, *P_tgt = P_half + ns, *P_B = P_tgt + nt, *P_Q = P_B + (uint64_t)nt * ns;
+    GRID_LOOP(i, total) {
+        const uint64_t poly = i / n;
+        const uint32_t x = (uint32_t)(i - poly * n);
+        const uint64_t *s = src + poly * src_pstride + x;
+        uint64_t v[MAXS];
+        for (uint32_t k = 0; k < ns; ++k) {
+            const Mod Mk = mods[P_src[k]];
+            const uint64_t xk = s[(uint64_t)k * n];
+            if (k == 0) { v[0] = xk; continue; }
+            uint64_t acc = v[k - 1] % Mk.q;
+            for (int j = (int)k - 2; j >= 0; --j)
+                acc = add_mod(mul_mod(acc, P_qm[k * ns + j], Mk), v[j] % Mk.q, Mk.q);
+            v[k] = mul_shoup(sub_mod(xk, acc, Mk.q), P_inv[k], P_invs[k], Mk.q);
+        }
+        bool neg = false;
+        for (int k = (int)ns - 1; k >= 0; --k) {
+            if (v[k] != P_half[k]) { neg = v[k] > P_half[k]; break; }
+        }
+        if (mode == 0) {
+            for (uint32_t t = 0; t < nt; ++t) {
+                const Mod Mt = mods[P_tgt[t]];
+                uint64_t acc = 0;
+                for (uint32_t k = 0; k < ns; ++k)
+                    acc = add_mod(acc, mul_mod(reduce64(v[k], Mt), P_B[(uint64_t)t * ns + k], Mt), Mt.q);
+                if (neg) acc = sub_mod(acc, P_Q[t], Mt.q);
+                const uint32_t lb = t < skip0 ? t : t + skipn;
+                out[poly * out_pstride + (uint64_t)lb * n + x] = acc;
+            }
+        } else {
+            // value mod p (last target in mode 1, only target in mode 2)
+            const uint32_t tp = nt - 1;
+            uint64_t rp = 0;
+            for (uint32_t k = 0; k < ns; ++k) rp = (rp + (v[k] % p) * P_B[(uint64_t)tp * ns + k]) % p;
+            if (neg) rp = (rp + p - P_Q[tp]) % p;
+            if (mode == 2) {
+                int32_t c = (int32_t)rp;
+                if (c > (int32_t)(p / 2)) c -= (int32_t)p;
+                out16[poly * n + x] = (int16_t)c;
+                continue;
+            }
+            // delta = r + Q * [-r]_p
+            int64_t tc = (int64_t)((p - rp) % p);
+            if (tc > (int64_t)(p / 2)) tc -= p;
+            for (uint32_t t = 0; t + 1 < nt; ++t) {
+                const Mod Mt = mods[P_tgt[t]];
+                uint64_t acc = 0;
+                for (uint32_t k = 0; k < ns; ++k)
+                    acc = add_mod(acc, mul_mod(reduce64(v[k], Mt), P_B[(uint64_t)t * ns + k], Mt), Mt.q);
+                if (neg) acc = sub_mod(acc, P_Q[t], Mt.q);
+                acc = add_mod(acc, mul_mod(P_Q[t], from_signed(tc, Mt.q), Mt), Mt.q);
+                out[poly * out_pstride + (uint64_t)t * n + x] = acc;
+            }
+        }
+    }
+}
+void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride, uint64_t *out,
+          uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0, uint32_t skipn, int mode,
+          cudaStream_t st) {
+    const uint64_t total = (uint64_t)npoly * n;
+    if (mode == 2)
+        k_lift<64><<<grid_for(total, 128), 128, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, out16,
+                                                         total, n, skip0, skipn, mode);
+    else
+        k_lift<16><<<grid_for(total, 256), 256, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, out16,
+                                                         total, n, skip0, skipn, mode);
+    LAUNCHED();
+}
+
+// =====================================================================================
+// counter-based sampler (R7)
+// =====================================================================================
+#define C_TAG 0xD1B54A32D192ED03ull
+#define C_STREAM 0x8CB92BA72F3D8DD7ull
+#define C_GOLD 0x9E3779B97F4A7C15ull
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+__device__ __forceinline__ uint64_t draw(uint64_t seed, uint32_t tag, uint64_t stream, uint64_t j) {
+    return mix64(seed + (uint64_t)tag * C_TAG + stream * C_STREAM + (j + 1) * C_GOLD);
+}
+
+__global__ void k_sample_small(const Mod *__restrict__ mods, uint64_t seed, uint32_t tag, uint64_t stream0,
+                               uint64_t stream_step, int kind, int64_t mult, const int16_t *__restrict__ add16,
+                               uint64_t *__restrict__ out, uint64_t total, uint32_t nl, uint32_t prime0,
+                               uint32_t n, uint64_t pstride) {
+    GRID_LOOP(i, total) {   // over npoly * n
+        const uint64_t poly = i / n;
+        const uint32_t x = (uint32_t)(i - poly * n);
+        int64_t v = 0;
+        if (kind >= 0) {
+            const uint64_t r = draw(seed, tag, stream0 + poly * stream_step, x);
+            if (kind == 0) v = (int64_t)(r % 3) - 1;
+            else v = (int64_t)__popcll(r & 0x1FFFFFull) - (int64_t)__popcll((r >> 21) & 0x1FFFFFull);
+            v *= mult;
+        }
+        if (add16) v += add16[i];
+        for (uint32_t l = 0; l < nl; ++l)
+            out[poly * pstride + (uint64_t)l * n + x] = from_signed(v, mods[prime0 + l].q);
+    }
+}
+void sample_small(const Mod *mods, uint64_t seed, uint32_t tag, uint64_t stream0, uint64_t stream_step, int kind,
+                  int64_t mult, const int16_t *add16, uint64_t *out, uint32_t npoly, uint32_t nl, uint32_t prime0,
+                  uint32_t n, uint64_t pstride, cudaStream_t st) {
+    const uint64_t total = (uint64_t)npoly * n;
+    k_sample_small<<<grid_for(total, 256), 256, 0, st>>>(mods, seed, tag, stream0, stream_step, kind, mult, add16,
+                                                         out, total, nl, prime0, n, pstride);
+    LAUNCHED();
+}
+
+__global__ void k_sample_uniform(const Mod *__restrict__ mods, uint64_t seed, uint32_t tag, uint64_t stream0,
+                                 uint64_t stream_step, uint64_t *__restrict__ out, uint64_t total, LimbMap lm,
+                                 uint32_t n, uint64_t pstride) {
+    GRID_LOOP(i, total) {   // over npoly * njl * n
+        const uint64_t r0 = i / n;
+        const uint32_t x = (uint32_t)(i - r0 * n);
+        const uint64_t poly = r0 / lm.njl;
+        const uint32_t jl = (uint32_t)(r0 - poly * lm.njl);
+        const uint32_t lb = lm.limb(jl), pr = lm.prime(lb);
+        const uint64_t q = mods[pr].q;
+        const uint64_t ci = (uint64_t)pr * n + x;
+        const uint64_t stream = stream0 + poly * stream_step;
+        const uint64_t r1 = draw(seed, tag, stream, 2 * ci), r2 = draw(seed, tag, stream, 2 * ci + 1);
+        // floor((r1*2^64 + r2) * q / 2^128) = floor((r1*q + floor(r2*q / 2^64)) / 2^64)
+        const uint64_t lo1 = r1 * q, hi1 = __umul64hi(r1, q);
+        const uint64_t hi2 = __umul64hi(r2, q);
+        const uint64_t s = lo1 + hi2;
+        const uint64_t carry = s < lo1 ? 1 : 0;
+        out[poly * pstride + (uint64_t)lb * n + x] = hi1 + carry;
+    }
+}
+void sample_uniform(const Mod *mods, uint64_t seed, uint32_t tag, uint64_t stream0, uint64_t stream_step,
+                    uint64_t *out, uint32_t npoly, LimbMap lm, uint32_t n, uint64_t pstride, cudaStream_t st) {
+    const uint64_t total = (uint64_t)npoly * lm.njl * n;
+    k_sample_uniform<<<grid_for(total, 256), 256, 0, st>>>(mods, seed, tag, stream0, stream_step, out, total, lm, n,
+                                                           pstride);
+    LAUNCHED();
+}
+
+// =====================================================================================
+// encode / decode: exact int8 x int8 -> int32 GEMM (entries centered mod p, |sum| < 2^31)
+// =====================================================================================
+#define GT 64
+#define GK 32
+__global__ void __launch_bounds__(256) k_gemm_s8(const int8_t *__restrict__ A, const int8_t *__restrict__ W,
+                                                 int32_t *__restrict__ C, uint32_t B, uint32_t N, uint32_t K) {
+    __shared__ int32_t sa[GK][GT + 1];
+    __shared__ int32_t sw[GK][GT + 1];
+    const uint32_t b0 = blockIdx.y * GT, j0 = blockIdx.x * GT;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    int32_t acc[4][4] = {};
+    for (uint32_t k0 = 0; k0 < K; k0 += GK) {
+        for (int e = threadIdx.x; e < GT * GK; e += 256) {
+            const int r = e / GK, k = e % GK;
+            const uint32_t kk = k0 + k;
+            sa[k][r] = (b0 + r < B && kk < K) ? (int32_t)A[(uint64_t)(b0 + r) * K + kk] : 0;
+            sw[k][r] = (j0 + r < N && kk < K) ? (int32_t)W[(uint64_t)(j0 + r) * K + kk] : 0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < GK; ++k) {
+            int32_t av[4], wv[4];
+            for (int u = 0; u < 4; ++u) { av[u] = sa[k][ty * 4 + u]; wv[u] = sw[k][tx * 4 + u]; }
+            for (int u = 0; u < 4; ++u)
+                for (int v = 0; v < 4; ++v) acc[u][v] += av[u] * wv[v];
+        }
+        __syncthreads();
+    }
+    for (int u = 0; u < 4; ++u)
+        for (int v = 0; v < 4; ++v) {
+            const uint32_t b = b0 + ty * 4 + u, j = j0 + tx * 4 + v;
+            if (b < B && j < N) C[(uint64_t)b * N + j] = acc[u][v];
+        }
+}
+void gemm_s8(const int8_t *A, const int8_t *W, int32_t *C, uint32_t B, uint32_t N, uint32_t K, cudaStream_t st) {
+    dim3 g((N + GT - 1) / GT, (B + GT - 1) / GT);
+    k_gemm_s8<<<g, 256, 0, st>>>(A, W, C, B, N, K);
+    LAUNCHED();
+}
+
+__device__ __forceinline__ int32_t center_p(int64_t v, int32_t p) {
+    int64_t r = v % p;
+    if (r < 0) r += p;
+    if (r > p / 2) r -= p;
+    return (int32_t)r;
+}
+
+__global__ void k_mod_p_center(const int32_t *__restrict__ in, int16_t *__restrict__ out, uint64_t total, int32_t p) {
+    GRID_LOOP(i, total) out[i] = (int16_t)center_p(in[i], p);
+}
+void mod_p_center(const int32_t *in, int16_t *out, uint64_t count, int32_t p, cudaStream_t st) {
+    k_mod_p_center<<<grid_for(count, 256), 256, 0, st>>>(in, out, count, p);
+    LAUNCHED();
+}
+__global__ void k_s16_to_s8(const int16_t *__restrict__ in, int8_t *__restrict__ out, uint64_t total, int32_t p) {
+    GRID_LOOP(i, total) out[i] = (int8_t)center_p(in[i], p);
+}
+void s16_to_s8(const int16_t *in, int8_t *out, uint64_t count, int32_t p, cudaStream_t st) {
+    k_s16_to_s8<<<grid_for(count, 256), 256, 0, st>>>(in, out, count, p);
+    LAUNCHED();
+}
+
+// Em[j][s*D+i] = V(j) + sum_{k>=n} V(k) red[k-n][j], V(e) = E0_i[(e t_s) mod m]  (sigma_{t_s^-1} of the
+// slot-0 idempotent basis, P:271 CRT);  prime m: red = x^{m-1} -> -1 everywhere.
+__global__ void k_build_enc(const int16_t *__restrict__ E0, const uint32_t *__restrict__ ts,
+                            const int8_t *__restrict__ red, int8_t *__restrict__ Em, uint32_t n, uint32_t m,
+                            uint32_t D, uint32_t S, int32_t p) {
+    const uint64_t total = (uint64_t)n * n;
+    GRID_LOOP(i, total) {
+        const uint32_t j = (uint32_t)(i / n), col = (uint32_t)(i - (uint64_t)j * n);
+        const uint32_t s = col / D, ii = col - s * D;
+        const uint64_t t = ts[s];
+        const int16_t *E = E0 + (uint64_t)ii * m;
+        int64_t v = E[(j * t) % m];
+        if (!red) {
+            v -= E[((uint64_t)(m - 1) * t) % m];
+        } else {
+            for (uint32_t k = n; k < m; ++k) {
+                const int8_t f = red[(uint64_t)(k - n) * n + j];
+                if (f) v += (int64_t)f * E[((uint64_t)k * t) % m];
+            }
+        }
+        Em[i] = (int8_t)center_p(v, p);
+    }
+}
+void build_encode_matrix(const int16_t *E0, const uint32_t *ts, const int8_t *red, int8_t *Em, uint32_t n,
+                         uint32_t m, uint32_t D, uint32_t S, int32_t p, cudaStream_t st) {
+    k_build_enc<<<grid_for((uint64_t)n * n, 256), 256, 0, st>>>(E0, ts, red, Em, n, m, D, S, p);
+    LAUNCHED();
+}
+
+// Dm[s*D+i][j] = coeff_i(zeta^{t_s j mod m})  (decode: beta_s = a(zeta^{t_s}))
+__global__ void k_build_dec(const int16_t *__restrict__ zpow, const uint32_t *__restrict__ ts,
+                            int8_t *__restrict__ Dm, uint32_t n, uint32_t m, uint32_t D, int32_t p) {
+    const uint64_t total = (uint64_t)n * n;
+    GRID_LOOP(i, total) {
+        const uint32_t row = (uint32_t)(i / n), j = (uint32_t)(i - (uint64_t)row * n);
+        const uint32_t s = row / D, ii = row - s * D;
+        Dm[i] = (int8_t)center_p(zpow[((uint64_t)ts[s] * j % m) * D + ii], p);
+    }
+}
+void build_decode_matrix(const int16_t *zpow, const uint32_t *ts, int8_t *Dm, uint32_t n, uint32_t m, uint32_t D,
+                         uint32_t S, int32_t p, cudaStream_t st) {
+    k_build_dec<<<grid_for((uint64_t)n * n, 256), 256, 0, st>>>(zpow, ts, Dm, n, m, D, p);
+    LAUNCHED();
+}
+
+__global__ void k_s16_to_rns(const Mod *__restrict__ mods, const int16_t *__restrict__ in, uint64_t *__restrict__ out,
+                             uint64_t total, uint32_t nl, uint32_t n) {
+    GRID_LOOP(i, total) {   // over npoly * n
+        const uint64_t poly = i / n;
+        const uint32_t x = (uint32_t)(i - poly * n);
+        const int64_t v = in[i];
+        for (uint32_t l = 0; l < nl; ++l) out[(poly * nl + l) * n + x] = from_signed(v, mods[l].q);
+    }
+}
+void s16_to_rns(const Mod *mods, const int16_t *in, uint64_t *out, uint32_t npoly, uint32_t nl, uint32_t n,
+                cudaStream_t st) {
+    const uint64_t total = (uint64_t)npoly * n;
+    k_s16_to_rns<<<grid_for(total, 256), 256, 0, st>>>(mods, in, out, total, nl, n);
+    LAUNCHED();
+}
+
+__global__ void k_dec_dot(const Mod *__restrict__ mods, const uint64_t *__restrict__ ct,
+                          const uint64_t *__restrict__ s, uint64_t *__restrict__ o, uint64_t total, uint32_t lvl,
+                          uint32_t n) {
+    const uint64_t ln = (uint64_t)lvl * n;
+    GRID_LOOP(i, total) {
+        const uint64_t b = i / ln, r = i - b * ln;
+        const uint32_t limb = (uint32_t)(r / n);
+        const Mod M = mods[limb];
+        o[i] = add_mod(ct[b * 2 * ln + r], mul_mod(ct[b * 2 * ln + ln + r], s[r], M), M.q);
+    }
+}
+void dec_dot(const Mod *mods, const uint64_t *ct, const uint64_t *s, uint64_t *o, uint32_t B, uint32_t lvl,
+             uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * lvl * n;
+    k_dec_dot<<<grid_for(total, 256), 256, 0, st>>>(mods, ct, s, o, total, lvl, n);
+    LAUNCHED();
+}
+
+}  // namespace bc

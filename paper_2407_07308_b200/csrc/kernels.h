@@ -1,0 +1,122 @@
+// kernels.h -- launch wrappers for the sm_100a kernels of the BoostCom hot path.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace bc {
+
+struct u64x2 { uint64_t w, ws; };   // value + Shoup companion
+
+// Device tables of the Bluestein transforms (§8(a) a1/a2), one slice per prime.
+struct NttTables {
+    const u64x2 *psi;     // [P][M]  psi^e (size-M root, free internal choice)
+    const u64x2 *tf1;     // [P][m]  TF1_j = omega^(h j^2)            (forward input chirp)
+    const u64x2 *tf1i;    // [P][m]  omega^(-h j^2)                    (inverse input chirp)
+    const u64x2 *tfo;     // [P][m]  TF1_j * M^-1                      (forward output chirp)
+    const u64x2 *tfoi;    // [P][m]  omega^(-h j^2) * M^-1 * m^-1      (inverse output chirp)
+    const u64x2 *dhf;     // [P][M]  NTT_M(D_pad) in the pass layout   (forward)
+    const u64x2 *dhi;     // [P][M]  NTT_M(D'_pad)                     (inverse)
+    const int32_t *pos;   // [m]     position of t in Z_m^* (ascending) or -1 (Listing 2 prefix sum)
+    const int32_t *z;     // [n]     Z_m^* ascending
+    const int8_t *phi;    // [n+1]   Phi_m coefficients (for composite m)
+    const Mod *mods;      // [P]
+    uint32_t m, n, M, R, C, logR, logC;
+    int prime_m;          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
+};
+
+// Limb -> prime map of a batched job list: poly p in [0,npoly), jl in [0,njl):
+//   limb = jl < skip0 ? jl : jl + skipn;  prime = limb < split ? limb + off_lo : limb - split + off_hi
+struct LimbMap {
+    uint32_t njl, skip0, skipn, split, off_lo, off_hi;
+    __host__ __device__ uint32_t limb(uint32_t jl) const { return jl < skip0 ? jl : jl + skipn; }
+    __host__ __device__ uint32_t prime(uint32_t lb) const { return lb < split ? lb + off_lo : lb - split + off_hi; }
+};
+inline LimbMap limbmap_plain(uint32_t nl, uint32_t prime0) { return LimbMap{nl, nl, 0, 0xffffffffu, prime0, 0}; }
+
+// Batched Bluestein transforms.  in/out poly p limb lb at base + p*pstride + lb*n.
+// scratch: npoly*njl*M words.
+void ntt_forward(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                 uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st);
+void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                 uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st);
+
+// ---- element-wise over [B][parts][level][n] (limb i uses prime i) ----
+void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B,
+            uint32_t parts, uint32_t lvl, uint32_t n, int sub, cudaStream_t st);
+// o = a (parts pa) + b (parts pb) where the extra parts are copied (3-part + 2-part etc.)
+void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
+            uint32_t n, cudaStream_t st);
+void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
+               uint32_t lvl, uint32_t n, cudaStream_t st);
+// part 0 += c (constant polynomial: every evaluation point)
+void ew_add_const(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
+                  uint32_t lvl, uint32_t n, cudaStream_t st);
+// o = a (.) pt, pt u64[L][n] eval (first lvl limbs used), every part
+void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B,
+              uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
+void ew_add_pt(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B,
+               uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
+void ew_tensor(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B,
+               uint32_t lvl, uint32_t n, cudaStream_t st);
+void ew_automorph(const NttTables &T, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts,
+                  uint32_t lvl, uint32_t t, cudaStream_t st);
+void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in, uint32_t part0,
+                   uint32_t nparts, uint32_t lvl_in, uint32_t lvl_out, uint32_t n, uint32_t parts_out,
+                   uint32_t opart0, cudaStream_t st);
+
+// ---- key switching ----
+// KIP: u[b][k][r][x] = sum_j ext[b][j][r][x] * key_j[k][klimb(r)][x], k in {0 (b-part),1 (a-part)};
+// for r in G_j the digit is read from d (eval input) instead of ext.
+void ks_kip(const Mod *mods, const uint64_t *d, const uint64_t *ext, const uint64_t *key, uint64_t *u,
+            uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig,
+            uint32_t n, cudaStream_t st);
+// out[b][k][i] = (u[b][k][i] - delta[b][k][i]) * inv_i  (Shoup constants per limb)
+void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *delta,
+                  const u64x2 *inv, uint64_t *o, uint32_t npoly, uint32_t lvl, uint32_t n,
+                  cudaStream_t st);
+
+// Exact centered CRT lift (Garner) -- plan blob layout in kernels.cu.
+//  mode 0: residues mod each target prime -> out limbs (LimbMap-style skip over [skip0, skip0+skipn))
+//  mode 1: delta = r + Q [-r]_p mod each target prime (modulus/ModDown correction, R13/R14)
+//  mode 2: centered value mod p (as int16, centered in (-p/2, p/2]) -> out16[poly][n]
+void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride,
+          uint64_t *out, uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n,
+          uint32_t skip0, uint32_t skipn, int mode, cudaStream_t st);
+
+// ---- sampling (R7) ----
+// integer poly per (poly, coeff) -> residues on limbs prime0..prime0+nl-1
+// kind 0 ternary, 1 cbd21; mult = multiplier applied to the integer (e.g. p for p*e);
+// add16: optional int16[npoly][n] added after multiplication (message m~)
+void sample_small(const Mod *mods, uint64_t seed, uint32_t tag, uint64_t stream0, uint64_t stream_step,
+                  int kind, int64_t mult, const int16_t *add16, uint64_t *out, uint32_t npoly,
+                  uint32_t nl, uint32_t prime0, uint32_t n, uint64_t pstride, cudaStream_t st);
+// uniform residues: poly p limb lb (prime = lm.prime(lb)), counter limb index = klimb0 + lb
+void sample_uniform(const Mod *mods, uint64_t seed, uint32_t tag, uint64_t stream0, uint64_t stream_step,
+                    uint64_t *out, uint32_t npoly, LimbMap lm, uint32_t n, uint64_t pstride,
+                    cudaStream_t st);
+
+// ---- plaintext encode/decode (F_p linear maps as int8 GEMM) ----
+// C[b][j] = sum_k A[b][k] * W[j][k]  (int8 x int8 -> int32), A [B][K], W [N][K]
+void gemm_s8(const int8_t *A, const int8_t *W, int32_t *C, uint32_t B, uint32_t N, uint32_t K,
+             cudaStream_t st);
+// int32 -> centered mod p int16 (in (-p/2, p/2])
+void mod_p_center(const int32_t *in, int16_t *out, uint64_t count, int32_t p, cudaStream_t st);
+void s16_to_s8(const int16_t *in, int8_t *out, uint64_t count, int32_t p, cudaStream_t st);
+// build encode matrix Em[j][s*D+i] (centered int8) from E0 (int16 [D][m]) and reduction rows
+void build_encode_matrix(const int16_t *E0, const uint32_t *ts, const int8_t *red, int8_t *Em,
+                         uint32_t n, uint32_t m, uint32_t D, uint32_t S, int32_t p, cudaStream_t st);
+void build_decode_matrix(const int16_t *zpow, const uint32_t *ts, int8_t *Dm, uint32_t n, uint32_t m,
+                         uint32_t D, uint32_t S, int32_t p, cudaStream_t st);
+// int16 centered poly [npoly][n] -> residues on limbs 0..nl-1 (eval form needs an NTT after)
+void s16_to_rns(const Mod *mods, const int16_t *in, uint64_t *out, uint32_t npoly, uint32_t nl,
+                uint32_t n, cudaStream_t st);
+// decrypt dot: x = c0 + c1 * s (eval), s eval [L][n]
+void dec_dot(const Mod *mods, const uint64_t *ct, const uint64_t *s, uint64_t *o, uint32_t B,
+             uint32_t lvl, uint32_t n, cudaStream_t st);
+
+uint64_t &launch_counter();
+
+}  // namespace bc

@@ -1,0 +1,38 @@
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs the product kernels")
+    config.addinivalue_line("markers", "slow: long-running oracle computation")
+
+
+def load_cfg(name):
+    with open(os.path.join(ROOT, "params", name + ".json")) as f:
+        return json.load(f)
+
+
+def golden(name):
+    with open(os.path.join(ROOT, "tests", "golden", name)) as f:
+        return json.load(f)
+
+
+_P = {}
+
+
+@pytest.fixture(scope="session")
+def oracle_params():
+    from oracle import bgv
+
+    def get(name):
+        if name not in _P:
+            _P[name] = bgv.Params(load_cfg(name))
+        return _P[name]
+    return get

@@ -1,0 +1,188 @@
+"""Pins for the oracle's comparison circuits.
+
+The schedules run on plaintext slot values (PlainEval) so they can be checked exhaustively
+against brute-force comparison; the ciphertext versions are pinned in test_oracle_bgv.py.
+"""
+import math
+import random
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import circuits, cyclo, slots
+
+PRIMES = [3, 5, 7, 11, 13, 17, 19, 23, 29, 31]
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_digit_polys_truth_tables(p):
+    h = (p - 1) // 2
+    lt = circuits.lt_univariate_coeffs(p)
+    eq = circuits.eq_coeffs(p)
+    for x in range(h + 1):
+        for y in range(h + 1):
+            z = (x - y) % p
+            assert circuits.eval_poly_fp(lt, z, p) == (1 if x < y else 0)
+            assert circuits.eval_poly_fp(eq, z, p) == (1 if x == y else 0)
+    # structure (A.5): odd powers plus ((p+1)/2) z^{p-1}
+    assert lt[p - 1] == (p + 1) // 2 and lt[0] == 0
+    assert all(lt[k] == 0 for k in range(2, p - 1, 2))
+
+
+@pytest.mark.parametrize("p", [3, 5, 7, 11, 13])
+def test_bivariate_truth_table_and_structure(p):
+    c = circuits.lt_bivariate_coeffs(p)
+    for x in range(p):
+        for y in range(p):
+            v = 0
+            for j in range(len(c)):
+                for k in range(len(c[j])):
+                    if c[j][k]:
+                        v += c[j][k] * pow(y, j, p) * pow((x - y) % p, k, p)
+            assert v % p == (1 if x < y else 0)
+    assert all(c[0][k] == 0 for k in range(len(c[0])))          # no Y^0 terms (A.5)
+    assert max(j + k for j in range(len(c)) for k in range(len(c[j])) if c[j][k]) == p  # total degree p
+
+
+def test_spec_lt_digit_examples():
+    g = golden("spec_examples.json")["lt_digit"]
+    c = circuits.lt_bivariate_coeffs(3)
+    for x, y, want in g["bivariate_p3"]:
+        v = sum(c[j][k] * pow(y, j, 3) * pow((x - y) % 3, k, 3) for j in range(len(c)) for k in range(len(c[j])))
+        assert v % 3 == want
+    lt5 = circuits.lt_univariate_coeffs(5)
+    for z, want in g["univariate_p5_sign"]:
+        assert circuits.eval_poly_fp(lt5, z, 5) == want
+
+
+class _FpAlg:
+    """minimal stand-in for a slot algebra whose slots are F_p (D = 1)."""
+
+    def __init__(self, p, S):
+        self.p, self.D, self.S = p, 1, S
+        self.gf = slots.GF(p, [0, 1])
+
+
+def _digit_run(p, kind):
+    """run the schedule on one F_p value per slot covering every digit pair."""
+    h = (p - 1) // 2 if kind == "U" else p - 1
+    A = _FpAlg(p, (h + 1) ** 2)       # F_p itself (D = 1): one digit pair per slot
+    ev = circuits.PlainEval(A)
+    h = (p - 1) // 2 if kind == "U" else p - 1
+    pairs = [(x, y) for x in range(h + 1) for y in range(h + 1)]
+    res = []
+    for i0 in range(0, len(pairs), A.S):
+        chunk = pairs[i0:i0 + A.S]
+        X = np.zeros((A.S, A.D), dtype=np.int64)
+        Y = np.zeros((A.S, A.D), dtype=np.int64)
+        for s, (x, y) in enumerate(chunk):
+            X[s, 0], Y[s, 0] = x, y
+        ev.counts["mul"] = 0
+        if kind == "U":
+            lt, eq = circuits.univariate_lt_eq(ev, circuits.PlainValue((X - Y) % p), p)
+        else:
+            lt, eq = circuits.bivariate_lt_eq(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p)
+        for s, (x, y) in enumerate(chunk):
+            res.append((x, y, int(lt.v[s, 0]), int(eq.v[s, 0])))
+            assert not lt.v[s, 1:].any() and not eq.v[s, 1:].any()
+    return res, ev.counts["mul"], lt.depth
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_univariate_schedule_truth_and_budget(p):
+    res, mults, depth = _digit_run(p, "U")
+    for x, y, lt, eq in res:
+        assert (lt, eq) == (int(x < y), int(x == y))
+    # sqrt(p-3) + O(log p); SPEC budget: <= 2 ceil(sqrt p) + 2 ceil(log2 p)
+    assert mults <= 2 * math.ceil(math.sqrt(p)) + 2 * math.ceil(math.log2(p))
+    assert depth <= math.ceil(math.log2(p)) + 2
+
+
+@pytest.mark.parametrize("p", [3, 5, 7, 11, 13, 17])
+def test_bivariate_schedule_truth_and_3p_minus_5(p):
+    res, mults, _ = _digit_run(p, "B")
+    for x, y, lt, eq in res:
+        assert (lt, eq) == (int(x < y), int(x == y))
+    assert mults == 3 * p - 5      # P:71 [Tan]: 3p-5 non-scalar multiplications (with EQ)
+
+
+def test_spec_lex_example():
+    g = golden("spec_examples.json")["lex"]
+    p = g["p"]
+    A = slots.SlotAlgebra(p, cyclo.Ring(91))
+    ev = circuits.PlainEval(A)
+    a = g["a_msb_first"][::-1]
+    b = g["b_msb_first"][::-1]
+    lts, eqs = [], []
+    for x, y in zip(a, b):
+        v = np.zeros((A.S, A.D), dtype=np.int64)
+        v[:, 0] = int(x < y)
+        w = np.zeros((A.S, A.D), dtype=np.int64)
+        w[:, 0] = int(x == y)
+        lts.append(circuits.PlainValue(v))
+        eqs.append(circuits.PlainValue(w))
+    lt, _ = circuits.lex_tree(ev, lts, eqs)
+    assert int(lt.v[0, 0]) == g["lt"]
+
+
+def _plain_words(A, words, d, l, base):
+    return circuits.PlainValue(slots.words_to_slots(words, A, d, l, base))
+
+
+@pytest.mark.parametrize("circ,p,m,d,l", [("U", 3, 91, 2, 2), ("U", 13, 859, 4, 6), ("B", 3, 91, 2, 2),
+                                          ("B", 5, 31, 3, 1)])
+def test_compare_plain_vs_bruteforce(circ, p, m, d, l):
+    A = slots.SlotAlgebra(p, cyclo.Ring(m))
+    base = slots.digit_base(p, circ)
+    ints = A.S // l
+    cap = min(base ** (d * l), 2 ** 64)
+    rng = random.Random(p * 31 + d)
+    ev = circuits.PlainEval(A)
+    for trial in range(3):
+        wa = [rng.randrange(cap) for _ in range(ints)]
+        wb = [rng.randrange(cap) for _ in range(ints)]
+        for j in range(0, ints, 3):
+            wb[j] = wa[j]
+        if ints > 1:
+            wb[1] = min(wa[1] + 1, cap - 1)
+        lt, eq = circuits.compare(ev, _plain_words(A, wa, d, l, base), _plain_words(A, wb, d, l, base),
+                                  circ, d, l, ints)
+        for j in range(ints):
+            assert int(lt.v[j * l, 0]) == int(wa[j] < wb[j])
+            assert int(eq.v[j * l, 0]) == int(wa[j] == wb[j])
+
+
+def test_spec_compare_min_examples():
+    """(5,7) -> lt=1, eq=0; x vs x -> (0,1); min [3,1,2,9] -> 1."""
+    A = slots.SlotAlgebra(3, cyclo.Ring(91))
+    d, l, base = 2, 2, 2   # 4-bit words, 6 per ciphertext
+    ev = circuits.PlainEval(A)
+    ints = A.S // l
+    g = golden("spec_examples.json")
+    wa = [c[0] for c in g["compare_ints"]["cases"]] + [0] * (ints - 2)
+    wb = [c[1] for c in g["compare_ints"]["cases"]] + [0] * (ints - 2)
+    lt, eq = circuits.compare(ev, _plain_words(A, wa, d, l, base), _plain_words(A, wb, d, l, base), "U", d, l, ints)
+    for j, c in enumerate(g["compare_ints"]["cases"]):
+        assert (int(lt.v[j * l, 0]), int(eq.v[j * l, 0])) == (c[2], c[3])
+    vals = g["min"]["values"]
+    cur = [_plain_words(A, [v] * ints, d, l, base) for v in vals]
+    while len(cur) > 1:
+        cur = [circuits.vmin(ev, cur[i], cur[i + 1], "U", d, l, ints) for i in range(0, len(cur), 2)]
+    got = slots.slots_to_words(cur[0].v, d, l, base, ints)
+    assert got == [g["min"]["min"]] * ints
+
+
+def test_select_and_broadcast_plain():
+    A = slots.SlotAlgebra(13, cyclo.Ring(859))
+    d, l, base = 4, 6, 7
+    ints = A.S // l
+    rng = random.Random(9)
+    ev = circuits.PlainEval(A)
+    wa = [rng.randrange(2 ** 64) for _ in range(ints)]
+    wb = [rng.randrange(2 ** 64) for _ in range(ints)]
+    a, b = _plain_words(A, wa, d, l, base), _plain_words(A, wb, d, l, base)
+    mn = circuits.vmin(ev, a, b, "U", d, l, ints)
+    mx = circuits.vmax(ev, a, b, "U", d, l, ints)
+    assert slots.slots_to_words(mn.v, d, l, base, ints) == [min(x, y) for x, y in zip(wa, wb)]
+    assert slots.slots_to_words(mx.v, d, l, base, ints) == [max(x, y) for x, y in zip(wa, wb)]
