@@ -406,3 +406,47 @@ def load_params(name_or_path):
         path = os.path.join(_HERE, "..", "params", name_or_path + ".json")
     with open(path) as f:
         return json.load(f)
+
+
+# ------------------------------------------------------------------------------------------
+# roofline probe of the dominant kernel family (Bluestein NTT passes)
+# ------------------------------------------------------------------------------------------
+IMAD_PER_SM_PER_CLK = 64          # B200 integer multiply-add issue rate per SM (guide)
+SMS = 148
+IMAD_PER_MULMOD = 10              # 64-bit Shoup product: mul.hi.u64 (4) + 2 x mul.lo.u64 (3): SASS-checked
+
+
+def ntt_work(ctx):
+    """algorithmic 64-bit modular multiplications of one limb-transform (forward Bluestein):
+    two size-M NTTs (M/2 log2 M butterflies each), the pointwise D^ product (M), two chirps (n+m)."""
+    import math
+    M = ctx.M
+    return M * int(math.log2(M)) + M + ctx.n + ctx.m
+
+
+def profile_ntt(ctx, npoly=64, reps=5, sm_mhz=1965.0):
+    torch = _torch()
+    L = ctx.n_cipher
+    g = torch.Generator(device=ctx.device)
+    g.manual_seed(1)
+    x = torch.randint(0, 1 << 40, (npoly, L, ctx.n), dtype=torch.int64, device=ctx.device, generator=g)
+    out = torch.empty_like(x)
+    scratch = ctx.workspace(max(npoly * L * ctx.M * 8 + (1 << 22), 1 << 26))
+    st = _stream()
+    for _ in range(2):
+        _check(_lib.bc_ntt_fwd(ctx._h, _ptr(x), _ptr(out), npoly, L, 0, _ptr(scratch), scratch.numel(), st), "ntt")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        _check(_lib.bc_ntt_fwd(ctx._h, _ptr(x), _ptr(out), npoly, L, 0, _ptr(scratch), scratch.numel(), st), "ntt")
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    work = npoly * L * ntt_work(ctx)
+    achieved = work / (ms / 1e3) / 1e12
+    peak = SMS * IMAD_PER_SM_PER_CLK * sm_mhz * 1e6 / IMAD_PER_MULMOD / 1e12
+    return {"bound": "alu", "kernel": "bluestein_ntt (passA+passB+passC)", "achieved": achieved, "peak": peak,
+            "unit": "T mulmod64/s", "frac": achieved / peak, "traffic": None,
+            "per_launch_ms": ms, "limb_transforms_per_launch": npoly * L,
+            "work_per_limb_transform": ntt_work(ctx),
+            "peak_note": "148 SM x 64 IMAD/clk x %.0f MHz / %d IMAD per 64-bit mulmod" % (sm_mhz, IMAD_PER_MULMOD)}

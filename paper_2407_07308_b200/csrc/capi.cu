@@ -121,11 +121,15 @@ static size_t compare_peak(bc_ctx *X, const bc_keys *keys, uint32_t B, uint32_t 
 }
 
 extern "C" size_t bc_workspace_bytes(bc_ctx *X, uint32_t batch) {
-    try {
-        return compare_peak(X, nullptr, batch, X->L1, 2) + (1u << 20);
-    } catch (...) {
-        return 0;
+    // max over compare (lt + eq) and min/max/select where the chain allows them
+    size_t best = 0;
+    for (int which : {1, 2}) {
+        try {
+            best = std::max(best, compare_peak(X, nullptr, batch, X->L1, which));
+        } catch (...) {
+        }
     }
+    return best + best / 4 + (64u << 20);   // slack for fragmentation of the first-fit arena
 }
 
 extern "C" uint32_t bc_compare_out_level(bc_ctx *X, uint32_t level, int which) {
@@ -151,14 +155,15 @@ extern "C" uint32_t bc_compare_out_level(bc_ctx *X, uint32_t level, int which) {
 
 // choose the largest chunk whose dry-run peak fits the workspace
 static uint32_t choose_chunk(bc_ctx *X, const bc_keys *keys, uint32_t B, uint32_t lvl, int which, size_t ws) {
-    size_t p1 = compare_peak(X, keys, 1, lvl, which);
+    auto need = [&](uint32_t b) { size_t pk = compare_peak(X, keys, b, lvl, which); return pk + pk / 4 + (32u << 20); };
+    size_t p1 = need(1);
     if (p1 > ws) BC_THROW(BC_E_OOM, "workspace smaller than one pair needs (" + std::to_string(p1) + " bytes)");
     if (B == 1) return 1;
-    size_t p2 = compare_peak(X, keys, 2, lvl, which);
+    size_t p2 = need(2);
     size_t per = p2 > p1 ? p2 - p1 : p1;
     uint64_t c = 1 + (ws - p1) / per;
     uint32_t chunk = (uint32_t)std::min<uint64_t>(B, c);
-    while (chunk > 1 && compare_peak(X, keys, chunk, lvl, which) > ws) chunk = chunk * 7 / 8;
+    while (chunk > 1 && need(chunk) > ws) chunk = chunk * 7 / 8;
     return std::max<uint32_t>(chunk, 1);
 }
 

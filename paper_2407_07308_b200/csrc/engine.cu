@@ -33,15 +33,17 @@ void Arena::init(void *b, size_t c, bool dry_) {
 char *Arena::alloc(size_t bytes) {
     bytes = (bytes + ALIGN - 1) / ALIGN * ALIGN;
     if (bytes == 0) bytes = ALIGN;
-    for (auto it = freel.begin(); it != freel.end(); ++it) {
-        if (it->second >= bytes) {
-            size_t off = it->first, sz = it->second;
-            freel.erase(it);
-            if (sz > bytes) freel[off + bytes] = sz - bytes;
-            used += bytes;
-            peak = std::max(peak, used);
-            return base + off;
-        }
+    // best fit (smallest free block that fits; lowest address on ties) limits fragmentation
+    auto best = freel.end();
+    for (auto it = freel.begin(); it != freel.end(); ++it)
+        if (it->second >= bytes && (best == freel.end() || it->second < best->second)) best = it;
+    if (best != freel.end()) {
+        size_t off = best->first, sz = best->second;
+        freel.erase(best);
+        if (sz > bytes) freel[off + bytes] = sz - bytes;
+        used += bytes;
+        peak = std::max(peak, used);
+        return base + off;
     }
     BC_THROW(BC_E_OOM, "workspace exhausted (" + std::to_string(bytes) + " bytes requested, " +
                            std::to_string(cap - used) + " free, fragmented)");
@@ -520,10 +522,19 @@ CT Eng::sub(const CT &a, uint32_t b0, uint32_t nb) {
     return c;
 }
 
+// scratch polys per NTT launch group: at most ~1 GiB, the whole batch, or what the arena has free
+static uint32_t ntt_chunk(const Arena *A, uint32_t npoly, uint64_t per_words) {
+    uint64_t c = std::min<uint64_t>(npoly, (1ull << 27) / per_words);
+    if (!A->dry) {
+        const uint64_t free_words = (A->cap - A->used) / 8;
+        c = std::min<uint64_t>(c, free_words > per_words ? free_words / per_words - 1 : 1);
+    }
+    return (uint32_t)std::max<uint64_t>(1, c);
+}
+
 void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
-    // bound the scratch: at most ~1 GiB (or the whole batch if smaller) per launch group
     const uint64_t per = (uint64_t)lm.njl * X->M;
-    uint32_t chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(npoly, (1ull << 27) / per));
+    uint32_t chunk = ntt_chunk(A, npoly, per);
     BufP scr = alloc_words((uint64_t)chunk * per);
     if (dry()) return;
     for (uint32_t p0 = 0; p0 < npoly; p0 += chunk) {
@@ -533,7 +544,7 @@ void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
 }
 void Eng::ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
     const uint64_t per = (uint64_t)lm.njl * X->M;
-    uint32_t chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(npoly, (1ull << 27) / per));
+    uint32_t chunk = ntt_chunk(A, npoly, per);
     BufP scr = alloc_words((uint64_t)chunk * per);
     if (dry()) return;
     for (uint32_t p0 = 0; p0 < npoly; p0 += chunk) {

@@ -160,17 +160,17 @@ static bc_status encrypt_impl(bc_ctx *X, const bc_keys *keys, const int16_t *h_s
         cudaStream_t st = (cudaStream_t)stv;
         const uint32_t n = X->n, L1 = X->L1;
         const uint64_t cw = (uint64_t)L1 * n;
-        // process in chunks that fit the workspace
-        const size_t per = (size_t)n * (2 + 2 + 1 + 4) + cw * 8 * 3 + 4096;
-        const size_t fixed = (size_t)L1 * X->M * 8 * 64 + (1 << 20);
+        // process in chunks that fit the workspace (per ct: slots, m~, u/t0/t1, NTT scratch)
+        const size_t sd = (size_t)X->alg.S * X->alg.D;
+        const size_t per = sd * 2 + (size_t)n * 2 + cw * 8 * 3 + (size_t)L1 * X->M * 8 + 4 * 256;
+        const size_t fixed = (size_t)n * (1 + 4) * 1 + (1 << 20);
         if (wsb < per + fixed) BC_THROW(BC_E_OOM, "encrypt: workspace too small");
-        const uint32_t chunk = (uint32_t)std::max<size_t>(1, std::min<size_t>(B, (wsb - fixed) / (per + (size_t)L1 * X->M * 8)));
+        const uint32_t chunk = (uint32_t)std::max<size_t>(1, std::min<size_t>(B, (wsb - fixed) / (per + (size_t)n * 5)));
         for (uint32_t b0 = 0; b0 < B; b0 += chunk) {
             const uint32_t nb = std::min(chunk, B - b0);
             Arena A;
             A.init(ws, wsb, false);
             Eng E{X, keys, &A, st};
-            const size_t sd = (size_t)X->alg.S * X->alg.D;
             BufP sl(new Buf{&A, A.alloc((size_t)nb * sd * 2), (size_t)nb * sd * 2});
             BufP mt(new Buf{&A, A.alloc((size_t)nb * n * 2), (size_t)nb * n * 2});
             CK(cudaMemcpyAsync(sl->p, h_slots + (size_t)b0 * sd, (size_t)nb * sd * 2, cudaMemcpyHostToDevice, st));

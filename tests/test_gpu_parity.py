@@ -1,0 +1,275 @@
+"""GPU parity: every §8(a) row of the CUDA path vs the oracle, bit-exact, on seeded inputs.
+
+Runs on a B200 (``-m gpu``).  Ciphertexts are compared in evaluation form: the oracle's
+coefficient-form result is mapped by naive evaluation at omega_i^{z_k} (R3).
+"""
+import numpy as np
+import pytest
+
+from gpu_util import SEED_ENC, SEED_KEYS, Pair, from_u64, galois_for, mixed_pairs, to_u64
+
+pytestmark = pytest.mark.gpu
+
+_PAIRS = {}
+
+
+@pytest.fixture(scope="module")
+def pair(oracle_params):
+    def get(name):
+        if name not in _PAIRS:
+            _PAIRS[name] = Pair(name, oracle_params)
+        return _PAIRS[name]
+    return get
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2"])
+def test_tables_match_oracle(pair, cfg):
+    T = pair(cfg)
+    q, w = T.ctx.moduli()
+    assert q == T.P.moduli
+    assert w == T.P.omega
+    if cfg != "c2":
+        G, z, t = T.ctx.slots()
+        A = T.P.alg
+        assert list(G) == list(A.G)
+        assert list(z) == [int(x) for x in A.zeta]
+        assert list(t) == list(A.t)
+        assert sorted(T.ctx.galois()) == galois_for(T.P)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_ntt_forward_inverse(pair, cfg):
+    """a1/a2: Bluestein forward == naive evaluation; inverse recovers coefficients (all limbs)."""
+    import torch
+    T = pair(cfg)
+    P = T.P
+    rng = np.random.default_rng(11)
+    nl = P.L1 + P.K
+    coef = np.stack([np.stack([rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.moduli])
+                     for _ in range(3)])                              # [3, nl, n]
+    x = from_u64(coef, T.ctx.device)
+    ev = to_u64(T.ctx.ntt_fwd(x))
+    for b in range(3):
+        want = P.__class__ and np.stack([P.ring.to_eval(coef[b, i], P.omega[i], P.moduli[i]) for i in range(nl)])
+        assert np.array_equal(ev[b], want), "forward NTT mismatch (poly %d)" % b
+    back = to_u64(T.ctx.ntt_inv(from_u64(ev, T.ctx.device)))
+    assert np.array_equal(back, coef)
+    torch.cuda.synchronize()
+
+
+def test_ntt_full_size_sampled(pair):
+    """a1/a2 at C2's full ring (n = 30940, M = 65536): two limbs vs naive evaluation."""
+    T = pair("c2")
+    P = T.P
+    rng = np.random.default_rng(12)
+    coef = np.stack([rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.moduli])[None]
+    ev = to_u64(T.ctx.ntt_fwd(from_u64(coef, T.ctx.device)))
+    for i in (0, P.L1 + P.K - 1):
+        want = P.ring.to_eval(coef[0, i], P.omega[i], P.moduli[i])
+        assert np.array_equal(ev[0, i], want)
+    back = to_u64(T.ctx.ntt_inv(from_u64(ev, T.ctx.device)))
+    assert np.array_equal(back, coef)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_encrypt_decrypt_match_oracle(pair, cfg):
+    """R9/R10 + R7 sampler: the product's ciphertexts equal the oracle's bit for bit."""
+    T = pair(cfg)
+    P = T.P
+    rng = np.random.default_rng(13)
+    ints = T.ctx.ints_per_ct
+    a, b = mixed_pairs(P, rng, ints)
+    words = np.array([a, b], dtype=np.uint64)
+    ct = T.ctx.encrypt(T.keys, words, SEED_ENC, ct_index0=5)
+    g = to_u64(ct)
+    for i in range(2):
+        o = T.oracle_ct(list(words[i]), 5 + i)
+        assert np.array_equal(g[i], T.ct_eval(o)), "ciphertext %d differs from oracle" % i
+    dec = T.ctx.decrypt(T.keys, ct)
+    assert np.array_equal(dec, words)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_ops_match_oracle(pair, cfg):
+    """a3 tensor, a4 automorphism, a5 key switching (relin / rotation / Frobenius), a6 modswitch."""
+    T = pair(cfg)
+    P, bgv = T.P, T.bgv
+    rng = np.random.default_rng(14)
+    ints = T.ctx.ints_per_ct
+    a, b = mixed_pairs(P, rng, ints)
+    ct = T.ctx.encrypt(T.keys, np.array([a, b], dtype=np.uint64), SEED_ENC, ct_index0=20)
+    oa, ob = T.oracle_ct(a, 20), T.oracle_ct(b, 21)
+    ca, cb = ct[0:1], ct[1:2]
+    # tensor
+    tg = to_u64(T.ctx.tensor(ca, cb))[0]
+    assert np.array_equal(tg, T.ct_eval(bgv.tensor(P, oa, ob)))
+    # automorphism (no key switch)
+    t = pow(P.alg.g, 1, P.m)
+    ag = to_u64(T.ctx.automorph(ca, t))[0]
+    idx = list(range(P.L1))
+    want = np.stack([bgv.to_eval(P, np.stack([P.ring.automorph_mod(c[r], t, P.moduli[r]) for r in idx]), idx)
+                     for c in oa.parts])
+    assert np.array_equal(ag, want)
+    # modswitch
+    assert np.array_equal(to_u64(T.ctx.modswitch(ca))[0], T.ct_eval(bgv.modswitch(P, oa)))
+    # key switch of c1 with the relinearisation key
+    d = ca[:, 1].contiguous()
+    u = to_u64(T.ctx.keyswitch(T.keys, d, 0))[0]
+    u0, u1 = bgv.keyswitch(P, T.okeys, oa.parts[1], P.L1, 0)
+    assert np.array_equal(u, np.stack([bgv.to_eval(P, u0, idx), bgv.to_eval(P, u1, idx)]))
+    # mul (tensor + relin + modswitch), rotation, Frobenius
+    assert np.array_equal(to_u64(T.ctx.mul(T.keys, ca, cb))[0], T.ct_eval(bgv.mul(P, T.okeys, oa, ob)))
+    assert np.array_equal(to_u64(T.ctx.rotate(T.keys, ca, 1))[0], T.ct_eval(bgv.rotate(P, T.okeys, oa, 1)))
+    assert np.array_equal(to_u64(T.ctx.rotate(T.keys, ca, -1))[0], T.ct_eval(bgv.rotate(P, T.okeys, oa, -1)))
+    assert np.array_equal(to_u64(T.ctx.frobenius(T.keys, ca, 1))[0], T.ct_eval(bgv.frobenius(P, T.okeys, oa, 1)))
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c1l2"])
+def test_compare_matches_oracle(pair, cfg):
+    """a7-a9 end to end: compare_lt / compare_eq ciphertexts bit-exact; decrypted bits = [a<b]."""
+    from oracle import circuits
+    T = pair(cfg)
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(15)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=30)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=31)
+    lt, eq = T.ctx.compare(T.keys, ca, cb)
+    bits = T.ctx.decrypt(T.keys, lt, as_bits=True)[0]
+    ebits = T.ctx.decrypt(T.keys, eq, as_bits=True)[0]
+    assert list(bits) == [int(x < y) for x, y in zip(a, b)]
+    assert list(ebits) == [int(x == y) for x, y in zip(a, b)]
+    ev = circuits.OracleEval(P, T.okeys)
+    olt, oeq = circuits.compare(ev, T.oracle_ct(a, 30), T.oracle_ct(b, 31), P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(lt)[0], T.ct_eval(olt))
+    assert np.array_equal(to_u64(eq)[0], T.ct_eval(oeq))
+    lt2 = T.ctx.compare_lt(T.keys, ca, cb)
+    assert np.array_equal(to_u64(lt2), to_u64(lt))
+
+
+def test_extract_matches_oracle(pair):
+    from oracle import circuits
+    T = pair("c1")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(16)
+    a, _ = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=40)
+    dg = to_u64(T.ctx.extract(T.keys, ca))[0]
+    ev = circuits.OracleEval(P, T.okeys)
+    od = circuits.extract_digits(ev, T.oracle_ct(a, 40), P.d)
+    for i in range(P.d):
+        assert np.array_equal(dg[i], T.ct_eval(od[i]))
+
+
+def test_select_min_max_match_oracle(pair):
+    from oracle import circuits
+    T = pair("c1m")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(17)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=50)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=51)
+    mn = T.ctx.min(T.keys, ca, cb)
+    mx = T.ctx.max(T.keys, ca, cb)
+    assert list(T.ctx.decrypt(T.keys, mn)[0]) == [min(x, y) for x, y in zip(a, b)]
+    assert list(T.ctx.decrypt(T.keys, mx)[0]) == [max(x, y) for x, y in zip(a, b)]
+    ev = circuits.OracleEval(P, T.okeys)
+    omn = circuits.vmin(ev, T.oracle_ct(a, 50), T.oracle_ct(b, 51), P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(mn)[0], T.ct_eval(omn))
+
+
+def test_compaction_fig7(pair):
+    """a10: 4 ciphertexts at 25% block utilisation (every 4th block, Fig. 7) -> 1 ciphertext."""
+    from oracle import circuits
+    T = pair("c1m")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(18)
+    words = [[int(x) for x in rng.integers(0, P.base ** (P.d * P.l), size=ints)] for _ in range(4)]
+    useful = np.zeros((4, ints), dtype=np.uint8)
+    useful[:, 3::4] = 1
+    for c in range(4):
+        for j in range(ints):
+            if not useful[c, j]:
+                words[c][j] = 0
+    cts = T.ctx.encrypt(T.keys, np.array(words, dtype=np.uint64), SEED_ENC, ct_index0=60)
+    out, dest = T.ctx.compact(T.keys, cts, useful)
+    assert out.shape[0] == int(np.ceil(useful.sum() / ints))
+    dec = T.ctx.decrypt(T.keys, out)
+    for c in range(4):
+        for j in range(ints):
+            if useful[c, j]:
+                ct_i, blk = divmod(int(dest[c, j]), ints)
+                assert dec[ct_i][blk] == words[c][j]
+    ev = circuits.OracleEval(P, T.okeys)
+    oin = [T.oracle_ct(words[c], 60 + c) for c in range(4)]
+    outs, _ = circuits.compact(ev, oin, [list(np.nonzero(useful[c])[0]) for c in range(4)], P.l, ints, 3)
+    for k in range(out.shape[0]):
+        assert np.array_equal(to_u64(out)[k], T.ct_eval(outs[k]))
+
+
+def test_non_blocking_matches_blocking(pair):
+    """a11: compare on a side stream joined by an event == the blocking result; double wait fails."""
+    import torch
+    T = pair("c1")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(19)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=70)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=71)
+    ref = T.ctx.compare_lt(T.keys, ca, cb)
+    side = torch.cuda.Stream()
+    ws = torch.empty(T.ctx.workspace_bytes(1), dtype=torch.uint8, device=T.ctx.device)
+    out = T.ctx.ct_empty(1, ref.shape[2])
+    torch.cuda.synchronize()
+    h = T.ctx.compare_lt_async(T.keys, ca, cb, out, side, ws)
+    main = torch.cuda.current_stream()
+    busy = ca.clone() * 1                # independent main-stream work meanwhile
+    assert T.ctx.wait(h, main) == 0
+    assert T.ctx.wait(h, main) == 7      # BC_E_CONSUMED
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    del busy
+
+
+@pytest.mark.slow
+def test_compare_shadow_c2_bit_exact(pair):
+    """C2's circuit (p=13 univariate, (d,l)=(4,6), 11+3 primes) on its shadow ring m=859:
+    whole compare_lt ciphertext bit-exact vs the oracle (takes ~2 minutes of oracle time)."""
+    from oracle import circuits
+    T = pair("c2s")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(20)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=80)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=81)
+    lt = T.ctx.compare_lt(T.keys, ca, cb)
+    assert list(T.ctx.decrypt(T.keys, lt, as_bits=True)[0]) == [int(x < y) for x, y in zip(a, b)]
+    ev = circuits.OracleEval(P, T.okeys)
+    olt, _ = circuits.compare(ev, T.oracle_ct(a, 80), T.oracle_ct(b, 81), P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(lt)[0], T.ct_eval(olt))
+
+
+def test_compare_full_c2_decrypts(pair):
+    """C2 at full size (n = 30940): every block of 2 ciphertext pairs decrypts to [a<b]."""
+    T = pair("c2")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(21)
+    A, B = [], []
+    for _ in range(2):
+        a, b = mixed_pairs(P, rng, ints)
+        A.append(a)
+        B.append(b)
+    ca = T.ctx.encrypt(T.keys, np.array(A, dtype=np.uint64), SEED_ENC, ct_index0=0)
+    cb = T.ctx.encrypt(T.keys, np.array(B, dtype=np.uint64), SEED_ENC, ct_index0=2)
+    assert np.array_equal(T.ctx.decrypt(T.keys, ca), np.array(A, dtype=np.uint64))
+    lt = T.ctx.compare_lt(T.keys, ca, cb)
+    bits = T.ctx.decrypt(T.keys, lt, as_bits=True)
+    for i in range(2):
+        assert list(bits[i]) == [int(x < y) for x, y in zip(A[i], B[i])]
