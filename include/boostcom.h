@@ -187,6 +187,9 @@ bc_status bc_compact(bc_ctx *ctx, const bc_keys *keys, bc_ct in, const uint8_t *
                      bc_ct out, uint32_t *n_out, int32_t *h_dest, void *d_ws, size_t ws_bytes,
                      void *stream);
 
+/* NTT kernel family: 0 = register-blocked radix-16/8 passes where the (R, C) shape is
+ * supported (default), 1 = radix-2 shared-memory passes (reference kernels for tests) */
+void bc_set_ntt_impl(int impl);
 /* number of CUDA kernel launches issued by this thread since the last reset */
 uint64_t bc_launch_count(int reset);
 const char *bc_last_error(void);

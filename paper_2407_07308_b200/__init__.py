@@ -90,6 +90,7 @@ _sig("bc_rotate", _st, _vp, _vp, bc_ct, ctypes.c_int32, bc_ct, _vp, _sz, _vp)
 _sig("bc_frobenius", _st, _vp, _vp, bc_ct, _u32, bc_ct, _vp, _sz, _vp)
 _sig("bc_extract", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
 _sig("bc_launch_count", _u64, ctypes.c_int)
+_sig("bc_set_ntt_impl", None, ctypes.c_int)
 _sig("bc_last_error", ctypes.c_char_p)
 _sig("bc_compact", _st, _vp, _vp, bc_ct, _vp, bc_ct, ctypes.POINTER(_u32), _vp, _vp, _sz, _vp)
 
@@ -104,6 +105,11 @@ def _check(status, what):
     if status != 0:
         msg = _lib.bc_last_error()
         raise BoostComError("%s failed (status %d): %s" % (what, status, msg.decode() if msg else ""))
+
+
+def set_ntt_impl(impl):
+    """0 = register-blocked NTT passes (default), 1 = radix-2 reference passes."""
+    _lib.bc_set_ntt_impl(int(impl))
 
 
 def launch_count(reset=False):

@@ -29,6 +29,7 @@ static void check_launch() {
 extern "C" {
 
 const char *bc_last_error(void) { return last_error().c_str(); }
+void bc_set_ntt_impl(int impl) { g_ntt_impl = impl; }
 uint64_t bc_launch_count(int reset) {
     uint64_t c = launch_counter();
     if (reset) launch_counter() = 0;

@@ -337,6 +337,27 @@ void ctx_build(bc_ctx *X) {
                 dhi[(size_t)i * M + (size_t)rp * X->C + cp] = sh2(Di[k], q);
             }
     }
+    // register-pass twiddles omega_L^{+-j} (j < L/2), omega_L = psi^{M/L}
+    std::vector<u64x2> twR((size_t)NP * (X->R / 2)), twRi((size_t)NP * (X->R / 2)), twC((size_t)NP * (X->C / 2)),
+        twCi((size_t)NP * (X->C / 2));
+    for (uint32_t i = 0; i < NP; ++i) {
+        const uint64_t q = X->moduli[i];
+        const uint64_t ps = psi[(size_t)i * M + 1].w, psinv = invmod_h(ps, q);
+        const uint64_t wR = powmod_h(ps, M / X->R, q), wRi = powmod_h(psinv, M / X->R, q);
+        const uint64_t wC = powmod_h(ps, M / X->C, q), wCi = powmod_h(psinv, M / X->C, q);
+        uint64_t a = 1, b = 1;
+        for (uint32_t j = 0; j < X->R / 2; ++j) {
+            twR[(size_t)i * (X->R / 2) + j] = sh2(a, q);
+            twRi[(size_t)i * (X->R / 2) + j] = sh2(b, q);
+            a = mulmod_h(a, wR, q); b = mulmod_h(b, wRi, q);
+        }
+        a = 1; b = 1;
+        for (uint32_t j = 0; j < X->C / 2; ++j) {
+            twC[(size_t)i * (X->C / 2) + j] = sh2(a, q);
+            twCi[(size_t)i * (X->C / 2) + j] = sh2(b, q);
+            a = mulmod_h(a, wC, q); b = mulmod_h(b, wCi, q);
+        }
+    }
     std::vector<int32_t> pos(m, -1), z;
     for (uint32_t t = 0; t < m; ++t)
         if (gcd_u64(t, m) == 1) { pos[t] = (int32_t)z.size(); z.push_back((int32_t)t); }
@@ -348,6 +369,7 @@ void ctx_build(bc_ctx *X) {
     NttTables &T = X->T;
     T.psi = dev_upload(X, psi); T.tf1 = dev_upload(X, tf1); T.tf1i = dev_upload(X, tf1i);
     T.tfo = dev_upload(X, tfo); T.tfoi = dev_upload(X, tfoi); T.dhf = dev_upload(X, dhf); T.dhi = dev_upload(X, dhi);
+    T.twR = dev_upload(X, twR); T.twRi = dev_upload(X, twRi); T.twC = dev_upload(X, twC); T.twCi = dev_upload(X, twCi);
     T.pos = dev_upload(X, pos); T.z = dev_upload(X, z); T.phi = dev_upload(X, phi8); T.mods = X->d_mods;
     T.m = m; T.n = n; T.M = M; T.R = X->R; T.C = X->C; T.logR = X->logR; T.logC = X->logC;
     T.prime_m = X->prime_m ? 1 : 0;

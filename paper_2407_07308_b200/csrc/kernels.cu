@@ -14,6 +14,8 @@
 
 namespace bc {
 
+int g_ntt_impl = 0;
+
 uint64_t &launch_counter() {
     static thread_local uint64_t c = 0;
     return c;
@@ -265,10 +267,21 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
         attr_set = true;
     }
     const uint64_t chunk = 65535;
+    const bool v2 = g_ntt_impl == 0 && ntt2_supported(T);
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
-        if (!inv) {
+        if (v2) {
+            ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
+            if (inv) {
+                if (T.prime_m)
+                    k_reduce_prime<<<grid_for((uint64_t)nj * T.n, 256), 256, 0, st>>>(T, out, out_pstride, lm, j0, nj,
+                                                                                     scratch);
+                else
+                    k_reduce_composite<<<nj, 256, 0, st>>>(T, out, out_pstride, lm, j0, scratch);
+                launch_counter() += 1;
+            }
+        } else if (!inv) {
             k_passA<0><<<gA, 256, smA, st>>>(T, in, in_pstride, lm, j0, scratch, lTC);
             k_passB<0><<<gB, 256, smB, st>>>(T, lm, j0, scratch, lTR);
             k_passC<0><<<gA, 256, smA, st>>>(T, out, out_pstride, lm, j0, scratch, lTC);

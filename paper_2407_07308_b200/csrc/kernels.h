@@ -23,6 +23,7 @@ struct NttTables {
     const int32_t *z;     // [n]     Z_m^* ascending
     const int8_t *phi;    // [n+1]   Phi_m coefficients (for composite m)
     const Mod *mods;      // [P]
+    const u64x2 *twR, *twRi, *twC, *twCi;   // [P][R/2], [P][C/2]: omega_R^{+-j}, omega_C^{+-j} (register passes)
     uint32_t m, n, M, R, C, logR, logC;
     int prime_m;          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
 };
@@ -118,5 +119,11 @@ void dec_dot(const Mod *mods, const uint64_t *ct, const uint64_t *s, uint64_t *o
              uint32_t lvl, uint32_t n, cudaStream_t st);
 
 uint64_t &launch_counter();
+
+// register-blocked passes (ntt2.cu) for the supported (R, C) shapes
+bool ntt2_supported(const NttTables &T);
+void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
+extern int g_ntt_impl;   // 0 = auto (register passes when supported), 1 = radix-2 passes
 
 }  // namespace bc
