@@ -187,9 +187,13 @@ bc_status bc_compact(bc_ctx *ctx, const bc_keys *keys, bc_ct in, const uint8_t *
                      bc_ct out, uint32_t *n_out, int32_t *h_dest, void *d_ws, size_t ws_bytes,
                      void *stream);
 
-/* NTT kernel family: 0 = register-blocked radix-16/8 passes where the (R, C) shape is
- * supported (default), 1 = radix-2 shared-memory passes (reference kernels for tests) */
+/* NTT kernel family: 0 = register-blocked passes, 8 registers per thread (default where the
+ * (R, C) shape is supported), 1 = radix-2 shared-memory passes (reference kernels for
+ * tests), 2 = register-blocked passes with 16 registers per thread */
 void bc_set_ntt_impl(int impl);
+/* tuning knobs (benchmarks / tests): "ntt_group_bytes" = transform scratch per launch group
+ * (default: the whole batch in one group; smaller groups measured slower on B200). Returns 0 if known. */
+int bc_tune(const char *key, int64_t value);
 /* number of CUDA kernel launches issued by this thread since the last reset */
 uint64_t bc_launch_count(int reset);
 const char *bc_last_error(void);

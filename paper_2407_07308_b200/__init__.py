@@ -91,10 +91,15 @@ _sig("bc_frobenius", _st, _vp, _vp, bc_ct, _u32, bc_ct, _vp, _sz, _vp)
 _sig("bc_extract", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
 _sig("bc_launch_count", _u64, ctypes.c_int)
 _sig("bc_set_ntt_impl", None, ctypes.c_int)
+_sig("bc_tune", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64)
 _sig("bc_last_error", ctypes.c_char_p)
 _sig("bc_compact", _st, _vp, _vp, bc_ct, _vp, bc_ct, ctypes.POINTER(_u32), _vp, _vp, _sz, _vp)
 
 EXPORTS = [n for n in dir(_lib) if n.startswith("bc_")]
+if os.environ.get("BC_NTT_GROUP_MB"):
+    _lib.bc_tune(b"ntt_group_bytes", int(os.environ["BC_NTT_GROUP_MB"]) << 20)
+if os.environ.get("BC_NTT_IMPL"):
+    _lib.bc_set_ntt_impl(int(os.environ["BC_NTT_IMPL"]))
 
 
 class BoostComError(RuntimeError):

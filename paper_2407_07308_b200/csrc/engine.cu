@@ -369,6 +369,24 @@ void ctx_build(bc_ctx *X) {
     NttTables &T = X->T;
     T.psi = dev_upload(X, psi); T.tf1 = dev_upload(X, tf1); T.tf1i = dev_upload(X, tf1i);
     T.tfo = dev_upload(X, tfo); T.tfoi = dev_upload(X, tfoi); T.dhf = dev_upload(X, dhf); T.dhi = dev_upload(X, dhi);
+    {
+        // contiguous cross twiddles for the register passes
+        std::vector<u64x2> xta((size_t)NP * M), xtb((size_t)NP * M);
+        for (uint32_t i = 0; i < NP; ++i) {
+            const uint64_t q = X->moduli[i];
+            for (uint32_t r = 0; r < X->R; ++r) {
+                const uint32_t k1 = brev_h(r, X->logR);
+                for (uint32_t c = 0; c < X->C; ++c) {
+                    const uint32_t e1 = (c * k1) & (M - 1);
+                    xta[(size_t)i * M + (size_t)r * X->C + c] = psi[(size_t)i * M + e1];
+                    xtb[(size_t)i * M + (size_t)r * X->C + c] = psi[(size_t)i * M + ((M - e1) & (M - 1))];
+                }
+            }
+            (void)q;
+        }
+        T.xta = dev_upload(X, xta);
+        T.xtb = dev_upload(X, xtb);
+    }
     T.twR = dev_upload(X, twR); T.twRi = dev_upload(X, twRi); T.twC = dev_upload(X, twC); T.twCi = dev_upload(X, twCi);
     T.pos = dev_upload(X, pos); T.z = dev_upload(X, z); T.phi = dev_upload(X, phi8); T.mods = X->d_mods;
     T.m = m; T.n = n; T.M = M; T.R = X->R; T.C = X->C; T.logR = X->logR; T.logC = X->logC;
@@ -544,35 +562,22 @@ CT Eng::sub(const CT &a, uint32_t b0, uint32_t nb) {
     return c;
 }
 
-// scratch polys per NTT launch group: at most ~1 GiB, the whole batch, or what the arena has free
-static uint32_t ntt_chunk(const Arena *A, uint32_t npoly, uint64_t per_words) {
-    uint64_t c = std::min<uint64_t>(npoly, (1ull << 27) / per_words);
-    if (!A->dry) {
-        const uint64_t free_words = (A->cap - A->used) / 8;
-        c = std::min<uint64_t>(c, free_words > per_words ? free_words / per_words - 1 : 1);
-    }
-    return (uint32_t)std::max<uint64_t>(1, c);
+// transform scratch: one L2-sized launch group of jobs (kernels.cu processes the batch group by group)
+static uint64_t ntt_scratch_words(const bc_ctx *X, uint32_t npoly, uint32_t njl) {
+    const uint64_t jobs = (uint64_t)npoly * njl;
+    const uint64_t group = std::max<uint64_t>(1, g_ntt_group_bytes / ((uint64_t)X->M * 8));
+    return std::min(jobs, group) * X->M;
 }
 
 void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
-    const uint64_t per = (uint64_t)lm.njl * X->M;
-    uint32_t chunk = ntt_chunk(A, npoly, per);
-    BufP scr = alloc_words((uint64_t)chunk * per);
+    BufP scr = alloc_words(ntt_scratch_words(X, npoly, lm.njl));
     if (dry()) return;
-    for (uint32_t p0 = 0; p0 < npoly; p0 += chunk) {
-        uint32_t np = std::min(chunk, npoly - p0);
-        ntt_forward(X->T, in + (uint64_t)p0 * ips, out + (uint64_t)p0 * ops, np, lm, ips, ops, (uint64_t *)scr->p, st);
-    }
+    ntt_forward(X->T, in, out, npoly, lm, ips, ops, (uint64_t *)scr->p, st);
 }
 void Eng::ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
-    const uint64_t per = (uint64_t)lm.njl * X->M;
-    uint32_t chunk = ntt_chunk(A, npoly, per);
-    BufP scr = alloc_words((uint64_t)chunk * per);
+    BufP scr = alloc_words(ntt_scratch_words(X, npoly, lm.njl));
     if (dry()) return;
-    for (uint32_t p0 = 0; p0 < npoly; p0 += chunk) {
-        uint32_t np = std::min(chunk, npoly - p0);
-        ntt_inverse(X->T, in + (uint64_t)p0 * ips, out + (uint64_t)p0 * ops, np, lm, ips, ops, (uint64_t *)scr->p, st);
-    }
+    ntt_inverse(X->T, in, out, npoly, lm, ips, ops, (uint64_t *)scr->p, st);
 }
 
 // R13: c'_i = (c_i - delta) q^{-1}, delta = r + q [-r]_p, r = [c]_q (last prime)

@@ -10,11 +10,14 @@
 // R7     counter-based sampler.  Encode/decode as exact int8 GEMMs over F_p.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace bc {
 
 int g_ntt_impl = 0;
+uint64_t g_ntt_group_bytes = 1ull << 40;   // one launch group (measured best on B200)
 
 uint64_t &launch_counter() {
     static thread_local uint64_t c = 0;
@@ -93,8 +96,8 @@ struct JobInfo {
 };
 __device__ __forceinline__ JobInfo job_info(const LimbMap &lm, uint32_t job) {
     JobInfo j;
-    j.poly = job / lm.njl;
-    uint32_t jl = job - j.poly * lm.njl;
+    const uint32_t jl = job / lm.npoly;          // limb-major: polys sharing a prime are adjacent
+    j.poly = job - jl * lm.npoly;
     j.lb = lm.limb(jl);
     j.pr = lm.prime(j.lb);
     return j;
@@ -266,8 +269,10 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
         cudaFuncSetAttribute(k_passC<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         attr_set = true;
     }
-    const uint64_t chunk = 65535;
-    const bool v2 = g_ntt_impl == 0 && ntt2_supported(T);
+    lm.npoly = npoly;
+    // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65535, (uint64_t)g_ntt_group_bytes / ((uint64_t)T.M * 8)));
+    const bool v2 = g_ntt_impl != 1 && ntt2_supported(T);
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);

@@ -24,6 +24,8 @@ struct NttTables {
     const int8_t *phi;    // [n+1]   Phi_m coefficients (for composite m)
     const Mod *mods;      // [P]
     const u64x2 *twR, *twRi, *twC, *twCi;   // [P][R/2], [P][C/2]: omega_R^{+-j}, omega_C^{+-j} (register passes)
+    const u64x2 *xta;     // [P][M]  psi^(c brev(rp)) at rp*C + c   (pass A epilogue, contiguous)
+    const u64x2 *xtb;     // [P][M]  psi^(-c brev(r)) at r*C + c    (pass B epilogue, contiguous)
     uint32_t m, n, M, R, C, logR, logC;
     int prime_m;          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
 };
@@ -32,6 +34,7 @@ struct NttTables {
 //   limb = jl < skip0 ? jl : jl + skipn;  prime = limb < split ? limb + off_lo : limb - split + off_hi
 struct LimbMap {
     uint32_t njl, skip0, skipn, split, off_lo, off_hi;
+    uint32_t npoly = 0;   // set by the transform driver: jobs are ordered limb-major (job = jl * npoly + poly)
     __host__ __device__ uint32_t limb(uint32_t jl) const { return jl < skip0 ? jl : jl + skipn; }
     __host__ __device__ uint32_t prime(uint32_t lb) const { return lb < split ? lb + off_lo : lb - split + off_hi; }
 };
@@ -124,6 +127,7 @@ uint64_t &launch_counter();
 bool ntt2_supported(const NttTables &T);
 void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
-extern int g_ntt_impl;   // 0 = auto (register passes when supported), 1 = radix-2 passes
+extern uint64_t g_ntt_group_bytes;   // scratch bytes per transform launch group (L2 residency)
+extern int g_ntt_impl;   // 0 = register passes (E=8) when supported, 1 = radix-2 passes, 2 = register passes E=16
 
 }  // namespace bc

@@ -1,0 +1,2 @@
+cd $GRAFT_REPO_ROOT
+python tools/ntt_micro.py c2 128 2>&1 | tail -6

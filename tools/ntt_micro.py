@@ -1,0 +1,45 @@
+"""Microbenchmark of the batched Bluestein NTT (forward + inverse) per kernel family / group size."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2407_07308_b200 as bc  # noqa: E402
+
+cfg = bc.load_params(sys.argv[1] if len(sys.argv) > 1 else "c2")
+ctx = bc.Context(cfg)
+L = ctx.n_cipher
+npoly = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+x = torch.randint(0, 1 << 40, (npoly, L, ctx.n), dtype=torch.int64, device="cuda")
+ws = ctx.workspace(npoly * L * ctx.M * 8 + (64 << 20))
+work = bc.ntt_work(ctx) * npoly * L
+ref = None
+for impl, gmb in [(1, 4096), (0, 4096), (2, 4096), (3, 4096), (4, 4096), (5, 4096), (6, 4096)]:
+    bc.set_ntt_impl(impl)
+    bc._lib.bc_tune(b"ntt_group_bytes", gmb << 20)
+    for _ in range(2):
+        y = ctx.ntt_fwd(x, ws=ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        y = ctx.ntt_fwd(x, ws=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    f = e0.elapsed_time(e1) / 5
+    e0.record()
+    for _ in range(5):
+        z = ctx.ntt_inv(y, ws=ws)
+    e1.record()
+    torch.cuda.synchronize()
+    i = e0.elapsed_time(e1) / 5
+    if ref is None:
+        ref = y.clone()
+    ok = bool(torch.equal(y, ref))
+    print(json.dumps({"limbs": npoly * L, "impl": impl, "group_mb": gmb, "fwd_ms": round(f, 3), "inv_ms": round(i, 3),
+                      "us_per_limb_fwd": round(1000 * f / (npoly * L), 3),
+                      "Tmulmod_s": round(work / (f / 1e3) / 1e12, 3), "matches_radix2": ok}), flush=True)
+bc.set_ntt_impl(0)
+bc._lib.bc_tune(b"ntt_group_bytes", 48 << 20)
