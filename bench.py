@@ -307,10 +307,12 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        torch.cuda.nvtx.range_push("step")
         e0.record()
         for _ in range(args.steps):
             step(ca, cb, out)
         e1.record()
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
     ms = e0.elapsed_time(e1) / args.steps

@@ -112,21 +112,22 @@ static uint32_t brev_h(uint32_t x, uint32_t bits) {
     return r;
 }
 
-static uint64_t mod_of(uint64_t tgt_is_p, uint64_t v, uint64_t T) { (void)tgt_is_p; return v % T; }
-
 // lift plan blob (see kernels.cu k_lift)
 static std::vector<uint64_t> build_plan(const bc_ctx *X, const std::vector<uint32_t> &src,
                                         const std::vector<int64_t> &tgt /* prime idx or -1 for p */) {
     const uint32_t ns = (uint32_t)src.size(), nt = (uint32_t)tgt.size();
     std::vector<uint64_t> qs(ns);
     for (uint32_t k = 0; k < ns; ++k) qs[k] = X->moduli[src[k]];
-    std::vector<uint64_t> inv(ns), invs(ns), qm((size_t)ns * ns, 0), half(ns);
+    std::vector<uint64_t> inv(ns), invs(ns), qm((size_t)ns * ns, 0), qms((size_t)ns * ns, 0), half(ns);
     for (uint32_t k = 0; k < ns; ++k) {
         uint64_t pre = 1;
         for (uint32_t j = 0; j < k; ++j) pre = mulmod_h(pre, qs[j] % qs[k], qs[k]);
         inv[k] = k ? invmod_h(pre, qs[k]) : 1;
         invs[k] = shoup(inv[k], qs[k]);
-        for (uint32_t j = 0; j < k; ++j) qm[(size_t)k * ns + j] = qs[j] % qs[k];
+        for (uint32_t j = 0; j < k; ++j) {
+            qm[(size_t)k * ns + j] = qs[j] % qs[k];
+            qms[(size_t)k * ns + j] = shoup(qs[j] % qs[k], qs[k]);
+        }
     }
     // mixed-radix digits of (Q-1)/2: its residues are (q_k - 1)/2 (Q = 0 mod q_k, Q odd)
     for (uint32_t k = 0; k < ns; ++k) {
@@ -143,23 +144,28 @@ static std::vector<uint64_t> build_plan(const bc_ctx *X, const std::vector<uint3
     blob.insert(blob.end(), inv.begin(), inv.end());
     blob.insert(blob.end(), invs.begin(), invs.end());
     blob.insert(blob.end(), qm.begin(), qm.end());
+    blob.insert(blob.end(), qms.begin(), qms.end());
     blob.insert(blob.end(), half.begin(), half.end());
     for (uint32_t t = 0; t < nt; ++t) blob.push_back(tgt[t] < 0 ? ~0ull : (uint64_t)tgt[t]);
-    std::vector<uint64_t> Qm(nt);
+    std::vector<uint64_t> B((size_t)nt * ns), Bs((size_t)nt * ns, 0), Qm(nt), Qms(nt, 0);
     for (uint32_t t = 0; t < nt; ++t) {
-        uint64_t T = tgt[t] < 0 ? X->p : X->moduli[tgt[t]];
+        const uint64_t T = tgt[t] < 0 ? X->p : X->moduli[tgt[t]];
         uint64_t pre = 1 % T;
         for (uint32_t k = 0; k < ns; ++k) {
-            blob.push_back(pre);
+            B[(size_t)t * ns + k] = pre;
+            if (tgt[t] >= 0) Bs[(size_t)t * ns + k] = shoup(pre, T);
             pre = mulmod_h(pre, qs[k] % T, T);
         }
         Qm[t] = pre;
+        if (tgt[t] >= 0) Qms[t] = shoup(pre, T);
     }
+    blob.insert(blob.end(), B.begin(), B.end());
+    blob.insert(blob.end(), Bs.begin(), Bs.end());
     blob.insert(blob.end(), Qm.begin(), Qm.end());
-    (void)mod_of;
+    blob.insert(blob.end(), Qms.begin(), Qms.end());
+    blob.push_back((uint64_t)(~0ull / X->p));    // floor((2^64 - 1) / p) ~ floor(2^64 / p)
     return blob;
 }
-
 
 // F_p interpolation: coefficients c with sum_k c_k v^k = f(v) for all v in F_p (Vandermonde solve)
 static std::vector<int64_t> interp_fp(int64_t p, const std::function<int64_t(int64_t)> &f) {
@@ -678,12 +684,7 @@ CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uin
         ntt_fwd(E + (uint64_t)j * nl * n, E + (uint64_t)j * nl * n, B, lm, eps, eps);
     }
     BufP u = alloc_words((uint64_t)B * 2 * nl * n);
-    if (!dry()) {
-        if (dps == (uint64_t)lvl * n)
-            ks_kip(X->d_mods, d, E, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig, n, st);
-        else
-            BC_THROW(BC_E_INTERNAL, "keyswitch: strided input must be compacted first");
-    }
+    if (!dry()) ks_kip(X->d_mods, d, dps, E, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig, n, st);
     dc.reset();
     ext.reset();
     // ModDown of both parts: 2B polys with stride nl*n
@@ -707,21 +708,12 @@ CT Eng::mul(const CT &a0, const CT &b0) {
     CT a = modswitch_to(a0, lv), b = modswitch_to(b0, lv);
     const uint32_t n = X->n, B = a.B;
     if (a.bstride != (uint64_t)2 * lv * n || b.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "mul: strided");
-    BufP t = alloc_words((uint64_t)B * 3 * lv * n);
+    const uint64_t tw = (uint64_t)3 * lv * n;
+    BufP t = alloc_words((uint64_t)B * tw);
     if (!dry()) ew_tensor(X->d_mods, a.d, b.d, (uint64_t *)t->p, B, lv, n, st);
-    // d2 compacted to [B][lv][n]
-    BufP d2 = alloc_words((uint64_t)B * lv * n);
-    if (!dry()) ew_copy_parts((uint64_t *)t->p, (uint64_t *)d2->p, B, 3, 2, 1, lv, lv, n, 1, 0, st);
-    CT u = keyswitch((uint64_t *)d2->p, (uint64_t)lv * n, B, lv, 0);
-    d2.reset();
-    // u += (d0, d1)
-    {
-        BufP t01 = alloc_words((uint64_t)B * 2 * lv * n);
-        if (!dry()) {
-            ew_copy_parts((uint64_t *)t->p, (uint64_t *)t01->p, B, 3, 0, 2, lv, lv, n, 2, 0, st);
-            ew_add(X->d_mods, u.d, (uint64_t *)t01->p, u.d, B, 2, lv, n, 0, st);
-        }
-    }
+    // relinearise d2 (part 2 of each 3-part product, read in place) and add (d0, d1)
+    CT u = keyswitch((uint64_t *)t->p + (uint64_t)2 * lv * n, tw, B, lv, 0);
+    if (!dry()) ew_add_bs(X->d_mods, u.d, u.bstride, (uint64_t *)t->p, tw, u.d, u.bstride, B, 2, lv, n, st);
     t.reset();
     return modswitch(u);
 }
@@ -731,19 +723,9 @@ CT Eng::automorph(const CT &a, uint32_t t) {
     if (a.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "automorph: strided");
     CT pm = ct_alloc(B, lv, 2);
     if (!dry()) ew_automorph(X->T, a.d, pm.d, B, 2, lv, t, st);
-    BufP c1 = alloc_words((uint64_t)B * lv * n);
-    if (!dry()) ew_copy_parts(pm.d, (uint64_t *)c1->p, B, 2, 1, 1, lv, lv, n, 1, 0, st);
-    CT u = keyswitch((uint64_t *)c1->p, (uint64_t)lv * n, B, lv, t);
-    c1.reset();
-    {
-        // u part 0 += pm part 0 (pm part 1 is replaced by the key-switch output)
-        BufP c0 = alloc_words((uint64_t)B * 2 * lv * n);
-        if (!dry()) {
-            CK(cudaMemsetAsync(c0->p, 0, (size_t)B * 2 * lv * n * 8, st));
-            ew_copy_parts(pm.d, (uint64_t *)c0->p, B, 2, 0, 1, lv, lv, n, 2, 0, st);
-            ew_add(X->d_mods, u.d, (uint64_t *)c0->p, u.d, B, 2, lv, n, 0, st);
-        }
-    }
+    // key-switch sigma_t(c1) (part 1, read in place); part 0 of the result += sigma_t(c0)
+    CT u = keyswitch(pm.d + (uint64_t)lv * n, pm.bstride, B, lv, t);
+    if (!dry()) ew_add_bs(X->d_mods, u.d, u.bstride, pm.d, pm.bstride, u.d, u.bstride, B, 1, lv, n, st);
     return u;
 }
 

@@ -485,7 +485,24 @@ void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in
 // =====================================================================================
 // key switching: KIP and ModDown scaling
 // =====================================================================================
-__global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__ d,
+// x < 2^(2b+4) (sums of up to 16 products of residues): Barrett estimate + correction loop
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, const Mod &M) {
+    const uint32_t s = M.b - 1, t = M.b + 1;
+    const uint64_t x1 = (lo >> s) | (hi << (64 - s));
+    const uint64_t plo = x1 * M.mu, phi = __umul64hi(x1, M.mu);
+    const uint64_t qhat = (plo >> t) | (phi << (64 - t));
+    uint64_t r = lo - qhat * M.q;
+    while (r >= M.q) r -= M.q;
+    return r;
+}
+
+__device__ __forceinline__ void mac128(uint64_t &hi, uint64_t &lo, uint64_t a, uint64_t b) {
+    const uint64_t pl = a * b, ph = __umul64hi(a, b);
+    lo += pl;
+    hi += ph + (lo < pl ? 1 : 0);
+}
+
+__global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__ d, uint64_t dps,
                       const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
                       uint64_t *__restrict__ u, uint64_t total, uint32_t lvl, uint32_t K, uint32_t L1,
                       uint32_t alpha, uint32_t ndig, uint32_t n) {
@@ -497,21 +514,38 @@ __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__
         const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
         const Mod M = mods[kl];
         const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
-        uint64_t s0 = 0, s1 = 0;
+        uint64_t h0 = 0, l0 = 0, h1 = 0, l1 = 0;
         for (uint32_t j = 0; j < ndig; ++j) {
-            const uint64_t dig = (j == jr) ? d[(b * lvl + r) * n + x] : ext[((b * ndig + j) * nl + r) * n + x];
+            const uint64_t dig = (j == jr) ? d[b * dps + (uint64_t)r * n + x] : ext[((b * ndig + j) * nl + r) * n + x];
             const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
-            s0 = add_mod(s0, mul_mod(dig, kj[(uint64_t)kl * n + x], M), M.q);
-            s1 = add_mod(s1, mul_mod(dig, kj[(uint64_t)(L1 + K + kl) * n + x], M), M.q);
+            mac128(h0, l0, dig, kj[(uint64_t)kl * n + x]);
+            mac128(h1, l1, dig, kj[(uint64_t)(L1 + K + kl) * n + x]);
         }
-        u[(b * 2 + 0) * ln + rr] = s0;
-        u[(b * 2 + 1) * ln + rr] = s1;
+        u[(b * 2 + 0) * ln + rr] = reduce128(h0, l0, M);
+        u[(b * 2 + 1) * ln + rr] = reduce128(h1, l1, M);
     }
 }
-void ks_kip(const Mod *mods, const uint64_t *d, const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B,
-            uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
+void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
+            uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
     const uint64_t total = (uint64_t)B * (lvl + K) * n;
-    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, ext, key, u, total, lvl, K, L1, alpha, ndig, n);
+    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, dps, ext, key, u, total, lvl, K, L1, alpha, ndig, n);
+    LAUNCHED();
+}
+
+// o[b] = a[b] + b[b] over parts x lvl x n words per ciphertext, with per-operand batch strides
+__global__ void k_add_bs(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, uint64_t abs,
+                         const uint64_t *__restrict__ b, uint64_t bbs, uint64_t *__restrict__ o, uint64_t obs,
+                         uint64_t total, uint64_t per, uint32_t lvl, uint32_t n) {
+    GRID_LOOP(i, total) {
+        const uint64_t bi = i / per, r = i - bi * per;
+        const uint32_t limb = (uint32_t)((r / n) % lvl);
+        o[bi * obs + r] = add_mod(a[bi * abs + r], b[bi * bbs + r], mods[limb].q);
+    }
+}
+void ew_add_bs(const Mod *mods, const uint64_t *a, uint64_t abs, const uint64_t *b, uint64_t bbs, uint64_t *o,
+               uint64_t obs, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t per = (uint64_t)parts * lvl * n, total = (uint64_t)B * per;
+    k_add_bs<<<grid_for(total, 256), 256, 0, st>>>(mods, a, abs, b, bbs, o, obs, total, per, lvl, n);
     LAUNCHED();
 }
 
@@ -538,9 +572,15 @@ void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const 
 // =====================================================================================
 // exact centered CRT lift (Garner mixed radix + lexicographic sign test)
 // plan blob (u64 words): [0]=ns [1]=nt, then
-//   src[ns] inv[ns] invs[ns] qm[ns*ns] half[ns] tgt[nt] Bt[nt*ns] Qm[nt]
-// tgt[t] = prime index, or ~0 for the plaintext modulus p.
+//   src[ns] inv[ns] invs[ns] qm[ns*ns] qms[ns*ns] half[ns] tgt[nt] B[nt*ns] Bs[nt*ns] Qm[nt] Qms[nt] pmu
+// tgt[t] = prime index, or ~0 for the plaintext modulus p.  All constant products use Shoup
+// companions (lazy outputs < 2T), one Barrett reduction per target.
 // =====================================================================================
+__device__ __forceinline__ uint64_t mod_small(uint64_t v, uint32_t p, uint64_t pmu) {
+    uint64_t r = v - __umul64hi(v, pmu) * p;
+    return r >= p ? r - p : r;
+}
+
 template <int MAXS>
 __global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict__ mods, uint32_t p,
                        const uint64_t *__restrict__ src, uint64_t src_pstride, uint64_t *__restrict__ out,
@@ -548,19 +588,23 @@ __global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict_
                        uint32_t skip0, uint32_t skipn, int mode) {
     const uint32_t ns = (uint32_t)plan[0], nt = (uint32_t)plan[1];
     const uint64_t *P_src = plan + 2, *P_inv = P_src + ns, *P_invs = P_inv + ns, *P_qm = P_invs + ns;
-    const uint64_t *P_half = P_qm + ns * ns, *P_tgt = P_half + ns, *P_B = P_tgt + nt, *P_Q = P_B + (uint64_t)nt * ns;
+    const uint64_t *P_qms = P_qm + ns * ns, *P_half = P_qms + ns * ns, *P_tgt = P_half + ns;
+    const uint64_t *P_B = P_tgt + nt, *P_Bs = P_B + (uint64_t)nt * ns, *P_Q = P_Bs + (uint64_t)nt * ns;
+    const uint64_t *P_Qs = P_Q + nt;
+    const uint64_t pmu = P_Qs[nt];
     GRID_LOOP(i, total) {
         const uint64_t poly = i / n;
         const uint32_t x = (uint32_t)(i - poly * n);
         const uint64_t *s = src + poly * src_pstride + x;
         uint64_t v[MAXS];
         for (uint32_t k = 0; k < ns; ++k) {
-            const Mod Mk = mods[P_src[k]];
             const uint64_t xk = s[(uint64_t)k * n];
             if (k == 0) { v[0] = xk; continue; }
-            uint64_t acc = v[k - 1] % Mk.q;
+            const Mod Mk = mods[P_src[k]];
+            uint64_t acc = v[k - 1];
             for (int j = (int)k - 2; j >= 0; --j)
-                acc = add_mod(mul_mod(acc, P_qm[k * ns + j], Mk), v[j] % Mk.q, Mk.q);
+                acc = mul_shoup_lazy(acc, P_qm[k * ns + j], P_qms[k * ns + j], Mk.q) + v[j];
+            acc = reduce64(acc, Mk);
             v[k] = mul_shoup(sub_mod(xk, acc, Mk.q), P_inv[k], P_invs[k], Mk.q);
         }
         bool neg = false;
@@ -570,9 +614,10 @@ __global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict_
         if (mode == 0) {
             for (uint32_t t = 0; t < nt; ++t) {
                 const Mod Mt = mods[P_tgt[t]];
+                const uint64_t *B = P_B + (uint64_t)t * ns, *Bs = P_Bs + (uint64_t)t * ns;
                 uint64_t acc = 0;
-                for (uint32_t k = 0; k < ns; ++k)
-                    acc = add_mod(acc, mul_mod(reduce64(v[k], Mt), P_B[(uint64_t)t * ns + k], Mt), Mt.q);
+                for (uint32_t k = 0; k < ns; ++k) acc += mul_shoup_lazy(v[k], B[k], Bs[k], Mt.q);
+                acc = reduce64(acc, Mt);
                 if (neg) acc = sub_mod(acc, P_Q[t], Mt.q);
                 const uint32_t lb = t < skip0 ? t : t + skipn;
                 out[poly * out_pstride + (uint64_t)lb * n + x] = acc;
@@ -581,7 +626,8 @@ __global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict_
             // value mod p (last target in mode 1, only target in mode 2)
             const uint32_t tp = nt - 1;
             uint64_t rp = 0;
-            for (uint32_t k = 0; k < ns; ++k) rp = (rp + (v[k] % p) * P_B[(uint64_t)tp * ns + k]) % p;
+            for (uint32_t k = 0; k < ns; ++k) rp += mod_small(v[k], p, pmu) * P_B[(uint64_t)tp * ns + k];
+            rp %= p;
             if (neg) rp = (rp + p - P_Q[tp]) % p;
             if (mode == 2) {
                 int32_t c = (int32_t)rp;
@@ -592,13 +638,16 @@ __global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict_
             // delta = r + Q * [-r]_p
             int64_t tc = (int64_t)((p - rp) % p);
             if (tc > (int64_t)(p / 2)) tc -= p;
+            const uint64_t atc = (uint64_t)(tc < 0 ? -tc : tc);
             for (uint32_t t = 0; t + 1 < nt; ++t) {
                 const Mod Mt = mods[P_tgt[t]];
+                const uint64_t *B = P_B + (uint64_t)t * ns, *Bs = P_Bs + (uint64_t)t * ns;
                 uint64_t acc = 0;
-                for (uint32_t k = 0; k < ns; ++k)
-                    acc = add_mod(acc, mul_mod(reduce64(v[k], Mt), P_B[(uint64_t)t * ns + k], Mt), Mt.q);
+                for (uint32_t k = 0; k < ns; ++k) acc += mul_shoup_lazy(v[k], B[k], Bs[k], Mt.q);
+                acc = reduce64(acc, Mt);
                 if (neg) acc = sub_mod(acc, P_Q[t], Mt.q);
-                acc = add_mod(acc, mul_mod(P_Q[t], from_signed(tc, Mt.q), Mt), Mt.q);
+                const uint64_t qc = mul_shoup(atc, P_Q[t], P_Qs[t], Mt.q);     // (Q mod T) |c|
+                acc = tc < 0 ? sub_mod(acc, qc, Mt.q) : add_mod(acc, qc, Mt.q);
                 out[poly * out_pstride + (uint64_t)t * n + x] = acc;
             }
         }

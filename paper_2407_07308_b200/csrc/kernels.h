@@ -74,9 +74,12 @@ void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in
 // ---- key switching ----
 // KIP: u[b][k][r][x] = sum_j ext[b][j][r][x] * key_j[k][klimb(r)][x], k in {0 (b-part),1 (a-part)};
 // for r in G_j the digit is read from d (eval input) instead of ext.
-void ks_kip(const Mod *mods, const uint64_t *d, const uint64_t *ext, const uint64_t *key, uint64_t *u,
+void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
             uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig,
             uint32_t n, cudaStream_t st);
+// o[b] = a[b] + b[b] (parts x lvl x n words per ciphertext), per-operand batch strides in words
+void ew_add_bs(const Mod *mods, const uint64_t *a, uint64_t abs, const uint64_t *b, uint64_t bbs, uint64_t *o,
+               uint64_t obs, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
 // out[b][k][i] = (u[b][k][i] - delta[b][k][i]) * inv_i  (Shoup constants per limb)
 void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *delta,
                   const u64x2 *inv, uint64_t *o, uint32_t npoly, uint32_t lvl, uint32_t n,
