@@ -189,8 +189,8 @@ def circuits_product_count(P):
     ev.alg = alg
     # replace mask / kappa constructors by stubs (cost only)
     orig_mask, orig_kappa = circuits.block_mask, circuits.kappa_slots
-    circuits.block_mask = lambda *a, **k: None
-    circuits.kappa_slots = lambda *a, **k: None
+    circuits.block_mask = lambda *a, **k: np.zeros((1, 2), dtype=np.int64)
+    circuits.kappa_slots = lambda *a, **k: np.zeros((1, 2), dtype=np.int64)
     try:
         circuits.compare(ev, CV(P.L1), CV(P.L1), P.circuit, P.d, P.l, 1)
     finally:
