@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libboostcom.so")
+_SO = os.environ.get("BC_LIB_PATH") or os.path.join(_HERE, "libboostcom.so")
 
 if not os.path.exists(_SO):
     raise ImportError("libboostcom.so not built: run __graft_entry__.build() "
@@ -456,8 +456,17 @@ def profile_ntt(ctx, npoly=64, reps=5, sm_mhz=1965.0):
     work = npoly * L * ntt_work(ctx)
     achieved = work / (ms / 1e3) / 1e12
     peak = SMS * IMAD_PER_SM_PER_CLK * sm_mhz * 1e6 / IMAD_PER_MULMOD / 1e12
+    traffic = None
+    try:
+        import json
+        prof = os.path.join(_HERE, "..", "profiles", "r1_ntt_probe_ncu.json")
+        if npoly == 64 and ctx.n == 30940 and os.path.exists(prof):
+            traffic = json.load(open(prof))["traffic_bytes_per_probe_launch"]
+    except Exception:
+        traffic = None
     return {"bound": "alu", "kernel": "bluestein_ntt (passA+passB+passC)", "achieved": achieved, "peak": peak,
-            "unit": "T mulmod64/s", "frac": achieved / peak, "traffic": None,
+            "unit": "T mulmod64/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_note": "DRAM bytes per probe launch from profiles/r1_ntt_probe_ncu.json (ncu --set full)",
             "per_launch_ms": ms, "limb_transforms_per_launch": npoly * L,
             "work_per_limb_transform": ntt_work(ctx),
             "peak_note": "148 SM x 64 IMAD/clk x %.0f MHz / %d IMAD per 64-bit mulmod" % (sm_mhz, IMAD_PER_MULMOD)}

@@ -151,6 +151,12 @@ __device__ __forceinline__ void col_transform(uint64_t (&v)[1 << LOGE], uint32_t
 
 __device__ __forceinline__ uint32_t brev_n(uint32_t x, int bits) { return __brev(x) >> (32 - bits); }
 
+// minimum resident blocks per SM requested from ptxas (caps registers at 65536 / (threads * minb))
+#ifndef NTT_REG_TARGET
+#define NTT_REG_TARGET 64
+#endif
+#define NTT_MINB(threads) ((65536 / NTT_REG_TARGET) / (threads) > 0 ? (65536 / NTT_REG_TARGET) / (threads) : 1)
+
 struct JobInfoLite {
     uint32_t poly, lb, pr;
 };
@@ -168,7 +174,7 @@ __device__ __forceinline__ JobInfoLite job_lite(const LimbMap &lm, uint32_t job)
 // pass A: chirp-multiply input, column DIF (length R), x psi^(c k1), store scratch[rp*C + c]
 // block = TC columns (lanes) x R/E threads (warps); grid (C/TC, jobs)
 template <int LOGR, int LOGE, int TC, int INV>
-__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE))) k2_passA(NttTables T,
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), NTT_MINB(TC * (1 << (LOGR - LOGE)))) k2_passA(NttTables T,
                                                                       const uint64_t *__restrict__ in, uint64_t in_pstride,
                                                                       LimbMap lm, uint64_t job0, uint64_t *__restrict__ scratch) {
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE))) k2_passA(NttTables 
 
 // pass B: row DIF (length C), x D^, row DIT, x psi^(-c k1); block = RB rows x C/E threads
 template <int LOGC, int LOGE, int RB, int INV>
-__global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE))) k2_passB(NttTables T, LimbMap lm, uint64_t job0,
+__global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), NTT_MINB(RB * (1 << (LOGC - LOGE)))) k2_passB(NttTables T, LimbMap lm, uint64_t job0,
                                                                       uint64_t *__restrict__ scratch) {
     constexpr int E = 1 << LOGE, C = 1 << LOGC, TPR = C / E;
     constexpr int ROWW = C + C / E;        // padded row width in smem
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE))) k2_passB(NttTables 
 
 // pass C: column DIT (length R) -> natural t, output chirp, Z_m^* gather (fwd) or A_t (inv)
 template <int LOGR, int LOGE, int TC, int INV>
-__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE))) k2_passC(NttTables T, uint64_t *__restrict__ out,
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), NTT_MINB(TC * (1 << (LOGR - LOGE)))) k2_passC(NttTables T, uint64_t *__restrict__ out,
                                                                       uint64_t out_pstride, LimbMap lm, uint64_t job0,
                                                                       uint64_t *__restrict__ scratch) {
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
