@@ -32,6 +32,25 @@ def load_json(p):
         return json.load(f)
 
 
+def shard(rank, world, pairs):
+    """Weak scaling: rank r owns global pairs [r*pairs, (r+1)*pairs); its a-ciphertexts use global
+    ciphertext indices [2*pairs*r, 2*pairs*r + pairs) and its b-ciphertexts the next `pairs`
+    (the counter-based sampler makes every ciphertext independent of the rank layout, R7)."""
+    base = 2 * pairs * rank
+    return {"pair0": rank * pairs, "ct_a0": base, "ct_b0": base + pairs, "input_seed": SEED_INPUT + rank}
+
+
+def max_over_ranks(x, world, device=None):
+    """max of a per-rank float over the process group (the timing rule: max over ranks)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -264,13 +283,14 @@ def main():
     ints = ctx.ints_per_ct
     B = args.pairs
     # shard: rank r owns global pairs [r*B, (r+1)*B) (weak scaling, no collective on the path)
-    rng = np.random.default_rng(SEED_INPUT + rank)
+    sh = shard(rank, world, B)
+    rng = np.random.default_rng(sh["input_seed"])
     A, Bw = word_pairs(rng, B * ints, ctx.base, ctx.d * ctx.l)
     A = np.array(A, dtype=np.uint64).reshape(B, ints)
     Bw = np.array(Bw, dtype=np.uint64).reshape(B, ints)
     ws = ctx.workspace(max(ctx.workspace_bytes(1), 4 << 30))
-    ca = ctx.encrypt(keys, A, SEED_ENC, ct_index0=2 * B * rank, ws=ws)
-    cb = ctx.encrypt(keys, Bw, SEED_ENC, ct_index0=2 * B * rank + B, ws=ws)
+    ca = ctx.encrypt(keys, A, SEED_ENC, ct_index0=sh["ct_a0"], ws=ws)
+    cb = ctx.encrypt(keys, Bw, SEED_ENC, ct_index0=sh["ct_b0"], ws=ws)
     lvl_out = ctx.out_level(ctx.n_cipher, 0)
     out = ctx.ct_empty(B, lvl_out)
     free, total = torch.cuda.mem_get_info(dev)
@@ -315,12 +335,7 @@ def main():
         torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
     total_pairs = B * world
     value = total_pairs * ints / (ms / 1000.0)
     clocks = clk.summary()
@@ -342,12 +357,7 @@ def main():
             ho.copy_(out, non_blocking=True)
         e3.record()
         barrier()
-        ms2 = e2.elapsed_time(e3) / args.steps
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([ms2], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms2 = float(t.item())
+        ms2 = max_over_ranks(e2.elapsed_time(e3) / args.steps, world, dev)
         e2e = {"value": total_pairs * ints / (ms2 / 1000.0), "unit": "int-compares/s",
                "h2d_bytes_per_step": int(ha.numel() * 8 + hb.numel() * 8),
                "d2h_bytes_per_step": int(ho.numel() * 8), "ms_per_step": ms2}
