@@ -321,6 +321,68 @@ def vmax(ev, a, b, circuit, d, l, ints):
     return select(ev, lt, b, a, l, ints)
 
 
+def tournament(ev, elems, op, circuit, d, l, ints):
+    """R20 min/max over T elements (slot-wise), fixed tree over element indices (SURVEY §8(e),
+    S:540-548 min_tournament): round r pairs (i, i + 2^r) for i = 0 mod 2^(r+1), the lower index
+    is `a`, result stored at i; an element without a partner passes through unchanged."""
+    f = vmin if op == "min" else vmax
+    cur = list(elems)
+    T = len(cur)
+    sh = 1
+    while sh < T:
+        for i in range(0, T, 2 * sh):
+            if i + sh < T:
+                cur[i] = f(ev, cur[i], cur[i + sh], circuit, d, l, ints)
+        sh *= 2
+    return cur[0]
+
+
+def sort_rank(ev, xs, circuit, d, l, ints):
+    """R21 rank sort of T elements slot-wise (S:549-557 sort_rank, ties broken by index).
+    For i < j: (lt, eq) = compare(x_i, x_j), le_ij = lt + eq = [x_i <= x_j].
+    S_j = sum_{i<j} le_ij + sum_{i>j} (-1) * le_ji (i ascending); rank_j = S_j + (T-1-j), so
+    rank_j = #{i : x_i < x_j or (x_i = x_j and i < j)}.
+    v_jk = S_j + (T-1-j-k) (one constant, mod p) = rank_j - k;  e_jk = 1 - v_jk^(p-1) (power rule,
+    = [rank_j = k] since |rank_j - k| < T <= p);  out_k = sum_j bcast(e_jk) * x_j (j ascending).
+    Needs T <= p (ranks distinct in F_p)."""
+    p = ev.p
+    T = len(xs)
+    assert 1 <= T <= p, "sort_rank needs T <= p"
+    le = {}
+    for i in range(T):
+        for j in range(i + 1, T):
+            lt, eq = compare(ev, xs[i], xs[j], circuit, d, l, ints)
+            le[(i, j)] = ev.add(lt, eq)
+    outs = [None] * T
+    e = {}
+    for j in range(T):
+        S = None
+        for i in range(T):
+            if i == j:
+                continue
+            t = le[(i, j)] if i < j else ev.scalar(le[(j, i)], -1)
+            S = t if S is None else ev.add(S, t)
+        for k in range(T):
+            c = (T - 1 - j - k) % p
+            v = S if S is not None else None
+            if v is None:                      # T == 1: rank 0 = k
+                e[(j, k)] = 1
+                continue
+            v = ev.add_const(v, c) if c else v
+            w = Powers(ev, v)(p - 1)
+            e[(j, k)] = ev.add_const(ev.scalar(w, -1), 1)
+    for k in range(T):
+        acc = None
+        for j in range(T):
+            if is_const(e[(j, k)]):
+                t = xs[j]
+            else:
+                t = ev.mul(broadcast(ev, e[(j, k)], l, ints), xs[j])
+            acc = t if acc is None else ev.add(acc, t)
+        outs[k] = acc
+    return outs
+
+
 # ----------------------------------------------------------------------------------------
 # evaluators
 # ----------------------------------------------------------------------------------------

@@ -126,3 +126,53 @@ def test_min_select_ciphertext(oracle_params):
     vb = circuits.PlainValue(slots.words_to_slots(wb, A, P.d, P.l, P.base))
     mn = circuits.vmin(ev, va, vb, P.circuit, P.d, P.l, ints)
     assert slots.slots_to_words(mn.v, P.d, P.l, P.base, ints) == [min(x, y) for x, y in zip(wa, wb)]
+
+
+def _gal_all(P):
+    A = P.alg
+    gal = {pow(P.p, k, P.m) for k in range(1, A.D)}
+    sh = 1
+    while sh < P.l:
+        gal |= {pow(A.g, sh, P.m), pow(A.g, -sh, P.m)}
+        sh *= 2
+    return sorted(gal)
+
+
+@pytest.fixture(scope="module")
+def c1t(oracle_params):
+    P = oracle_params("c1t")
+    return P, bgv.keygen(P, SEED_KEYS, _gal_all(P))
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_tournament_ciphertext(c1t, op):
+    """R20 fixed-tree min/max of 4 encrypted vectors decrypts to the brute-force min/max."""
+    P, K = c1t
+    A, ints = P.alg, P.ints_per_ct
+    rng = np.random.default_rng(11)
+    W = [[int(x) for x in rng.integers(0, 4, size=ints)] for _ in range(4)]
+    cts = [bgv.encrypt(P, K, A.encode(slots.words_to_slots(w, A, P.d, P.l, P.base)), SEED_ENC, 300 + t)
+           for t, w in enumerate(W)]
+    ev = circuits.OracleEval(P, K)
+    r = circuits.tournament(ev, cts, op, P.circuit, P.d, P.l, ints)
+    f = min if op == "min" else max
+    got = slots.slots_to_words(A.decode(bgv.decrypt(P, K, r)), P.d, P.l, P.base, ints)
+    assert got == [f(W[t][j] for t in range(4)) for j in range(ints)]
+    assert r.level == P.L1 - 6
+
+
+def test_sort_ciphertext(c1t):
+    """R21 rank sort of 3 encrypted vectors (S:555 sort [3,1,2] -> [1,2,3] in block 0)."""
+    P, K = c1t
+    A, ints = P.alg, P.ints_per_ct
+    rng = np.random.default_rng(12)
+    W = [[int(x) for x in rng.integers(0, 4, size=ints)] for _ in range(3)]
+    W[0][0], W[1][0], W[2][0] = 3, 1, 2
+    cts = [bgv.encrypt(P, K, A.encode(slots.words_to_slots(w, A, P.d, P.l, P.base)), SEED_ENC, 400 + t)
+           for t, w in enumerate(W)]
+    ev = circuits.OracleEval(P, K)
+    out = circuits.sort_rank(ev, cts, P.circuit, P.d, P.l, ints)
+    got = [slots.slots_to_words(A.decode(bgv.decrypt(P, K, o)), P.d, P.l, P.base, ints) for o in out]
+    for j in range(ints):
+        assert [got[k][j] for k in range(3)] == sorted(W[t][j] for t in range(3))
+    assert [got[k][0] for k in range(3)] == [1, 2, 3]

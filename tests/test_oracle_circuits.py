@@ -186,3 +186,71 @@ def test_select_and_broadcast_plain():
     mx = circuits.vmax(ev, a, b, "U", d, l, ints)
     assert slots.slots_to_words(mn.v, d, l, base, ints) == [min(x, y) for x, y in zip(wa, wb)]
     assert slots.slots_to_words(mx.v, d, l, base, ints) == [max(x, y) for x, y in zip(wa, wb)]
+
+
+def _words_matrix(rng, T, ints, cap, tie_rate=4):
+    """T word vectors; every tie_rate-th block copies a value from another element (ties)."""
+    W = [[rng.randrange(cap) for _ in range(ints)] for _ in range(T)]
+    for j in range(0, ints, tie_rate):
+        if T > 1:
+            W[rng.randrange(T)][j] = W[rng.randrange(T)][j]
+    return W
+
+
+def test_spec_sort_example():
+    """sort [3,1,2] -> [1,2,3], slot-wise in every block, at p = 3 (T = 3 <= p)."""
+    g = golden("spec_examples.json")["sort"]
+    A = slots.SlotAlgebra(3, cyclo.Ring(91))
+    d, l, base = 2, 2, 2
+    ints = A.S // l
+    ev = circuits.PlainEval(A)
+    import itertools
+    perms = list(itertools.permutations(g["values"]))
+    cols = [perms[j % len(perms)] for j in range(ints)]       # block j holds a permutation
+    xs = [_plain_words(A, [cols[j][t] for j in range(ints)], d, l, base) for t in range(len(g["values"]))]
+    out = circuits.sort_rank(ev, xs, "U", d, l, ints)
+    for k, o in enumerate(out):
+        assert slots.slots_to_words(o.v, d, l, base, ints) == [g["sorted"][k]] * ints
+
+
+@pytest.mark.parametrize("circ,p,m,d,l,T", [("U", 5, 31, 2, 2, 5), ("B", 5, 31, 2, 1, 4), ("U", 3, 91, 1, 2, 3)])
+def test_sort_plain_vs_bruteforce(circ, p, m, d, l, T):
+    A = slots.SlotAlgebra(p, cyclo.Ring(m))
+    base = slots.digit_base(p, circ)
+    ints = A.S // l
+    cap = base ** (d * l)
+    rng = random.Random(1000 + p * T)
+    ev = circuits.PlainEval(A)
+    W = _words_matrix(rng, T, ints, cap, tie_rate=2)
+    xs = [_plain_words(A, W[t], d, l, base) for t in range(T)]
+    out = circuits.sort_rank(ev, xs, circ, d, l, ints)
+    got = [slots.slots_to_words(o.v, d, l, base, ints) for o in out]
+    for j in range(ints):
+        assert [got[k][j] for k in range(T)] == sorted(W[t][j] for t in range(T))
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+@pytest.mark.parametrize("T", [1, 2, 4, 5, 7])
+def test_tournament_plain_vs_bruteforce(op, T):
+    A = slots.SlotAlgebra(5, cyclo.Ring(31))
+    d, l, base = 2, 2, 3
+    ints = A.S // l
+    rng = random.Random(77 + T)
+    ev = circuits.PlainEval(A)
+    W = _words_matrix(rng, T, ints, base ** (d * l))
+    xs = [_plain_words(A, W[t], d, l, base) for t in range(T)]
+    r = circuits.tournament(ev, xs, op, "U", d, l, ints)
+    f = min if op == "min" else max
+    assert slots.slots_to_words(r.v, d, l, base, ints) == [f(W[t][j] for t in range(T)) for j in range(ints)]
+
+
+def test_spec_min_tournament_example():
+    """min_tournament [3,1,2,9] -> 1 through the R20 fixed tree."""
+    g = golden("spec_examples.json")["min"]
+    A = slots.SlotAlgebra(3, cyclo.Ring(91))
+    d, l, base = 2, 2, 2
+    ints = A.S // l
+    ev = circuits.PlainEval(A)
+    xs = [_plain_words(A, [v] * ints, d, l, base) for v in g["values"]]
+    r = circuits.tournament(ev, xs, "min", "U", d, l, ints)
+    assert slots.slots_to_words(r.v, d, l, base, ints) == [g["min"]] * ints
