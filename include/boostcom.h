@@ -140,6 +140,29 @@ bc_status bc_max(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out, 
 /* output level of compare_lt / select for an input level (for sizing outputs) */
 uint32_t bc_compare_out_level(bc_ctx *ctx, uint32_t level, int which /*0 lt, 1 eq, 2 min*/);
 
+/* ---- vectors of ciphertexts: min/max tournament, rank sort -------------- */
+/* Each element v[i] is a batch of `batch` ciphertexts (the same batch for all i); the operation
+ * is slot-wise across the T elements.
+ * bc_min_tree / bc_max_tree (R20): fixed tree over element indices -- round r pairs
+ *   (i, i + 2^r) for i = 0 mod 2^(r+1), the lower index is `a` of min(a, b) = b + LT(a,b)(a - b)
+ *   (max: a + LT(a,b)(b - a)); unpaired elements pass through.  The tree does not depend on how
+ *   the elements are later sharded over GPUs.  out.level = bc_vec_out_level(ctx, 0|1, ...).
+ * bc_sort (R21): out[k] = k-th smallest element (ties by index), via ranks
+ *   rank_j = #{i: x_i < x_j or (x_i = x_j and i < j)} and out_k = sum_j [rank_j = k] x_j with
+ *   [v = 0] = 1 - v^(p-1); needs T <= p and all inputs at one level; out[T] views at
+ *   bc_vec_out_level(ctx, 2, ...).
+ * Everything runs inside the caller's workspace of at least bc_vec_workspace_bytes() bytes (no
+ * chunking: BC_E_OOM if smaller). */
+bc_status bc_min_tree(bc_ctx *ctx, const bc_keys *keys, const bc_ct *v, uint32_t T, bc_ct out, void *d_ws,
+                      size_t ws_bytes, void *stream);
+bc_status bc_max_tree(bc_ctx *ctx, const bc_keys *keys, const bc_ct *v, uint32_t T, bc_ct out, void *d_ws,
+                      size_t ws_bytes, void *stream);
+bc_status bc_sort(bc_ctx *ctx, const bc_keys *keys, const bc_ct *v, uint32_t T, bc_ct *out, void *d_ws,
+                  size_t ws_bytes, void *stream);
+/* which: 0 min tree, 1 max tree, 2 sort; levels[T] = element levels.  0 on error. */
+uint32_t bc_vec_out_level(bc_ctx *ctx, int which, const uint32_t *levels, uint32_t T);
+size_t bc_vec_workspace_bytes(bc_ctx *ctx, int which, const uint32_t *levels, uint32_t T, uint32_t batch);
+
 /* ---- non-blocking comparison (a11, Listing 5) ------------------------- */
 bc_status bc_compare_lt_async(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out,
                               void *d_ws, size_t ws_bytes, void *side_stream, bc_handle *h);

@@ -93,6 +93,11 @@ _sig("bc_launch_count", _u64, ctypes.c_int)
 _sig("bc_set_ntt_impl", None, ctypes.c_int)
 _sig("bc_tune", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64)
 _sig("bc_last_error", ctypes.c_char_p)
+_sig("bc_min_tree", _st, _vp, _vp, _vp, _u32, bc_ct, _vp, _sz, _vp)
+_sig("bc_max_tree", _st, _vp, _vp, _vp, _u32, bc_ct, _vp, _sz, _vp)
+_sig("bc_sort", _st, _vp, _vp, _vp, _u32, _vp, _vp, _sz, _vp)
+_sig("bc_vec_out_level", _u32, _vp, ctypes.c_int, _vp, _u32)
+_sig("bc_vec_workspace_bytes", _sz, _vp, ctypes.c_int, _vp, _u32, _u32)
 _sig("bc_compact", _st, _vp, _vp, bc_ct, _vp, bc_ct, ctypes.POINTER(_u32), _vp, _vp, _sz, _vp)
 
 EXPORTS = [n for n in dir(_lib) if n.startswith("bc_")]
@@ -327,6 +332,49 @@ class Context:
                               wb, _stream()), "bc_select")
         del torch
         return out
+
+    # ---- vectors: tournament / sort (R20, R21) ----
+    _VEC = {"min": 0, "max": 1, "sort": 2}
+
+    def vec_out_level(self, op, levels):
+        lv = np.ascontiguousarray(levels, dtype=np.uint32)
+        r = int(_lib.bc_vec_out_level(self._h, self._VEC[op], lv.ctypes.data, len(lv)))
+        if r == 0:
+            raise BoostComError("bc_vec_out_level: no valid schedule for %s over levels %s" % (op, list(levels)))
+        return r
+
+    def vec_workspace_bytes(self, op, levels, batch):
+        lv = np.ascontiguousarray(levels, dtype=np.uint32)
+        return int(_lib.bc_vec_workspace_bytes(self._h, self._VEC[op], lv.ctypes.data, len(lv), batch))
+
+    def _vec(self, op, keys, elems, ws):
+        T = len(elems)
+        views = (bc_ct * T)(*[self.view(e) for e in elems])
+        levels = [e.shape[2] for e in elems]
+        lvl = self.vec_out_level(op, levels)
+        nout = T if op == "sort" else 1
+        outs = [self.ct_empty(elems[0].shape[0], lvl) for _ in range(nout)]
+        if ws is None:
+            ws = self.workspace(self.vec_workspace_bytes(op, levels, elems[0].shape[0]))
+        w, wb = _ptr(ws), ws.numel()
+        ov = (bc_ct * nout)(*[self.view(o) for o in outs])
+        if op == "sort":
+            _check(_lib.bc_sort(self._h, keys.keys, views, T, ov, w, wb, _stream()), "bc_sort")
+            return outs
+        fn = _lib.bc_min_tree if op == "min" else _lib.bc_max_tree
+        _check(fn(self._h, keys.keys, views, T, ov[0], w, wb, _stream()), fn.__name__)
+        return outs[0]
+
+    def min_tree(self, keys, elems, ws=None):
+        """R20 slot-wise min over the T ciphertext batches `elems` (fixed tree)."""
+        return self._vec("min", keys, elems, ws)
+
+    def max_tree(self, keys, elems, ws=None):
+        return self._vec("max", keys, elems, ws)
+
+    def sort(self, keys, elems, ws=None):
+        """R21 slot-wise rank sort of T <= p ciphertext batches -> T outputs (ascending)."""
+        return self._vec("sort", keys, elems, ws)
 
     # ---- primitives (parity tests) ----
     def ntt_fwd(self, x, prime0=0, ws=None):

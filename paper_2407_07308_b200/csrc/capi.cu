@@ -415,3 +415,80 @@ bc_status bc_extract(bc_ctx *X, const bc_keys *k, bc_ct a, void *out, void *ws, 
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ vectors: tournament / sort
+// which: 0 min tree, 1 max tree, 2 sort.  Returns the output level(s) of a dry run.
+static std::vector<CT> vec_run(Eng &E, int which, const std::vector<CT> &v) {
+    if (which == 2) return sort_batch(E, v);
+    return {tournament_batch(E, v, which == 1)};
+}
+
+static std::vector<CT> vec_views(bc_ctx *X, Eng &E, const bc_ct *v, uint32_t T) {
+    if (!v || T == 0) BC_THROW(BC_E_ARG, "empty element list");
+    std::vector<CT> out;
+    for (uint32_t i = 0; i < T; ++i) {
+        check_ct(X, v[i], "v[i]");
+        if (v[i].batch != v[0].batch) BC_THROW(BC_E_ARG, "element batches differ");
+        out.push_back(E.view((uint64_t *)v[i].data, v[i].batch, v[i].level));
+    }
+    return out;
+}
+
+extern "C" uint32_t bc_vec_out_level(bc_ctx *X, int which, const uint32_t *levels, uint32_t T) {
+    try {
+        if (!X || !levels || T == 0) return 0;
+        Arena A;
+        A.init(nullptr, (size_t)1 << 62, true);
+        Eng E{X, nullptr, &A, 0};
+        std::vector<CT> v;
+        for (uint32_t i = 0; i < T; ++i) v.push_back(E.view((uint64_t *)(uintptr_t)256, 1, levels[i]));
+        return vec_run(E, which, v)[0].lvl;
+    } catch (...) {
+        return 0;
+    }
+}
+
+extern "C" size_t bc_vec_workspace_bytes(bc_ctx *X, int which, const uint32_t *levels, uint32_t T, uint32_t batch) {
+    try {
+        if (!X || !levels || T == 0) return 0;
+        size_t pk = dry_peak(X, nullptr, [&](Eng &E) {
+            std::vector<CT> v;
+            for (uint32_t i = 0; i < T; ++i) v.push_back(E.view((uint64_t *)(uintptr_t)256, batch, levels[i]));
+            vec_run(E, which, v);
+        });
+        return pk + pk / 4 + (64u << 20);
+    } catch (...) {
+        return 0;
+    }
+}
+
+static bc_status run_vec(bc_ctx *X, const bc_keys *k, int which, const bc_ct *v, uint32_t T, bc_ct *out, void *ws,
+                         size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !k || !out) BC_THROW(BC_E_ARG, "null argument");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    std::vector<CT> r = vec_run(E, which, vec_views(X, E, v, T));
+    for (size_t i = 0; i < r.size(); ++i) {
+        if (out[i].batch != r[i].B) BC_THROW(BC_E_ARG, "output batch mismatch");
+        out_copy(E, r[i], out[i], 0);
+    }
+    check_launch();
+    API_END
+}
+
+extern "C" {
+bc_status bc_min_tree(bc_ctx *X, const bc_keys *k, const bc_ct *v, uint32_t T, bc_ct out, void *ws, size_t wsb,
+                      void *st) {
+    return run_vec(X, k, 0, v, T, &out, ws, wsb, st);
+}
+bc_status bc_max_tree(bc_ctx *X, const bc_keys *k, const bc_ct *v, uint32_t T, bc_ct out, void *ws, size_t wsb,
+                      void *st) {
+    return run_vec(X, k, 1, v, T, &out, ws, wsb, st);
+}
+bc_status bc_sort(bc_ctx *X, const bc_keys *k, const bc_ct *v, uint32_t T, bc_ct *out, void *ws, size_t wsb,
+                  void *st) {
+    return run_vec(X, k, 2, v, T, out, ws, wsb, st);
+}
+}  // extern "C"

@@ -967,7 +967,9 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
     if (eq) *eq = EQ.ct;
 }
 
-CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2) {
+// R17 broadcast: copy block slot 0 to every slot of its block (mask0, then rotate by -2^r and add
+// under [(s mod l) >= 2^r])
+CT broadcast_batch(Eng &E, const CT &cond) {
     bc_ctx *X = E.X;
     const uint32_t l = X->l;
     CT c = E.ptmul(cond, ctx_pt(X, "bm0", block_mask(X, [](uint32_t t) { return t == 0; }), E.st));
@@ -975,8 +977,142 @@ CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2) {
         const uint64_t *mk = ctx_pt(X, "bmr:" + std::to_string(sh), block_mask(X, [sh](uint32_t t) { return t >= sh; }), E.st);
         c = E.add(c, E.ptmul(E.rotate(c, -(int64_t)sh), mk));
     }
+    return c;
+}
+
+CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2) {
+    CT c = broadcast_batch(E, cond);
     CT diff = E.add(x1, E.scalar(x2, -1));
     return E.add(x2, E.mul(c, diff));
+}
+
+// one contiguous batch from several batches of equal level (a single view is returned as is)
+CT concat_batch(Eng &E, const std::vector<CT> &parts) {
+    if (parts.empty()) BC_THROW(BC_E_ARG, "concat: no parts");
+    if (parts.size() == 1) return parts[0];
+    uint32_t B = 0;
+    for (const CT &c : parts) {
+        if (c.lvl != parts[0].lvl || c.parts != parts[0].parts) BC_THROW(BC_E_INTERNAL, "concat: level mismatch");
+        B += c.B;
+    }
+    CT o = E.ct_alloc(B, parts[0].lvl, parts[0].parts);
+    uint32_t b0 = 0;
+    for (const CT &c : parts) {
+        if (!E.dry()) {
+            if (c.bstride == o.bstride) {
+                CK(cudaMemcpyAsync(o.d + (uint64_t)b0 * o.bstride, c.d, (size_t)c.B * c.bstride * 8,
+                                   cudaMemcpyDeviceToDevice, E.st));
+            } else {
+                for (uint32_t i = 0; i < c.B; ++i)
+                    CK(cudaMemcpyAsync(o.d + (uint64_t)(b0 + i) * o.bstride, c.d + (uint64_t)i * c.bstride,
+                                       (size_t)o.bstride * 8, cudaMemcpyDeviceToDevice, E.st));
+            }
+        }
+        b0 += c.B;
+    }
+    return o;
+}
+
+// R20 min/max tournament: round r pairs (i, i + 2^r), i = 0 mod 2^(r+1), lower index = a, result at
+// i; unpaired elements pass through.  All pairs of a round with the same (level_a, level_b) run as
+// one batched compare + select (every op is per-ciphertext, so batching never changes bits).
+CT tournament_batch(Eng &E, std::vector<CT> cur, bool is_max) {
+    const uint32_t T = (uint32_t)cur.size();
+    if (T == 0) BC_THROW(BC_E_ARG, "tournament: no elements");
+    const uint32_t B = cur[0].B;
+    for (const CT &c : cur)
+        if (c.B != B) BC_THROW(BC_E_ARG, "tournament: batch mismatch");
+    for (uint32_t sh = 1; sh < T; sh <<= 1) {
+        std::map<std::pair<uint32_t, uint32_t>, std::vector<uint32_t>> groups;
+        for (uint32_t i = 0; i + sh < T; i += 2 * sh) groups[{cur[i].lvl, cur[i + sh].lvl}].push_back(i);
+        for (auto &g : groups) {
+            std::vector<CT> as, bs;
+            for (uint32_t i : g.second) { as.push_back(cur[i]); bs.push_back(cur[i + sh]); }
+            CT A = concat_batch(E, as), Bv = concat_batch(E, bs);
+            CT lt;
+            compare_batch(E, A, Bv, &lt, nullptr);
+            CT r = is_max ? select_batch(E, lt, Bv, A) : select_batch(E, lt, A, Bv);
+            for (size_t k = 0; k < g.second.size(); ++k) cur[g.second[k]] = E.sub(r, (uint32_t)k * B, B);
+        }
+    }
+    return cur[0];
+}
+
+// R21 rank sort: le_ij = LT + EQ of compare(x_i, x_j) (i < j, one batched compare);
+// S_j = sum_{i<j} le_ij + sum_{i>j} (-1) le_ji; v_jk = S_j + (T-1-j-k) (skipped if 0 mod p);
+// e_jk = 1 - v_jk^(p-1); out_k = sum_j bcast(e_jk) * x_j.  All (j, k) run as one batch of T^2 B.
+std::vector<CT> sort_batch(Eng &E, const std::vector<CT> &x) {
+    bc_ctx *X = E.X;
+    const uint32_t T = (uint32_t)x.size();
+    const int64_t p = X->p;
+    if (T == 0 || (int64_t)T > p) BC_THROW(BC_E_ARG, "sort: need 1 <= T <= p");
+    const uint32_t B = x[0].B;
+    for (const CT &c : x) {
+        if (c.B != B) BC_THROW(BC_E_ARG, "sort: batch mismatch");
+        if (c.lvl != x[0].lvl) BC_THROW(BC_E_LEVEL, "sort: all elements must share one level");
+    }
+    if (T == 1) return {x[0]};
+    std::vector<CT> as, bs;
+    std::vector<std::vector<int>> pidx(T, std::vector<int>(T, -1));
+    int np = 0;
+    for (uint32_t i = 0; i < T; ++i)
+        for (uint32_t j = i + 1; j < T; ++j) { as.push_back(x[i]); bs.push_back(x[j]); pidx[i][j] = np++; }
+    CT lt, eq;
+    compare_batch(E, concat_batch(E, as), concat_batch(E, bs), &lt, &eq);
+    as.clear(); bs.clear();
+    CT le = E.add(lt, eq);
+    lt = CT(); eq = CT();
+    std::vector<CT> S(T);
+    for (uint32_t j = 0; j < T; ++j) {
+        bool have = false;
+        for (uint32_t i = 0; i < T; ++i) {
+            if (i == j) continue;
+            CT t = i < j ? E.sub(le, (uint32_t)pidx[i][j] * B, B) : E.scalar(E.sub(le, (uint32_t)pidx[j][i] * B, B), -1);
+            S[j] = have ? E.add(S[j], t) : t;
+            have = true;
+        }
+    }
+    le = CT();
+    const uint32_t lS = S[0].lvl;
+    CT V = E.ct_alloc(T * T * B, lS, 2);
+    for (uint32_t j = 0; j < T; ++j)
+        for (uint32_t k = 0; k < T; ++k) {
+            const int64_t c = (((int64_t)T - 1 - j - k) % p + p) % p;
+            CT dst = E.sub(V, (j * T + k) * B, B);
+            if (c) {
+                if (!E.dry()) ew_add_const(X->d_mods, S[j].d, c > p / 2 ? c - p : c, dst.d, B, 2, lS, X->n, E.st);
+            } else {
+                E.copy_into(S[j], dst.d);
+            }
+        }
+    S.clear();
+    CT W;
+    {
+        Powers pw(E, VT(V));
+        W = pw.get((int)p - 1).ct;
+    }
+    V = CT();
+    CT e = E.add_const(E.scalar(W, -1), 1);
+    W = CT();
+    CT bc = broadcast_batch(E, e);
+    e = CT();
+    std::vector<CT> xr;
+    {
+        std::vector<CT> xa(T);
+        for (uint32_t j = 0; j < T; ++j) xa[j] = E.modswitch_to(x[j], bc.lvl);
+        for (uint32_t j = 0; j < T; ++j)
+            for (uint32_t k = 0; k < T; ++k) xr.push_back(xa[j]);
+    }
+    CT prod = E.mul(bc, concat_batch(E, xr));
+    xr.clear();
+    bc = CT();
+    std::vector<CT> out(T);
+    for (uint32_t k = 0; k < T; ++k)
+        for (uint32_t j = 0; j < T; ++j) {
+            CT t = E.sub(prod, (j * T + k) * B, B);
+            out[k] = j ? E.add(out[k], t) : t;
+        }
+    return out;
 }
 
 }  // namespace bc

@@ -142,5 +142,9 @@ void encode_slots_dev(bc_ctx *X, const int16_t *d_slots, uint32_t B, int16_t *d_
 void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq);
 CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2);
 std::vector<CT> extract_batch(Eng &E, const CT &a);
+CT broadcast_batch(Eng &E, const CT &cond);
+CT concat_batch(Eng &E, const std::vector<CT> &parts);
+CT tournament_batch(Eng &E, std::vector<CT> elems, bool is_max);
+std::vector<CT> sort_batch(Eng &E, const std::vector<CT> &x);
 
 }  // namespace bc

@@ -295,3 +295,48 @@ def test_compare_full_c2_decrypts(pair):
     bits = T.ctx.decrypt(T.keys, lt, as_bits=True)
     for i in range(2):
         assert list(bits[i]) == [int(x < y) for x, y in zip(A[i], B[i])]
+
+
+@pytest.mark.parametrize("op,T", [("min", 4), ("max", 4), ("min", 3)])
+def test_tournament_matches_oracle(pair, op, T):
+    """R20 fixed-tree min/max over T element batches (2 ciphertexts each): every output
+    ciphertext bit-exact vs the oracle's tournament, and decrypts to the brute-force min/max."""
+    from oracle import circuits
+    Tp = pair("c1t")
+    P = Tp.P
+    ints = Tp.ctx.ints_per_ct
+    rng = np.random.default_rng(30 + T)
+    W = [[[int(x) for x in rng.integers(0, P.base ** (P.d * P.l), size=ints)] for _ in range(2)] for _ in range(T)]
+    W[0][0][0] = W[1][0][0]                                   # a tie
+    elems = [Tp.ctx.encrypt(Tp.keys, np.array(W[t], dtype=np.uint64), SEED_ENC, ct_index0=500 + 2 * t)
+             for t in range(T)]
+    r = Tp.ctx.max_tree(Tp.keys, elems) if op == "max" else Tp.ctx.min_tree(Tp.keys, elems)
+    f = min if op == "min" else max
+    dec = Tp.ctx.decrypt(Tp.keys, r)
+    ev = circuits.OracleEval(P, Tp.okeys)
+    for c in range(2):
+        assert list(dec[c]) == [f(W[t][c][j] for t in range(T)) for j in range(ints)]
+        o = circuits.tournament(ev, [Tp.oracle_ct(W[t][c], 500 + 2 * t + c) for t in range(T)], op,
+                                P.circuit, P.d, P.l, ints)
+        assert np.array_equal(to_u64(r)[c], Tp.ct_eval(o))
+
+
+def test_sort_matches_oracle(pair):
+    """R21 rank sort of T = 3 = p element batches: bit-exact vs the oracle, sorted."""
+    from oracle import circuits
+    Tp = pair("c1t")
+    P = Tp.P
+    ints = Tp.ctx.ints_per_ct
+    rng = np.random.default_rng(40)
+    W = [[int(x) for x in rng.integers(0, 4, size=ints)] for _ in range(3)]
+    W[0][0], W[1][0], W[2][0] = 3, 1, 2
+    elems = [Tp.ctx.encrypt(Tp.keys, np.array([W[t]], dtype=np.uint64), SEED_ENC, ct_index0=600 + t)
+             for t in range(3)]
+    outs = Tp.ctx.sort(Tp.keys, elems)
+    got = [Tp.ctx.decrypt(Tp.keys, o)[0] for o in outs]
+    for j in range(ints):
+        assert [int(got[k][j]) for k in range(3)] == sorted(W[t][j] for t in range(3))
+    ev = circuits.OracleEval(P, Tp.okeys)
+    oo = circuits.sort_rank(ev, [Tp.oracle_ct(W[t], 600 + t) for t in range(3)], P.circuit, P.d, P.l, ints)
+    for k in range(3):
+        assert np.array_equal(to_u64(outs[k])[0], Tp.ct_eval(oo[k]))
