@@ -261,12 +261,21 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verify", type=int, default=1)
+    ap.add_argument("--workload", default=None, choices=[None, "compare", "tournament", "sort"],
+                    help="compare (default; C2), tournament (C4 min over T vectors), sort (C5 rank sort)")
+    ap.add_argument("--T", type=int, default=16, help="tournament / sort: number of elements")
+    ap.add_argument("--cts", type=int, default=0, help="ciphertexts per element (tournament: 5 -> 4096 words)")
+    ap.add_argument("--vec-chunk", type=int, default=0, help="max ct pairs per batched compare (0 = all)")
     args = ap.parse_args()
     cfg = load_json(os.path.join(ROOT, "params", args.config + ".json"))
     rank, world, local = dist_env()
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
+        return
+    workload = args.workload or {"c4": "tournament", "c5": "sort"}.get(args.config, "compare")
+    if workload in ("tournament", "sort"):
+        run_vector_workload(args, cfg, rank, world, local, workload)
         return
 
     import torch
@@ -324,6 +333,8 @@ def main():
                 sys.exit(3)
     barrier()
     bc.launch_count(reset=True)
+    bc.ntt_timing(True)
+    bc.ntt_timing()                      # drop anything recorded before the timed region
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -335,7 +346,10 @@ def main():
         torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
+    live = bc.ntt_timing()
+    bc.ntt_timing(False)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, world, dev)
     total_pairs = B * world
     value = total_pairs * ints / (ms / 1000.0)
     clocks = clk.summary()
@@ -362,7 +376,7 @@ def main():
                "h2d_bytes_per_step": int(ha.numel() * 8 + hb.numel() * 8),
                "d2h_bytes_per_step": int(ho.numel() * 8), "ms_per_step": ms2}
 
-    roof = roofline(ctx, keys, bc, torch, cfg)
+    roof = roofline(ctx, bc, live, ms_local * args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         t_mul, count, reps, cores = oracle_sample(cfg)
@@ -388,14 +402,150 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(ctx, keys, bc, torch, cfg):
-    """Dominant kernel (Bluestein NTT passes, integer-pipe bound): algorithmic 64-bit modular
-    multiplications per launch / measured duration vs the IMAD-derived peak."""
+def run_vector_workload(args, cfg, rank, world, local, workload):
+    """C4: slot-wise min over T encrypted vectors of 4096 32-bit words (T x 4096 = 2^16 words at T = 16),
+    R20 fixed tree; elements sharded contiguously over ranks, cross-rank rounds via NCCL send/recv
+    (paper_2407_07308_b200/dist.py) -> strong scaling (total work fixed).
+    C5: R21 rank sort of T = 16 encrypted elements per GPU (one ciphertext each: ints_per_ct
+    independent groups of 16 words) -> weak scaling, no collective."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2407_07308_b200 as bc
+    from paper_2407_07308_b200 import dist as bdist
+    ctx = bc.Context(cfg, device=local)
+    keys = ctx.keygen(SEED_KEYS)
+    ints = ctx.ints_per_ct
+    T = args.T
+    if args.vec_chunk:
+        bc._lib.bc_tune(b"vec_chunk", args.vec_chunk)
+    cap = min(ctx.base ** (ctx.d * ctx.l), 2 ** 64)
+    if workload == "tournament":
+        V = args.cts or 5
+        words_per_vec = min(4096, V * ints)
+        lo, hi = bdist.shard(T, world, rank)
+        rng = np.random.default_rng(SEED_INPUT)            # every rank regenerates all vectors (verify on rank 0)
+        W = rng.integers(0, cap, size=(T, V * ints), dtype=np.uint64)
+        W[:, words_per_vec:] = 0
+        mine = list(range(lo, hi))
+    else:
+        V = args.cts or 1
+        rng = np.random.default_rng(SEED_INPUT + rank)
+        W = rng.integers(0, cap, size=(T, V * ints), dtype=np.uint64)
+        W[:, ::7] = W[0, ::7]                              # ties (stable by index)
+        mine = list(range(T))
+    elems = [ctx.encrypt(keys, W[t].reshape(V, ints), SEED_ENC,
+                         ct_index0=(t if workload == "tournament" else rank * T + t) * V) for t in mine]
+    levels = [ctx.n_cipher] * len(elems)
+    op = "min" if workload == "tournament" else "sort"
+    need = ctx.vec_workspace_bytes(op, levels, V) if len(elems) > 1 else 0
+    if workload == "tournament":
+        need = max(need, ctx.workspace_bytes(V))
+    free, _ = torch.cuda.mem_get_info(dev)
+    if need > free - (1 << 30):
+        raise SystemExit("workspace %.1f GB > free %.1f GB: use --vec-chunk" % (need / 1e9, free / 1e9))
+    ctx.workspace(need)
+    ops = bdist.ProductOps(ctx, keys)
+
+    def step():
+        if workload == "tournament":
+            return bdist.tournament(ops, elems, "min")
+        return ctx.sort(keys, elems)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    verified = None
+    for w in range(args.warmup):
+        r = step()
+        if w == 0 and args.verify:
+            torch.cuda.synchronize()
+            if workload == "tournament":
+                if rank == 0:
+                    got = ctx.decrypt(keys, r).reshape(-1)
+                    verified = bool(np.array_equal(got, W.min(axis=0)))
+            else:
+                got = np.stack([ctx.decrypt(keys, o).reshape(-1) for o in r])
+                verified = bool(np.array_equal(got, np.sort(W, axis=0)))
+            if verified is False:
+                print("VERIFY FAILED", file=sys.stderr)
+                sys.exit(3)
+    barrier()
+    bc.launch_count(reset=True)
+    bc.ntt_timing(True)
+    bc.ntt_timing()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    launches = bc.launch_count(reset=True)
+    live = bc.ntt_timing()
+    bc.ntt_timing(False)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, world, dev)
+    if workload == "tournament":
+        words = T * words_per_vec
+        line = {"metric": "encrypted min over %d 32-bit words (R20 tournament, %d vectors)" % (words, T),
+                "value": words / (ms / 1e3), "unit": "words/s", "scaling": "strong",
+                "ms_per_tournament": ms}
+    else:
+        words = world * T * V * ints
+        line = {"metric": "encrypted rank sort of groups of %d 32-bit words (R21)" % T,
+                "value": words / (ms / 1e3), "unit": "words sorted/s", "scaling": "weak",
+                "ms_per_sort": ms, "groups_per_gpu": V * ints}
+    if rank == 0:
+        line.update({"n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                     "higher_is_better": True, "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                     "config": {"workload": args.config + " " + workload, "params": args.config, "T": T,
+                                "cts_per_element": V, "ints_per_ct": ints, "n_cipher": ctx.n_cipher,
+                                "n_special": ctx.n_special, "alpha": cfg["alpha"], "vec_chunk": args.vec_chunk,
+                                "l2": "inputs larger than L2"},
+                     "verified": verified, "gpu_launches": launches, "clocks": clk.summary(),
+                     "roofline": roofline(ctx, bc, live, ms_local * args.steps), "e2e": None,
+                     "cpu_baseline": None})
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def roofline(ctx, bc, live, step_ms_total):
+    """Dominant kernel family (Bluestein NTT passes, integer-pipe bound), measured LIVE in the timed
+    region: CUDA event pairs around every NTT call on the launching stream (bc_ntt_timing).
+    achieved = limb-transforms x algorithmic 64-bit modular multiplications per limb-transform
+     / summed NTT time; peak = IMAD-derived mulmod rate at the max SM clock."""
+    ms, jobs, calls = live
+    if not calls or ms <= 0:
+        return {"bound": "alu", "error": "no NTT calls timed"}
+    work = bc.ntt_work(ctx)
+    achieved = jobs * work / (ms / 1e3) / 1e12
+    peak = bc.SMS * bc.IMAD_PER_SM_PER_CLK * 1965.0e6 / bc.IMAD_PER_MULMOD / 1e12
+    traffic = None
     try:
-        prof = bc.profile_ntt(ctx)
-    except Exception as e:  # pragma: no cover
-        return {"bound": "alu", "error": str(e)}
-    return prof
+        prof = load_json(os.path.join(ROOT, "profiles", "ntt_traffic.json"))
+        if prof.get("n") == ctx.n:
+            traffic = prof["dram_bytes_per_limb_transform"] * jobs / calls
+    except Exception:
+        traffic = None
+    return {"bound": "alu", "kernel": "bluestein_ntt (passA+passB+passC [+reduce]) per ntt_forward/ntt_inverse call",
+            "achieved": achieved, "peak": peak, "unit": "T mulmod64/s", "frac": achieved / peak,
+            "traffic": traffic, "per_launch_ms": ms / calls, "limb_transforms_per_launch": jobs / calls,
+            "work_per_limb_transform": work, "launches_timed": calls, "share_of_step": ms / step_ms_total,
+            "how": "CUDA events on the launching stream around every NTT call inside the timed region",
+            "traffic_note": "ncu --set full dram__bytes_read+write per limb-transform (profiles/ntt_traffic.json) x "
+                            "limb-transforms per call",
+            "peak_note": "148 SM x 64 IMAD/clk x 1965 MHz / %d IMAD per 64-bit Shoup mulmod (guide unit counts)"
+                         % bc.IMAD_PER_MULMOD}
 
 
 if __name__ == "__main__":

@@ -214,9 +214,15 @@ bc_status bc_compact(bc_ctx *ctx, const bc_keys *keys, bc_ct in, const uint8_t *
  * (R, C) shape is supported), 1 = radix-2 shared-memory passes (reference kernels for
  * tests), 2 = register-blocked passes with 16 registers per thread */
 void bc_set_ntt_impl(int impl);
-/* tuning knobs (benchmarks / tests): "ntt_group_bytes" = transform scratch per launch group
+/* tuning knobs (benchmarks / tests): "ntt_timing" (0/1, see bc_ntt_timing),
+ * "vec_chunk" = max ciphertext pairs per batched compare inside bc_min_tree/bc_max_tree/bc_sort
+ * (0 = one batch per round; bounds the workspace, never changes bits), "ntt_group_bytes" = transform scratch per launch group
  * (default: the whole batch in one group; smaller groups measured slower on B200). Returns 0 if known. */
 int bc_tune(const char *key, int64_t value);
+/* live NTT timing: after bc_tune("ntt_timing", 1) every forward/inverse Bluestein NTT call records
+ * a CUDA event pair on its stream.  bc_ntt_timing synchronises those events and returns (then
+ * clears) the summed duration in ms, the number of limb-transforms and of calls.  0 on success. */
+int bc_ntt_timing(double *ms, uint64_t *limb_transforms, uint64_t *calls);
 /* number of CUDA kernel launches issued by this thread since the last reset */
 uint64_t bc_launch_count(int reset);
 const char *bc_last_error(void);

@@ -90,6 +90,7 @@ _sig("bc_rotate", _st, _vp, _vp, bc_ct, ctypes.c_int32, bc_ct, _vp, _sz, _vp)
 _sig("bc_frobenius", _st, _vp, _vp, bc_ct, _u32, bc_ct, _vp, _sz, _vp)
 _sig("bc_extract", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
 _sig("bc_launch_count", _u64, ctypes.c_int)
+_sig("bc_ntt_timing", ctypes.c_int, _vp, _vp, _vp)
 _sig("bc_set_ntt_impl", None, ctypes.c_int)
 _sig("bc_tune", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64)
 _sig("bc_last_error", ctypes.c_char_p)
@@ -120,6 +121,17 @@ def _check(status, what):
 def set_ntt_impl(impl):
     """0 = register-blocked NTT passes (default), 1 = radix-2 reference passes."""
     _lib.bc_set_ntt_impl(int(impl))
+
+
+def ntt_timing(enable=None):
+    """enable/disable live NTT event timing; with enable=None collect -> (ms, limb_transforms, calls)."""
+    if enable is not None:
+        _lib.bc_tune(b"ntt_timing", 1 if enable else 0)
+        return None
+    ms, j, c = ctypes.c_double(0), ctypes.c_uint64(0), ctypes.c_uint64(0)
+    if _lib.bc_ntt_timing(ctypes.byref(ms), ctypes.byref(j), ctypes.byref(c)) != 0:
+        raise BoostComError("bc_ntt_timing failed")
+    return ms.value, j.value, c.value
 
 
 def launch_count(reset=False):

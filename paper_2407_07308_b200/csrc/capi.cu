@@ -32,8 +32,13 @@ const char *bc_last_error(void) { return last_error().c_str(); }
 void bc_set_ntt_impl(int impl) { g_ntt_impl = impl; }
 int bc_tune(const char *key, int64_t value) {
     if (!key) return -1;
+    if (!strcmp(key, "vec_chunk")) { g_vec_chunk = (uint64_t)std::max<int64_t>(value, 0); return 0; }
+    if (!strcmp(key, "ntt_timing")) { g_ntt_timing = value ? 1 : 0; return 0; }
     if (!strcmp(key, "ntt_group_bytes")) { g_ntt_group_bytes = (uint64_t)std::max<int64_t>(value, 1 << 20); return 0; }
     return -1;
+}
+int bc_ntt_timing(double *ms, uint64_t *limb_transforms, uint64_t *calls) {
+    return ntt_timing_collect(ms, limb_transforms, calls);
 }
 uint64_t bc_launch_count(int reset) {
     uint64_t c = launch_counter();

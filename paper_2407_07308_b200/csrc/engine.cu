@@ -1026,13 +1026,18 @@ CT tournament_batch(Eng &E, std::vector<CT> cur, bool is_max) {
         std::map<std::pair<uint32_t, uint32_t>, std::vector<uint32_t>> groups;
         for (uint32_t i = 0; i + sh < T; i += 2 * sh) groups[{cur[i].lvl, cur[i + sh].lvl}].push_back(i);
         for (auto &g : groups) {
-            std::vector<CT> as, bs;
-            for (uint32_t i : g.second) { as.push_back(cur[i]); bs.push_back(cur[i + sh]); }
-            CT A = concat_batch(E, as), Bv = concat_batch(E, bs);
-            CT lt;
-            compare_batch(E, A, Bv, &lt, nullptr);
-            CT r = is_max ? select_batch(E, lt, Bv, A) : select_batch(E, lt, A, Bv);
-            for (size_t k = 0; k < g.second.size(); ++k) cur[g.second[k]] = E.sub(r, (uint32_t)k * B, B);
+            // sub-groups of at most g_vec_chunk ciphertext pairs bound the workspace
+            const size_t per = g_vec_chunk ? std::max<size_t>(1, g_vec_chunk / B) : g.second.size();
+            for (size_t k0 = 0; k0 < g.second.size(); k0 += per) {
+                const size_t k1 = std::min(g.second.size(), k0 + per);
+                std::vector<CT> as, bs;
+                for (size_t k = k0; k < k1; ++k) { as.push_back(cur[g.second[k]]); bs.push_back(cur[g.second[k] + sh]); }
+                CT A = concat_batch(E, as), Bv = concat_batch(E, bs);
+                CT lt;
+                compare_batch(E, A, Bv, &lt, nullptr);
+                CT r = is_max ? select_batch(E, lt, Bv, A) : select_batch(E, lt, A, Bv);
+                for (size_t k = k0; k < k1; ++k) cur[g.second[k]] = E.sub(r, (uint32_t)(k - k0) * B, B);
+            }
         }
     }
     return cur[0];
@@ -1057,22 +1062,29 @@ std::vector<CT> sort_batch(Eng &E, const std::vector<CT> &x) {
     int np = 0;
     for (uint32_t i = 0; i < T; ++i)
         for (uint32_t j = i + 1; j < T; ++j) { as.push_back(x[i]); bs.push_back(x[j]); pidx[i][j] = np++; }
-    CT lt, eq;
-    compare_batch(E, concat_batch(E, as), concat_batch(E, bs), &lt, &eq);
+    // le for every pair, compared in chunks of at most g_vec_chunk ciphertext pairs
+    const int per = g_vec_chunk ? std::max<int>(1, (int)(g_vec_chunk / B)) : np;
+    std::vector<CT> lec;
+    for (int k0 = 0; k0 < np; k0 += per) {
+        const int k1 = std::min(np, k0 + per);
+        std::vector<CT> ca(as.begin() + k0, as.begin() + k1), cb(bs.begin() + k0, bs.begin() + k1);
+        CT lt, eq;
+        compare_batch(E, concat_batch(E, ca), concat_batch(E, cb), &lt, &eq);
+        lec.push_back(E.add(lt, eq));
+    }
     as.clear(); bs.clear();
-    CT le = E.add(lt, eq);
-    lt = CT(); eq = CT();
+    auto le_of = [&](int k) { return E.sub(lec[k / per], (uint32_t)(k % per) * B, B); };
     std::vector<CT> S(T);
     for (uint32_t j = 0; j < T; ++j) {
         bool have = false;
         for (uint32_t i = 0; i < T; ++i) {
             if (i == j) continue;
-            CT t = i < j ? E.sub(le, (uint32_t)pidx[i][j] * B, B) : E.scalar(E.sub(le, (uint32_t)pidx[j][i] * B, B), -1);
+            CT t = i < j ? le_of(pidx[i][j]) : E.scalar(le_of(pidx[j][i]), -1);
             S[j] = have ? E.add(S[j], t) : t;
             have = true;
         }
     }
-    le = CT();
+    lec.clear();
     const uint32_t lS = S[0].lvl;
     CT V = E.ct_alloc(T * T * B, lS, 2);
     for (uint32_t j = 0; j < T; ++j)

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "kernels.h"
 
@@ -24,6 +25,52 @@ uint64_t &launch_counter() {
     return c;
 }
 #define LAUNCHED() (++launch_counter())
+
+// live timing of the NTT family (bench roofline): an event pair around every ntt_forward /
+// ntt_inverse call on the caller's stream, with the number of limb-transforms it ran
+int g_ntt_timing = 0;
+uint64_t g_vec_chunk = 0;   // max ciphertext pairs per batched compare in tournament / sort (0 = all)
+struct NttRec {
+    cudaEvent_t a, b;
+    uint64_t jobs;
+};
+static std::vector<NttRec> &ntt_recs() {
+    static std::vector<NttRec> r;
+    return r;
+}
+static std::vector<cudaEvent_t> &ev_pool() {
+    static std::vector<cudaEvent_t> p;
+    return p;
+}
+static cudaEvent_t ev_get() {
+    auto &p = ev_pool();
+    if (!p.empty()) {
+        cudaEvent_t e = p.back();
+        p.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls) {
+    double t = 0;
+    uint64_t j = 0, c = 0;
+    for (auto &r : ntt_recs()) {
+        float x = 0;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&x, r.a, r.b) != cudaSuccess) return -1;
+        t += x;
+        j += r.jobs;
+        ++c;
+        ev_pool().push_back(r.a);
+        ev_pool().push_back(r.b);
+    }
+    ntt_recs().clear();
+    if (ms) *ms = t;
+    if (jobs) *jobs = j;
+    if (calls) *calls = c;
+    return 0;
+}
 
 static inline unsigned grid_for(uint64_t total, unsigned threads, unsigned cap = 148u * 32u) {
     uint64_t g = (total + threads - 1) / threads;
@@ -305,13 +352,25 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     }
 }
 
+static void ntt_timed(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                      uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st, int inv) {
+    if (!g_ntt_timing) {
+        ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
+        return;
+    }
+    NttRec r{ev_get(), ev_get(), (uint64_t)npoly * lm.njl};
+    cudaEventRecord(r.a, st);
+    ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
+    cudaEventRecord(r.b, st);
+    ntt_recs().push_back(r);
+}
 void ntt_forward(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                  uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st) {
-    ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 0);
+    ntt_timed(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 0);
 }
 void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                  uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st) {
-    ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 1);
+    ntt_timed(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 1);
 }
 
 // =====================================================================================

@@ -131,6 +131,9 @@ bool ntt2_supported(const NttTables &T);
 void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
 extern uint64_t g_ntt_group_bytes;   // scratch bytes per transform launch group (L2 residency)
+extern uint64_t g_vec_chunk;
+extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)
+int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);
 extern int g_ntt_impl;   // 0 = register passes (E=8) when supported, 1 = radix-2 passes, 2 = register passes E=16
 
 }  // namespace bc
