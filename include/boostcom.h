@@ -186,7 +186,7 @@ bc_status bc_keyswitch(bc_ctx *ctx, const bc_keys *keys, const void *d_poly, uin
                        void *stream);
 /* a6: modulus switch of a 2-part batch from level to level-1 */
 bc_status bc_modswitch(bc_ctx *ctx, bc_ct a, bc_ct out, void *d_ws, size_t ws_bytes, void *stream);
-/* a3+a5+a6: out = modswitch(relin(tensor(a, b))) */
+/* a3+a5+a6: out = R15 fused product: tensor, ModUp + KIP of d2, one scale-down by P q_{level-1} */
 bc_status bc_mul(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out, void *d_ws,
                  size_t ws_bytes, void *stream);
 /* a4+a5: rotation (slot s receives slot s+k) and Frobenius sigma_{p^k} */

@@ -277,10 +277,10 @@ def modswitch_to(P, ct, level):
     return ct
 
 
-def keyswitch(P, K, d, level, key_id):
-    """R14 (hybrid): ModUp -- for each digit j the exact centered lift of d restricted to G_j;
-    KIP -- (u0, u1) = sum_j x_j (b_j, a_j) over the level's cipher limbs and all special limbs;
-    ModDown -- r = [u]_P, delta = r + P [-r]_p, u' = (u - delta) P^{-1}."""
+def keyswitch_up(P, K, d, level, key_id):
+    """R14 ModUp + key inner product: for each digit j the exact centered lift of d restricted to
+    G_j, embedded in every target limb; (u0, u1) = sum_j x_j (b_j, a_j) over the level's cipher
+    limbs and all special limbs (rows: cipher 0..level-1, then special)."""
     key = K.ksk[key_id]
     tgt = list(range(level)) + P.special
     u0 = np.zeros((len(tgt), P.n), dtype=np.uint64)
@@ -296,6 +296,13 @@ def keyswitch(P, K, d, level, key_id):
         ka = a[tgt]
         u0 = _add(u0, _mul(xr, kb, P, tgt), P, tgt)
         u1 = _add(u1, _mul(xr, ka, P, tgt), P, tgt)
+    return u0, u1
+
+
+def keyswitch(P, K, d, level, key_id):
+    """R14 (hybrid): ModUp and KIP (keyswitch_up), then ModDown -- r = [u]_P,
+    delta = r + P [-r]_p, u' = (u - delta) P^{-1}."""
+    u0, u1 = keyswitch_up(P, K, d, level, key_id)
     Pprod = 1
     for q in P.P:
         Pprod *= q
@@ -387,10 +394,38 @@ def relinearize(P, K, ct):
     return Ciphertext([_add(d0, u0, P, idx), _add(d1, u1, P, idx)], ct.level)
 
 
-def mul(P, K, a, b):
-    """R15: mul = align -> tensor -> relinearise -> modswitch."""
+def mul_unfused(P, K, a, b):
+    """align -> tensor -> relinearise (ModDown by P) -> modswitch (by q_{l-1}): the two-step
+    definition; decrypts like mul() (a test pin), different rounding bits."""
     a, b = align(P, a, b)
     return modswitch(P, relinearize(P, K, tensor(P, a, b)))
+
+
+def mul(P, K, a, b):
+    """R15 (fused ModDown + modulus switch): align -> tensor (d0, d1, d2) -> ModUp + KIP of d2 ->
+    w_k = P d_k + u_k (k = 0, 1) over the cipher limbs of the level and the special limbs ->
+    one scale-down by D = P q_{l-1}: r = [w]_D (exact centered CRT over the special primes and
+    q_{l-1}), delta = r + D [-r]_p, w'_i = (w_i - delta) D^{-1} mod q_i for i < l-1 (R13/R14 with
+    Qdrop = D; D = 1 mod p keeps the plaintext)."""
+    a, b = align(P, a, b)
+    lv = a.level
+    assert lv >= 2, "OutOfLevels"
+    d0, d1, d2 = tensor(P, a, b).parts
+    u0, u1 = keyswitch_up(P, K, d2, lv, 0)
+    Pprod = 1
+    for q in P.P:
+        Pprod *= q
+    D = Pprod * P.moduli[lv - 1]
+    cidx = list(range(lv))
+    drop_rows = list(range(lv, lv + P.K)) + [lv - 1]
+    drop_idx = P.special + [lv - 1]
+    parts = []
+    for dk, u in ((d0, u0), (d1, u1)):
+        w = u.copy()
+        w[:lv] = _add(_scal(dk, Pprod, P, cidx), u[:lv], P, cidx)
+        r, _ = lift_centered(P, w[drop_rows], drop_idx)
+        parts.append(_scale_down(P, w[:lv - 1], list(range(lv - 1)), None, r, D))
+    return Ciphertext(parts, lv - 1)
 
 
 def automorphism(P, K, ct, t):

@@ -428,6 +428,10 @@ void ctx_build(bc_ctx *X) {
             for (uint32_t i = 0; i + 1 < lv; ++i) tgt.push_back(i);
             tgt.push_back(-1);
             add_plan("ms:" + std::to_string(lv), {lv - 1}, tgt);
+            // fused ModDown + modulus switch of a product (R15): sources q_{lv-1}, P_0 .. P_{K-1}
+            std::vector<uint32_t> src{lv - 1};
+            for (uint32_t k = 0; k < X->K; ++k) src.push_back(X->L1 + k);
+            add_plan("fd:" + std::to_string(lv), src, tgt);
         }
         {
             std::vector<uint32_t> src;
@@ -449,8 +453,22 @@ void ctx_build(bc_ctx *X) {
                 uint64_t q = X->moduli[i];
                 iq[(size_t)lv * X->L1 + i] = sh2(invmod_h(X->moduli[lv - 1] % q, q), q);
             }
+        // fused ModDown + modswitch: P mod q_i and (P q_{lv-1})^{-1} mod q_i (row lv)
+        std::vector<u64x2> pm(X->L1), iD((size_t)(X->L1 + 1) * X->L1, u64x2{0, 0});
+        for (uint32_t i = 0; i < X->L1; ++i) {
+            uint64_t q = X->moduli[i], P = 1;
+            for (uint32_t k = 0; k < X->K; ++k) P = mulmod_h(P, X->moduli[X->L1 + k] % q, q);
+            pm[i] = sh2(P, q);
+        }
+        for (uint32_t lv = 2; lv <= X->L1; ++lv)
+            for (uint32_t i = 0; i + 1 < lv; ++i) {
+                const uint64_t q = X->moduli[i];
+                iD[(size_t)lv * X->L1 + i] = sh2(mulmod_h(ip[i].w, iq[(size_t)lv * X->L1 + i].w, q), q);
+            }
         X->d_invP = dev_upload(X, ip);
         X->d_invq = dev_upload(X, iq);
+        X->d_Pm = dev_upload(X, pm);
+        X->d_invD = dev_upload(X, iD);
     }
     // ---------------- encode / decode matrices ----------------
     {
@@ -657,8 +675,8 @@ CT Eng::add_pt(const CT &a, const uint64_t *pt) {
     return o;
 }
 
-// R14 hybrid key switching: ModUp (exact lift per digit + NTT), KIP, ModDown.
-CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
+// R14 hybrid key switching: ModUp (exact lift per digit + NTT) and KIP -> u [B][2][lvl+K][n] (eval)
+BufP Eng::ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
     const uint64_t *kptr = nullptr;
     if (keys) {
         auto kit = keys->ksk.find(key_id);
@@ -685,8 +703,12 @@ CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uin
     }
     BufP u = alloc_words((uint64_t)B * 2 * nl * n);
     if (!dry()) ks_kip(X->d_mods, d, dps, E, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig, n, st);
-    dc.reset();
-    ext.reset();
+    return u;
+}
+
+CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
+    const uint32_t n = X->n, K = X->K, L1 = X->L1, nl = lvl + K;
+    BufP u = ks_up(d, dps, B, lvl, key_id);
     // ModDown of both parts: 2B polys with stride nl*n
     BufP sp = alloc_words((uint64_t)2 * B * K * n);
     ntt_inv((uint64_t *)u->p + (uint64_t)lvl * n, (uint64_t *)sp->p, 2 * B, LimbMap{K, K, 0, 0, 0, L1}, (uint64_t)nl * n,
@@ -703,19 +725,39 @@ CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uin
     return o;
 }
 
+// R15 fused: tensor -> ModUp + KIP of d2 -> w_k = P d_k + u_k -> one scale-down by D = P q_{lv-1}
+// (INTT of the K special limbs and limb lv-1, exact lift r = [w]_D, delta = r + D [-r]_p, NTT of
+// delta into the lv-1 remaining limbs, w' = (w - delta) D^{-1}).
 CT Eng::mul(const CT &a0, const CT &b0) {
     const uint32_t lv = std::min(a0.lvl, b0.lvl);
+    if (lv < 2) BC_THROW(BC_E_LEVEL, "mul: out of levels");
     CT a = modswitch_to(a0, lv), b = modswitch_to(b0, lv);
-    const uint32_t n = X->n, B = a.B;
+    const uint32_t n = X->n, B = a.B, K = X->K, L1 = X->L1, nl = lv + K;
     if (a.bstride != (uint64_t)2 * lv * n || b.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "mul: strided");
     const uint64_t tw = (uint64_t)3 * lv * n;
     BufP t = alloc_words((uint64_t)B * tw);
     if (!dry()) ew_tensor(X->d_mods, a.d, b.d, (uint64_t *)t->p, B, lv, n, st);
-    // relinearise d2 (part 2 of each 3-part product, read in place) and add (d0, d1)
-    CT u = keyswitch((uint64_t *)t->p + (uint64_t)2 * lv * n, tw, B, lv, 0);
-    if (!dry()) ew_add_bs(X->d_mods, u.d, u.bstride, (uint64_t *)t->p, tw, u.d, u.bstride, B, 2, lv, n, st);
-    t.reset();
-    return modswitch(u);
+    BufP u = ks_up((uint64_t *)t->p + (uint64_t)2 * lv * n, tw, B, lv, 0);
+    const uint64_t ups = (uint64_t)nl * n;
+    uint64_t *U = (uint64_t *)u->p, *Tt = (uint64_t *)t->p;
+    // limb lv-1 of w must be complete before its INTT
+    if (!dry()) ew_fused_down(X->d_mods, U, ups, Tt, tw, (uint64_t)lv * n, nullptr, X->d_Pm, nullptr, nullptr, B, lv, n, st);
+    // INTT of rows lv-1 .. lv+K-1 (q_{lv-1}, P_0 .. P_{K-1}) of both parts
+    BufP sp = alloc_words((uint64_t)2 * B * (K + 1) * n);
+    ntt_inv(U + (uint64_t)(lv - 1) * n, (uint64_t *)sp->p, 2 * B, LimbMap{K + 1, K + 1, 0, 1, lv - 1, L1}, ups,
+            (uint64_t)(K + 1) * n);
+    BufP delta = alloc_words((uint64_t)2 * B * (lv - 1) * n);
+    if (!dry())
+        lift(X->plan("fd:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)(K + 1) * n,
+             (uint64_t *)delta->p, (uint64_t)(lv - 1) * n, nullptr, 2 * B, n, 0, 0, 1, st);
+    sp.reset();
+    ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
+            (uint64_t)(lv - 1) * n);
+    CT o = ct_alloc(B, lv - 1, 2);
+    if (!dry())
+        ew_fused_down_out(X->d_mods, U, ups, Tt, tw, (uint64_t)lv * n, (uint64_t *)delta->p, X->d_Pm,
+                          X->d_invD + (size_t)lv * L1, o.d, B, lv - 1, n, st);
+    return o;
 }
 
 CT Eng::automorph(const CT &a, uint32_t t) {

@@ -73,6 +73,8 @@ struct bc_ctx {
     std::map<std::string, size_t> plan_off;
     bc::u64x2 *d_invP = nullptr;                // [L1] P^{-1} mod q_i
     bc::u64x2 *d_invq = nullptr;                // [L1+1][L1] q_{l-1}^{-1} mod q_i (row l)
+    bc::u64x2 *d_Pm = nullptr;                  // [L1] P mod q_i
+    bc::u64x2 *d_invD = nullptr;                // [L1+1][L1] (P q_{l-1})^{-1} mod q_i (row l)
     int8_t *d_Em = nullptr, *d_Dm = nullptr;    // encode / decode matrices (n x n)
     int16_t *d_E0 = nullptr, *d_zpow = nullptr;
     uint32_t *d_ts = nullptr;
@@ -126,6 +128,7 @@ struct Eng {
     CT add_pt(const CT &a, const uint64_t *pt);
     // key switch of polys d (ct b at d + b*dps, lvl limbs, eval) -> [B][2][lvl][n]
     CT keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);
+    BufP ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);  // ModUp + KIP
     CT mul(const CT &a, const CT &b);
     CT automorph(const CT &a, uint32_t t);
     CT rotate(const CT &a, int64_t k);

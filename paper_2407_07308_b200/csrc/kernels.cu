@@ -628,6 +628,56 @@ void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const 
     LAUNCHED();
 }
 
+// fused ModDown + modulus switch (R15): u[b][k][i] += Pm_i d_k[i] on limb `limb` only (before its INTT)
+__global__ void k_axpy_limb(const Mod *__restrict__ mods, uint64_t *__restrict__ u, uint64_t u_pstride,
+                            const uint64_t *__restrict__ d, uint64_t d_bstride, uint64_t d_kstride,
+                            const u64x2 *__restrict__ pm, uint32_t limb, uint64_t total, uint32_t n) {
+    const uint64_t q = mods[limb].q;
+    const u64x2 w = pm[limb];
+    GRID_LOOP(i, total) {
+        const uint64_t poly = i / n, x = i - poly * n;      // poly = b * 2 + k
+        const uint64_t b = poly >> 1, k = poly & 1;
+        uint64_t *pu = u + poly * u_pstride + (uint64_t)limb * n + x;
+        const uint64_t dv = d[b * d_bstride + k * d_kstride + (uint64_t)limb * n + x];
+        *pu = add_mod(*pu, mul_shoup(dv, w.w, w.ws, q), q);
+    }
+}
+// out[b][k][i] = (u[b][k][i] + Pm_i d_k[i] - delta[b][k][i]) Dinv_i, i < lvl (= level - 1)
+__global__ void k_fused_down(const Mod *__restrict__ mods, const uint64_t *__restrict__ u, uint64_t u_pstride,
+                             const uint64_t *__restrict__ d, uint64_t d_bstride, uint64_t d_kstride,
+                             const uint64_t *__restrict__ delta, const u64x2 *__restrict__ pm,
+                             const u64x2 *__restrict__ dinv, uint64_t *__restrict__ o, uint64_t total, uint32_t lvl,
+                             uint32_t n) {
+    const uint64_t ln = (uint64_t)lvl * n;
+    GRID_LOOP(i, total) {
+        const uint64_t poly = i / ln, rr = i - poly * ln;
+        const uint32_t limb = (uint32_t)(rr / n);
+        const uint64_t b = poly >> 1, k = poly & 1;
+        const uint64_t q = mods[limb].q;
+        const u64x2 w = pm[limb], v = dinv[limb];
+        const uint64_t dv = d[b * d_bstride + k * d_kstride + rr];
+        uint64_t x = add_mod(u[poly * u_pstride + rr], mul_shoup(dv, w.w, w.ws, q), q);
+        x = sub_mod(x, delta[i], q);
+        o[i] = mul_shoup(x, v.w, v.ws, q);
+    }
+}
+void ew_fused_down(const Mod *mods, uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
+                   uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
+                   uint32_t B, uint32_t level, uint32_t n, cudaStream_t st) {
+    const uint64_t t1 = (uint64_t)2 * B * n;
+    k_axpy_limb<<<grid_for(t1, 256), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, pm, level - 1, t1, n);
+    LAUNCHED();
+    (void)delta; (void)dinv; (void)o;
+}
+void ew_fused_down_out(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
+                       uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
+                       uint32_t B, uint32_t lvl_out, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)2 * B * lvl_out * n;
+    k_fused_down<<<grid_for(total, 256), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, delta, pm, dinv,
+                                                       o, total, lvl_out, n);
+    LAUNCHED();
+}
+
 // =====================================================================================
 // exact centered CRT lift (Garner mixed radix + lexicographic sign test)
 // plan blob (u64 words): [0]=ns [1]=nt, then

@@ -47,6 +47,16 @@ void ntt_forward(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t
 void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                  uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st);
 
+// ---- fused ModDown + modulus switch of a product (R15) ----
+// step 1: u[b][k][level-1] += (P mod q) d_k[level-1]   (u: [B][2] polys of stride u_pstride)
+void ew_fused_down(const Mod *mods, uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
+                   uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
+                   uint32_t B, uint32_t level, uint32_t n, cudaStream_t st);
+// step 2: o[b][k][i] = (u + Pm d_k - delta) Dinv for i < lvl_out  (o, delta: [B][2][lvl_out][n])
+void ew_fused_down_out(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
+                       uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
+                       uint32_t B, uint32_t lvl_out, uint32_t n, cudaStream_t st);
+
 // ---- element-wise over [B][parts][level][n] (limb i uses prime i) ----
 void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B,
             uint32_t parts, uint32_t lvl, uint32_t n, int sub, cudaStream_t st);

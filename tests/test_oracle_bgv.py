@@ -176,3 +176,23 @@ def test_sort_ciphertext(c1t):
     for j in range(ints):
         assert [got[k][j] for k in range(3)] == sorted(W[t][j] for t in range(3))
     assert [got[k][0] for k in range(3)] == [1, 2, 3]
+
+
+def test_fused_mul_decrypts_like_two_step(c1):
+    """R15 fused ModDown + modulus switch: same plaintext and level as relinearise -> modswitch
+    (the two-step definition), noise within 2 bits of it; a dropped P factor, a wrong delta sign or
+    a missing D^{-1} breaks one of these."""
+    P, K = c1
+    A = P.alg
+    rng = np.random.default_rng(5)
+    for idx in range(3):
+        b1 = rng.integers(0, P.p, size=(A.S, A.D))
+        b2 = rng.integers(0, P.p, size=(A.S, A.D))
+        c1_, c2_ = _enc_slots(P, K, b1, 20 + 2 * idx), _enc_slots(P, K, b2, 21 + 2 * idx)
+        f = bgv.mul(P, K, c1_, c2_)
+        u = bgv.mul_unfused(P, K, c1_, c2_)
+        assert f.level == u.level == c1_.level - 1
+        want = A.gf.mul(b1, b2)
+        assert np.array_equal(A.decode(bgv.decrypt(P, K, f)), want)
+        assert np.array_equal(A.decode(bgv.decrypt(P, K, u)), want)
+        assert bgv.noise_bits(P, K, f)[0] <= bgv.noise_bits(P, K, u)[0] + 2
