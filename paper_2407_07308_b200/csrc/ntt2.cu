@@ -34,28 +34,44 @@ __device__ __forceinline__ uint64_t shoup4(uint64_t x, uint64_t w, uint64_t wp, 
 //   DIF global stage g (g = LOGL-1-log h): inputs < B_g = 4q 2^g; x' = x + y < B_{g+1};
 //       y' = shoup4(x + B_g - y) < 4q.        (B_9 = 2^11 q < 2^62)
 //   DIT: y' = shoup4(y) < 4q; x' = x + y', y'' = x + 4q - y': bound grows by 4q per stage.
-template <int LOGE, int NS, bool DIF>
-__device__ __forceinline__ void reg_pass(uint64_t (&v)[1 << LOGE], int lo, uint32_t base_mod, const u64x2 *__restrict__ tw,
+// In the pass with lowest stage 2^0 (LO = 0) the twiddle index is a compile-time constant and
+// index 0 (omega^0 = 1) needs no product: DIF y' = x + B_g - y (< 2 B_g = B_{g+1}, the next
+// stage's bound); DIT y' = x + B_s - y with stage input bound B_s = 4q 2^s (this pass is the first
+// DIT pass, inputs < 4q; each of its stages at most doubles the bound: 2^NS * 4q <= 2^6 q).
+// That skips 15 of the 32 products of a 16-register pass (23% of a 256-point transform).
+template <int LOGE, int NS, bool DIF, int LO>
+__device__ __forceinline__ void reg_pass(uint64_t (&v)[1 << LOGE], uint32_t base_mod, const u64x2 *__restrict__ tw,
                                          int logL, uint64_t q) {
     constexpr int E = 1 << LOGE;
     const uint64_t q4 = 4 * q, nq = 0 - q;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
         const int u = DIF ? (NS - 1 - s) : s;
-        const int lh = lo + u;                       // log2 h
+        const int lh = LO + u;                       // log2 h
         const int tsh = logL - 1 - lh;               // twiddle omega_{2h}^{i mod h} = omega_L^{(i mod h) L/2h}
         const uint64_t Bg = q4 << tsh;               // DIF input bound at this stage (g = tsh)
+        const uint64_t Bs = q4 << s;                 // DIT input bound in the LO = 0 pass
 #pragma unroll
         for (int k = 0; k < E; ++k) {
             if (k & (1 << u)) continue;
             const int k2 = k + (1 << u);
-            const uint32_t imod = base_mod + ((uint32_t)(k & ((1 << u) - 1)) << lo);
-            const u64x2 w = tw[imod << tsh];
+            const uint32_t kpart = (uint32_t)(k & ((1 << u) - 1));
+            const bool trivial = LO == 0 && kpart == 0;
             if (DIF) {
                 const uint64_t x = v[k], y = v[k2];
                 v[k] = x + y;
-                v[k2] = shoup4(x + Bg - y, w.w, w.ws, nq);
+                if (trivial) {
+                    v[k2] = x + Bg - y;
+                } else {
+                    const u64x2 w = tw[(base_mod + (kpart << LO)) << tsh];
+                    v[k2] = shoup4(x + Bg - y, w.w, w.ws, nq);
+                }
+            } else if (trivial) {
+                const uint64_t x = v[k], y = v[k2];
+                v[k] = x + y;
+                v[k2] = x + Bs - y;
             } else {
+                const u64x2 w = tw[(base_mod + (kpart << LO)) << tsh];
                 const uint64_t x = v[k];
                 const uint64_t y = shoup4(v[k2], w.w, w.ws, nq);
                 v[k] = x + y;
@@ -112,7 +128,7 @@ __device__ __forceinline__ void rt_pass(uint64_t (&v)[1 << LOGE], uint32_t tau, 
         }
         __syncthreads();
     }
-    reg_pass<LOGE, ns, DIF>(v, lo, tau & ((1u << lo) - 1), tw, LOGL, q);
+    reg_pass<LOGE, ns, DIF, lo>(v, tau & ((1u << lo) - 1), tw, LOGL, q);
     if (P + 1 < PS::NP) rt_pass<LOGL, LOGE, DIF, (P + 1 < PS::NP ? P + 1 : P)>(v, tau, srow, tw, q);
 }
 
@@ -139,7 +155,7 @@ __device__ __forceinline__ void ct_pass(uint64_t (&v)[1 << LOGE], uint32_t tau, 
         for (int k = 0; k < E; ++k) v[k] = scol[held_index<LOGE>(tau, lo, k) * TC + col];
         __syncthreads();
     }
-    reg_pass<LOGE, ns, DIF>(v, lo, tau & ((1u << lo) - 1), tw, LOGL, q);
+    reg_pass<LOGE, ns, DIF, lo>(v, tau & ((1u << lo) - 1), tw, LOGL, q);
     if (P + 1 < PS::NP) ct_pass<LOGL, LOGE, DIF, TC, (P + 1 < PS::NP ? P + 1 : P)>(v, tau, col, scol, tw, q);
 }
 
@@ -196,10 +212,10 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), NTT_MINB(TC * (1 <<
         const uint32_t t = r * T.C + c;
         uint64_t x = 0;
         if (!INV) {
-            if (t < T.n) { const u64x2 w = tf[t]; x = shoup4(src[t], w.w, w.ws, 0 - q); }
+            if (t < T.n) { const u64x2 w = tf[t]; x = shoup4(__ldcs(src + t), w.w, w.ws, 0 - q); }
         } else if (t < T.m) {
             const int ps = T.pos[t];
-            if (ps >= 0) { const u64x2 w = tf[t]; x = shoup4(src[ps], w.w, w.ws, 0 - q); }
+            if (ps >= 0) { const u64x2 w = tf[t]; x = shoup4(__ldcs(src + ps), w.w, w.ws, 0 - q); }
         }
         v[k] = x;
     }
@@ -211,7 +227,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), NTT_MINB(TC * (1 <<
     for (int k = 0; k < E; ++k) {
         const uint32_t rp = held_index<LOGE>(tau, 0, k);
         const u64x2 w = xt[rp * T.C + c];
-        dst[rp * T.C + c] = shoup4(v[k], w.w, w.ws, 0 - q);     // [0, 4q)
+        __stcs(dst + rp * T.C + c, shoup4(v[k], w.w, w.ws, 0 - q));     // [0, 4q); streaming: keep tables in L2
     }
 }
 
@@ -236,7 +252,7 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), NTT_MINB(RB * (1 <<
     }
     uint64_t v[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) v[k] = grow[held_index<LOGE>(tau, LOGC - LOGE, k)];
+    for (int k = 0; k < E; ++k) v[k] = __ldcs(grow + held_index<LOGE>(tau, LOGC - LOGE, k));
     __syncthreads();
     row_transform<LOGC, LOGE, true>(v, tau, srow, tw, q);
     // contiguous positions tau*E + k: pointwise product with D^ (same pass layout)
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), NTT_MINB(RB * (1 <<
     for (int k = 0; k < E; ++k) {
         const uint32_t cc = held_index<LOGE>(tau, LOGC - LOGE, k);
         const u64x2 w = xt[cc];
-        grow[cc] = shoup4(v[k], w.w, w.ws, 0 - q);
+        __stcs(grow + cc, shoup4(v[k], w.w, w.ws, 0 - q));
     }
 }
 
@@ -273,7 +289,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), NTT_MINB(TC * (1 <<
     for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = T.twRi[(uint64_t)J.pr * (R / 2) + j];
     uint64_t v[E];
 #pragma unroll
-    for (int k = 0; k < E; ++k) v[k] = scr[held_index<LOGE>(tau, 0, k) * T.C + c];
+    for (int k = 0; k < E; ++k) v[k] = __ldcs(scr + held_index<LOGE>(tau, 0, k) * T.C + c);
     __syncthreads();
     col_transform<LOGR, LOGE, false, TC>(v, tau, col, sm2, stw, q);
     const u64x2 *tfo = (INV ? T.tfoi : T.tfo) + (uint64_t)J.pr * T.m;
@@ -288,7 +304,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), NTT_MINB(TC * (1 <<
         const uint64_t x = mul_shoup(v[k], w.w, w.ws, q);      // canonical [0, q)
         if (!INV) {
             const int ps = T.pos[t];
-            if (ps >= 0) dst[ps] = x;
+            if (ps >= 0) __stcs(dst + ps, x);
         } else {
             scr[t] = x;
         }
