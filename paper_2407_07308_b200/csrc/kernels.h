@@ -8,7 +8,7 @@
 
 namespace bc {
 
-struct u64x2 { uint64_t w, ws; };   // value + Shoup companion
+struct __align__(16) u64x2 { uint64_t w, ws; };   // value + Shoup companion (16-byte aligned: one 128-bit load)
 
 // Device tables of the Bluestein transforms (§8(a) a1/a2), one slice per prime.
 struct NttTables {
