@@ -277,32 +277,40 @@ def modswitch_to(P, ct, level):
     return ct
 
 
-def keyswitch_up(P, K, d, level, key_id):
-    """R14 ModUp + key inner product: for each digit j the exact centered lift of d restricted to
-    G_j, embedded in every target limb; (u0, u1) = sum_j x_j (b_j, a_j) over the level's cipher
-    limbs and all special limbs (rows: cipher 0..level-1, then special)."""
-    key = K.ksk[key_id]
+def modup(P, d, level):
+    """R14 ModUp: for each digit j the exact centered lift x_j of d restricted to G_j, embedded
+    in every target limb (rows: cipher 0..level-1, then special).  -> [(j, x_j rows)]."""
     tgt = list(range(level)) + P.special
-    u0 = np.zeros((len(tgt), P.n), dtype=np.uint64)
-    u1 = np.zeros((len(tgt), P.n), dtype=np.uint64)
+    out = []
     for j in range(P.dnum):
         G = P.digit_group(j, level)
         if not G:
             continue
         x, _ = lift_centered(P, d[G], G)
-        xr = int_poly_to_rns(P, x, tgt)
+        out.append((j, int_poly_to_rns(P, x, tgt)))
+    return out
+
+
+def kip(P, K, digits, level, key_id):
+    """R14 key inner product: (u0, u1) = sum_j x_j (b_j, a_j) over the target limbs."""
+    key = K.ksk[key_id]
+    tgt = list(range(level)) + P.special
+    u0 = np.zeros((len(tgt), P.n), dtype=np.uint64)
+    u1 = np.zeros((len(tgt), P.n), dtype=np.uint64)
+    for j, xr in digits:
         b, a = key[j]
-        kb = b[tgt]
-        ka = a[tgt]
-        u0 = _add(u0, _mul(xr, kb, P, tgt), P, tgt)
-        u1 = _add(u1, _mul(xr, ka, P, tgt), P, tgt)
+        u0 = _add(u0, _mul(xr, b[tgt], P, tgt), P, tgt)
+        u1 = _add(u1, _mul(xr, a[tgt], P, tgt), P, tgt)
     return u0, u1
 
 
-def keyswitch(P, K, d, level, key_id):
-    """R14 (hybrid): ModUp and KIP (keyswitch_up), then ModDown -- r = [u]_P,
-    delta = r + P [-r]_p, u' = (u - delta) P^{-1}."""
-    u0, u1 = keyswitch_up(P, K, d, level, key_id)
+def keyswitch_up(P, K, d, level, key_id):
+    """R14 ModUp + key inner product (rows: cipher 0..level-1, then special)."""
+    return kip(P, K, modup(P, d, level), level, key_id)
+
+
+def moddown(P, u0, u1, level):
+    """R14 ModDown: r = [u]_P, delta = r + P [-r]_p, u' = (u - delta) P^{-1}."""
     Pprod = 1
     for q in P.P:
         Pprod *= q
@@ -312,6 +320,12 @@ def keyswitch(P, K, d, level, key_id):
         r, _ = lift_centered(P, u[sp_rows], P.special)
         out.append(_scale_down(P, u[:level], list(range(level)), None, r, Pprod))
     return out[0], out[1]
+
+
+def keyswitch(P, K, d, level, key_id):
+    """R14 (hybrid): ModUp and KIP (keyswitch_up), then ModDown."""
+    u0, u1 = keyswitch_up(P, K, d, level, key_id)
+    return moddown(P, u0, u1, level)
 
 
 # ----------------------------------------------------------------------------------------
@@ -436,6 +450,26 @@ def automorphism(P, K, ct, t):
     c1 = np.stack([P.ring.automorph_mod(ct.parts[1][r], t, P.moduli[i]) for r, i in enumerate(idx)])
     u0, u1 = keyswitch(P, K, c1, lv, t)
     return Ciphertext([_add(c0, u0, P, idx), u1], lv)
+
+
+def automorphisms_hoisted(P, K, ct, ts):
+    """R22 hoisted key switching for several automorphisms of ONE ciphertext:
+    the ModUp digits x_j of c1 are lifted once; for each t: u = sum_j sigma_t(x_j) (b_j, a_j)^(t)
+    (sigma_t of an integer digit, applied limb-wise: sigma_t is a ring map of Z[x]/Phi_m), ModDown,
+    and the result is (sigma_t(c0) + u0', u1').  Decrypts like automorphism(); different bits
+    (sigma_t(lift(c1)) instead of lift(sigma_t(c1)))."""
+    lv = ct.level
+    idx = list(range(lv))
+    tgt = idx + P.special
+    digits = modup(P, ct.parts[1], lv)
+    outs = []
+    for t in ts:
+        sd = [(j, np.stack([P.ring.automorph_mod(xr[r], t, P.moduli[i]) for r, i in enumerate(tgt)]))
+              for j, xr in digits]
+        u0, u1 = moddown(P, *kip(P, K, sd, lv, t), lv)
+        c0 = np.stack([P.ring.automorph_mod(ct.parts[0][r], t, P.moduli[i]) for r, i in enumerate(idx)])
+        outs.append(Ciphertext([_add(c0, u0, P, idx), u1], lv))
+    return outs
 
 
 def rotate(P, K, ct, k):

@@ -222,7 +222,7 @@ def kappa_slots(alg, i, k):
 def extract_digits(ev, ct, d):
     """digit_i = sum_{k<D} kappa_{i,k} (.) sigma_{p^k}(ct), i < d  (P:286 "mod extract")."""
     D = ev.alg.D
-    F = [ct] + [ev.frobenius(ct, k) for k in range(1, D)]
+    F = [ct] + ev.frobenius_hoisted(ct, list(range(1, D)))    # R22: one ModUp for the D-1 maps
     out = []
     for i in range(d):
         acc = None
@@ -430,6 +430,10 @@ class OracleEval:
         self.counts["ks"] += 1
         return bgv.frobenius(self.P, self.K, a, k)
 
+    def frobenius_hoisted(self, a, ks):
+        self.counts["ks"] += len(ks)
+        return bgv.automorphisms_hoisted(self.P, self.K, a, [pow(self.P.p, k, self.P.m) for k in ks])
+
     def modswitch(self, a):
         return bgv.modswitch(self.P, a)
 
@@ -504,6 +508,9 @@ class PlainEval:
 
     def frobenius(self, a, k):
         return PlainValue(self.gf.pow(a.v, self.p ** k), a.depth)
+
+    def frobenius_hoisted(self, a, ks):
+        return [self.frobenius(a, k) for k in ks]
 
     def modswitch(self, a):
         return PlainValue(a.v, a.depth + 1)

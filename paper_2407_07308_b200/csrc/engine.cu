@@ -676,15 +676,9 @@ CT Eng::add_pt(const CT &a, const uint64_t *pt) {
 }
 
 // R14 hybrid key switching: ModUp (exact lift per digit + NTT) and KIP -> u [B][2][lvl+K][n] (eval)
-BufP Eng::ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
-    const uint64_t *kptr = nullptr;
-    if (keys) {
-        auto kit = keys->ksk.find(key_id);
-        if (kit == keys->ksk.end()) BC_THROW(BC_E_KEY, "missing Galois key for t=" + std::to_string(key_id));
-        kptr = kit->second;
-    } else if (!dry()) {
-        BC_THROW(BC_E_ARG, "keyswitch without keys");
-    }
+// R14 ModUp: INTT of d, exact lift of every digit into the other limbs, NTT -> E [B][ndig][lvl+K][n]
+// (eval; the digit's own limbs are not written: KIP reads them from d)
+BufP Eng::ks_modup(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl) {
     const uint32_t n = X->n, K = X->K, L1 = X->L1, al = X->alpha, nl = lvl + K;
     const uint32_t ndig = (lvl + al - 1) / al;
     BufP dc = alloc_words((uint64_t)B * lvl * n);
@@ -701,15 +695,38 @@ BufP Eng::ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint3
         LimbMap lm{nl - (g1 - g0), g0, g1 - g0, lvl, 0, L1};
         ntt_fwd(E + (uint64_t)j * nl * n, E + (uint64_t)j * nl * n, B, lm, eps, eps);
     }
+    return ext;
+}
+
+// R14 key inner product with the key for Galois element key_id; perm_t != 0 reads every digit
+// (and d) through the evaluation-index permutation of sigma_{perm_t} (R22 hoisting)
+BufP Eng::ks_kip(const uint64_t *d, uint64_t dps, const BufP &ext, uint32_t B, uint32_t lvl, uint32_t key_id,
+                 uint32_t perm_t) {
+    const uint64_t *kptr = nullptr;
+    if (keys) {
+        auto kit = keys->ksk.find(key_id);
+        if (kit == keys->ksk.end()) BC_THROW(BC_E_KEY, "missing Galois key for t=" + std::to_string(key_id));
+        kptr = kit->second;
+    } else if (!dry()) {
+        BC_THROW(BC_E_ARG, "keyswitch without keys");
+    }
+    const uint32_t n = X->n, K = X->K, L1 = X->L1, al = X->alpha, nl = lvl + K;
+    const uint32_t ndig = (lvl + al - 1) / al;
     BufP u = alloc_words((uint64_t)B * 2 * nl * n);
-    if (!dry()) ks_kip(X->d_mods, d, dps, E, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig, n, st);
+    if (!dry())
+        ks_kip_perm(X->d_mods, X->T, perm_t, d, dps, (uint64_t *)ext->p, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig,
+                    n, st);
     return u;
 }
 
-CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
+BufP Eng::ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
+    BufP ext = ks_modup(d, dps, B, lvl);
+    return ks_kip(d, dps, ext, B, lvl, key_id, 0);
+}
+
+// R14 ModDown of u [B][2][lvl+K][n]: r = [u]_P, delta = r + P [-r]_p, u' = (u - delta) P^{-1}
+CT Eng::ks_moddown(const BufP &u, uint32_t B, uint32_t lvl) {
     const uint32_t n = X->n, K = X->K, L1 = X->L1, nl = lvl + K;
-    BufP u = ks_up(d, dps, B, lvl, key_id);
-    // ModDown of both parts: 2B polys with stride nl*n
     BufP sp = alloc_words((uint64_t)2 * B * K * n);
     ntt_inv((uint64_t *)u->p + (uint64_t)lvl * n, (uint64_t *)sp->p, 2 * B, LimbMap{K, K, 0, 0, 0, L1}, (uint64_t)nl * n,
             (uint64_t)K * n);
@@ -723,6 +740,35 @@ CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uin
     if (!dry())
         ew_scale_sub(X->d_mods, (uint64_t *)u->p, (uint64_t)nl * n, (uint64_t *)delta->p, X->d_invP, o.d, 2 * B, lvl, n, st);
     return o;
+}
+
+CT Eng::keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id) {
+    BufP u = ks_up(d, dps, B, lvl, key_id);
+    return ks_moddown(u, B, lvl);
+}
+
+// R22 hoisted automorphisms of one batch: ModUp of c1 once; per t: permuted KIP, ModDown,
+// part 0 += sigma_t(c0)
+std::vector<CT> Eng::automorph_hoisted(const CT &a, const std::vector<uint32_t> &ts) {
+    const uint32_t n = X->n, lv = a.lvl, B = a.B;
+    if (a.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "automorph_hoisted: strided");
+    const uint64_t *c1 = a.d + (uint64_t)lv * n;
+    BufP ext = ks_modup(c1, a.bstride, B, lv);
+    std::vector<CT> outs;
+    for (uint32_t t : ts) {
+        CT o;
+        {
+            BufP u = ks_kip(c1, a.bstride, ext, B, lv, t, t);
+            o = ks_moddown(u, B, lv);
+        }
+        CT c0 = ct_alloc(B, lv, 1);
+        if (!dry()) {
+            ew_automorph_part(X->T, a.d, a.bstride, c0.d, B, lv, t, st);
+            ew_add_bs(X->d_mods, o.d, o.bstride, c0.d, c0.bstride, o.d, o.bstride, B, 1, lv, n, st);
+        }
+        outs.push_back(o);
+    }
+    return outs;
 }
 
 // R15 fused: tensor -> ModUp + KIP of d2 -> w_k = P d_k + u_k -> one scale-down by D = P q_{lv-1}
@@ -915,7 +961,12 @@ std::vector<CT> extract_batch(Eng &E, const CT &a) {
     bc_ctx *X = E.X;
     const uint32_t D = X->alg.D, d = X->d, S = X->alg.S;
     std::vector<CT> F{a};
-    for (uint32_t k = 1; k < D; ++k) F.push_back(E.frobenius(a, k));
+    {
+        std::vector<uint32_t> ts;       // R22: the D-1 Frobenius maps share one ModUp
+        for (uint32_t k = 1; k < D; ++k) ts.push_back((uint32_t)powmod_h(X->p, k, X->m));
+        std::vector<CT> h = E.automorph_hoisted(a, ts);
+        F.insert(F.end(), h.begin(), h.end());
+    }
     CT all = E.ct_alloc(a.B * d, a.lvl, 2);
     std::vector<CT> out;
     for (uint32_t i = 0; i < d; ++i) {

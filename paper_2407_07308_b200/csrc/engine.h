@@ -129,6 +129,11 @@ struct Eng {
     // key switch of polys d (ct b at d + b*dps, lvl limbs, eval) -> [B][2][lvl][n]
     CT keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);
     BufP ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);  // ModUp + KIP
+    BufP ks_modup(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl);
+    BufP ks_kip(const uint64_t *d, uint64_t dps, const BufP &ext, uint32_t B, uint32_t lvl, uint32_t key_id,
+                uint32_t perm_t);
+    CT ks_moddown(const BufP &u, uint32_t B, uint32_t lvl);
+    std::vector<CT> automorph_hoisted(const CT &a, const std::vector<uint32_t> &ts);   // R22
     CT mul(const CT &a, const CT &b);
     CT automorph(const CT &a, uint32_t t);
     CT rotate(const CT &a, int64_t k);

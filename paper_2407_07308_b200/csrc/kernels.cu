@@ -509,6 +509,24 @@ __global__ void k_automorph(NttTables T, const uint64_t *__restrict__ a, uint64_
         o[i] = a[r * T.n + src];
     }
 }
+// part 0 of each ciphertext of a (batch stride abs) -> o [B][1][lvl][n], permuted by sigma_t
+__global__ void k_automorph_part(NttTables T, const uint64_t *__restrict__ a, uint64_t abs, uint64_t *__restrict__ o,
+                                 uint64_t total, uint32_t lvl, uint32_t t) {
+    const uint64_t per = (uint64_t)lvl * T.n;
+    GRID_LOOP(i, total) {
+        const uint64_t b = i / per, rr = i - b * per;
+        const uint64_t r = rr / T.n;
+        const uint32_t x = (uint32_t)(rr - r * T.n);
+        const uint32_t src = (uint32_t)T.pos[(uint32_t)(((uint64_t)t * (uint32_t)T.z[x]) % T.m)];
+        o[i] = a[b * abs + r * T.n + src];
+    }
+}
+void ew_automorph_part(const NttTables &T, const uint64_t *a, uint64_t abs, uint64_t *o, uint32_t B, uint32_t lvl,
+                       uint32_t t, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * lvl * T.n;
+    k_automorph_part<<<grid_for(total, 256), 256, 0, st>>>(T, a, abs, o, total, lvl, t);
+    LAUNCHED();
+}
 void ew_automorph(const NttTables &T, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
                   uint32_t t, cudaStream_t st) {
     const uint64_t total = (uint64_t)B * parts * lvl * T.n;
@@ -564,12 +582,15 @@ __device__ __forceinline__ void mac128(uint64_t &hi, uint64_t &lo, uint64_t a, u
 __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__ d, uint64_t dps,
                       const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
                       uint64_t *__restrict__ u, uint64_t total, uint32_t lvl, uint32_t K, uint32_t L1,
-                      uint32_t alpha, uint32_t ndig, uint32_t n) {
+                      uint32_t alpha, uint32_t ndig, uint32_t n, const int32_t *__restrict__ pos,
+                      const int32_t *__restrict__ zt, uint32_t m, uint32_t perm_t) {
     const uint32_t nl = lvl + K;
     const uint64_t ln = (uint64_t)nl * n;
     GRID_LOOP(i, total) {   // over B * nl * n
         const uint64_t b = i / ln, rr = i - b * ln;
-        const uint32_t r = (uint32_t)(rr / n), x = (uint32_t)(rr - (uint64_t)r * n);
+        const uint32_t r = (uint32_t)(rr / n), xo = (uint32_t)(rr - (uint64_t)r * n);
+        // R22: digits read through sigma_t's evaluation-index permutation
+        const uint32_t x = perm_t ? (uint32_t)pos[(uint32_t)(((uint64_t)perm_t * (uint32_t)zt[xo]) % m)] : xo;
         const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
         const Mod M = mods[kl];
         const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
@@ -577,8 +598,8 @@ __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__
         for (uint32_t j = 0; j < ndig; ++j) {
             const uint64_t dig = (j == jr) ? d[b * dps + (uint64_t)r * n + x] : ext[((b * ndig + j) * nl + r) * n + x];
             const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
-            mac128(h0, l0, dig, kj[(uint64_t)kl * n + x]);
-            mac128(h1, l1, dig, kj[(uint64_t)(L1 + K + kl) * n + x]);
+            mac128(h0, l0, dig, kj[(uint64_t)kl * n + xo]);
+            mac128(h1, l1, dig, kj[(uint64_t)(L1 + K + kl) * n + xo]);
         }
         u[(b * 2 + 0) * ln + rr] = reduce128(h0, l0, M);
         u[(b * 2 + 1) * ln + rr] = reduce128(h1, l1, M);
@@ -587,7 +608,16 @@ __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__
 void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
             uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
     const uint64_t total = (uint64_t)B * (lvl + K) * n;
-    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, dps, ext, key, u, total, lvl, K, L1, alpha, ndig, n);
+    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, dps, ext, key, u, total, lvl, K, L1, alpha, ndig, n, nullptr,
+                                                nullptr, 1, 0);
+    LAUNCHED();
+}
+void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uint64_t *d, uint64_t dps,
+                 const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1,
+                 uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
+    const uint64_t total = (uint64_t)B * (lvl + K) * n;
+    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, dps, ext, key, u, total, lvl, K, L1, alpha, ndig, n, T.pos, T.z,
+                                                T.m, perm_t);
     LAUNCHED();
 }
 

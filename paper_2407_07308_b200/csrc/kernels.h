@@ -84,6 +84,12 @@ void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in
 // ---- key switching ----
 // KIP: u[b][k][r][x] = sum_j ext[b][j][r][x] * key_j[k][klimb(r)][x], k in {0 (b-part),1 (a-part)};
 // for r in G_j the digit is read from d (eval input) instead of ext.
+// R22: KIP reading d and the extended digits through sigma_{perm_t}'s evaluation permutation
+void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uint64_t *d, uint64_t dps,
+                 const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1,
+                 uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st);
+void ew_automorph_part(const NttTables &T, const uint64_t *a, uint64_t abs, uint64_t *o, uint32_t B, uint32_t lvl,
+                       uint32_t t, cudaStream_t st);
 void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
             uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig,
             uint32_t n, cudaStream_t st);

@@ -196,3 +196,25 @@ def test_fused_mul_decrypts_like_two_step(c1):
         assert np.array_equal(A.decode(bgv.decrypt(P, K, f)), want)
         assert np.array_equal(A.decode(bgv.decrypt(P, K, u)), want)
         assert bgv.noise_bits(P, K, f)[0] <= bgv.noise_bits(P, K, u)[0] + 2
+
+
+def test_hoisted_automorphisms_decrypt_like_plain(c1):
+    """R22 hoisted key switching: every sigma_t of one ciphertext decrypts exactly like the
+    non-hoisted automorphism (Frobenius: slot-wise p^k power; rotations: slot
+    shift) with noise within 2 bits; the bits differ (sigma_t(lift(c1)) vs lift(sigma_t(c1)))."""
+    P, K = c1
+    A = P.alg
+    rng = np.random.default_rng(6)
+    b1 = rng.integers(0, P.p, size=(A.S, A.D))
+    c = _enc_slots(P, K, b1, 30)
+    ts = [pow(P.p, k, P.m) for k in range(1, A.D)] + [A.g, pow(A.g, -1, P.m)]
+    hs = bgv.automorphisms_hoisted(P, K, c, ts)
+    dec = lambda x: A.decode(bgv.decrypt(P, K, x))
+    for t, h in zip(ts, hs):
+        plain = bgv.automorphism(P, K, c, t)
+        assert np.array_equal(dec(h), dec(plain))
+        assert bgv.noise_bits(P, K, h)[0] <= bgv.noise_bits(P, K, plain)[0] + 2
+    for k in range(1, A.D):
+        assert np.array_equal(dec(hs[k - 1]), A.gf.pow(b1, P.p ** k))
+    assert np.array_equal(dec(hs[A.D - 1]), np.roll(b1, -1, axis=0))
+    assert not np.array_equal(hs[0].parts[1], bgv.automorphism(P, K, c, ts[0]).parts[1])
