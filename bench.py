@@ -261,7 +261,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verify", type=int, default=1)
-    ap.add_argument("--workload", default=None, choices=[None, "compare", "tournament", "sort"],
+    ap.add_argument("--workload", default=None, choices=[None, "compare", "tournament", "sort", "compact_compare"],
                     help="compare (default; C2), tournament (C4 min over T vectors), sort (C5 rank sort)")
     ap.add_argument("--T", type=int, default=16, help="tournament / sort: number of elements")
     ap.add_argument("--cts", type=int, default=0, help="ciphertexts per element (tournament: 5 -> 4096 words)")
@@ -273,9 +273,12 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
-    workload = args.workload or {"c4": "tournament", "c5": "sort"}.get(args.config, "compare")
+    workload = args.workload or {"c4": "tournament", "c5": "sort", "c3": "compact_compare"}.get(args.config, "compare")
     if workload in ("tournament", "sort"):
         run_vector_workload(args, cfg, rank, world, local, workload)
+        return
+    if workload == "compact_compare":
+        run_compact_compare(args, cfg, rank, world, local)
         return
 
     import torch
@@ -513,6 +516,113 @@ def run_vector_workload(args, cfg, rank, world, local, workload):
                      "verified": verified, "gpu_launches": launches, "clocks": clk.summary(),
                      "roofline": roofline(ctx, bc, live, ms_local * args.steps), "e2e": None,
                      "cpu_baseline": None})
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_compact_compare(args, cfg, rank, world, local):
+    """C3: sparse ciphertext pairs at 25% block utilisation (blocks = 3 mod 4 useful, Fig. 7) are
+    compacted 4 -> 1 (R17: one mask product + rotation per (block set, offset) bucket, one batched
+    modulus switch), then the dense pairs are compared (bivariate circuit).  --pairs = dense pairs
+    per GPU (4x as many sparse pairs); weak scaling, no collective."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2407_07308_b200 as bc
+    from inputs import word_pairs
+    ctx = bc.Context(cfg, device=local)
+    keys = ctx.keygen(SEED_KEYS)
+    ints = ctx.ints_per_ct
+    Bd = args.pairs
+    Bs = 4 * Bd
+    rng = np.random.default_rng(SEED_INPUT + rank)
+    A, Bw = word_pairs(rng, Bs * ints, ctx.base, ctx.d * ctx.l)
+    A = np.array(A, dtype=np.uint64).reshape(Bs, ints)
+    Bw = np.array(Bw, dtype=np.uint64).reshape(Bs, ints)
+    useful = np.zeros((Bs, ints), dtype=np.uint8)
+    useful[:, 3::4] = 1
+    A[useful == 0] = 0
+    Bw[useful == 0] = 0
+    base = 2 * Bs * rank
+    ws = ctx.workspace(max(ctx.workspace_bytes(1), 4 << 30))
+    ca = ctx.encrypt(keys, A, SEED_ENC, ct_index0=base, ws=ws)
+    cb = ctx.encrypt(keys, Bw, SEED_ENC, ct_index0=base + Bs, ws=ws)
+    free, _ = torch.cuda.mem_get_info(dev)
+    ws = ctx.workspace(int(min(max(ctx.workspace_bytes(1), int(free * 0.80)), free - (2 << 30))))
+    lvl_c = ctx.n_cipher - 1
+    lvl_out = ctx.out_level(lvl_c, 0)
+    out = ctx.ct_empty(Bd, lvl_out)
+    da, db = ctx.ct_empty(Bs, lvl_c), ctx.ct_empty(Bs, lvl_c)
+    dest = np.zeros((Bs, ints), dtype=np.int32)
+    nout = bc._u32(0)
+    uptr = useful.ctypes.data
+    wsp = bc._ptr(ws)
+
+    def step():
+        for src, dst in ((ca, da), (cb, db)):
+            bc._check(bc._lib.bc_compact(ctx._h, keys.keys, ctx.view(src), uptr, ctx.view(dst), bc.ctypes.byref(nout),
+                                         dest.ctypes.data, wsp, ws.numel(), bc._stream()), "bc_compact")
+        n = nout.value
+        bc._check(bc._lib.bc_compare_lt(ctx._h, keys.keys, ctx.view(da[:n]), ctx.view(db[:n]), ctx.view(out[:n]), wsp,
+                                        ws.numel(), bc._stream()), "bc_compare_lt")
+        return n
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    verified = None
+    for w in range(args.warmup):
+        n = step()
+        if w == 0 and args.verify:
+            torch.cuda.synchronize()
+            bits = ctx.decrypt(keys, out[:n], as_bits=True)
+            ok = True
+            for c in range(Bs):
+                for j in range(3, ints, 4):
+                    ct_i, blk = divmod(int(dest[c, j]), ints)
+                    ok &= int(bits[ct_i][blk]) == int(A[c, j] < Bw[c, j])
+            verified = bool(ok and n == Bd)
+            if not verified:
+                print("VERIFY FAILED (n_out %d)" % n, file=sys.stderr)
+                sys.exit(3)
+    barrier()
+    bc.launch_count(reset=True)
+    bc.ntt_timing(True)
+    bc.ntt_timing()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    launches = bc.launch_count(reset=True)
+    live = bc.ntt_timing()
+    bc.ntt_timing(False)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, world, dev)
+    useful_ints = int(useful.sum()) * world
+    if rank == 0:
+        line = {"metric": "encrypted slot-comparisons/s after slot compaction (C3, bivariate p=31)",
+                "value": useful_ints / (ms / 1e3), "unit": "int-compares/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": "c3 compact_compare", "params": args.config, "sparse_pairs_per_gpu": Bs,
+                           "dense_pairs_per_gpu": Bd, "ints_per_ct": ints, "utilisation": 0.25,
+                           "n_cipher": ctx.n_cipher, "n_special": ctx.n_special, "alpha": cfg["alpha"],
+                           "l2": "inputs larger than L2"},
+                "ms_per_dense_compare": ms / Bd, "verified": verified, "gpu_launches": launches,
+                "clocks": clk.summary(), "roofline": roofline(ctx, bc, live, ms_local * args.steps), "e2e": None,
+                "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

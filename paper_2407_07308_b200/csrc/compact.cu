@@ -2,6 +2,7 @@
 // offsets bucketed so that each (input, output, offset) group costs one plaintext mask product
 // and one rotation; one modulus switch per output at the end.
 #include <algorithm>
+#include <map>
 #include <set>
 
 #include "engine.h"
@@ -62,22 +63,16 @@ static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful,
     return groups;
 }
 
-// encode a 0/1 block mask into an evaluation-form plaintext inside the workspace
-static BufP encode_mask(Eng &E, const std::vector<uint32_t> &blocks) {
+// 0/1 block mask as an evaluation-form plaintext, cached in the context by its block set
+static const uint64_t *mask_pt(Eng &E, const std::vector<uint32_t> &blocks) {
     bc_ctx *X = E.X;
-    const uint32_t S = X->alg.S, D = X->alg.D, n = X->n, L1 = X->L1, l = X->l;
+    const uint32_t S = X->alg.S, D = X->alg.D, l = X->l;
+    std::string key = "cm:";
+    for (uint32_t b : blocks) key += std::to_string(b) + ",";
     std::vector<int16_t> sl((size_t)S * D, 0);
     for (uint32_t b : blocks)
         for (uint32_t s = b * l; s < (b + 1) * l; ++s) sl[(size_t)s * D] = 1;
-    BufP s16(new Buf{E.A, E.A->alloc(sl.size() * 2), sl.size() * 2});
-    BufP c16(new Buf{E.A, E.A->alloc((size_t)n * 2), (size_t)n * 2});
-    BufP pt = E.alloc_words((uint64_t)L1 * n);
-    if (!E.dry()) CK(cudaMemcpyAsync(s16->p, sl.data(), sl.size() * 2, cudaMemcpyHostToDevice, E.st));
-    encode_slots_dev(X, (int16_t *)s16->p, 1, (int16_t *)c16->p, E.A, E.st);
-    if (!E.dry()) s16_to_rns(X->d_mods, (int16_t *)c16->p, (uint64_t *)pt->p, 1, L1, n, E.st);
-    E.ntt_fwd((uint64_t *)pt->p, (uint64_t *)pt->p, 1, limbmap_plain(L1, 0), (uint64_t)L1 * n, (uint64_t)L1 * n);
-    if (!E.dry()) CK(cudaStreamSynchronize(E.st));   // the host mask vector dies here
-    return pt;
+    return ctx_pt(X, key, sl, E.st);
 }
 
 }  // namespace bc
@@ -106,22 +101,32 @@ extern "C" bc_status bc_compact(bc_ctx *X, const bc_keys *keys, bc_ct in, const 
         A.init(ws, wsb, false);
         Eng E{X, keys, &A, (cudaStream_t)stv};
         const uint64_t cw = (uint64_t)2 * in.level * X->n;
-        std::vector<CT> acc(nout);
+        // groups with the same (block set, offset) run as one batch: one mask product and one
+        // (batched) rotation; every op is per ciphertext, so the bits equal the group-by-group order
+        std::map<std::pair<std::vector<uint32_t>, int32_t>, std::vector<const Group *>> buckets;
+        for (const Group &g : groups)
+            if (!g.blocks.empty()) buckets[{g.blocks, g.dl}].push_back(&g);
+        CT accb = E.ct_alloc(nout, in.level, 2);
         std::vector<bool> have(nout, false);
-        for (const Group &g : groups) {
-            if (g.blocks.empty()) continue;
-            BufP mk = encode_mask(E, g.blocks);
-            CT src = E.view((uint64_t *)in.data + (uint64_t)g.c * cw, 1, in.level);
-            CT t = E.ptmul(src, (uint64_t *)mk->p);
-            if (g.dl) t = E.rotate(t, (int64_t)g.dl * X->l);
-            acc[g.cp] = have[g.cp] ? E.add(acc[g.cp], t) : t;
-            have[g.cp] = true;
+        for (auto &bk : buckets) {
+            const uint64_t *mk = mask_pt(E, bk.first.first);
+            std::vector<CT> srcs;
+            for (const Group *g : bk.second) srcs.push_back(E.view((uint64_t *)in.data + (uint64_t)g->c * cw, 1, in.level));
+            CT t = E.ptmul(concat_batch(E, srcs), mk);
+            if (bk.first.second) t = E.rotate(t, (int64_t)bk.first.second * X->l);
+            for (size_t k = 0; k < bk.second.size(); ++k) {
+                const uint32_t cp = bk.second[k]->cp;
+                CT dst = E.sub(accb, cp, 1), tk = E.sub(t, (uint32_t)k, 1);
+                if (!have[cp]) {
+                    E.copy_into(tk, dst.d);
+                    have[cp] = true;
+                } else if (!E.dry()) {
+                    ew_add(X->d_mods, dst.d, tk.d, dst.d, 1, 2, in.level, X->n, 0, E.st);
+                }
+            }
         }
-        const uint64_t ow = (uint64_t)2 * out.level * X->n;
-        for (uint32_t cp = 0; cp < nout; ++cp) {
-            CT r = E.modswitch(acc[cp]);
-            CK(cudaMemcpyAsync((uint64_t *)out.data + (uint64_t)cp * ow, r.d, ow * 8, cudaMemcpyDeviceToDevice, E.st));
-        }
+        CT r = E.modswitch(accb);                  // one batched modulus switch for all outputs
+        CK(cudaMemcpyAsync(out.data, r.d, (size_t)nout * r.bstride * 8, cudaMemcpyDeviceToDevice, E.st));
         CK(cudaGetLastError());
         *n_out = nout;
     } catch (BcError &e) {

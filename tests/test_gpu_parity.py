@@ -340,3 +340,53 @@ def test_sort_matches_oracle(pair):
     oo = circuits.sort_rank(ev, [Tp.oracle_ct(W[t], 600 + t) for t in range(3)], P.circuit, P.d, P.l, ints)
     for k in range(3):
         assert np.array_equal(to_u64(outs[k])[0], Tp.ct_eval(oo[k]))
+
+
+def test_bivariate_compare_matches_oracle(pair):
+    """a7 bivariate path (digits < p, base p; P:71 [Tan] 3p-5 products): compare ciphertexts
+    bit-exact vs the oracle, decrypted bits = [a<b] and [a=b]."""
+    from oracle import circuits
+    T = pair("c1b")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(41)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=800)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=801)
+    lt, eq = T.ctx.compare(T.keys, ca, cb)
+    assert list(T.ctx.decrypt(T.keys, lt, as_bits=True)[0]) == [int(x < y) for x, y in zip(a, b)]
+    assert list(T.ctx.decrypt(T.keys, eq, as_bits=True)[0]) == [int(x == y) for x, y in zip(a, b)]
+    ev = circuits.OracleEval(P, T.okeys)
+    olt, oeq = circuits.compare(ev, T.oracle_ct(a, 800), T.oracle_ct(b, 801), P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(lt)[0], T.ct_eval(olt))
+    assert np.array_equal(to_u64(eq)[0], T.ct_eval(oeq))
+
+
+def test_compare_full_c3_decrypts(pair):
+    """C3 stand-in at full size (p = 31 bivariate, m = 17351, (d,l) = (5,3)): compaction of 4
+    sparse ciphertexts (Fig. 7 pattern) to 1, then compare_lt decrypts to [a<b] in every block."""
+    T = pair("c3")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(42)
+    A, B = [], []
+    for _ in range(4):
+        a, b = mixed_pairs(P, rng, ints)
+        A.append(a)
+        B.append(b)
+    A, B = np.array(A, dtype=np.uint64), np.array(B, dtype=np.uint64)
+    useful = np.zeros((4, ints), dtype=np.uint8)
+    useful[:, 3::4] = 1
+    A[useful == 0] = 0
+    B[useful == 0] = 0
+    ca = T.ctx.encrypt(T.keys, A, SEED_ENC, ct_index0=0)
+    cb = T.ctx.encrypt(T.keys, B, SEED_ENC, ct_index0=4)
+    da, dest = T.ctx.compact(T.keys, ca, useful)
+    db, dest2 = T.ctx.compact(T.keys, cb, useful)
+    assert da.shape[0] == 1 and np.array_equal(dest, dest2)
+    lt = T.ctx.compare_lt(T.keys, da, db)
+    bits = T.ctx.decrypt(T.keys, lt, as_bits=True)
+    for c in range(4):
+        for j in range(3, ints, 4):
+            ct_i, blk = divmod(int(dest[c, j]), ints)
+            assert int(bits[ct_i][blk]) == int(A[c, j] < B[c, j])
