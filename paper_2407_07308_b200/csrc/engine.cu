@@ -402,6 +402,7 @@ void ctx_build(bc_ctx *X) {
     std::vector<uint64_t> blob;
     auto add_plan = [&](const std::string &k, const std::vector<uint32_t> &src, const std::vector<int64_t> &tgt) {
         X->plan_off[k] = blob.size();
+        X->plan_dims[k] = {(uint32_t)src.size(), (uint32_t)tgt.size()};
         auto b = build_plan(X, src, tgt);
         blob.insert(blob.end(), b.begin(), b.end());
     };
@@ -511,6 +512,16 @@ void ctx_build(bc_ctx *X) {
     }
 }
 
+// lift with the plan's (sources, targets) known on the host: selects the register-resident kernel
+void lift_p(bc_ctx *X, const std::string &key, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride,
+            uint64_t *out, uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0,
+            uint32_t skipn, int mode, cudaStream_t st) {
+    auto it = X->plan_dims.find(key);
+    if (it == X->plan_dims.end()) BC_THROW(BC_E_INTERNAL, "missing lift plan " + key);
+    lift(X->plan(key), mods, p, src, src_pstride, out, out_pstride, out16, npoly, n, skip0, skipn, mode, st,
+         it->second.first, it->second.second);
+}
+
 void ctx_free(bc_ctx *X) {
     for (void *p : X->owned) cudaFree(p);
     X->owned.clear();
@@ -615,7 +626,7 @@ CT Eng::modswitch(const CT &a) {
     if (a.bstride != (uint64_t)a.parts * lv * n) BC_THROW(BC_E_INTERNAL, "modswitch: strided batch");
     ntt_inv(a.d + (uint64_t)(lv - 1) * n, (uint64_t *)last->p, np, limbmap_plain(1, lv - 1), (uint64_t)lv * n, n);
     if (!dry())
-        lift(X->plan("ms:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)last->p, n, (uint64_t *)delta->p,
+        lift_p(X, ("ms:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)last->p, n, (uint64_t *)delta->p,
              (uint64_t)(lv - 1) * n, nullptr, np, n, 0, 0, 1, st);
     ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, np, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
             (uint64_t)(lv - 1) * n);
@@ -689,7 +700,7 @@ BufP Eng::ks_modup(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl) {
     for (uint32_t j = 0; j < ndig; ++j) {
         const uint32_t g0 = j * al, g1 = std::min(lvl, (j + 1) * al);
         if (!dry())
-            lift(X->plan("up:" + std::to_string(lvl) + ":" + std::to_string(j)), X->d_mods, X->p,
+            lift_p(X, ("up:" + std::to_string(lvl) + ":" + std::to_string(j)), X->d_mods, X->p,
                  (uint64_t *)dc->p + (uint64_t)g0 * n, (uint64_t)lvl * n, E + (uint64_t)j * nl * n, eps, nullptr, B, n, g0,
                  g1 - g0, 0, st);
         LimbMap lm{nl - (g1 - g0), g0, g1 - g0, lvl, 0, L1};
@@ -732,7 +743,7 @@ CT Eng::ks_moddown(const BufP &u, uint32_t B, uint32_t lvl) {
             (uint64_t)K * n);
     BufP delta = alloc_words((uint64_t)2 * B * lvl * n);
     if (!dry())
-        lift(X->plan("down:" + std::to_string(lvl)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)K * n,
+        lift_p(X, ("down:" + std::to_string(lvl)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)K * n,
              (uint64_t *)delta->p, (uint64_t)lvl * n, nullptr, 2 * B, n, 0, 0, 1, st);
     sp.reset();
     ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lvl, 0), (uint64_t)lvl * n, (uint64_t)lvl * n);
@@ -794,7 +805,7 @@ CT Eng::mul(const CT &a0, const CT &b0) {
             (uint64_t)(K + 1) * n);
     BufP delta = alloc_words((uint64_t)2 * B * (lv - 1) * n);
     if (!dry())
-        lift(X->plan("fd:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)(K + 1) * n,
+        lift_p(X, ("fd:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)(K + 1) * n,
              (uint64_t *)delta->p, (uint64_t)(lv - 1) * n, nullptr, 2 * B, n, 0, 0, 1, st);
     sp.reset();
     ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,

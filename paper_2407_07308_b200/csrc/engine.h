@@ -71,6 +71,7 @@ struct bc_ctx {
     bc::NttTables T;
     uint64_t *d_plans = nullptr;
     std::map<std::string, size_t> plan_off;
+    std::map<std::string, std::pair<uint32_t, uint32_t>> plan_dims;   // (sources, targets)
     bc::u64x2 *d_invP = nullptr;                // [L1] P^{-1} mod q_i
     bc::u64x2 *d_invq = nullptr;                // [L1+1][L1] q_{l-1}^{-1} mod q_i (row l)
     bc::u64x2 *d_Pm = nullptr;                  // [L1] P mod q_i
@@ -101,6 +102,9 @@ namespace bc {
 
 void ctx_build(bc_ctx *X);
 void ctx_free(bc_ctx *X);
+void lift_p(bc_ctx *X, const std::string &key, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride,
+            uint64_t *out, uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0,
+            uint32_t skipn, int mode, cudaStream_t st);
 
 // engine: batched BGV ops on one stream over a workspace arena
 struct Eng {

@@ -792,10 +792,96 @@ __global__ void k_lift(const uint64_t *__restrict__ plan, const Mod *__restrict_
         }
     }
 }
+// Specialised lift for a compile-time source count NS (digits in registers, fully unrolled Garner)
+// with the plan staged in shared memory once per block.  Same arithmetic as k_lift (modes 0, 1).
+template <int NS>
+__global__ void __launch_bounds__(256) k_lift_ns(const uint64_t *__restrict__ plan, const Mod *__restrict__ mods,
+                                                 uint32_t p, const uint64_t *__restrict__ src, uint64_t src_pstride,
+                                                 uint64_t *__restrict__ out, uint64_t out_pstride, uint64_t total,
+                                                 uint32_t n, uint32_t skip0, uint32_t skipn, int mode) {
+    __shared__ uint64_t sp[1024];
+    __shared__ Mod smod[64];
+    const uint32_t nt = (uint32_t)plan[1];
+    const uint32_t words = 2 + 3 * NS + 2 * NS * NS + NS + nt + 2 * nt * NS + 2 * nt + 1;
+    for (uint32_t i = threadIdx.x; i < words && i < 1024; i += blockDim.x) sp[i] = plan[i];
+    __syncthreads();
+    const uint64_t *P_src = sp + 2, *P_inv = P_src + NS, *P_invs = P_inv + NS, *P_qm = P_invs + NS;
+    const uint64_t *P_qms = P_qm + NS * NS, *P_half = P_qms + NS * NS, *P_tgt = P_half + NS;
+    const uint64_t *P_B = P_tgt + nt, *P_Bs = P_B + (uint64_t)nt * NS, *P_Q = P_Bs + (uint64_t)nt * NS;
+    const uint64_t *P_Qs = P_Q + nt;
+    const uint64_t pmu = P_Qs[nt];
+    for (uint32_t t = threadIdx.x; t < nt && t < 64; t += blockDim.x)
+        smod[t] = P_tgt[t] == ~0ull ? Mod{p, 0, 0, 0} : mods[P_tgt[t]];
+    __shared__ Mod ssrc[NS];
+    if (threadIdx.x < NS) ssrc[threadIdx.x] = mods[P_src[threadIdx.x]];
+    __syncthreads();
+    GRID_LOOP(i, total) {
+        const uint64_t poly = i / n;
+        const uint32_t x = (uint32_t)(i - poly * n);
+        const uint64_t *s = src + poly * src_pstride + x;
+        uint64_t v[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) v[k] = __ldcs(s + (uint64_t)k * n);
+#pragma unroll
+        for (int k = 1; k < NS; ++k) {
+            const uint64_t qk = ssrc[k].q;
+            uint64_t acc = v[k - 1];
+#pragma unroll
+            for (int j = k - 2; j >= 0; --j) acc = mul_shoup_lazy(acc, P_qm[k * NS + j], P_qms[k * NS + j], qk) + v[j];
+            acc = reduce64(acc, ssrc[k]);
+            v[k] = mul_shoup(sub_mod(v[k], acc, qk), P_inv[k], P_invs[k], qk);
+        }
+        bool neg = false;
+#pragma unroll
+        for (int k = NS - 1; k >= 0; --k) {
+            if (v[k] != P_half[k]) { neg = v[k] > P_half[k]; break; }
+        }
+        int64_t tc = 0;
+        if (mode == 1) {
+            const uint32_t tp = nt - 1;
+            uint64_t rp = 0;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) rp += mod_small(v[k], p, pmu) * P_B[(uint64_t)tp * NS + k];
+            rp %= p;
+            if (neg) rp = (rp + p - P_Q[tp]) % p;
+            tc = (int64_t)((p - rp) % p);
+            if (tc > (int64_t)(p / 2)) tc -= p;
+        }
+        const uint64_t atc = (uint64_t)(tc < 0 ? -tc : tc);
+        const uint32_t ntw = mode == 1 ? nt - 1 : nt;
+        for (uint32_t t = 0; t < ntw; ++t) {
+            const Mod Mt = smod[t];
+            const uint64_t *B = P_B + (uint64_t)t * NS, *Bs = P_Bs + (uint64_t)t * NS;
+            uint64_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) acc += mul_shoup_lazy(v[k], B[k], Bs[k], Mt.q);
+            acc = reduce64(acc, Mt);
+            if (neg) acc = sub_mod(acc, P_Q[t], Mt.q);
+            if (mode == 1) {
+                const uint64_t qc = mul_shoup(atc, P_Q[t], P_Qs[t], Mt.q);
+                acc = tc < 0 ? sub_mod(acc, qc, Mt.q) : add_mod(acc, qc, Mt.q);
+                out[poly * out_pstride + (uint64_t)t * n + x] = acc;
+            } else {
+                const uint32_t lb = t < skip0 ? t : t + skipn;
+                out[poly * out_pstride + (uint64_t)lb * n + x] = acc;
+            }
+        }
+    }
+}
+
 void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride, uint64_t *out,
           uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0, uint32_t skipn, int mode,
-          cudaStream_t st) {
+          cudaStream_t st, uint32_t ns_hint, uint32_t nt_hint) {
     const uint64_t total = (uint64_t)npoly * n;
+    const uint32_t words = 2 + 3 * ns_hint + 2 * ns_hint * ns_hint + ns_hint + nt_hint + 2 * nt_hint * ns_hint + 2 * nt_hint + 1;
+    if (mode != 2 && ns_hint >= 1 && ns_hint <= 8 && nt_hint <= 64 && words <= 1024) {
+        const unsigned g = grid_for(total, 256);
+#define LIFT_NS(K) case K: k_lift_ns<K><<<g, 256, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, total, n, skip0, skipn, mode); break;
+        switch (ns_hint) { LIFT_NS(1) LIFT_NS(2) LIFT_NS(3) LIFT_NS(4) LIFT_NS(5) LIFT_NS(6) LIFT_NS(7) LIFT_NS(8) }
+#undef LIFT_NS
+        LAUNCHED();
+        return;
+    }
     if (mode == 2)
         k_lift<64><<<grid_for(total, 128), 128, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, out16,
                                                          total, n, skip0, skipn, mode);

@@ -107,7 +107,7 @@ void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const 
 //  mode 2: centered value mod p (as int16, centered in (-p/2, p/2]) -> out16[poly][n]
 void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride,
           uint64_t *out, uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n,
-          uint32_t skip0, uint32_t skipn, int mode, cudaStream_t st);
+          uint32_t skip0, uint32_t skipn, int mode, cudaStream_t st, uint32_t ns_hint = 0, uint32_t nt_hint = 0);
 
 // ---- sampling (R7) ----
 // integer poly per (poly, coeff) -> residues on limbs prime0..prime0+nl-1
