@@ -390,3 +390,23 @@ def test_compare_full_c3_decrypts(pair):
         for j in range(3, ints, 4):
             ct_i, blk = divmod(int(dest[c, j]), ints)
             assert int(bits[ct_i][blk]) == int(A[c, j] < B[c, j])
+
+
+@pytest.mark.slow
+def test_compare_c3t_bivariate_p31_bit_exact(pair):
+    """C3's p = 31 bivariate digit circuit (88 products, R16) on a small ring (c3t: m = 1129,
+    (d,l) = (1,2), 9 + 4 primes): whole compare_lt ciphertext bit-exact vs the oracle (~4 min of
+    oracle time), decrypted bits = [a<b]."""
+    from oracle import circuits
+    T = pair("c3t")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(43)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=900)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=901)
+    lt = T.ctx.compare_lt(T.keys, ca, cb)
+    assert list(T.ctx.decrypt(T.keys, lt, as_bits=True)[0]) == [int(x < y) for x, y in zip(a, b)]
+    ev = circuits.OracleEval(P, T.okeys)
+    olt, _ = circuits.compare(ev, T.oracle_ct(a, 900), T.oracle_ct(b, 901), P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(lt)[0], T.ct_eval(olt))
