@@ -191,6 +191,11 @@ def circuits_product_count(P):
             self.ks(a.level)
             return CV(a.level)
 
+        def frobenius_hoisted(self, a, ks):
+            for _ in ks:
+                self.ks(a.level)
+            return [CV(a.level) for _ in ks]
+
     class AlgStub:
         def __init__(self):
             self.S = 1
