@@ -392,6 +392,49 @@ void ctx_build(bc_ctx *X) {
         }
         T.xta = dev_upload(X, xta);
         T.xtb = dev_upload(X, xtb);
+        // binary64 copies for ntt3.cu (needs every prime < 2^50: |4q| < 2^52)
+        bool f_ok = true;
+        for (uint32_t i = 0; i < NP; ++i) f_ok = f_ok && X->moduli[i] < (1ull << 50);
+        T.fmods = nullptr;
+        if (f_ok) {
+            auto fd = [&](const std::vector<u64x2> &v, size_t per) {
+                std::vector<double2> o(v.size());
+                for (size_t k = 0; k < v.size(); ++k) {
+                    const uint64_t q = X->moduli[k / per], w = v[k].w;
+                    const int64_t wc = w > q / 2 ? (int64_t)w - (int64_t)q : (int64_t)w;
+                    o[k] = make_double2((double)wc, (double)wc / (double)q);
+                }
+                return dev_upload(X, o);
+            };
+            auto brv_tab = [&](const std::vector<u64x2> &tw, uint32_t half, uint32_t logh) {
+                std::vector<u64x2> o(tw.size());
+                for (uint32_t i = 0; i < NP; ++i)
+                    for (uint32_t j = 0; j < half; ++j) o[(size_t)i * half + j] = tw[(size_t)i * half + brev_h(j, logh)];
+                return o;
+            };
+            std::vector<double2> fm(NP);
+            for (uint32_t i = 0; i < NP; ++i) fm[i] = make_double2((double)X->moduli[i], 1.0 / (double)X->moduli[i]);
+            T.ftwRb = fd(brv_tab(twR, X->R / 2, X->logR - 1), X->R / 2);
+            T.ftwCb = fd(brv_tab(twC, X->C / 2, X->logC - 1), X->C / 2);
+            T.ftwRi = fd(twRi, X->R / 2);
+            T.ftwCi = fd(twCi, X->C / 2);
+            T.ftf1 = fd(tf1, m); T.ftf1i = fd(tf1i, m); T.ftfo = fd(tfo, m); T.ftfoi = fd(tfoi, m);
+            {
+                const uint32_t le = (uint32_t)nttf_row_loge(X->logR, X->logC), E = 1u << le, tpr = X->C >> le;
+                auto perm = [&](const std::vector<u64x2> &v) {
+                    std::vector<u64x2> o(v.size());
+                    for (size_t i = 0; i < NP; ++i)
+                        for (uint32_t r = 0; r < X->R; ++r)
+                            for (uint32_t t = 0; t < tpr; ++t)
+                                for (uint32_t k = 0; k < E; ++k)
+                                    o[i * M + (size_t)r * X->C + k * tpr + t] = v[i * M + (size_t)r * X->C + t * E + k];
+                    return o;
+                };
+                T.fdhf = fd(perm(dhf), M); T.fdhi = fd(perm(dhi), M);
+            }
+            T.fxta = fd(xta, M); T.fxtb = fd(xtb, M);
+            T.fmods = dev_upload(X, fm);
+        }
     }
     T.twR = dev_upload(X, twR); T.twRi = dev_upload(X, twRi); T.twC = dev_upload(X, twC); T.twCi = dev_upload(X, twCi);
     T.pos = dev_upload(X, pos); T.z = dev_upload(X, z); T.phi = dev_upload(X, phi8); T.mods = X->d_mods;

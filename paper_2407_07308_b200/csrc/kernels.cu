@@ -319,12 +319,16 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     lm.npoly = npoly;
     // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
     const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65535, (uint64_t)g_ntt_group_bytes / ((uint64_t)T.M * 8)));
+    const bool vf = (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T);
     const bool v2 = g_ntt_impl != 1 && ntt2_supported(T);
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
         if (v2) {
-            ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
+            if (vf)
+                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
+            else
+                ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
             if (inv) {
                 if (T.prime_m)
                     k_reduce_prime<<<grid_for((uint64_t)nj * T.n, 256), 256, 0, st>>>(T, out, out_pstride, lm, j0, nj,

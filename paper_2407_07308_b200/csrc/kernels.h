@@ -26,6 +26,11 @@ struct NttTables {
     const u64x2 *twR, *twRi, *twC, *twCi;   // [P][R/2], [P][C/2]: omega_R^{+-j}, omega_C^{+-j} (register passes)
     const u64x2 *xta;     // [P][M]  psi^(c brev(rp)) at rp*C + c   (pass A epilogue, contiguous)
     const u64x2 *xtb;     // [P][M]  psi^(-c brev(r)) at r*C + c    (pass B epilogue, contiguous)
+    // binary64 variants (ntt3.cu): entry = (w centred in (-q/2, q/2], fl(w/q)); null when some q >= 2^50
+    const double2 *fmods;                   // [P] (q, fl(1/q))
+    const double2 *ftwRb, *ftwCb;           // [P][R/2], [P][C/2]: omega_L^{brev_{logL-1}(j)} (forward CT blocks)
+    const double2 *ftwRi, *ftwCi;           // omega_L^{-j} (inverse)
+    const double2 *ftf1, *ftf1i, *ftfo, *ftfoi, *fdhf, *fdhi, *fxta, *fxtb;   // as the u64x2 tables
     uint32_t m, n, M, R, C, logR, logC;
     int prime_m;          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
 };
@@ -145,6 +150,11 @@ uint64_t &launch_counter();
 // register-blocked passes (ntt2.cu) for the supported (R, C) shapes
 bool ntt2_supported(const NttTables &T);
 void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
+// binary64-FMA passes (ntt3.cu)
+bool nttf_supported(const NttTables &T);
+int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: position r*C + tau*E + k at r*C + k*(C/E) + tau
+void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
 extern uint64_t g_ntt_group_bytes;   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;

@@ -1,0 +1,480 @@
+// ntt3.cu -- Bluestein NTT passes in binary64 FMA arithmetic for sm_100a (a1/a2).
+//
+// Why binary64: every prime of the paper's sets must be = 1 (mod lcm(p, m, M)) (R1), which is
+// > 2^32 for all of them, so residues need 64-bit words.  On B200 the FP64 pipe issues 64 DFMA per
+// clock per SM -- the same rate as the 32-bit IMAD pipe -- and one exact modular product of
+// residues below 2^50 costs 6 binary64 operations (DMUL, 3 DFMA, 2 DADD) against ~10 IMAD-class
+// plus 4-6 ALU instructions for the 64-bit Shoup product (ntt2.cu).  Measured on B200 in a register
+// microbenchmark (tools/micro/bfly_micro.cu): 1.53e12 FP64 butterflies/s vs 0.89e12 Shoup ones.
+//
+// Representation: a residue class mod q (q < 2^50) is held as a signed integer-valued double v,
+// |v| <= 8q < 2^53 (exact).  The modular product with a table entry (w, wq), w in (-q/2, q/2]
+// centred and wq = fl(w/q), is
+//     h = fl(a w); l = a w - h (exact, one FMA); t = rint(a wq) (FMA with 1.5*2^52, DADD);
+//     r = (h - t q) + l   (both steps exact: the results are integers below 2^53),
+// exact for |a| <= 4q, with |r| <= (1/2 + 1/8) q.  A reduction x - rint(x/q) q gives |x| <= q/2 + 2.
+// Bounds are tracked per register at compile time (units of q/16) and a value is reduced only when
+// the next operation would leave the exact range, so the lazy growth of the Cooley-Tukey
+// butterflies (+0.625 q per stage) costs about one reduction per value per six stages.
+//
+// Structure, layouts and tables are those of ntt2.cu (four-step M = R x C; pass A: chirp + column
+// forward transform + cross twiddle; pass B: row forward, x D^, row inverse, cross twiddle; pass C:
+// column inverse + output chirp + Z_m^* gather or reduction input), except that the forward
+// (natural -> bit-reversed) sub-transforms use Cooley-Tukey butterflies (x + s y, x - s y) with one
+// twiddle s = omega_L^{brev(b)} per block b (the CRT splitting X^{2h} - c = (X^h - s)(X^h + s)),
+// whose bounds grow linearly, instead of Gentleman-Sande butterflies whose sums double per stage.
+// The output order (bit-reversed) and therefore every table and the results are unchanged.
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace bc {
+
+namespace f64 {
+
+constexpr int UQ = 16;        // canonical residue, [0, q)
+constexpr int UMUL = 10;      // fmm output, |r| <= 0.625 q
+constexpr int URED = 9;       // fred output, |r| <= q/2 + 2
+constexpr int LIM_MUL = 64;   // fmm input, |a| <= 4q (q < 2^50: |a wq| <= 2q < 2^51, |a| < 2^52)
+constexpr int LIM_VAL = 128;  // any value, |v| <= 8q < 2^53
+
+constexpr double RND = 6755399441055744.0;   // 1.5 * 2^52: fl(x + RND) - RND = rint(x) for |x| < 2^51
+
+__device__ __forceinline__ double fmm(double a, double2 w, double q) {
+    const double h = __dmul_rn(a, w.x);
+    const double l = __fma_rn(a, w.x, -h);
+    const double t = __dsub_rn(__fma_rn(a, w.y, RND), RND);
+    const double r = __fma_rn(-t, q, h);
+    return __dadd_rn(r, l);
+}
+__device__ __forceinline__ double fred(double x, double q, double qi) {
+    const double t = __dsub_rn(__fma_rn(x, qi, RND), RND);
+    return __fma_rn(-t, q, x);
+}
+// canonical residue of |x| <= 0.625 q (after fmm) or <= q/2 + 2 (after fred) -> u64
+__device__ __forceinline__ uint64_t to_u64(double x, double q) {
+    const double c = x < 0.0 ? __dadd_rn(x, q) : x;
+    return (uint64_t)__double_as_longlong(__dadd_rn(c, 4503599627370496.0)) - 0x4330000000000000ull;
+}
+__device__ __forceinline__ double from_u64(uint64_t x) {   // x < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), 4503599627370496.0);
+}
+
+// make v[k] a valid fmm input / keep the exact range
+template <int E>
+__device__ __forceinline__ void need(double (&v)[E], int (&bd)[E], int k, int lim, double q, double qi) {
+    if (bd[k] > lim) { v[k] = fred(v[k], q, qi); bd[k] = URED; }
+}
+// at a register-pass boundary: every register takes the largest bound (the exchange permutes them);
+// if the NS stages ahead would push fmm inputs past LIM_MUL, reduce all now (each value once per pass
+// instead of the y operands of every later stage and the epilogue operands)
+template <int E>
+__device__ __forceinline__ void flatten(double (&v)[E], int (&bd)[E], int ns, double q, double qi) {
+    int mx = 0;
+#pragma unroll
+    for (int k = 0; k < E; ++k) mx = bd[k] > mx ? bd[k] : mx;
+    const bool red = mx + UMUL * ns > LIM_MUL;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        if (red) v[k] = fred(v[k], q, qi);
+        bd[k] = red ? URED : mx;
+    }
+}
+
+// One register pass of NS <= LOGE stages on registers k, k + 2^u (u = stage within the pass).
+// FWD (natural -> bit-reversed, DIF order u = NS-1 .. 0): block b = i >> (lh+1) of the held index i,
+//   s = tb[b] = omega_L^{brev_{logL-1}(b)};  b = ((tau >> LO) << (LOGE-u-1)) + (k >> (u+1)).
+// INV (bit-reversed -> natural, u = 0 .. NS-1): s = omega_L^{-(i mod h) L/2h} (as ntt2.cu).
+// Both: y' = s y, (x, y) <- (x + y', x - y').  s = 1 is skipped where it is known at compile time.
+// Passes after the first take their twiddles from a per-thread table pt[e * TPR] (smem, entry-major,
+// thread-minor: conflict-free), e = the entry of (stage u, block or kpart) below; the first pass
+// (FWD: TOP, INV: LO = 0) has compile-time indices into tw (broadcast reads).
+__host__ __device__ constexpr int pt_entry_f(int LOGE, int u, int bk) { return (1 << LOGE) - (1 << (LOGE - u)) + bk; }
+__host__ __device__ constexpr int pt_entry_i(int u, int kp) { return (1 << u) - 1 + kp; }
+
+template <int LOGE, int NS, bool FWD, int LO, bool TOP>
+__device__ __forceinline__ void freg_pass(double (&v)[1 << LOGE], int (&bd)[1 << LOGE], uint32_t tau, const double2 *__restrict__ tw,
+                                          const double2 *__restrict__ pt, int TPR, int logL, double q, double qi) {
+    constexpr int E = 1 << LOGE;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int u = FWD ? (NS - 1 - s) : s;
+        const int lh = LO + u;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            if (k & (1 << u)) continue;
+            const int k2 = k + (1 << u);
+            bool trivial;
+            uint32_t ti;
+            if (FWD) {
+                const uint32_t bk = (uint32_t)(k >> (u + 1));
+                trivial = TOP && bk == 0;                       // TOP: tau >> LO == 0
+                ti = TOP ? bk : (((tau >> LO) << (LOGE - u - 1)) + bk);
+            } else {
+                const uint32_t kpart = (uint32_t)(k & ((1 << u) - 1));
+                trivial = LO == 0 && kpart == 0;
+                ti = ((tau & ((1u << LO) - 1)) + (kpart << LO)) << (logL - 1 - lh);
+            }
+            double y;
+            int by;
+            if (trivial) {
+                y = v[k2];
+                by = bd[k2];
+                if (bd[k] + by > LIM_VAL) { need(v, bd, k2, 0, q, qi); y = v[k2]; by = URED; }
+            } else {
+                need(v, bd, k2, LIM_MUL, q, qi);
+                const bool first = FWD ? TOP : (LO == 0);
+                const int e = FWD ? pt_entry_f(LOGE, u, k >> (u + 1)) : pt_entry_i(u, k & ((1 << u) - 1));
+                y = fmm(v[k2], first ? tw[ti] : pt[e * TPR], q);
+                by = UMUL;
+            }
+            need(v, bd, k, LIM_VAL - by, q, qi);
+            const double x = v[k];
+            v[k] = __dadd_rn(x, y);
+            v[k2] = __dsub_rn(x, y);
+            bd[k] = bd[k2] = bd[k] + by;
+        }
+    }
+}
+
+template <int LOGL, int LOGE>
+struct Passes {
+    static constexpr int REM = LOGL % LOGE;
+    static constexpr int NFULL = LOGL / LOGE;
+    static constexpr int NP = NFULL + (REM ? 1 : 0);
+    __device__ static constexpr int dif_lo(int p) { return p < NFULL ? LOGL - LOGE * (p + 1) : 0; }
+    __device__ static constexpr int dif_ns(int p) { return p < NFULL ? LOGE : REM; }
+    __device__ static constexpr int dit_lo(int p) { return REM ? (p == 0 ? 0 : REM + LOGE * (p - 1)) : LOGE * p; }
+    __device__ static constexpr int dit_ns(int p) { return REM ? (p == 0 ? REM : LOGE) : LOGE; }
+};
+
+template <int LOGE>
+__device__ __forceinline__ uint32_t held_index(uint32_t tau, int lo, int k) {
+    return (tau & ((1u << lo) - 1)) + ((tau >> lo) << (lo + LOGE)) + ((uint32_t)k << lo);
+}
+
+// per-thread twiddle tables of passes 1 .. NP-1 of one transform direction: pt[((P-1) NE + e) TPR + tau]
+template <int LOGL, int LOGE, bool FWD>
+struct PtTab {
+    static constexpr int NE = (1 << LOGE) - 1;
+    static constexpr int TPR = 1 << (LOGL - LOGE);
+    static constexpr int NPT = Passes<LOGL, LOGE>::NP - 1;
+    static constexpr int WORDS = NPT > 0 ? NPT * NE * TPR : 1;   // double2 entries
+    __device__ static void fill(double2 *pt, uint32_t tau, const double2 *__restrict__ tw) {
+        typedef Passes<LOGL, LOGE> PS;
+#pragma unroll
+        for (int P = 1; P < PS::NP; ++P) {
+            const int lo = FWD ? PS::dif_lo(P) : PS::dit_lo(P);
+            const int ns = FWD ? PS::dif_ns(P) : PS::dit_ns(P);
+            double2 *d = pt + (size_t)(P - 1) * NE * TPR + tau;
+            for (int u = 0; u < ns; ++u) {
+                if (FWD) {
+                    for (int j = 0; j < (1 << (LOGE - 1 - u)); ++j)
+                        d[pt_entry_f(LOGE, u, j) * TPR] = tw[((tau >> lo) << (LOGE - u - 1)) + j];
+                } else {
+                    for (int j = 0; j < (1 << u); ++j)
+                        d[pt_entry_i(u, j) * TPR] = tw[((tau & ((1u << lo) - 1)) + ((uint32_t)j << lo)) << (LOGL - 1 - lo - u)];
+                }
+            }
+        }
+    }
+};
+
+// row transform (element i at srow[i + (i >> LOGE)])
+template <int LOGL, int LOGE, bool FWD, int P>
+__device__ __forceinline__ void frt_pass(double (&v)[1 << LOGE], int (&bd)[1 << LOGE], uint32_t tau, double *srow,
+                                         const double2 *__restrict__ tw, const double2 *__restrict__ pt, double q, double qi) {
+    typedef Passes<LOGL, LOGE> PS;
+    constexpr int E = 1 << LOGE;
+    constexpr int lo = FWD ? PS::dif_lo(P) : PS::dit_lo(P);
+    constexpr int ns = FWD ? PS::dif_ns(P) : PS::dit_ns(P);
+    if (P > 0) {
+        constexpr int plo = FWD ? PS::dif_lo(P > 0 ? P - 1 : 0) : PS::dit_lo(P > 0 ? P - 1 : 0);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const uint32_t i = held_index<LOGE>(tau, plo, k);
+            srow[i + (i >> LOGE)] = v[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const uint32_t i = held_index<LOGE>(tau, lo, k);
+            v[k] = srow[i + (i >> LOGE)];
+        }
+        __syncthreads();
+        flatten(v, bd, ns, q, qi);
+    }
+    constexpr int TPR = 1 << (LOGL - LOGE);
+    freg_pass<LOGE, ns, FWD, lo, (FWD && P == 0)>(v, bd, tau, tw, pt + (size_t)(P > 0 ? P - 1 : 0) * (E - 1) * TPR + tau,
+                                                  TPR, LOGL, q, qi);
+    if (P + 1 < PS::NP) frt_pass<LOGL, LOGE, FWD, (P + 1 < PS::NP ? P + 1 : P)>(v, bd, tau, srow, tw, pt, q, qi);
+}
+
+// column transform (element i of column col at scol[i * TC + col])
+template <int LOGL, int LOGE, bool FWD, int TC, int P>
+__device__ __forceinline__ void fct_pass(double (&v)[1 << LOGE], int (&bd)[1 << LOGE], uint32_t tau, uint32_t col,
+                                         double *scol, const double2 *__restrict__ tw, const double2 *__restrict__ pt, double q, double qi) {
+    typedef Passes<LOGL, LOGE> PS;
+    constexpr int E = 1 << LOGE;
+    constexpr int lo = FWD ? PS::dif_lo(P) : PS::dit_lo(P);
+    constexpr int ns = FWD ? PS::dif_ns(P) : PS::dit_ns(P);
+    if (P > 0) {
+        constexpr int plo = FWD ? PS::dif_lo(P > 0 ? P - 1 : 0) : PS::dit_lo(P > 0 ? P - 1 : 0);
+#pragma unroll
+        for (int k = 0; k < E; ++k) scol[held_index<LOGE>(tau, plo, k) * TC + col] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < E; ++k) v[k] = scol[held_index<LOGE>(tau, lo, k) * TC + col];
+        __syncthreads();
+        flatten(v, bd, ns, q, qi);
+    }
+    constexpr int TPR = 1 << (LOGL - LOGE);
+    freg_pass<LOGE, ns, FWD, lo, (FWD && P == 0)>(v, bd, tau, tw, pt + (size_t)(P > 0 ? P - 1 : 0) * (E - 1) * TPR + tau,
+                                                  TPR, LOGL, q, qi);
+    if (P + 1 < PS::NP) fct_pass<LOGL, LOGE, FWD, TC, (P + 1 < PS::NP ? P + 1 : P)>(v, bd, tau, col, scol, tw, pt, q, qi);
+}
+
+#ifndef NTT_REG_TARGET
+#define NTT_REG_TARGET 64
+#endif
+#define FNTT_MINB(threads) ((65536 / NTT_REG_TARGET) / (threads) > 0 ? (65536 / NTT_REG_TARGET) / (threads) : 1)
+
+struct JobF {
+    uint32_t poly, lb, pr;
+};
+__device__ __forceinline__ JobF job_f(const LimbMap &lm, uint32_t job) {
+    JobF j;
+    const uint32_t jl = job / lm.npoly;
+    j.poly = job - jl * lm.npoly;
+    j.lb = lm.limb(jl);
+    j.pr = lm.prime(j.lb);
+    return j;
+}
+
+// pass A: chirp, column forward transform (length R), x psi^(c brev(rp)); scratch[rp*C + c] (doubles, |v| <= 0.625q)
+template <int LOGR, int LOGE, int TC, int INV, int LOGC>
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 << (LOGR - LOGE))))
+    kf_passA(NttTables T, const uint64_t *__restrict__ in, uint64_t in_pstride, LimbMap lm, uint64_t job0,
+             double *__restrict__ scratch) {
+    constexpr int E = 1 << LOGE, R = 1 << LOGR;
+    constexpr uint32_t CC = 1u << LOGC;
+    extern __shared__ double smf[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobF J = job_f(lm, job);
+    const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+    const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
+    const uint32_t c = blockIdx.x * TC + col;
+    const double2 *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
+    const uint64_t *src = in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
+    typedef PtTab<LOGR, LOGE, true> PTT;
+    double2 *stw = (double2 *)(smf + (size_t)R * TC), *spt = stw + R / 2;
+    const double2 *gtw = T.ftwRb + (uint64_t)J.pr * (R / 2);
+    for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = gtw[j];
+    if (col == 0) PTT::fill(spt, tau, gtw);
+    double v[E];
+    int bd[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
+        const uint32_t t = r * CC + c;
+        double x = 0.0;
+        if (!INV) {
+            if (t < T.n) x = fmm(from_u64(__ldcs(src + t)), tf[t], q);
+        } else if (t < T.m) {
+            const int ps = T.pos[t];
+            if (ps >= 0) x = fmm(from_u64(__ldcs(src + ps)), tf[t], q);
+        }
+        v[k] = x;
+        bd[k] = UMUL;
+    }
+    __syncthreads();
+    fct_pass<LOGR, LOGE, true, TC, 0>(v, bd, tau, col, smf, stw, spt, q, qi);
+    const double2 *xt = T.fxta + (uint64_t)J.pr * T.M;
+    double *dst = scratch + (uint64_t)blockIdx.y * T.M;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const uint32_t rp = held_index<LOGE>(tau, 0, k);
+        need(v, bd, k, LIM_MUL, q, qi);
+        __stcs(dst + rp * CC + c, fmm(v[k], xt[rp * CC + c], q));
+    }
+}
+
+// pass B: row forward (length C), x D^, row inverse, x psi^(-c brev(r)); block = RB rows x C/E threads
+template <int LOGC, int LOGE, int RB, int INV>
+__global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), FNTT_MINB(RB * (1 << (LOGC - LOGE))))
+    kf_passB(NttTables T, LimbMap lm, uint64_t job0, double *__restrict__ scratch) {
+    constexpr int E = 1 << LOGE, C = 1 << LOGC, TPR = C / E;
+    constexpr int ROWW = C + C / E;
+    extern __shared__ double smf[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobF J = job_f(lm, job);
+    const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+    const uint32_t rr = threadIdx.x / TPR, tau = threadIdx.x % TPR;
+    const uint32_t row = blockIdx.x * RB + rr;
+    double *srow = smf + rr * ROWW;
+    double *grow = scratch + (uint64_t)blockIdx.y * T.M + (uint64_t)row * C;
+    typedef PtTab<LOGC, LOGE, true> PTF;
+    typedef PtTab<LOGC, LOGE, false> PTI;
+    double2 *tw = (double2 *)(smf + (size_t)RB * ROWW), *twi = tw + C / 2, *ptf = twi + C / 2, *pti = ptf + PTF::WORDS;
+    const double2 *gtw = T.ftwCb + (uint64_t)J.pr * (C / 2), *gtwi = T.ftwCi + (uint64_t)J.pr * (C / 2);
+    for (int j = threadIdx.x; j < C / 2; j += blockDim.x) {
+        tw[j] = gtw[j];
+        twi[j] = gtwi[j];
+    }
+    if (rr == 0) PTF::fill(ptf, tau, gtw);
+    if (rr == 1 % RB) PTI::fill(pti, tau, gtwi);
+    double v[E];
+    int bd[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        v[k] = __ldcs(grow + held_index<LOGE>(tau, LOGC - LOGE, k));
+        bd[k] = UMUL;
+    }
+    __syncthreads();
+    frt_pass<LOGC, LOGE, true, 0>(v, bd, tau, srow, tw, ptf, q, qi);
+    // D^ in the thread-minor layout of this pass (entry of position tau*E + k at k*TPR + tau: coalesced)
+    const double2 *dh = (INV ? T.fdhi : T.fdhf) + (uint64_t)J.pr * T.M + (uint64_t)row * C + tau;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        need(v, bd, k, LIM_MUL, q, qi);
+        v[k] = fmm(v[k], dh[k * TPR], q);
+        bd[k] = UMUL;
+    }
+    frt_pass<LOGC, LOGE, false, 0>(v, bd, tau, srow, twi, pti, q, qi);
+    const double2 *xt = T.fxtb + (uint64_t)J.pr * T.M + (uint64_t)row * C;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const uint32_t cc = held_index<LOGE>(tau, LOGC - LOGE, k);
+        need(v, bd, k, LIM_MUL, q, qi);
+        __stcs(grow + cc, fmm(v[k], xt[cc], q));
+    }
+}
+
+// pass C: column inverse (length R) -> natural t, output chirp, canonical u64: Z_m^* gather (fwd) or A_t (inv)
+template <int LOGR, int LOGE, int TC, int INV, int LOGC>
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 << (LOGR - LOGE))))
+    kf_passC(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride, LimbMap lm, uint64_t job0,
+             double *__restrict__ scratch) {
+    constexpr int E = 1 << LOGE, R = 1 << LOGR;
+    constexpr uint32_t CC = 1u << LOGC;
+    extern __shared__ double smf[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobF J = job_f(lm, job);
+    const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+    const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
+    const uint32_t c = blockIdx.x * TC + col;
+    double *scr = scratch + (uint64_t)blockIdx.y * T.M;
+    typedef PtTab<LOGR, LOGE, false> PTT;
+    double2 *stw = (double2 *)(smf + (size_t)R * TC), *spt = stw + R / 2;
+    const double2 *gtw = T.ftwRi + (uint64_t)J.pr * (R / 2);
+    for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = gtw[j];
+    if (col == 0) PTT::fill(spt, tau, gtw);
+    double v[E];
+    int bd[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        v[k] = __ldcs(scr + held_index<LOGE>(tau, 0, k) * CC + c);
+        bd[k] = UMUL;
+    }
+    __syncthreads();
+    fct_pass<LOGR, LOGE, false, TC, 0>(v, bd, tau, col, smf, stw, spt, q, qi);
+    const double2 *tfo = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
+    uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
+    uint64_t *scru = (uint64_t *)scr;
+    if (INV) __syncthreads();   // all columns of this block read before in-place writes of A_t
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
+        const uint32_t t = r * CC + c;
+        need(v, bd, k, LIM_MUL, q, qi);
+        if (t >= T.m) continue;
+        const uint64_t x = to_u64(fmm(v[k], tfo[t], q), q);
+        if (!INV) {
+            const int ps = T.pos[t];
+            if (ps >= 0) __stcs(dst + ps, x);
+        } else {
+            scru[t] = x;
+        }
+    }
+}
+
+template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_, int RB_>
+struct Shape {
+    static constexpr int TC = TC_, RB = RB_ ? RB_ : ((LOGC - LOGEC) >= 6 ? 4 : ((LOGC - LOGEC) >= 4 ? 8 : 16));
+    static constexpr int THA = TC << (LOGR - LOGER), THB = RB << (LOGC - LOGEC);
+    static constexpr size_t SMA = (size_t)(1 << LOGR) * TC * 8 + (size_t)(1 << LOGR) / 2 * 16 +
+                                  (size_t)(PtTab<LOGR, LOGER, true>::WORDS > PtTab<LOGR, LOGER, false>::WORDS
+                                               ? PtTab<LOGR, LOGER, true>::WORDS : PtTab<LOGR, LOGER, false>::WORDS) * 16;
+    static constexpr size_t SMB = (size_t)RB * ((1 << LOGC) + (1 << (LOGC - LOGEC))) * 8 + (size_t)(1 << LOGC) * 16 +
+                                  (size_t)(PtTab<LOGC, LOGEC, true>::WORDS + PtTab<LOGC, LOGEC, false>::WORDS) * 16;
+};
+
+template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
+static void runf(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
+    typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 0, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 1, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 0, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 1, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
+        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
+        init = true;
+    }
+    double *scr = (double *)scratch;
+    dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
+    if (!inv) {
+        kf_passA<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
+        kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
+        kf_passC<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr);
+    } else {
+        kf_passA<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
+        kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
+        kf_passC<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr);
+    }
+    launch_counter() += 3;
+}
+
+}  // namespace f64
+
+// register count E = 2^LOGE of the pass-B row transform of each shape (the D^ table layout depends on it)
+int nttf_row_loge(uint32_t logR, uint32_t logC) {
+    switch (logR * 16 + logC) {
+        case 8 * 16 + 9: case 6 * 16 + 6: case 5 * 16 + 6: return 3;
+        default: return 4;
+    }
+}
+
+bool nttf_supported(const NttTables &T) {
+    return T.fmods != nullptr && ntt2_supported(T);
+}
+
+void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
+#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st)
+    switch (T.logR * 16 + T.logC) {
+        case 8 * 16 + 8:
+            switch (g_ntt_impl) {
+                case 11: RUNF(8, 4, 8, 4, 4); break;
+                case 12: RUNF(8, 4, 8, 4, 8); break;
+                case 14: RUNF(8, 4, 8, 4, 16, 4); break;
+                default: RUNF(8, 4, 8, 4, 16); break;      // measured best (1.06 us per limb-transform)
+            }
+            break;
+        case 8 * 16 + 9:
+            if (g_ntt_impl == 12) RUNF(8, 4, 9, 3, 8);
+            else RUNF(8, 4, 9, 3, 16);
+            break;
+        case 7 * 16 + 8: RUNF(7, 4, 8, 4, 16); break;
+        case 7 * 16 + 7: RUNF(7, 4, 7, 4, 16); break;
+        case 6 * 16 + 7: RUNF(6, 3, 7, 4, 16); break;
+        case 6 * 16 + 6: RUNF(6, 3, 6, 3, 16); break;
+        case 5 * 16 + 6: RUNF(5, 4, 6, 3, 16); break;
+        default: break;
+    }
+#undef RUNF
+}
+
+}  // namespace bc

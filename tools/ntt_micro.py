@@ -16,7 +16,8 @@ x = torch.randint(0, 1 << 40, (npoly, L, ctx.n), dtype=torch.int64, device="cuda
 ws = ctx.workspace(npoly * L * ctx.M * 8 + (64 << 20))
 work = bc.ntt_work(ctx) * npoly * L
 ref = None
-for impl, gmb in [(1, 4096), (0, 4096), (2, 4096), (3, 4096), (4, 4096), (5, 4096), (6, 4096)]:
+ref_inv = None
+for impl, gmb in [(1, 4096), (7, 4096), (0, 4096), (0, 64), (0, 256), (11, 4096), (12, 4096), (13, 4096), (14, 4096)]:
     bc.set_ntt_impl(impl)
     bc._lib.bc_tune(b"ntt_group_bytes", gmb << 20)
     for _ in range(2):
@@ -37,9 +38,11 @@ for impl, gmb in [(1, 4096), (0, 4096), (2, 4096), (3, 4096), (4, 4096), (5, 409
     i = e0.elapsed_time(e1) / 5
     if ref is None:
         ref = y.clone()
-    ok = bool(torch.equal(y, ref))
+    if ref_inv is None:
+        ref_inv = z.clone()
+    ok = bool(torch.equal(y, ref)) and bool(torch.equal(z, ref_inv))
     print(json.dumps({"limbs": npoly * L, "impl": impl, "group_mb": gmb, "fwd_ms": round(f, 3), "inv_ms": round(i, 3),
                       "us_per_limb_fwd": round(1000 * f / (npoly * L), 3),
-                      "Tmulmod_s": round(work / (f / 1e3) / 1e12, 3), "matches_radix2": ok}), flush=True)
+                      "Tmulmod_s": round(work / (f / 1e3) / 1e12, 3), "matches_radix2": ok, "roundtrip": bool(torch.equal(ctx.ntt_inv(y, ws=ws), x))}), flush=True)
 bc.set_ntt_impl(0)
 bc._lib.bc_tune(b"ntt_group_bytes", 48 << 20)
