@@ -638,13 +638,13 @@ def roofline(ctx, bc, live, step_ms_total):
     """Dominant kernel family (Bluestein NTT passes, integer-pipe bound), measured LIVE in the timed
     region: CUDA event pairs around every NTT call on the launching stream (bc_ntt_timing).
     achieved = limb-transforms x algorithmic 64-bit modular multiplications per limb-transform
-     / summed NTT time; peak = IMAD-derived mulmod rate at the max SM clock."""
+     / summed NTT time; peak = FP64-pipe modular-butterfly rate at the max SM clock."""
     ms, jobs, calls = live
     if not calls or ms <= 0:
         return {"bound": "alu", "error": "no NTT calls timed"}
     work = bc.ntt_work(ctx)
     achieved = jobs * work / (ms / 1e3) / 1e12
-    peak = bc.SMS * bc.IMAD_PER_SM_PER_CLK * 1965.0e6 / bc.IMAD_PER_MULMOD / 1e12
+    peak = bc.ntt_peak(1965.0)
     traffic = None
     try:
         prof = load_json(os.path.join(ROOT, "profiles", "ntt_traffic.json"))
@@ -653,14 +653,14 @@ def roofline(ctx, bc, live, step_ms_total):
     except Exception:
         traffic = None
     return {"bound": "alu", "kernel": "bluestein_ntt (passA+passB+passC [+reduce]) per ntt_forward/ntt_inverse call",
-            "achieved": achieved, "peak": peak, "unit": "T mulmod64/s", "frac": achieved / peak,
+            "achieved": achieved, "peak": peak, "unit": "T modmul/s", "frac": achieved / peak,
             "traffic": traffic, "per_launch_ms": ms / calls, "limb_transforms_per_launch": jobs / calls,
             "work_per_limb_transform": work, "launches_timed": calls, "share_of_step": ms / step_ms_total,
             "how": "CUDA events on the launching stream around every NTT call inside the timed region",
             "traffic_note": "ncu --set full dram__bytes_read+write per limb-transform (profiles/ntt_traffic.json) x "
                             "limb-transforms per call",
-            "peak_note": "148 SM x 64 IMAD/clk x 1965 MHz / %d IMAD per 64-bit Shoup mulmod (guide unit counts)"
-                         % bc.IMAD_PER_MULMOD}
+            "peak_note": "148 SM x 64 DFMA/clk (measured 18.2e12/s, tools/micro/bfly_micro.cu) x 1965 MHz / %d "
+                         "binary64 ops per modular butterfly (ntt3.cu)" % bc.FP64_PER_MODBFLY}
 
 
 if __name__ == "__main__":

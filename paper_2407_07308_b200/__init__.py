@@ -482,9 +482,16 @@ def load_params(name_or_path):
 # ------------------------------------------------------------------------------------------
 # roofline probe of the dominant kernel family (Bluestein NTT passes)
 # ------------------------------------------------------------------------------------------
-IMAD_PER_SM_PER_CLK = 64          # B200 integer multiply-add issue rate per SM (guide)
 SMS = 148
+FP64_PER_SM_PER_CLK = 64          # B200 DFMA lanes per SM per clock: measured 18.2e12/s (tools/micro/bfly_micro.cu)
+FP64_PER_MODBFLY = 8              # one modular butterfly in binary64 (ntt3.cu): DMUL + 3 DFMA + 2 DADD (product) + 2 DADD
+IMAD_PER_SM_PER_CLK = 64          # integer path (ntt2.cu, impl 7): IMAD issue rate per SM (guide)
 IMAD_PER_MULMOD = 10              # 64-bit Shoup product: mul.hi.u64 (4) + 2 x mul.lo.u64 (3): SASS-checked
+
+
+def ntt_peak(sm_mhz=1965.0):
+    """peak modular butterflies (or pointwise products) per second of the binary64 NTT, in T/s"""
+    return SMS * FP64_PER_SM_PER_CLK * sm_mhz * 1e6 / FP64_PER_MODBFLY / 1e12
 
 
 def ntt_work(ctx):
@@ -515,7 +522,7 @@ def profile_ntt(ctx, npoly=64, reps=5, sm_mhz=1965.0):
     ms = e0.elapsed_time(e1) / reps
     work = npoly * L * ntt_work(ctx)
     achieved = work / (ms / 1e3) / 1e12
-    peak = SMS * IMAD_PER_SM_PER_CLK * sm_mhz * 1e6 / IMAD_PER_MULMOD / 1e12
+    peak = ntt_peak(sm_mhz)
     traffic = None
     try:
         import json
@@ -525,8 +532,8 @@ def profile_ntt(ctx, npoly=64, reps=5, sm_mhz=1965.0):
     except Exception:
         traffic = None
     return {"bound": "alu", "kernel": "bluestein_ntt (passA+passB+passC)", "achieved": achieved, "peak": peak,
-            "unit": "T mulmod64/s", "frac": achieved / peak, "traffic": traffic,
+            "unit": "T modmul/s", "frac": achieved / peak, "traffic": traffic,
             "traffic_note": "DRAM bytes per probe launch from profiles/r1_ntt_probe_ncu.json (ncu --set full)",
             "per_launch_ms": ms, "limb_transforms_per_launch": npoly * L,
             "work_per_limb_transform": ntt_work(ctx),
-            "peak_note": "148 SM x 64 IMAD/clk x %.0f MHz / %d IMAD per 64-bit mulmod" % (sm_mhz, IMAD_PER_MULMOD)}
+            "peak_note": "148 SM x 64 DFMA/clk x %.0f MHz / %d FP64 ops per modular butterfly" % (sm_mhz, FP64_PER_MODBFLY)}

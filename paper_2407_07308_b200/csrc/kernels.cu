@@ -79,6 +79,16 @@ static inline unsigned grid_for(uint64_t total, unsigned threads, unsigned cap =
     return (unsigned)g;
 }
 
+// Row-wise 2D launches (no per-element 64-bit division): blockIdx.x/threadIdx.x over the n coefficients
+// of one row (a (ciphertext, part, limb) polynomial limb), blockIdx.y over rows.
+#define ROW_LOOP(RV_, XV_, NROWS_, N_)                                  \
+    const uint32_t XV_ = blockIdx.x * blockDim.x + threadIdx.x;         \
+    if (XV_ >= (N_)) return;                                            \
+    for (uint32_t RV_ = blockIdx.y; RV_ < (NROWS_); RV_ += gridDim.y)
+static inline dim3 grid_rows(uint32_t n, uint64_t rows, unsigned threads = 256) {
+    return dim3((n + threads - 1) / threads, (unsigned)(rows < 65535 ? (rows ? rows : 1) : 65535));
+}
+
 // =====================================================================================
 // NTT building blocks (shared memory, radix-2)
 // =====================================================================================
@@ -262,10 +272,7 @@ __global__ void __launch_bounds__(256) k_passC(NttTables T, uint64_t *__restrict
 __global__ void k_reduce_prime(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride,
                                LimbMap lm, uint64_t job0, uint32_t njobs,
                                const uint64_t *__restrict__ scratch) {
-    const uint64_t total = (uint64_t)njobs * T.n;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t jr = (uint32_t)(i / T.n), x = (uint32_t)(i - (uint64_t)jr * T.n);
+    ROW_LOOP(jr, x, njobs, T.n) {
         const JobInfo J = job_info(lm, (uint32_t)(job0 + jr));
         const uint64_t q = T.mods[J.pr].q;
         const uint64_t *A = scratch + (uint64_t)jr * T.M;
@@ -331,7 +338,7 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
                 ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
             if (inv) {
                 if (T.prime_m)
-                    k_reduce_prime<<<grid_for((uint64_t)nj * T.n, 256), 256, 0, st>>>(T, out, out_pstride, lm, j0, nj,
+                    k_reduce_prime<<<grid_rows(T.n, nj), 256, 0, st>>>(T, out, out_pstride, lm, j0, nj,
                                                                                      scratch);
                 else
                     k_reduce_composite<<<nj, 256, 0, st>>>(T, out, out_pstride, lm, j0, scratch);
@@ -347,7 +354,7 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
             k_passB<1><<<gB, 256, smB, st>>>(T, lm, j0, scratch, lTR);
             k_passC<1><<<gA, 256, smA, st>>>(T, out, out_pstride, lm, j0, scratch, lTC);
             if (T.prime_m)
-                k_reduce_prime<<<grid_for((uint64_t)nj * T.n, 256), 256, 0, st>>>(T, out, out_pstride, lm, j0,
+                k_reduce_prime<<<grid_rows(T.n, nj), 256, 0, st>>>(T, out, out_pstride, lm, j0,
                                                                                  nj, scratch);
             else
                 k_reduce_composite<<<nj, 256, 0, st>>>(T, out, out_pstride, lm, j0, scratch);
@@ -383,110 +390,111 @@ void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t
 #define GRID_LOOP(i, total) \
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (total); i += (uint64_t)gridDim.x * blockDim.x)
 
+// residue of a small signed constant (|c| < q: the engine's constants are in F_p or small)
+__device__ __forceinline__ uint64_t small_res(int64_t c, uint64_t q) {
+    if (c >= 0) return (uint64_t)c < q ? (uint64_t)c : (uint64_t)c % q;
+    const uint64_t a = (uint64_t)(-c);
+    return a < q ? (a ? q - a : 0) : from_signed(c, q);
+}
+
 __global__ void k_add(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
-                      uint64_t *__restrict__ o, uint64_t total, uint32_t lvl, uint32_t n, int sub) {
-    GRID_LOOP(i, total) {
-        const uint32_t limb = (uint32_t)((i / n) % lvl);
-        const uint64_t q = mods[limb].q;
+                      uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n, int sub) {
+    ROW_LOOP(r, x, rows, n) {
+        const uint64_t q = mods[r % lvl].q, i = (uint64_t)r * n + x;
         o[i] = sub ? sub_mod(a[i], b[i], q) : add_mod(a[i], b[i], q);
     }
 }
 void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t parts,
             uint32_t lvl, uint32_t n, int sub, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * n;
-    k_add<<<grid_for(total, 256), 256, 0, st>>>(mods, a, b, o, total, lvl, n, sub);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_add<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n, sub);
     LAUNCHED();
 }
 
 __global__ void k_neg(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, uint64_t *__restrict__ o,
-                      uint64_t total, uint32_t lvl, uint32_t n) {
-    GRID_LOOP(i, total) {
-        const uint32_t limb = (uint32_t)((i / n) % lvl);
-        o[i] = neg_mod(a[i], mods[limb].q);
+                      uint32_t rows, uint32_t lvl, uint32_t n) {
+    ROW_LOOP(r, x, rows, n) {
+        const uint64_t i = (uint64_t)r * n + x;
+        o[i] = neg_mod(a[i], mods[r % lvl].q);
     }
 }
 void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
             uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * n;
-    k_neg<<<grid_for(total, 256), 256, 0, st>>>(mods, a, o, total, lvl, n);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_neg<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
 __global__ void k_scalar(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, int64_t c,
-                         uint64_t *__restrict__ o, uint64_t total, uint32_t lvl, uint32_t n) {
-    GRID_LOOP(i, total) {
-        const uint32_t limb = (uint32_t)((i / n) % lvl);
-        const Mod M = mods[limb];
-        o[i] = mul_mod(a[i], from_signed(c, M.q), M);
+                         uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
+    ROW_LOOP(r, x, rows, n) {
+        const Mod M = mods[r % lvl];
+        const uint64_t i = (uint64_t)r * n + x;
+        o[i] = mul_mod(a[i], small_res(c, M.q), M);
     }
 }
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
                uint32_t lvl, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * n;
-    k_scalar<<<grid_for(total, 256), 256, 0, st>>>(mods, a, c, o, total, lvl, n);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_scalar<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
 __global__ void k_add_const(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, int64_t c,
-                            uint64_t *__restrict__ o, uint64_t total, uint32_t parts, uint32_t lvl, uint32_t n) {
-    GRID_LOOP(i, total) {
-        const uint64_t r = i / n;
-        const uint32_t limb = (uint32_t)(r % lvl);
-        const uint32_t part = (uint32_t)((r / lvl) % parts);
-        const uint64_t q = mods[limb].q;
-        o[i] = part == 0 ? add_mod(a[i], from_signed(c, q), q) : a[i];
+                            uint64_t *__restrict__ o, uint32_t rows, uint32_t parts, uint32_t lvl, uint32_t n) {
+    ROW_LOOP(r, x, rows, n) {
+        const uint32_t limb = r % lvl, part = (r / lvl) % parts;
+        const uint64_t q = mods[limb].q, i = (uint64_t)r * n + x;
+        o[i] = part == 0 ? add_mod(a[i], small_res(c, q), q) : a[i];
     }
 }
 void ew_add_const(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
                   uint32_t lvl, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * n;
-    k_add_const<<<grid_for(total, 256), 256, 0, st>>>(mods, a, c, o, total, parts, lvl, n);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_add_const<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, parts, lvl, n);
     LAUNCHED();
 }
 
 __global__ void k_ptmul(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
-                        const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint64_t total,
+                        const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint32_t rows,
                         uint32_t lvl, uint32_t n) {
-    GRID_LOOP(i, total) {
-        const uint64_t r = i / n;
-        const uint32_t x = (uint32_t)(i - r * n);
-        const uint32_t limb = (uint32_t)(r % lvl);
+    ROW_LOOP(r, x, rows, n) {
+        const uint32_t limb = r % lvl;
+        const uint64_t i = (uint64_t)r * n + x;
         o[i] = mul_mod(a[i], pt[(uint64_t)limb * n + x], mods[limb]);
     }
 }
 void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B, uint32_t parts,
               uint32_t lvl, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * n;
-    k_ptmul<<<grid_for(total, 256), 256, 0, st>>>(mods, a, pt, o, total, lvl, n);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_ptmul<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, pt, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
 __global__ void k_add_pt(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
-                         const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint64_t total,
+                         const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint32_t rows,
                          uint32_t parts, uint32_t lvl, uint32_t n) {
-    GRID_LOOP(i, total) {
-        const uint64_t r = i / n;
-        const uint32_t x = (uint32_t)(i - r * n);
-        const uint32_t limb = (uint32_t)(r % lvl);
-        const uint32_t part = (uint32_t)((r / lvl) % parts);
+    ROW_LOOP(r, x, rows, n) {
+        const uint32_t limb = r % lvl, part = (r / lvl) % parts;
+        const uint64_t i = (uint64_t)r * n + x;
         o[i] = part == 0 ? add_mod(a[i], pt[(uint64_t)limb * n + x], mods[limb].q) : a[i];
     }
 }
 void ew_add_pt(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B, uint32_t parts,
                uint32_t lvl, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * n;
-    k_add_pt<<<grid_for(total, 256), 256, 0, st>>>(mods, a, pt, o, total, parts, lvl, n);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_add_pt<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, pt, o, (uint32_t)rows, parts, lvl, n);
     LAUNCHED();
 }
 
 // tensor: (a0 b0, a0 b1 + a1 b0, a1 b1)
 __global__ void k_tensor(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
-                         const uint64_t *__restrict__ b, uint64_t *__restrict__ o, uint64_t total,
+                         const uint64_t *__restrict__ b, uint64_t *__restrict__ o, uint32_t rows,
                          uint32_t lvl, uint32_t n) {
     const uint64_t ln = (uint64_t)lvl * n;
-    GRID_LOOP(i, total) {   // i over B * lvl * n
-        const uint64_t bi = i / ln, r = i - bi * ln;
-        const uint32_t limb = (uint32_t)(r / n);
+    ROW_LOOP(rw, x, rows, n) {   // rows = B * lvl
+        const uint32_t bi = rw / lvl, limb = rw - bi * lvl;
+        const uint64_t r = (uint64_t)limb * n + x;
         const Mod M = mods[limb];
         const uint64_t a0 = a[bi * 2 * ln + r], a1 = a[bi * 2 * ln + ln + r];
         const uint64_t b0 = b[bi * 2 * ln + r], b1 = b[bi * 2 * ln + ln + r];
@@ -498,57 +506,51 @@ __global__ void k_tensor(const Mod *__restrict__ mods, const uint64_t *__restric
 }
 void ew_tensor(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t lvl,
                uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * lvl * n;
-    k_tensor<<<grid_for(total, 256), 256, 0, st>>>(mods, a, b, o, total, lvl, n);
+    const uint64_t rows = (uint64_t)B * lvl;
+    k_tensor<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
 // automorphism sigma_t in evaluation form: E'[k] = E[pos[t z_k mod m]]
 __global__ void k_automorph(NttTables T, const uint64_t *__restrict__ a, uint64_t *__restrict__ o,
-                            uint64_t total, uint32_t t) {
-    GRID_LOOP(i, total) {
-        const uint64_t r = i / T.n;
-        const uint32_t x = (uint32_t)(i - r * T.n);
-        const uint32_t src = (uint32_t)T.pos[(uint32_t)(((uint64_t)t * (uint32_t)T.z[x]) % T.m)];
-        o[i] = a[r * T.n + src];
-    }
+                            uint32_t rows, uint32_t t) {
+    const uint32_t xx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xx >= T.n) return;
+    const uint32_t src = (uint32_t)T.pos[(uint32_t)(((uint64_t)t * (uint32_t)T.z[xx]) % T.m)];
+    ROW_LOOP(r, x, rows, T.n) o[(uint64_t)r * T.n + x] = a[(uint64_t)r * T.n + src];
 }
 // part 0 of each ciphertext of a (batch stride abs) -> o [B][1][lvl][n], permuted by sigma_t
 __global__ void k_automorph_part(NttTables T, const uint64_t *__restrict__ a, uint64_t abs, uint64_t *__restrict__ o,
-                                 uint64_t total, uint32_t lvl, uint32_t t) {
-    const uint64_t per = (uint64_t)lvl * T.n;
-    GRID_LOOP(i, total) {
-        const uint64_t b = i / per, rr = i - b * per;
-        const uint64_t r = rr / T.n;
-        const uint32_t x = (uint32_t)(rr - r * T.n);
-        const uint32_t src = (uint32_t)T.pos[(uint32_t)(((uint64_t)t * (uint32_t)T.z[x]) % T.m)];
-        o[i] = a[b * abs + r * T.n + src];
+                                 uint32_t rows, uint32_t lvl, uint32_t t) {
+    const uint32_t xx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xx >= T.n) return;
+    const uint32_t src = (uint32_t)T.pos[(uint32_t)(((uint64_t)t * (uint32_t)T.z[xx]) % T.m)];
+    ROW_LOOP(rw, x, rows, T.n) {   // rows = B * lvl
+        const uint32_t b = rw / lvl, r = rw - b * lvl;
+        o[(uint64_t)rw * T.n + x] = a[(uint64_t)b * abs + (uint64_t)r * T.n + src];
     }
 }
 void ew_automorph_part(const NttTables &T, const uint64_t *a, uint64_t abs, uint64_t *o, uint32_t B, uint32_t lvl,
                        uint32_t t, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * lvl * T.n;
-    k_automorph_part<<<grid_for(total, 256), 256, 0, st>>>(T, a, abs, o, total, lvl, t);
+    const uint64_t rows = (uint64_t)B * lvl;
+    k_automorph_part<<<grid_rows(T.n, rows), 256, 0, st>>>(T, a, abs, o, (uint32_t)rows, lvl, t);
     LAUNCHED();
 }
 void ew_automorph(const NttTables &T, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
                   uint32_t t, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * parts * lvl * T.n;
-    k_automorph<<<grid_for(total, 256), 256, 0, st>>>(T, a, o, total, t);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_automorph<<<grid_rows(T.n, rows), 256, 0, st>>>(T, a, o, (uint32_t)rows, t);
     LAUNCHED();
 }
 
 // copy parts [part0, part0+nparts) of a [B][parts_in][lvl_in][n] (first lvl_out limbs) into
 // o [B][parts_out][lvl_out][n] at part opart0
-__global__ void k_copy_parts(const uint64_t *__restrict__ a, uint64_t *__restrict__ o, uint64_t total,
+__global__ void k_copy_parts(const uint64_t *__restrict__ a, uint64_t *__restrict__ o, uint32_t rows,
                              uint32_t parts_in, uint32_t part0, uint32_t nparts, uint32_t lvl_in,
                              uint32_t lvl_out, uint32_t n, uint32_t parts_out, uint32_t opart0) {
-    GRID_LOOP(i, total) {   // over B * nparts * lvl_out * n
-        uint64_t r = i / n;
-        const uint32_t x = (uint32_t)(i - r * n);
-        const uint32_t limb = (uint32_t)(r % lvl_out);
-        r /= lvl_out;
-        const uint32_t k = (uint32_t)(r % nparts);
+    ROW_LOOP(rw, x, rows, n) {   // rows = B * nparts * lvl_out
+        const uint32_t limb = rw % lvl_out, r = rw / lvl_out;
+        const uint32_t k = r % nparts;
         const uint64_t b = r / nparts;
         o[((b * parts_out + opart0 + k) * lvl_out + limb) * n + x] =
             a[((b * parts_in + part0 + k) * lvl_in + limb) * n + x];
@@ -557,8 +559,8 @@ __global__ void k_copy_parts(const uint64_t *__restrict__ a, uint64_t *__restric
 void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in, uint32_t part0, uint32_t nparts,
                    uint32_t lvl_in, uint32_t lvl_out, uint32_t n, uint32_t parts_out, uint32_t opart0,
                    cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * nparts * lvl_out * n;
-    k_copy_parts<<<grid_for(total, 256), 256, 0, st>>>(a, o, total, parts_in, part0, nparts, lvl_in, lvl_out, n,
+    const uint64_t rows = (uint64_t)B * nparts * lvl_out;
+    k_copy_parts<<<grid_rows(n, rows), 256, 0, st>>>(a, o, (uint32_t)rows, parts_in, part0, nparts, lvl_in, lvl_out, n,
                                                       parts_out, opart0);
     LAUNCHED();
 }
@@ -585,16 +587,19 @@ __device__ __forceinline__ void mac128(uint64_t &hi, uint64_t &lo, uint64_t a, u
 
 __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__ d, uint64_t dps,
                       const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
-                      uint64_t *__restrict__ u, uint64_t total, uint32_t lvl, uint32_t K, uint32_t L1,
+                      uint64_t *__restrict__ u, uint32_t rows, uint32_t lvl, uint32_t K, uint32_t L1,
                       uint32_t alpha, uint32_t ndig, uint32_t n, const int32_t *__restrict__ pos,
                       const int32_t *__restrict__ zt, uint32_t m, uint32_t perm_t) {
     const uint32_t nl = lvl + K;
     const uint64_t ln = (uint64_t)nl * n;
-    GRID_LOOP(i, total) {   // over B * nl * n
-        const uint64_t b = i / ln, rr = i - b * ln;
-        const uint32_t r = (uint32_t)(rr / n), xo = (uint32_t)(rr - (uint64_t)r * n);
-        // R22: digits read through sigma_t's evaluation-index permutation
-        const uint32_t x = perm_t ? (uint32_t)pos[(uint32_t)(((uint64_t)perm_t * (uint32_t)zt[xo]) % m)] : xo;
+    const uint32_t x0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x0 >= n) return;
+    // R22: digits read through sigma_t's evaluation-index permutation
+    const uint32_t x = perm_t ? (uint32_t)pos[(uint32_t)(((uint64_t)perm_t * (uint32_t)zt[x0]) % m)] : x0;
+    ROW_LOOP(rw, xo, rows, n) {   // rows = B * nl
+        const uint64_t b = rw / nl;
+        const uint32_t r = rw - (uint32_t)b * nl;
+        const uint64_t rr = (uint64_t)r * n + xo;
         const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
         const Mod M = mods[kl];
         const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
@@ -611,16 +616,16 @@ __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__
 }
 void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
             uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * (lvl + K) * n;
-    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, dps, ext, key, u, total, lvl, K, L1, alpha, ndig, n, nullptr,
+    const uint64_t rows = (uint64_t)B * (lvl + K);
+    k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n, nullptr,
                                                 nullptr, 1, 0);
     LAUNCHED();
 }
 void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uint64_t *d, uint64_t dps,
                  const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1,
                  uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)B * (lvl + K) * n;
-    k_kip<<<grid_for(total, 256), 256, 0, st>>>(mods, d, dps, ext, key, u, total, lvl, K, L1, alpha, ndig, n, T.pos, T.z,
+    const uint64_t rows = (uint64_t)B * (lvl + K);
+    k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n, T.pos, T.z,
                                                 T.m, perm_t);
     LAUNCHED();
 }
@@ -628,48 +633,46 @@ void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uin
 // o[b] = a[b] + b[b] over parts x lvl x n words per ciphertext, with per-operand batch strides
 __global__ void k_add_bs(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, uint64_t abs,
                          const uint64_t *__restrict__ b, uint64_t bbs, uint64_t *__restrict__ o, uint64_t obs,
-                         uint64_t total, uint64_t per, uint32_t lvl, uint32_t n) {
-    GRID_LOOP(i, total) {
-        const uint64_t bi = i / per, r = i - bi * per;
-        const uint32_t limb = (uint32_t)((r / n) % lvl);
-        o[bi * obs + r] = add_mod(a[bi * abs + r], b[bi * bbs + r], mods[limb].q);
+                         uint32_t rows, uint32_t per_rows, uint32_t lvl, uint32_t n) {
+    ROW_LOOP(rw, x, rows, n) {   // rows = B * parts * lvl
+        const uint32_t bi = rw / per_rows, rr = rw - bi * per_rows;
+        const uint64_t r = (uint64_t)rr * n + x;
+        o[bi * obs + r] = add_mod(a[bi * abs + r], b[bi * bbs + r], mods[rr % lvl].q);
     }
 }
 void ew_add_bs(const Mod *mods, const uint64_t *a, uint64_t abs, const uint64_t *b, uint64_t bbs, uint64_t *o,
                uint64_t obs, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st) {
-    const uint64_t per = (uint64_t)parts * lvl * n, total = (uint64_t)B * per;
-    k_add_bs<<<grid_for(total, 256), 256, 0, st>>>(mods, a, abs, b, bbs, o, obs, total, per, lvl, n);
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_add_bs<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, abs, b, bbs, o, obs, (uint32_t)rows, parts * lvl, lvl, n);
     LAUNCHED();
 }
 
 __global__ void k_scale_sub(const Mod *__restrict__ mods, const uint64_t *__restrict__ u, uint64_t u_pstride,
                             const uint64_t *__restrict__ delta, const u64x2 *__restrict__ inv,
-                            uint64_t *__restrict__ o, uint64_t total, uint32_t lvl, uint32_t n) {
-    const uint64_t ln = (uint64_t)lvl * n;
-    GRID_LOOP(i, total) {
-        const uint64_t pidx = i / ln, rr = i - pidx * ln;
-        const uint32_t limb = (uint32_t)(rr / n);
+                            uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
+    ROW_LOOP(rw, x, rows, n) {   // rows = npoly * lvl
+        const uint32_t pidx = rw / lvl, limb = rw - pidx * lvl;
+        const uint64_t rr = (uint64_t)limb * n + x, i = (uint64_t)rw * n + x;
         const uint64_t q = mods[limb].q;
-        const uint64_t v = sub_mod(u[pidx * u_pstride + rr], delta[i], q);
+        const uint64_t v = sub_mod(u[(uint64_t)pidx * u_pstride + rr], delta[i], q);
         const u64x2 w = inv[limb];
         o[i] = mul_shoup(v, w.w, w.ws, q);
     }
 }
 void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *delta, const u64x2 *inv,
                   uint64_t *o, uint32_t npoly, uint32_t lvl, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)npoly * lvl * n;
-    k_scale_sub<<<grid_for(total, 256), 256, 0, st>>>(mods, u, u_pstride, delta, inv, o, total, lvl, n);
+    const uint64_t rows = (uint64_t)npoly * lvl;
+    k_scale_sub<<<grid_rows(n, rows), 256, 0, st>>>(mods, u, u_pstride, delta, inv, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
 // fused ModDown + modulus switch (R15): u[b][k][i] += Pm_i d_k[i] on limb `limb` only (before its INTT)
 __global__ void k_axpy_limb(const Mod *__restrict__ mods, uint64_t *__restrict__ u, uint64_t u_pstride,
                             const uint64_t *__restrict__ d, uint64_t d_bstride, uint64_t d_kstride,
-                            const u64x2 *__restrict__ pm, uint32_t limb, uint64_t total, uint32_t n) {
+                            const u64x2 *__restrict__ pm, uint32_t limb, uint32_t rows, uint32_t n) {
     const uint64_t q = mods[limb].q;
     const u64x2 w = pm[limb];
-    GRID_LOOP(i, total) {
-        const uint64_t poly = i / n, x = i - poly * n;      // poly = b * 2 + k
+    ROW_LOOP(poly, x, rows, n) {      // poly = b * 2 + k
         const uint64_t b = poly >> 1, k = poly & 1;
         uint64_t *pu = u + poly * u_pstride + (uint64_t)limb * n + x;
         const uint64_t dv = d[b * d_bstride + k * d_kstride + (uint64_t)limb * n + x];
@@ -680,12 +683,12 @@ __global__ void k_axpy_limb(const Mod *__restrict__ mods, uint64_t *__restrict__
 __global__ void k_fused_down(const Mod *__restrict__ mods, const uint64_t *__restrict__ u, uint64_t u_pstride,
                              const uint64_t *__restrict__ d, uint64_t d_bstride, uint64_t d_kstride,
                              const uint64_t *__restrict__ delta, const u64x2 *__restrict__ pm,
-                             const u64x2 *__restrict__ dinv, uint64_t *__restrict__ o, uint64_t total, uint32_t lvl,
+                             const u64x2 *__restrict__ dinv, uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl,
                              uint32_t n) {
-    const uint64_t ln = (uint64_t)lvl * n;
-    GRID_LOOP(i, total) {
-        const uint64_t poly = i / ln, rr = i - poly * ln;
-        const uint32_t limb = (uint32_t)(rr / n);
+    ROW_LOOP(rw, x, rows, n) {   // rows = 2B * lvl
+        const uint64_t poly = rw / lvl;
+        const uint32_t limb = rw - (uint32_t)poly * lvl;
+        const uint64_t rr = (uint64_t)limb * n + x, i = (uint64_t)rw * n + x;
         const uint64_t b = poly >> 1, k = poly & 1;
         const uint64_t q = mods[limb].q;
         const u64x2 w = pm[limb], v = dinv[limb];
@@ -698,17 +701,16 @@ __global__ void k_fused_down(const Mod *__restrict__ mods, const uint64_t *__res
 void ew_fused_down(const Mod *mods, uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
                    uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
                    uint32_t B, uint32_t level, uint32_t n, cudaStream_t st) {
-    const uint64_t t1 = (uint64_t)2 * B * n;
-    k_axpy_limb<<<grid_for(t1, 256), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, pm, level - 1, t1, n);
+    k_axpy_limb<<<grid_rows(n, 2ull * B), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, pm, level - 1, 2 * B, n);
     LAUNCHED();
     (void)delta; (void)dinv; (void)o;
 }
 void ew_fused_down_out(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
                        uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
                        uint32_t B, uint32_t lvl_out, uint32_t n, cudaStream_t st) {
-    const uint64_t total = (uint64_t)2 * B * lvl_out * n;
-    k_fused_down<<<grid_for(total, 256), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, delta, pm, dinv,
-                                                       o, total, lvl_out, n);
+    const uint64_t rows = (uint64_t)2 * B * lvl_out;
+    k_fused_down<<<grid_rows(n, rows), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, delta, pm, dinv,
+                                                     o, (uint32_t)rows, lvl_out, n);
     LAUNCHED();
 }
 
@@ -819,10 +821,9 @@ __global__ void __launch_bounds__(256) k_lift_ns(const uint64_t *__restrict__ pl
     __shared__ Mod ssrc[NS];
     if (threadIdx.x < NS) ssrc[threadIdx.x] = mods[P_src[threadIdx.x]];
     __syncthreads();
-    GRID_LOOP(i, total) {
-        const uint64_t poly = i / n;
-        const uint32_t x = (uint32_t)(i - poly * n);
-        const uint64_t *s = src + poly * src_pstride + x;
+    const uint32_t npoly = (uint32_t)(total / n);
+    ROW_LOOP(poly, x, npoly, n) {
+        const uint64_t *s = src + (uint64_t)poly * src_pstride + x;
         uint64_t v[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) v[k] = __ldcs(s + (uint64_t)k * n);
@@ -864,10 +865,10 @@ __global__ void __launch_bounds__(256) k_lift_ns(const uint64_t *__restrict__ pl
             if (mode == 1) {
                 const uint64_t qc = mul_shoup(atc, P_Q[t], P_Qs[t], Mt.q);
                 acc = tc < 0 ? sub_mod(acc, qc, Mt.q) : add_mod(acc, qc, Mt.q);
-                out[poly * out_pstride + (uint64_t)t * n + x] = acc;
+                out[(uint64_t)poly * out_pstride + (uint64_t)t * n + x] = acc;
             } else {
                 const uint32_t lb = t < skip0 ? t : t + skipn;
-                out[poly * out_pstride + (uint64_t)lb * n + x] = acc;
+                out[(uint64_t)poly * out_pstride + (uint64_t)lb * n + x] = acc;
             }
         }
     }
@@ -879,7 +880,7 @@ void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src
     const uint64_t total = (uint64_t)npoly * n;
     const uint32_t words = 2 + 3 * ns_hint + 2 * ns_hint * ns_hint + ns_hint + nt_hint + 2 * nt_hint * ns_hint + 2 * nt_hint + 1;
     if (mode != 2 && ns_hint >= 1 && ns_hint <= 8 && nt_hint <= 64 && words <= 1024) {
-        const unsigned g = grid_for(total, 256);
+        const dim3 g = grid_rows(n, npoly);
 #define LIFT_NS(K) case K: k_lift_ns<K><<<g, 256, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, total, n, skip0, skipn, mode); break;
         switch (ns_hint) { LIFT_NS(1) LIFT_NS(2) LIFT_NS(3) LIFT_NS(4) LIFT_NS(5) LIFT_NS(6) LIFT_NS(7) LIFT_NS(8) }
 #undef LIFT_NS

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1200 python bench.py 2>gpurun_out/bench_default.err | tail -1 > gpurun_out/bench_default.json
+cut -c1-300 gpurun_out/bench_default.json
+timeout 900 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv python bench.py --pairs 32 --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_launch_c2.log 2>&1
+python tools/launches.py gpurun_out/launches_c2.csv | head -32
