@@ -406,6 +406,14 @@ void ctx_build(bc_ctx *X) {
                 }
                 return dev_upload(X, o);
             };
+            auto fd1 = [&](const std::vector<u64x2> &v, size_t per) {
+                std::vector<double> o(v.size());
+                for (size_t k = 0; k < v.size(); ++k) {
+                    const uint64_t q = X->moduli[k / per], w = v[k].w;
+                    o[k] = (double)(w > q / 2 ? (int64_t)w - (int64_t)q : (int64_t)w);
+                }
+                return dev_upload(X, o);
+            };
             auto brv_tab = [&](const std::vector<u64x2> &tw, uint32_t half, uint32_t logh) {
                 std::vector<u64x2> o(tw.size());
                 for (uint32_t i = 0; i < NP; ++i)
@@ -418,7 +426,7 @@ void ctx_build(bc_ctx *X) {
             T.ftwCb = fd(brv_tab(twC, X->C / 2, X->logC - 1), X->C / 2);
             T.ftwRi = fd(twRi, X->R / 2);
             T.ftwCi = fd(twCi, X->C / 2);
-            T.ftf1 = fd(tf1, m); T.ftf1i = fd(tf1i, m); T.ftfo = fd(tfo, m); T.ftfoi = fd(tfoi, m);
+            T.ftf1 = fd1(tf1, m); T.ftf1i = fd1(tf1i, m); T.ftfo = fd1(tfo, m); T.ftfoi = fd1(tfoi, m);
             {
                 const uint32_t le = (uint32_t)nttf_row_loge(X->logR, X->logC), E = 1u << le, tpr = X->C >> le;
                 auto perm = [&](const std::vector<u64x2> &v) {
@@ -430,9 +438,9 @@ void ctx_build(bc_ctx *X) {
                                     o[i * M + (size_t)r * X->C + k * tpr + t] = v[i * M + (size_t)r * X->C + t * E + k];
                     return o;
                 };
-                T.fdhf = fd(perm(dhf), M); T.fdhi = fd(perm(dhi), M);
+                T.fdhf = fd1(perm(dhf), M); T.fdhi = fd1(perm(dhi), M);
             }
-            T.fxta = fd(xta, M); T.fxtb = fd(xtb, M);
+            T.fxta = fd1(xta, M); T.fxtb = fd1(xtb, M);
             T.fmods = dev_upload(X, fm);
         }
     }

@@ -30,9 +30,10 @@ struct NttTables {
     const double2 *fmods;                   // [P] (q, fl(1/q))
     const double2 *ftwRb, *ftwCb;           // [P][R/2], [P][C/2]: omega_L^{brev_{logL-1}(j)} (forward CT blocks)
     const double2 *ftwRi, *ftwCi;           // omega_L^{-j} (inverse)
-    const double2 *ftf1, *ftf1i, *ftfo, *ftfoi, *fdhf, *fdhi, *fxta, *fxtb;   // as the u64x2 tables
+    const double *ftf1, *ftf1i, *ftfo, *ftfoi, *fdhf, *fdhi, *fxta, *fxtb;   // as the u64x2 tables, w only (8 bytes)
     uint32_t m, n, M, R, C, logR, logC;
-    int prime_m;          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
+    int prime_m;
+    int dbg;              // ntt3.cu timing experiments only (bc_tune "ntt_dbg"): skip table reads; results invalid          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
 };
 
 // Limb -> prime map of a batched job list: poly p in [0,npoly), jl in [0,njl):
@@ -156,7 +157,8 @@ bool nttf_supported(const NttTables &T);
 int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: position r*C + tau*E + k at r*C + k*(C/E) + tau
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
-extern uint64_t g_ntt_group_bytes;   // scratch bytes per transform launch group (L2 residency)
+extern uint64_t g_ntt_group_bytes;
+extern int g_ntt_dbg;   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;
 extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)
 int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);

@@ -47,13 +47,24 @@ __device__ __forceinline__ double fmm(double a, double2 w, double q) {
     const double r = __fma_rn(-t, q, h);
     return __dadd_rn(r, l);
 }
+// product with an 8-byte table entry w (wq = fl(w fl(1/q)) formed here: |wq - w/q| <= 2^-53, so
+// |a wq - a w/q| <= 1/2 for |a| <= 4q and |r| <= q).  Halves the table bytes of the pointwise products.
+constexpr int UMUL8 = 16;
+__device__ __forceinline__ double fmm8(double a, double w, double q, double qi) {
+    const double h = __dmul_rn(a, w);
+    const double l = __fma_rn(a, w, -h);
+    const double t = __dsub_rn(__fma_rn(a, __dmul_rn(w, qi), RND), RND);
+    const double r = __fma_rn(-t, q, h);
+    return __dadd_rn(r, l);
+}
 __device__ __forceinline__ double fred(double x, double q, double qi) {
     const double t = __dsub_rn(__fma_rn(x, qi, RND), RND);
     return __fma_rn(-t, q, x);
 }
-// canonical residue of |x| <= 0.625 q (after fmm) or <= q/2 + 2 (after fred) -> u64
+// canonical residue of |x| <= q (after fmm8, fmm or fred) -> u64
 __device__ __forceinline__ uint64_t to_u64(double x, double q) {
-    const double c = x < 0.0 ? __dadd_rn(x, q) : x;
+    double c = x < 0.0 ? __dadd_rn(x, q) : x;
+    c = c >= q ? __dsub_rn(c, q) : c;
     return (uint64_t)__double_as_longlong(__dadd_rn(c, 4503599627370496.0)) - 0x4330000000000000ull;
 }
 __device__ __forceinline__ double from_u64(uint64_t x) {   // x < 2^52
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
     const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
     const uint32_t c = blockIdx.x * TC + col;
-    const double2 *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
+    const double *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
     const uint64_t *src = in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
     typedef PtTab<LOGR, LOGE, true> PTT;
     double2 *stw = (double2 *)(smf + (size_t)R * TC), *spt = stw + R / 2;
@@ -279,23 +290,26 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         const uint32_t t = r * CC + c;
         double x = 0.0;
         if (!INV) {
-            if (t < T.n) x = fmm(from_u64(__ldcs(src + t)), tf[t], q);
+            if (t < T.n) {
+                const double xin = (T.dbg & 64) ? (double)t : from_u64(__ldcs(src + t));
+                x = (T.dbg & 1) ? xin : fmm8(xin, tf[t], q, qi);
+            }
         } else if (t < T.m) {
             const int ps = T.pos[t];
-            if (ps >= 0) x = fmm(from_u64(__ldcs(src + ps)), tf[t], q);
+            if (ps >= 0) x = fmm8(from_u64(__ldcs(src + ps)), tf[t], q, qi);
         }
         v[k] = x;
-        bd[k] = UMUL;
+        bd[k] = UMUL8;
     }
     __syncthreads();
     fct_pass<LOGR, LOGE, true, TC, 0>(v, bd, tau, col, smf, stw, spt, q, qi);
-    const double2 *xt = T.fxta + (uint64_t)J.pr * T.M;
+    const double *xt = T.fxta + (uint64_t)J.pr * T.M;
     double *dst = scratch + (uint64_t)blockIdx.y * T.M;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const uint32_t rp = held_index<LOGE>(tau, 0, k);
         need(v, bd, k, LIM_MUL, q, qi);
-        __stcs(dst + rp * CC + c, fmm(v[k], xt[rp * CC + c], q));
+        __stcs(dst + rp * CC + c, (T.dbg & 2) ? fred(v[k], q, qi) : fmm8(v[k], xt[rp * CC + c], q, qi));
     }
 }
 
@@ -328,25 +342,25 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), FNTT_MINB(RB * (1 <
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         v[k] = __ldcs(grow + held_index<LOGE>(tau, LOGC - LOGE, k));
-        bd[k] = UMUL;
+        bd[k] = UMUL8;
     }
     __syncthreads();
     frt_pass<LOGC, LOGE, true, 0>(v, bd, tau, srow, tw, ptf, q, qi);
     // D^ in the thread-minor layout of this pass (entry of position tau*E + k at k*TPR + tau: coalesced)
-    const double2 *dh = (INV ? T.fdhi : T.fdhf) + (uint64_t)J.pr * T.M + (uint64_t)row * C + tau;
+    const double *dh = (INV ? T.fdhi : T.fdhf) + (uint64_t)J.pr * T.M + (uint64_t)row * C + tau;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         need(v, bd, k, LIM_MUL, q, qi);
-        v[k] = fmm(v[k], dh[k * TPR], q);
-        bd[k] = UMUL;
+        v[k] = (T.dbg & 4) ? fred(v[k], q, qi) : fmm8(v[k], dh[k * TPR], q, qi);
+        bd[k] = UMUL8;
     }
     frt_pass<LOGC, LOGE, false, 0>(v, bd, tau, srow, twi, pti, q, qi);
-    const double2 *xt = T.fxtb + (uint64_t)J.pr * T.M + (uint64_t)row * C;
+    const double *xt = T.fxtb + (uint64_t)J.pr * T.M + (uint64_t)row * C;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const uint32_t cc = held_index<LOGE>(tau, LOGC - LOGE, k);
         need(v, bd, k, LIM_MUL, q, qi);
-        __stcs(grow + cc, fmm(v[k], xt[cc], q));
+        __stcs(grow + cc, (T.dbg & 8) ? fred(v[k], q, qi) : fmm8(v[k], xt[cc], q, qi));
     }
 }
 
@@ -374,11 +388,11 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         v[k] = __ldcs(scr + held_index<LOGE>(tau, 0, k) * CC + c);
-        bd[k] = UMUL;
+        bd[k] = UMUL8;
     }
     __syncthreads();
     fct_pass<LOGR, LOGE, false, TC, 0>(v, bd, tau, col, smf, stw, spt, q, qi);
-    const double2 *tfo = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
+    const double *tfo = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
     uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
     uint64_t *scru = (uint64_t *)scr;
     if (INV) __syncthreads();   // all columns of this block read before in-place writes of A_t
@@ -388,9 +402,9 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         const uint32_t t = r * CC + c;
         need(v, bd, k, LIM_MUL, q, qi);
         if (t >= T.m) continue;
-        const uint64_t x = to_u64(fmm(v[k], tfo[t], q), q);
+        const uint64_t x = to_u64((T.dbg & 16) ? fred(v[k], q, qi) : fmm8(v[k], tfo[t], q, qi), q);
         if (!INV) {
-            const int ps = T.pos[t];
+            const int ps = (T.dbg & 32) ? (t < T.n ? (int)t : -1) : T.pos[t];
             if (ps >= 0) __stcs(dst + ps, x);
         } else {
             scru[t] = x;
@@ -410,7 +424,7 @@ struct Shape {
 };
 
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
-static void runf(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
                  uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
     static bool init = false;
@@ -424,6 +438,8 @@ static void runf(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap 
         init = true;
     }
     double *scr = (double *)scratch;
+    NttTables T = T0;
+    T.dbg = g_ntt_dbg;
     dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
     if (!inv) {
         kf_passA<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
