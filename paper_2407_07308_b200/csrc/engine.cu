@@ -442,6 +442,9 @@ void ctx_build(bc_ctx *X) {
             }
             T.fxta = fd1(xta, M); T.fxtb = fd1(xtb, M);
             T.fmods = dev_upload(X, fm);
+            bool win = true;
+            for (uint32_t i = 0; i < NP; ++i) win = win && X->moduli[i] >= (1ull << 49);
+            X->d_fm = win ? T.fmods : nullptr;
         }
     }
     T.twR = dev_upload(X, twR); T.twRi = dev_upload(X, twRi); T.twC = dev_upload(X, twC); T.twCi = dev_upload(X, twCi);
@@ -570,7 +573,7 @@ void lift_p(bc_ctx *X, const std::string &key, const Mod *mods, uint32_t p, cons
     auto it = X->plan_dims.find(key);
     if (it == X->plan_dims.end()) BC_THROW(BC_E_INTERNAL, "missing lift plan " + key);
     lift(X->plan(key), mods, p, src, src_pstride, out, out_pstride, out16, npoly, n, skip0, skipn, mode, st,
-         it->second.first, it->second.second);
+         it->second.first, it->second.second, g_f64_elem ? X->d_fm : nullptr);
 }
 
 void ctx_free(bc_ctx *X) {
@@ -777,7 +780,7 @@ BufP Eng::ks_kip(const uint64_t *d, uint64_t dps, const BufP &ext, uint32_t B, u
     BufP u = alloc_words((uint64_t)B * 2 * nl * n);
     if (!dry())
         ks_kip_perm(X->d_mods, X->T, perm_t, d, dps, (uint64_t *)ext->p, kptr, (uint64_t *)u->p, B, lvl, K, L1, al, ndig,
-                    n, st);
+                    n, st, g_f64_elem ? X->d_fm : nullptr);
     return u;
 }
 
@@ -844,7 +847,7 @@ CT Eng::mul(const CT &a0, const CT &b0) {
     if (a.bstride != (uint64_t)2 * lv * n || b.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "mul: strided");
     const uint64_t tw = (uint64_t)3 * lv * n;
     BufP t = alloc_words((uint64_t)B * tw);
-    if (!dry()) ew_tensor(X->d_mods, a.d, b.d, (uint64_t *)t->p, B, lv, n, st);
+    if (!dry()) ew_tensor(X->d_mods, a.d, b.d, (uint64_t *)t->p, B, lv, n, st, g_f64_elem ? X->d_fm : nullptr);
     BufP u = ks_up((uint64_t *)t->p + (uint64_t)2 * lv * n, tw, B, lv, 0);
     const uint64_t ups = (uint64_t)nl * n;
     uint64_t *U = (uint64_t *)u->p, *Tt = (uint64_t *)t->p;

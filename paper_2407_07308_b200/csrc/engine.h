@@ -68,6 +68,7 @@ struct bc_ctx {
     // device
     std::vector<void *> owned;
     bc::Mod *d_mods = nullptr;
+    const double2 *d_fm = nullptr;    // (q, fl(1/q)) per prime when all primes are in [2^49, 2^50) (binary64 kernels)
     bc::NttTables T;
     uint64_t *d_plans = nullptr;
     std::map<std::string, size_t> plan_off;

@@ -14,11 +14,13 @@
 #include <vector>
 
 #include "kernels.h"
+#include "f64arith.cuh"
 
 namespace bc {
 
 int g_ntt_impl = 0;
 int g_ntt_dbg = 0;
+int g_f64_elem = 1;
 uint64_t g_ntt_group_bytes = 1ull << 40;   // one launch group (measured best on B200)
 
 uint64_t &launch_counter() {
@@ -505,10 +507,31 @@ __global__ void k_tensor(const Mod *__restrict__ mods, const uint64_t *__restric
         ob[2 * ln] = mul_mod(a1, b1, M);
     }
 }
+// binary64 variant (all primes in [2^49, 2^50)): four fmulv per coefficient
+__global__ void k_tensor_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ a,
+                           const uint64_t *__restrict__ b, uint64_t *__restrict__ o, uint32_t rows,
+                           uint32_t lvl, uint32_t n) {
+    using namespace f64;
+    const uint64_t ln = (uint64_t)lvl * n;
+    ROW_LOOP(rw, x, rows, n) {   // rows = B * lvl
+        const uint32_t bi = rw / lvl, limb = rw - bi * lvl;
+        const uint64_t r = (uint64_t)limb * n + x;
+        const double q = fm[limb].x, qi = fm[limb].y;
+        const double a0 = from_u64(a[bi * 2 * ln + r]), a1 = from_u64(a[bi * 2 * ln + ln + r]);
+        const double b0 = from_u64(b[bi * 2 * ln + r]), b1 = from_u64(b[bi * 2 * ln + ln + r]);
+        uint64_t *ob = o + bi * 3 * ln + r;
+        ob[0] = to_u64(fmulv(a0, b0, q, qi), q);
+        ob[ln] = to_u64(fred(__dadd_rn(fmulv(a0, b1, q, qi), fmulv(a1, b0, q, qi)), q, qi), q);
+        ob[2 * ln] = to_u64(fmulv(a1, b1, q, qi), q);
+    }
+}
 void ew_tensor(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t lvl,
-               uint32_t n, cudaStream_t st) {
+               uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * lvl;
-    k_tensor<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n);
+    if (fm)
+        k_tensor_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, a, b, o, (uint32_t)rows, lvl, n);
+    else
+        k_tensor<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
@@ -615,19 +638,59 @@ __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__
         u[(b * 2 + 1) * ln + rr] = reduce128(h1, l1, M);
     }
 }
+// binary64 variant: sum of 2 * ndig fmulv per output coefficient pair, one reduction each
+__global__ void k_kip_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ d, uint64_t dps,
+                        const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
+                        uint64_t *__restrict__ u, uint32_t rows, uint32_t lvl, uint32_t K, uint32_t L1,
+                        uint32_t alpha, uint32_t ndig, uint32_t n, const int32_t *__restrict__ pos,
+                        const int32_t *__restrict__ zt, uint32_t m, uint32_t perm_t) {
+    using namespace f64;
+    const uint32_t nl = lvl + K;
+    const uint64_t ln = (uint64_t)nl * n;
+    const uint32_t x0 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x0 >= n) return;
+    const uint32_t x = perm_t ? (uint32_t)pos[(uint32_t)(((uint64_t)perm_t * (uint32_t)zt[x0]) % m)] : x0;
+    ROW_LOOP(rw, xo, rows, n) {   // rows = B * nl
+        const uint64_t b = rw / nl;
+        const uint32_t r = rw - (uint32_t)b * nl;
+        const uint64_t rr = (uint64_t)r * n + xo;
+        const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
+        const double q = fm[kl].x, qi = fm[kl].y;
+        const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
+        double s0 = 0.0, s1 = 0.0;      // |s| <= 0.75 q ndig (ndig <= 10: < 8q)
+        for (uint32_t j = 0; j < ndig; ++j) {
+            const uint64_t dig = (j == jr) ? d[b * dps + (uint64_t)r * n + x] : ext[((b * ndig + j) * nl + r) * n + x];
+            const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
+            const double dg = from_u64(dig);
+            s0 = __dadd_rn(s0, fmulv(dg, from_u64(kj[(uint64_t)kl * n + xo]), q, qi));
+            s1 = __dadd_rn(s1, fmulv(dg, from_u64(kj[(uint64_t)(L1 + K + kl) * n + xo]), q, qi));
+        }
+        u[(b * 2 + 0) * ln + rr] = to_u64(fred(s0, q, qi), q);
+        u[(b * 2 + 1) * ln + rr] = to_u64(fred(s1, q, qi), q);
+    }
+}
 void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
-            uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
+            uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st,
+            const double2 *fm) {
     const uint64_t rows = (uint64_t)B * (lvl + K);
-    k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n, nullptr,
-                                                nullptr, 1, 0);
+    if (fm && ndig <= 10)
+        k_kip_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
+                                                    nullptr, nullptr, 1, 0);
+    else
+        k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
+                                                  nullptr, nullptr, 1, 0);
     LAUNCHED();
 }
 void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uint64_t *d, uint64_t dps,
                  const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1,
-                 uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st) {
+                 uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * (lvl + K);
-    k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n, T.pos, T.z,
-                                                T.m, perm_t);
+    if (fm && ndig <= 10)
+        k_kip_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
+                                                    T.pos, T.z, T.m, perm_t);
+    else
+        k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
+                                                  T.pos, T.z, T.m, perm_t);
     LAUNCHED();
 }
 
@@ -875,9 +938,103 @@ __global__ void __launch_bounds__(256) k_lift_ns(const uint64_t *__restrict__ pl
     }
 }
 
+// Binary64 lift (all primes in [2^49, 2^50), so every source digit is < 2 q_t of any target):
+// same plan and the same exact result as k_lift_ns (modes 0, 1).  Garner digits are made canonical
+// (they decide the sign test), the target sums use one fmm per digit (B[t][0] = 1 needs none).
+template <int NS>
+__global__ void __launch_bounds__(256) k_lift_f(const uint64_t *__restrict__ plan, const double2 *__restrict__ fm,
+                                                uint32_t p, const uint64_t *__restrict__ src, uint64_t src_pstride,
+                                                uint64_t *__restrict__ out, uint64_t out_pstride, uint32_t npoly,
+                                                uint32_t n, uint32_t skip0, uint32_t skipn, int mode) {
+    using namespace f64;
+    __shared__ double2 sB[64 * NS], sQ[64], sT[64], sqm[NS * NS], sinv[NS], ssrc[NS];
+    __shared__ double shalf[NS];
+    __shared__ uint64_t sBp[NS];
+    const uint32_t nt = (uint32_t)plan[1];
+    const uint64_t *P_src = plan + 2, *P_inv = P_src + NS, *P_invs = P_inv + NS, *P_qm = P_invs + NS;
+    const uint64_t *P_qms = P_qm + NS * NS, *P_half = P_qms + NS * NS, *P_tgt = P_half + NS;
+    const uint64_t *P_B = P_tgt + nt, *P_Bs = P_B + (uint64_t)nt * NS, *P_Q = P_Bs + (uint64_t)nt * NS;
+    const uint64_t *P_Qs = P_Q + nt;
+    const uint64_t pmu = P_Qs[nt];
+    const uint32_t ntq = mode == 1 ? nt - 1 : nt;       // prime targets (mode 1: the last target is p)
+    for (uint32_t i = threadIdx.x; i < ntq * NS; i += blockDim.x) {
+        const uint32_t t = i / NS;
+        const uint64_t qt = (uint64_t)fm[P_tgt[t]].x;
+        sB[i] = centred_entry(P_B[i], qt);
+    }
+    for (uint32_t t = threadIdx.x; t < ntq; t += blockDim.x) {
+        sT[t] = fm[P_tgt[t]];
+        const uint64_t qt = (uint64_t)sT[t].x;
+        sQ[t] = centred_entry(P_Q[t], qt);
+    }
+    if (threadIdx.x < NS) {
+        const uint32_t k = threadIdx.x;
+        ssrc[k] = fm[P_src[k]];
+        const uint64_t qk = (uint64_t)ssrc[k].x;
+        sinv[k] = centred_entry(P_inv[k], qk);
+        shalf[k] = (double)P_half[k];
+        for (uint32_t j = 0; j < NS; ++j) sqm[k * NS + j] = centred_entry(P_qm[k * NS + j], qk);
+        if (mode == 1) sBp[k] = P_B[(uint64_t)(nt - 1) * NS + k];
+    }
+    __syncthreads();
+    ROW_LOOP(poly, x, npoly, n) {
+        const uint64_t *s = src + (uint64_t)poly * src_pstride + x;
+        double v[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) v[k] = from_u64(__ldcs(s + (uint64_t)k * n));
+#pragma unroll
+        for (int k = 1; k < NS; ++k) {
+            const double qk = ssrc[k].x;
+            double acc = v[k - 1];                               // < 2 q_k
+#pragma unroll
+            for (int j = k - 2; j >= 0; --j) acc = __dadd_rn(fmm(acc, sqm[k * NS + j], qk), v[j]);   // < 2.625 q_k
+            v[k] = canon(fmm(__dsub_rn(v[k], acc), sinv[k], qk), qk);
+        }
+        bool neg = false;
+#pragma unroll
+        for (int k = NS - 1; k >= 0; --k) {
+            if (v[k] != shalf[k]) { neg = v[k] > shalf[k]; break; }
+        }
+        double tcd = 0.0;
+        if (mode == 1) {
+            uint64_t rp = 0;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                const uint64_t vk = (uint64_t)v[k];
+                rp += mod_small(vk, p, pmu) * sBp[k];
+            }
+            rp %= p;
+            if (neg) rp = (rp + p - P_Q[nt - 1]) % p;
+            int64_t tc = (int64_t)((p - rp) % p);
+            if (tc > (int64_t)(p / 2)) tc -= p;
+            tcd = (double)tc;
+        }
+        for (uint32_t t = 0; t < ntq; ++t) {
+            const double qt = sT[t].x, qit = sT[t].y;
+            const double2 *B = sB + t * NS;
+            double acc = v[0];                                   // B[t][0] = 1
+#pragma unroll
+            for (int k = 1; k < NS; ++k) acc = __dadd_rn(acc, fmm(v[k], B[k], qt));   // < (2 + 0.625 (NS-1)) q_t
+            if (neg) acc = __dsub_rn(acc, sQ[t].x);
+            if (mode == 1) acc = __dadd_rn(acc, fmm(tcd, sQ[t], qt));   // |tc| <= p/2 <= 4q; sum < 7.5 q_t
+            const uint64_t r = to_u64(fred(acc, qt, qit), qt);
+            const uint32_t lb = (mode == 1 || t < skip0) ? t : t + skipn;
+            out[(uint64_t)poly * out_pstride + (uint64_t)lb * n + x] = r;
+        }
+    }
+}
+
 void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride, uint64_t *out,
           uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0, uint32_t skipn, int mode,
-          cudaStream_t st, uint32_t ns_hint, uint32_t nt_hint) {
+          cudaStream_t st, uint32_t ns_hint, uint32_t nt_hint, const double2 *fm) {
+    if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 8 && nt_hint <= 64) {
+        const dim3 g = grid_rows(n, npoly);
+#define LIFT_F(K) case K: k_lift_f<K><<<g, 256, 0, st>>>(plan, fm, p, src, src_pstride, out, out_pstride, npoly, n, skip0, skipn, mode); break;
+        switch (ns_hint) { LIFT_F(1) LIFT_F(2) LIFT_F(3) LIFT_F(4) LIFT_F(5) LIFT_F(6) LIFT_F(7) LIFT_F(8) }
+#undef LIFT_F
+        LAUNCHED();
+        return;
+    }
     const uint64_t total = (uint64_t)npoly * n;
     const uint32_t words = 2 + 3 * ns_hint + 2 * ns_hint * ns_hint + ns_hint + nt_hint + 2 * nt_hint * ns_hint + 2 * nt_hint + 1;
     if (mode != 2 && ns_hint >= 1 && ns_hint <= 8 && nt_hint <= 64 && words <= 1024) {

@@ -79,8 +79,9 @@ void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *
               uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
 void ew_add_pt(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B,
                uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
+// fm: per-prime (q, fl(1/q)) when every prime is in [2^49, 2^50) -> binary64 kernels; nullptr -> integer kernels
 void ew_tensor(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B,
-               uint32_t lvl, uint32_t n, cudaStream_t st);
+               uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm = nullptr);
 void ew_automorph(const NttTables &T, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts,
                   uint32_t lvl, uint32_t t, cudaStream_t st);
 void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in, uint32_t part0,
@@ -93,12 +94,12 @@ void ew_copy_parts(const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts_in
 // R22: KIP reading d and the extended digits through sigma_{perm_t}'s evaluation permutation
 void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uint64_t *d, uint64_t dps,
                  const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1,
-                 uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st);
+                 uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st, const double2 *fm = nullptr);
 void ew_automorph_part(const NttTables &T, const uint64_t *a, uint64_t abs, uint64_t *o, uint32_t B, uint32_t lvl,
                        uint32_t t, cudaStream_t st);
 void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
             uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig,
-            uint32_t n, cudaStream_t st);
+            uint32_t n, cudaStream_t st, const double2 *fm = nullptr);
 // o[b] = a[b] + b[b] (parts x lvl x n words per ciphertext), per-operand batch strides in words
 void ew_add_bs(const Mod *mods, const uint64_t *a, uint64_t abs, const uint64_t *b, uint64_t bbs, uint64_t *o,
                uint64_t obs, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
@@ -113,7 +114,8 @@ void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const 
 //  mode 2: centered value mod p (as int16, centered in (-p/2, p/2]) -> out16[poly][n]
 void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride,
           uint64_t *out, uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n,
-          uint32_t skip0, uint32_t skipn, int mode, cudaStream_t st, uint32_t ns_hint = 0, uint32_t nt_hint = 0);
+          uint32_t skip0, uint32_t skipn, int mode, cudaStream_t st, uint32_t ns_hint = 0, uint32_t nt_hint = 0,
+          const double2 *fm = nullptr);
 
 // ---- sampling (R7) ----
 // integer poly per (poly, coeff) -> residues on limbs prime0..prime0+nl-1
@@ -158,7 +160,8 @@ int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: pos
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
 extern uint64_t g_ntt_group_bytes;
-extern int g_ntt_dbg;   // scratch bytes per transform launch group (L2 residency)
+extern int g_ntt_dbg;
+extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when the context allows them   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;
 extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)
 int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.h"
+#include "f64arith.cuh"
 
 namespace bc {
 
@@ -38,15 +39,6 @@ constexpr int URED = 9;       // fred output, |r| <= q/2 + 2
 constexpr int LIM_MUL = 64;   // fmm input, |a| <= 4q (q < 2^50: |a wq| <= 2q < 2^51, |a| < 2^52)
 constexpr int LIM_VAL = 128;  // any value, |v| <= 8q < 2^53
 
-constexpr double RND = 6755399441055744.0;   // 1.5 * 2^52: fl(x + RND) - RND = rint(x) for |x| < 2^51
-
-__device__ __forceinline__ double fmm(double a, double2 w, double q) {
-    const double h = __dmul_rn(a, w.x);
-    const double l = __fma_rn(a, w.x, -h);
-    const double t = __dsub_rn(__fma_rn(a, w.y, RND), RND);
-    const double r = __fma_rn(-t, q, h);
-    return __dadd_rn(r, l);
-}
 // product with an 8-byte table entry w (wq = fl(w fl(1/q)) formed here: |wq - w/q| <= 2^-53, so
 // |a wq - a w/q| <= 1/2 for |a| <= 4q and |r| <= q).  Halves the table bytes of the pointwise products.
 constexpr int UMUL8 = 16;
@@ -57,20 +49,6 @@ __device__ __forceinline__ double fmm8(double a, double w, double q, double qi) 
     const double r = __fma_rn(-t, q, h);
     return __dadd_rn(r, l);
 }
-__device__ __forceinline__ double fred(double x, double q, double qi) {
-    const double t = __dsub_rn(__fma_rn(x, qi, RND), RND);
-    return __fma_rn(-t, q, x);
-}
-// canonical residue of |x| <= q (after fmm8, fmm or fred) -> u64
-__device__ __forceinline__ uint64_t to_u64(double x, double q) {
-    double c = x < 0.0 ? __dadd_rn(x, q) : x;
-    c = c >= q ? __dsub_rn(c, q) : c;
-    return (uint64_t)__double_as_longlong(__dadd_rn(c, 4503599627370496.0)) - 0x4330000000000000ull;
-}
-__device__ __forceinline__ double from_u64(uint64_t x) {   // x < 2^52
-    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), 4503599627370496.0);
-}
-
 // make v[k] a valid fmm input / keep the exact range
 template <int E>
 __device__ __forceinline__ void need(double (&v)[E], int (&bd)[E], int k, int lim, double q, double qi) {

@@ -410,3 +410,28 @@ def test_compare_c3t_bivariate_p31_bit_exact(pair):
     ev = circuits.OracleEval(P, T.okeys)
     olt, _ = circuits.compare(ev, T.oracle_ct(a, 900), T.oracle_ct(b, 901), P.circuit, P.d, P.l, ints)
     assert np.array_equal(to_u64(lt)[0], T.ct_eval(olt))
+
+
+def test_binary64_kernels_match_integer_kernels(pair):
+    """C2 at full size: the binary64 NTT / lift / KIP / tensor kernels (default) and the 64-bit integer
+    kernels (ntt impl 7, f64_elem 0) give bit-identical compare_lt ciphertexts (both exact; the
+    integer path is the one the shadow-ring oracle parity tests pinned first)."""
+    import paper_2407_07308_b200 as bc
+    T = pair("c2")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(31)
+    a, b = mixed_pairs(P, rng, ints)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=0)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=1)
+    f = to_u64(T.ctx.compare_lt(T.keys, ca, cb))
+    try:
+        bc.set_ntt_impl(7)
+        bc._lib.bc_tune(b"f64_elem", 0)
+        g = to_u64(T.ctx.compare_lt(T.keys, ca, cb))
+    finally:
+        bc.set_ntt_impl(0)
+        bc._lib.bc_tune(b"f64_elem", 1)
+    assert np.array_equal(f, g)
+    bits = T.ctx.decrypt(T.keys, T.ctx.compare_lt(T.keys, ca, cb), as_bits=True)[0]
+    assert list(bits) == [int(x < y) for x, y in zip(a, b)]
