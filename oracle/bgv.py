@@ -56,7 +56,7 @@ class Params:
 
     @property
     def ints_per_ct(self):
-        return self.alg.S // self.l
+        return self.alg.ints(self.l)
 
     def digit_group(self, j, level):
         """R8: G_j = {j*alpha, ..., (j+1)*alpha-1} restricted to the primes present at `level`."""

@@ -250,9 +250,13 @@ def lex_tree(ev, lts, eqs):
 
 
 def block_mask(alg, l, ints, pred):
+    """1 at the slots of the first `ints` integer blocks whose position in the block satisfies pred
+    (R6 rows: slot s is position i = s mod S1 of its row; blocks cover i < floor(S1/l) l)"""
     m = np.zeros((alg.S, alg.D), dtype=np.int64)
+    wpr = alg.S1 // l
     for s in range(alg.S):
-        if s < ints * l and pred(s % l):
+        row, i = divmod(s, alg.S1)
+        if i < wpr * l and row * wpr + i // l < ints and pred(i % l):
             m[s, 0] = 1
     return m
 
@@ -527,12 +531,17 @@ def compaction_offsets(span):
     return out
 
 
-def plan_compaction(useful, ints, span):
+def plan_compaction(useful, ints, span, wpr=None):
     """R17 greedy plan.  useful[c] = sorted useful block indices of input ct c.  For each input
     in order, repeatedly pick (existing output c', offset delta) placing the most remaining blocks
     b at free blocks b - delta of c' (first maximum in the order outputs ascending x offsets
     0, 1, -1, ...); if nothing fits anywhere, open a new output with delta = 0.
     Returns (groups [(c, c', delta, blocks)], n_out, dest {(c, b): (c', b')})."""
+    wpr = wpr or ints          # blocks per row (R6 rows): a rotation by delta l moves blocks within a row
+
+    def fits(b, dl):
+        return 0 <= b - dl < ints and 0 <= b % wpr - dl < wpr
+
     occ = []
     groups = []
     dest = {}
@@ -542,14 +551,14 @@ def plan_compaction(useful, ints, span):
             best, best_cnt = None, 0
             for cp in range(len(occ)):
                 for dl in compaction_offsets(span):
-                    cnt = sum(1 for b in rem if 0 <= b - dl < ints and (b - dl) not in occ[cp])
+                    cnt = sum(1 for b in rem if fits(b, dl) and (b - dl) not in occ[cp])
                     if cnt > best_cnt:
                         best, best_cnt = (cp, dl), cnt
             if best is None:
                 occ.append(set())
                 best = (len(occ) - 1, 0)
             cp, dl = best
-            moved = [b for b in rem if 0 <= b - dl < ints and (b - dl) not in occ[cp]]
+            moved = [b for b in rem if fits(b, dl) and (b - dl) not in occ[cp]]
             for b in moved:
                 occ[cp].add(b - dl)
                 dest[(c, b)] = (cp, b - dl)
@@ -566,7 +575,7 @@ def compaction_galois(alg, l, span):
 def compact(ev, cts, useful, l, ints, span, modswitch=True):
     """out_{c'} = sum over groups (c, c', delta) of rot_{delta l}(cts[c] (.) mask(blocks)), then one
     modulus switch per output (R17).  Blocks of an output not written by any group are zero."""
-    groups, n_out, dest = plan_compaction(useful, ints, span)
+    groups, n_out, dest = plan_compaction(useful, ints, span, ev.alg.S1 // l)
     outs = [None] * n_out
     for c, cp, dl, blocks in groups:
         if not blocks:
@@ -585,5 +594,6 @@ def compact(ev, cts, useful, l, ints, span, modswitch=True):
 def block_mask_sets(alg, l, blocks):
     m = np.zeros((alg.S, alg.D), dtype=np.int64)
     for b in blocks:
-        m[b * l:(b + 1) * l, 0] = 1
+        w0 = alg.word_slot(b, l)
+        m[w0:w0 + l, 0] = 1
     return m

@@ -184,8 +184,9 @@ class SlotAlgebra:
         self.G = smallest_irreducible(p, self.D)
         self.gf = GF(p, self.G)
         self.zeta = self._find_zeta()
-        self.g = self._slot_generator()
-        self.t = [pow(self.g, s, m) for s in range(self.S)]
+        # R5: slot s = j*S1 + i <-> t_s = g^i g2^j (cyclic quotient: S1 = S, g2 = 1)
+        self.g, self.S1, self.g2, self.S2 = self._slot_generators()
+        self.t = [pow(self.g, s % self.S1, m) * pow(self.g2, s // self.S1, m) % m for s in range(self.S)]
         # zeta^e for e < m (evaluation table)
         zp = np.zeros((m, self.D), dtype=np.int64)
         x = self.gf.one()
@@ -209,29 +210,76 @@ class SlotAlgebra:
     def _powers_of_p(self):
         return {pow(self.p, k, self.m) for k in range(self.D)}
 
+    def _order(self, t):
+        """multiplicative order of t mod m: divide n = phi(m) by its prime factors while t^(o/r) = 1"""
+        if getattr(self, "_nf", None) is None:
+            self._nf = factorize(self.n)
+        o = self.n
+        for r in self._nf:
+            while o % r == 0 and pow(t, o // r, self.m) == 1:
+                o //= r
+        return o
+
     def quotient_order(self, t):
-        H = self._powers_of_p()
-        k, x = 1, t % self.m
-        while x not in H:
-            x = x * t % self.m
-            k += 1
+        """order of t in Z_m^* / <p>: the exponents k with t^k in <p> are the multiples of it, so
+        start from ord(t) and divide by primes r while t^(k/r) stays in <p>"""
+        if getattr(self, "_H", None) is None:
+            self._H = self._powers_of_p()
+        k = self._order(t)
+        for r in self._nf:
+            while k % r == 0 and pow(t, k // r, self.m) in self._H:
+                k //= r
         return k
 
-    def _slot_generator(self):
+    def _slot_generators(self):
+        """R5.  Cyclic Z_m^*/<p>: g = the smallest t of quotient order S with t^S = 1 (mod m) if one
+        exists ("good" generator), else the smallest of quotient order S; (S1, g2, S2) = (S, 1, 1).
+        Otherwise (hypercube Z_S1 x Z_S2, S1 = the largest quotient order): g = the smallest t of
+        quotient order S1 with t^S1 = 1 (mod m) if one exists, else the smallest of that order;
+        g2 = the smallest t outside <p, g> with t^S2 in <p, g>, preferring t^S2 = 1 (mod m); every
+        unit must be p^k g^i g2^j for exactly one (k, i, j)."""
         m, S = self.m, self.S
         if S == 1:
-            return 1
+            return 1, 1, 1, 1
+        units = [t for t in range(2, m) if gcd(t, m) == 1]
+        qo = {}
         first = None
-        for t in range(2, m):
-            if gcd(t, m) != 1 or self.quotient_order(t) != S:
-                continue
-            if pow(t, S, m) == 1:
-                return t                   # smallest t of quotient order S with t^S = 1 (mod m)
-            if first is None:
-                first = t
-        if first is None:
-            raise NotImplementedError("Z_m^*/<p> is not cyclic (hypercube slots)")
-        return first
+        for t in units:
+            o = self.quotient_order(t)
+            if o == S:
+                if pow(t, S, m) == 1:
+                    return t, S, 1, 1
+                if first is None:
+                    first = t
+            qo[t] = o
+        if first is not None:
+            return first, S, 1, 1
+        S1 = max(qo.values())
+        S2 = S // S1
+        cands = [t for t in units if qo[t] == S1]
+        g = next((t for t in cands if pow(t, S1, m) == 1), cands[0])
+        Hg = {pow(self.p, k, m) * pow(g, i, m) % m for k in range(self.D) for i in range(S1)}
+        c2 = [t for t in units if t not in Hg and pow(t, S2, m) in Hg
+              and all(pow(t, j, m) not in Hg for j in range(1, S2))]
+        if not c2:
+            raise NotImplementedError("Z_m^*/<p> is not Z_S1 x Z_S2")
+        g2 = next((t for t in c2 if pow(t, S2, m) == 1), c2[0])
+        cover = {h * pow(g2, j, m) % m for h in Hg for j in range(S2)}
+        if len(cover) != self.n:
+            raise NotImplementedError("Z_m^*/<p> is not generated by (p, g, g2)")
+        return g, S1, g2, S2
+
+    def words_per_row(self, l):
+        """R6 (hypercube rows): floor(S1 / l) integers per row of S1 slots"""
+        return self.S1 // l
+
+    def ints(self, l):
+        return self.S2 * (self.S1 // l)
+
+    def word_slot(self, w, l):
+        """first slot of integer w: row w // wpr, position (w mod wpr) * l in the row"""
+        wpr = self.S1 // l
+        return (w // wpr) * self.S1 + (w % wpr) * l
 
     # --- decode / encode ---------------------------------------------------------------
     def decode(self, a, chunk=512):
@@ -351,27 +399,30 @@ def int_to_digits(x, base, count):
 
 
 def words_to_slots(words, alg, d, l, base):
-    """Word j occupies slots j*l .. j*l+l-1; slot j*l+s holds sum_{i<d} a_{s,i} X^i where
-    x = sum_s sum_i a_{s,i} base^{s d + i} (little-endian).  Unused slots are 0."""
+    """Word j occupies slots w0 .. w0+l-1, w0 = alg.word_slot(j, l) (= j*l for a cyclic slot
+    structure); slot w0+s holds sum_{i<d} a_{s,i} X^i where x = sum_s sum_i a_{s,i} base^{s d + i}
+    (little-endian).  Unused slots are 0."""
     S, D = alg.S, alg.D
     assert d <= D
-    cap = S // l
+    cap = alg.ints(l)
     assert len(words) <= cap
     out = np.zeros((S, D), dtype=np.int64)
     for j, x in enumerate(words):
         dig = int_to_digits(int(x), base, d * l)
+        w0 = alg.word_slot(j, l)
         for s in range(l):
             for i in range(d):
-                out[j * l + s, i] = dig[s * d + i]
+                out[w0 + s, i] = dig[s * d + i]
     return out
 
 
-def slots_to_words(slots, d, l, base, count):
+def slots_to_words(slots, d, l, base, count, alg=None):
     out = []
     for j in range(count):
+        w0 = alg.word_slot(j, l) if alg is not None else j * l
         x = 0
         for s in range(l):
             for i in range(d):
-                x += int(slots[j * l + s][i]) * base ** (s * d + i)
+                x += int(slots[w0 + s][i]) * base ** (s * d + i)
         out.append(x)
     return out

@@ -721,7 +721,7 @@ static int64_t centered_p(int64_t c, int64_t p) {
 
 CT Eng::scalar(const CT &a, int64_t c) {
     CT o = ct_alloc(a.B, a.lvl, a.parts);
-    if (!dry()) ew_scalar(X->d_mods, a.d, centered_p(c, X->p), o.d, a.B, a.parts, a.lvl, X->n, st);
+    if (!dry()) ew_scalar(X->d_mods, a.d, centered_p(c, X->p), o.d, a.B, a.parts, a.lvl, X->n, st, g_f64_elem ? X->d_fm : nullptr);
     return o;
 }
 CT Eng::add_const(const CT &a, int64_t c) {
@@ -731,7 +731,7 @@ CT Eng::add_const(const CT &a, int64_t c) {
 }
 CT Eng::ptmul(const CT &a, const uint64_t *pt) {
     CT o = ct_alloc(a.B, a.lvl, a.parts);
-    if (!dry()) ew_ptmul(X->d_mods, a.d, pt, o.d, a.B, a.parts, a.lvl, X->n, st);
+    if (!dry()) ew_ptmul(X->d_mods, a.d, pt, o.d, a.B, a.parts, a.lvl, X->n, st, g_f64_elem ? X->d_fm : nullptr);
     return o;
 }
 CT Eng::add_pt(const CT &a, const uint64_t *pt) {

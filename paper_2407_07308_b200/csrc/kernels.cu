@@ -436,10 +436,24 @@ __global__ void k_scalar(const Mod *__restrict__ mods, const uint64_t *__restric
         o[i] = mul_mod(a[i], small_res(c, M.q), M);
     }
 }
+// binary64: c (|c| < p) times a canonical residue, |r| <= 0.75 q (wq = fl(c fl(1/q)), |c| << q)
+__global__ void k_scalar_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ a, int64_t c,
+                           uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
+    using namespace f64;
+    const double cd = (double)c;
+    ROW_LOOP(r, x, rows, n) {
+        const double q = fm[r % lvl].x, qi = fm[r % lvl].y;
+        const uint64_t i = (uint64_t)r * n + x;
+        o[i] = to_u64(fmulv(from_u64(a[i]), cd, q, qi), q);
+    }
+}
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
-               uint32_t lvl, uint32_t n, cudaStream_t st) {
+               uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * parts * lvl;
-    k_scalar<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, lvl, n);
+    if (fm && c > -(1 << 20) && c < (1 << 20))
+        k_scalar_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, a, c, o, (uint32_t)rows, lvl, n);
+    else
+        k_scalar<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
@@ -467,10 +481,24 @@ __global__ void k_ptmul(const Mod *__restrict__ mods, const uint64_t *__restrict
         o[i] = mul_mod(a[i], pt[(uint64_t)limb * n + x], mods[limb]);
     }
 }
+__global__ void k_ptmul_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ a,
+                          const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint32_t rows,
+                          uint32_t lvl, uint32_t n) {
+    using namespace f64;
+    ROW_LOOP(r, x, rows, n) {
+        const uint32_t limb = r % lvl;
+        const double q = fm[limb].x, qi = fm[limb].y;
+        const uint64_t i = (uint64_t)r * n + x;
+        o[i] = to_u64(fmulv(from_u64(a[i]), from_u64(pt[(uint64_t)limb * n + x]), q, qi), q);
+    }
+}
 void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B, uint32_t parts,
-              uint32_t lvl, uint32_t n, cudaStream_t st) {
+              uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * parts * lvl;
-    k_ptmul<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, pt, o, (uint32_t)rows, lvl, n);
+    if (fm)
+        k_ptmul_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, a, pt, o, (uint32_t)rows, lvl, n);
+    else
+        k_ptmul<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, pt, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 

@@ -70,13 +70,13 @@ void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, 
 void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
             uint32_t n, cudaStream_t st);
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
-               uint32_t lvl, uint32_t n, cudaStream_t st);
+               uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm = nullptr);
 // part 0 += c (constant polynomial: every evaluation point)
 void ew_add_const(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
                   uint32_t lvl, uint32_t n, cudaStream_t st);
 // o = a (.) pt, pt u64[L][n] eval (first lvl limbs used), every part
 void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B,
-              uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
+              uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm = nullptr);
 void ew_add_pt(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B,
                uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);
 // fm: per-prime (q, fl(1/q)) when every prime is in [2^49, 2^50) -> binary64 kernels; nullptr -> integer kernels
