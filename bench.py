@@ -262,7 +262,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--pairs", type=int, default=1000)
+    ap.add_argument("--pairs", type=int, default=None,
+                    help="ciphertext pairs per GPU (default: 1000 for compare (C2), 16 dense pairs for c3 compact_compare)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verify", type=int, default=1)
@@ -279,6 +280,8 @@ def main():
         run_reference(args, cfg, rank, world)
         return
     workload = args.workload or {"c4": "tournament", "c5": "sort", "c3": "compact_compare"}.get(args.config, "compare")
+    if args.pairs is None:
+        args.pairs = 16 if workload == "compact_compare" else 1000
     if workload in ("tournament", "sort"):
         run_vector_workload(args, cfg, rank, world, local, workload)
         return

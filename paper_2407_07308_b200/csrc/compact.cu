@@ -25,7 +25,12 @@ static std::vector<int32_t> offsets(uint32_t span) {
 
 // mirrors oracle/circuits.py plan_compaction (independent implementation of R17)
 static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful, uint32_t ints, uint32_t span,
-                               uint32_t *n_out) {
+                               uint32_t *n_out, uint32_t wpr) {
+    // a rotation by delta*l moves a block within its row of wpr blocks only (R6 rows, R17)
+    auto fits = [&](uint32_t b, int32_t dl) {
+        const int64_t t = (int64_t)b - dl, pos = (int64_t)(b % wpr) - dl;
+        return t >= 0 && t < (int64_t)ints && pos >= 0 && pos < (int64_t)wpr;
+    };
     std::vector<std::set<int64_t>> occ;
     std::vector<Group> groups;
     const std::vector<int32_t> offs = offsets(span);
@@ -39,7 +44,7 @@ static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful,
                     size_t cnt = 0;
                     for (uint32_t b : rem) {
                         int64_t t = (int64_t)b - dl;
-                        if (t >= 0 && t < (int64_t)ints && !occ[cp].count(t)) ++cnt;
+                        if (fits(b, dl) && !occ[cp].count(t)) ++cnt;
                     }
                     if (cnt > best_cnt) { best_cnt = cnt; best_cp = (int)cp; best_dl = dl; }
                 }
@@ -48,7 +53,7 @@ static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful,
             std::vector<uint32_t> left;
             for (uint32_t b : rem) {
                 int64_t t = (int64_t)b - best_dl;
-                if (t >= 0 && t < (int64_t)ints && !occ[best_cp].count(t)) {
+                if (fits(b, best_dl) && !occ[best_cp].count(t)) {
                     occ[best_cp].insert(t);
                     g.blocks.push_back(b);
                 } else {
@@ -71,7 +76,7 @@ static const uint64_t *mask_pt(Eng &E, const std::vector<uint32_t> &blocks) {
     for (uint32_t b : blocks) key += std::to_string(b) + ",";
     std::vector<int16_t> sl((size_t)S * D, 0);
     for (uint32_t b : blocks)
-        for (uint32_t s = b * l; s < (b + 1) * l; ++s) sl[(size_t)s * D] = 1;
+        for (uint32_t s = X->alg.word_slot(b, l); s < X->alg.word_slot(b, l) + l; ++s) sl[(size_t)s * D] = 1;
     return ctx_pt(X, key, sl, E.st);
 }
 
@@ -90,7 +95,7 @@ extern "C" bc_status bc_compact(bc_ctx *X, const bc_keys *keys, bc_ct in, const 
                 if (h_useful[(size_t)c * ints + b]) useful[c].push_back(b);
         uint32_t nout = 0;
         const uint32_t span = X->prm.compact_span ? X->prm.compact_span : 3;
-        std::vector<Group> groups = plan(useful, ints, span, &nout);
+        std::vector<Group> groups = plan(useful, ints, span, &nout, X->alg.words_per_row(X->l));
         if (nout > out.batch) BC_THROW(BC_E_ARG, "output capacity too small");
         if (h_dest) {
             for (size_t i = 0; i < (size_t)nin * ints; ++i) h_dest[i] = -1;

@@ -267,9 +267,9 @@ void ctx_build(bc_ctx *X) {
     // slot algebra (R5)
     if (!X->alg.build(X->p, X->m, X->phi, std::min<uint32_t>(P.d, (uint32_t)mult_order(X->p, X->m))))
         BC_THROW(BC_E_PARAM, X->alg.error);
-    if (P.d > X->alg.D || P.d < 1 || P.l < 1 || P.l > X->alg.S) BC_THROW(BC_E_PARAM, "(d, l) incompatible with the ring");
+    if (P.d > X->alg.D || P.d < 1 || P.l < 1 || P.l > X->alg.S1) BC_THROW(BC_E_PARAM, "(d, l) incompatible with the ring");
     X->base = P.circuit == 'B' ? X->p : (X->p + 1) / 2;
-    X->ints = X->alg.S / P.l;
+    X->ints = X->alg.S2 * X->alg.words_per_row(P.l);     // R6: row-aligned integers
     // circuit coefficients (R16)
     {
         const int64_t p = X->p, h = (p - 1) / 2;
@@ -396,6 +396,7 @@ void ctx_build(bc_ctx *X) {
         bool f_ok = true;
         for (uint32_t i = 0; i < NP; ++i) f_ok = f_ok && X->moduli[i] < (1ull << 50);
         T.fmods = nullptr;
+        T.fdhb1 = T.fdhb2 = nullptr;
         if (f_ok) {
             auto fd = [&](const std::vector<u64x2> &v, size_t per) {
                 std::vector<double2> o(v.size());
@@ -442,6 +443,52 @@ void ctx_build(bc_ctx *X) {
             }
             T.fxta = fd1(xta, M); T.fxtb = fd1(xtb, M);
             T.fmods = dev_upload(X, fm);
+            T.fdhb1 = T.fdhb2 = nullptr;
+            if (!X->prime_m) {
+                // Barrett reduction mod Phi_m (composite m): Ir = Phi_m^{-1} mod x^k, k = m - n, from
+                // Phi_m = prod_{d | m} (1 - x^d)^{mu(m/d)} (m > 1): divide by (1 - x^d) where mu = +1
+                // (stride-d prefix sums), multiply where mu = -1; exact small integers.  Phi_m is
+                // palindromic, so rev(Phi_m)^{-1} = Ir.
+                const uint32_t k = m - n;
+                for (uint32_t j = 0; j <= n; ++j)
+                    if (X->phi[j] != X->phi[n - j]) BC_THROW(BC_E_PARAM, "Phi_m not palindromic");
+                auto mobius = [](uint32_t v) {
+                    int mu = 1;
+                    for (uint32_t d = 2; d * d <= v; ++d)
+                        if (v % d == 0) { v /= d; if (v % d == 0) return 0; mu = -mu; }
+                    return v > 1 ? -mu : mu;
+                };
+                std::vector<int64_t> ir(k, 0);
+                ir[0] = 1;
+                for (uint32_t d = 1; d <= m; ++d) {
+                    if (m % d) continue;
+                    const int mu = mobius(m / d);
+                    if (mu == 1) { for (uint32_t i = d; i < k; ++i) ir[i] += ir[i - d]; }
+                    else if (mu == -1) { for (int64_t i = (int64_t)k - 1; i >= (int64_t)d; --i) ir[i] -= ir[i - d]; }
+                }
+                const uint32_t le = (uint32_t)nttf_row_loge(X->logR, X->logC), E = 1u << le, tpr = X->C >> le;
+                std::vector<u64x2> b1((size_t)NP * M), b2((size_t)NP * M);
+                for (uint32_t i = 0; i < NP; ++i) {
+                    const uint64_t q = X->moduli[i];
+                    const uint64_t ps = psi[(size_t)i * M + 1].w, Minv = invmod_h(M % q, q);
+                    std::vector<uint64_t> c1(M, 0), c2(M, 0);
+                    for (uint32_t j = 0; j < k; ++j) c1[j] = (uint64_t)(((ir[j] % (int64_t)q) + (int64_t)q) % (int64_t)q);
+                    for (uint32_t j = 0; j <= n; ++j) c2[j] = (uint64_t)(((X->phi[j] % (int64_t)q) + (int64_t)q) % (int64_t)q);
+                    host_ntt(c1, ps, q);
+                    host_ntt(c2, ps, q);
+                    for (uint32_t rp = 0; rp < X->R; ++rp)
+                        for (uint32_t t = 0; t < tpr; ++t)
+                            for (uint32_t e = 0; e < E; ++e) {
+                                const uint32_t cp = t * E + e;     // pass position rp*C + cp, thread-minor order
+                                const uint32_t kk = brev_h(rp, X->logR) + X->R * brev_h(cp, X->logC);
+                                const size_t o = (size_t)i * M + (size_t)rp * X->C + e * tpr + t;
+                                b1[o] = u64x2{mulmod_h(c1[kk], Minv, q), 0};
+                                b2[o] = u64x2{mulmod_h(c2[kk], Minv, q), 0};
+                            }
+                }
+                T.fdhb1 = fd1(b1, M);
+                T.fdhb2 = fd1(b2, M);
+            }
             bool win = true;
             for (uint32_t i = 0; i < NP; ++i) win = win && X->moduli[i] >= (1ull << 49);
             X->d_fm = win ? T.fmods : nullptr;
@@ -652,10 +699,10 @@ CT Eng::sub(const CT &a, uint32_t b0, uint32_t nb) {
 }
 
 // transform scratch: one L2-sized launch group of jobs (kernels.cu processes the batch group by group)
-static uint64_t ntt_scratch_words(const bc_ctx *X, uint32_t npoly, uint32_t njl) {
+static uint64_t ntt_scratch_words(const bc_ctx *X, uint32_t npoly, uint32_t njl, bool inv = false) {
     const uint64_t jobs = (uint64_t)npoly * njl;
-    const uint64_t group = std::max<uint64_t>(1, g_ntt_group_bytes / ((uint64_t)X->M * 8));
-    return std::min(jobs, group) * X->M;
+    const bool barrett = inv && ntt_inverse_barrett(X->T);
+    return ntt_group_jobs(X->T, jobs, barrett) * X->M * (barrett ? 2 : 1);
 }
 
 void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
@@ -664,7 +711,7 @@ void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
     ntt_forward(X->T, in, out, npoly, lm, ips, ops, (uint64_t *)scr->p, st);
 }
 void Eng::ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
-    BufP scr = alloc_words(ntt_scratch_words(X, npoly, lm.njl));
+    BufP scr = alloc_words(ntt_scratch_words(X, npoly, lm.njl, true));
     if (dry()) return;
     ntt_inverse(X->T, in, out, npoly, lm, ips, ops, (uint64_t *)scr->p, st);
 }
@@ -1016,8 +1063,11 @@ static void bivariate(Eng &E, const Val &x, const Val &y, Val *lt, Val *eq) {
 static std::vector<int16_t> block_mask(bc_ctx *X, const std::function<bool(uint32_t)> &pred) {
     const uint32_t S = X->alg.S, D = X->alg.D;
     std::vector<int16_t> m((size_t)S * D, 0);
-    for (uint32_t s = 0; s < S; ++s)
-        if (s < X->ints * X->l && pred(s % X->l)) m[(size_t)s * D] = 1;
+    const uint32_t S1 = X->alg.S1, wpr = X->alg.words_per_row(X->l);
+    for (uint32_t s = 0; s < S; ++s) {
+        const uint32_t row = s / S1, i = s - row * S1;    // R6 rows: position i of row `row`
+        if (i < wpr * X->l && row * wpr + i / X->l < X->ints && pred(i % X->l)) m[(size_t)s * D] = 1;
+    }
     return m;
 }
 

@@ -302,13 +302,21 @@ bool SlotAlgebra::build(int64_t p_, uint32_t m_, const std::vector<int64_t> &phi
         if (ok) { zeta = z; break; }
     }
     if (zeta.empty()) { error = "no element of order m"; return false; }
-    // slot generator: smallest t with order S in Z_m^*/<p>, preferring t^S = 1 mod m
+    // R5 slot generators.  Quotient orders: the exponents k with t^k in <p> are the multiples of the
+    // quotient order, so start from ord(t) (n divided by its primes while t^(o/r) = 1) and divide.
     std::set<uint32_t> H;
     for (uint32_t k = 0; k < D; ++k) H.insert((uint32_t)powmod_h((uint64_t)p, k, m));
-    auto qorder = [&](uint32_t t) { uint32_t k = 1; uint64_t x = t % m; while (!H.count((uint32_t)x)) { x = x * t % m; ++k; } return k; };
-    g = 0;
+    const std::vector<uint64_t> nf = prime_factors(n);
+    auto qorder = [&](uint32_t tt) {
+        uint64_t o = n;
+        for (uint64_t r : nf) while (o % r == 0 && powmod_h(tt, o / r, m) == 1) o /= r;
+        for (uint64_t r : nf) while (o % r == 0 && H.count((uint32_t)powmod_h(tt, o / r, m))) o /= r;
+        return (uint32_t)o;
+    };
+    g = 0; g2 = 1; S1 = S; S2 = 1;
     uint32_t first_any = 0;
     if (S == 1) g = 1;
+    // cyclic quotient: the smallest t of quotient order S with t^S = 1 (mod m), else the smallest of order S
     for (uint32_t tt = 2; tt < m && g == 0; ++tt) {
         if (gcd_u64(tt, m) != 1) continue;
         if (qorder(tt) != S) continue;
@@ -316,9 +324,49 @@ bool SlotAlgebra::build(int64_t p_, uint32_t m_, const std::vector<int64_t> &phi
         if (powmod_h(tt, S, m) == 1) g = tt;
     }
     if (!g) g = first_any;
-    if (!g) { error = "Z_m^*/<p> is not cyclic (hypercube slots unsupported)"; return false; }
+    if (!g) {
+        // hypercube Z_S1 x Z_S2: S1 = the largest quotient order; g the smallest of that order, preferring
+        // g^S1 = 1; g2 the smallest t outside <p, g> with t^S2 in <p, g> (and no smaller power), preferring t^S2 = 1
+        std::vector<uint32_t> qo(m, 0);
+        S1 = 0;
+        for (uint32_t tt = 2; tt < m; ++tt)
+            if (gcd_u64(tt, m) == 1) { qo[tt] = qorder(tt); S1 = std::max(S1, qo[tt]); }
+        S2 = S / S1;
+        uint32_t gf1 = 0;
+        for (uint32_t tt = 2; tt < m && !g; ++tt) {
+            if (qo[tt] != S1) continue;
+            if (!gf1) gf1 = tt;
+            if (powmod_h(tt, S1, m) == 1) g = tt;
+        }
+        if (!g) g = gf1;
+        std::vector<char> inHg(m, 0);
+        for (uint32_t k = 0; k < D; ++k)
+            for (uint32_t i = 0; i < S1; ++i)
+                inHg[powmod_h((uint64_t)p, k, m) * powmod_h(g, i, m) % m] = 1;
+        uint32_t c2 = 0, good2 = 0;
+        for (uint32_t tt = 2; tt < m && !good2; ++tt) {
+            if (gcd_u64(tt, m) != 1 || inHg[tt]) continue;
+            if (!inHg[powmod_h(tt, S2, m)]) continue;
+            bool ok = true;
+            for (uint32_t j = 1; j < S2 && ok; ++j) ok = !inHg[powmod_h(tt, j, m)];
+            if (!ok) continue;
+            if (!c2) c2 = tt;
+            if (powmod_h(tt, S2, m) == 1) good2 = tt;
+        }
+        g2 = good2 ? good2 : c2;
+        if (!g || !g2 || S1 * S2 != S) { error = "Z_m^*/<p> is not Z_S1 x Z_S2"; return false; }
+        std::vector<char> cover(m, 0);
+        uint64_t cnt = 0;
+        for (uint32_t tt = 1; tt < m; ++tt)
+            if (inHg[tt])
+                for (uint32_t j = 0; j < S2; ++j) {
+                    const uint64_t u = tt * powmod_h(g2, j, m) % m;
+                    if (!cover[u]) { cover[u] = 1; ++cnt; }
+                }
+        if (cnt != n) { error = "Z_m^*/<p> is not generated by (p, g, g2)"; return false; }
+    }
     t.resize(S);
-    for (uint32_t s = 0; s < S; ++s) t[s] = (uint32_t)powmod_h(g, s, m);
+    for (uint32_t s = 0; s < S; ++s) t[s] = (uint32_t)(powmod_h(g, s % S1, m) * powmod_h(g2, s / S1, m) % m);
     // zeta^e table
     zpow.assign((size_t)m * D, 0);
     std::vector<int64_t> x = gf.one();

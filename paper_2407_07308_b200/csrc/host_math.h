@@ -50,8 +50,11 @@ struct SlotAlgebra {
     uint32_t m, n, D, S;
     GF gf;
     std::vector<int64_t> zeta;          // D coefficients
-    uint32_t g;                          // slot generator
-    std::vector<uint32_t> t;             // t_s = g^s mod m
+    uint32_t g;                          // slot generator (rotations; rows of S1 slots)
+    uint32_t S1 = 0, g2 = 1, S2 = 1;     // hypercube: slot s = j*S1 + i <-> g^i g2^j (cyclic: S1 = S)
+    std::vector<uint32_t> t;             // t_s
+    uint32_t words_per_row(uint32_t l) const { return S1 / l; }
+    uint32_t word_slot(uint32_t w, uint32_t l) const { return (w / (S1 / l)) * S1 + (w % (S1 / l)) * l; }
     std::vector<int64_t> zpow;           // [m][D]: zeta^e
     std::vector<std::vector<int64_t>> E0;  // [D][n]: slot-0 idempotent basis, E0_i(zeta) = X^i
     std::vector<std::vector<int64_t>> kappa;  // [d*D][D]: kappa_{i,k} = mu_i^{p^k} (F_{p^D} values)

@@ -308,6 +308,15 @@ __global__ void k_reduce_composite(NttTables T, uint64_t *__restrict__ out, uint
     for (int j = threadIdx.x; j < (int)T.n; j += blockDim.x) dst[j] = A[j];
 }
 
+// jobs per launch group: scratch of one group stays within g_ntt_group_bytes (Barrett: two slots per job)
+uint64_t ntt_group_jobs(const NttTables &T, uint64_t jobs, bool barrett) {
+    const uint64_t g = std::max<uint64_t>(1, std::min<uint64_t>(65535, (uint64_t)g_ntt_group_bytes / ((uint64_t)T.M * 8 * (barrett ? 2 : 1))));
+    return std::max<uint64_t>(1, std::min(jobs, g));
+}
+bool ntt_inverse_barrett(const NttTables &T) {
+    return (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T) && !T.prime_m && T.fdhb1 != nullptr;
+}
+
 static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                        uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st,
                        int inv) {
@@ -328,18 +337,21 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     }
     lm.npoly = npoly;
     // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
-    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(65535, (uint64_t)g_ntt_group_bytes / ((uint64_t)T.M * 8)));
     const bool vf = (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T);
+    // composite m on the binary64 path: Barrett reduction mod Phi_m (needs a second M-word slot per job)
+    const bool barrett = inv && vf && !T.prime_m && T.fdhb1 != nullptr;
+    const uint64_t chunk = ntt_group_jobs(T, jobs, barrett);
     const bool v2 = g_ntt_impl != 1 && ntt2_supported(T);
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
         if (v2) {
             if (vf)
-                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
+                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st,
+                         barrett ? scratch + chunk * T.M : nullptr);
             else
                 ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
-            if (inv) {
+            if (inv && !barrett) {
                 if (T.prime_m)
                     k_reduce_prime<<<grid_rows(T.n, nj), 256, 0, st>>>(T, out, out_pstride, lm, j0, nj,
                                                                                      scratch);

@@ -31,6 +31,9 @@ struct NttTables {
     const double2 *ftwRb, *ftwCb;           // [P][R/2], [P][C/2]: omega_L^{brev_{logL-1}(j)} (forward CT blocks)
     const double2 *ftwRi, *ftwCi;           // omega_L^{-j} (inverse)
     const double *ftf1, *ftf1i, *ftfo, *ftfoi, *fdhf, *fdhi, *fxta, *fxtb;   // as the u64x2 tables, w only (8 bytes)
+    // composite m (binary64 path): Barrett reduction mod Phi_m by two size-M convolutions with constants, in
+    // the D^ layout, M^{-1} folded: NTT(rev(Phi)^{-1} mod x^{m-n}) and NTT(Phi); null -> long division
+    const double *fdhb1, *fdhb2;
     uint32_t m, n, M, R, C, logR, logC;
     int prime_m;
     int dbg;              // ntt3.cu timing experiments only (bc_tune "ntt_dbg"): skip table reads; results invalid          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
@@ -158,8 +161,10 @@ void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
 bool nttf_supported(const NttTables &T);
 int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: position r*C + tau*E + k at r*C + k*(C/E) + tau
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *scratch2 = nullptr);
 extern uint64_t g_ntt_group_bytes;
+uint64_t ntt_group_jobs(const NttTables &T, uint64_t jobs, bool barrett);
+bool ntt_inverse_barrett(const NttTables &T);
 extern int g_ntt_dbg;
 extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when the context allows them   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;

@@ -206,7 +206,8 @@ bc_status bc_encrypt_slots(bc_ctx *X, const bc_keys *keys, const int16_t *h_slot
     return encrypt_impl(X, keys, h_slots, batch, seed, ct_index0, out, ws, wsb, st);
 }
 
-// R6: word j -> slots j*l .. j*l+l-1; slot j*l+s coefficient i = digit s*d + i (little-endian)
+// R6: word j -> slots w0 .. w0+l-1, w0 = word_slot(j) (row-aligned; j*l when cyclic);
+// slot w0+s coefficient i = digit s*d + i (little-endian)
 bc_status bc_encrypt(bc_ctx *X, const bc_keys *keys, const uint64_t *h_words, uint32_t batch, uint64_t seed,
                      uint64_t ct_index0, bc_ct out, void *ws, size_t wsb, void *st) {
     if (!X || !h_words) { last_error() = "null argument"; return BC_E_ARG; }
@@ -226,7 +227,7 @@ bc_status bc_encrypt(bc_ctx *X, const bc_keys *keys, const uint64_t *h_words, ui
             if (!inf && (unsigned __int128)x >= cap) { last_error() = "word out of range"; return BC_E_RANGE; }
             for (uint32_t s = 0; s < l; ++s)
                 for (uint32_t i = 0; i < d; ++i) {
-                    slots[((size_t)b * S + j * l + s) * D + i] = (int16_t)(x % base);
+                    slots[((size_t)b * S + X->alg.word_slot(j, l) + s) * D + i] = (int16_t)(x % base);
                     x /= base;
                 }
         }
@@ -309,7 +310,7 @@ bc_status bc_decrypt(bc_ctx *X, const bc_sk *sk, bc_ct in, uint64_t *h_out, int 
     if (s != BC_OK) return s;
     for (uint32_t b = 0; b < in.batch; ++b)
         for (uint32_t j = 0; j < ints; ++j) {
-            const int16_t *blk = sl.data() + ((size_t)b * S + (size_t)j * l) * D;
+            const int16_t *blk = sl.data() + ((size_t)b * S + (size_t)X->alg.word_slot(j, l)) * D;
             if (as_bits) { h_out[(size_t)b * ints + j] = (uint64_t)blk[0]; continue; }
             unsigned __int128 x = 0, w = 1;
             for (uint32_t si = 0; si < l; ++si)

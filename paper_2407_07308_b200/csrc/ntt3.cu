@@ -253,8 +253,10 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
     const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
     const uint32_t c = blockIdx.x * TC + col;
-    const double *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
-    const uint64_t *src = in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
+    // INV: 0 Bluestein forward, 1 Bluestein inverse, 2/3 the Barrett reduction mod Phi_m of a composite m
+    // (2: quotient convolution, input rev(A)_t = A_{m-1-t}, t < m - n; 3: Phi_m * Q, input Q_t = A'_{n+t})
+    const double *tf = (INV == 1 ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
+    const uint64_t *src = INV >= 2 ? in + (uint64_t)blockIdx.y * T.M : in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
     typedef PtTab<LOGR, LOGE, true> PTT;
     double2 *stw = (double2 *)(smf + (size_t)R * TC), *spt = stw + R / 2;
     const double2 *gtw = T.ftwRb + (uint64_t)J.pr * (R / 2);
@@ -267,14 +269,18 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
         const uint32_t t = r * CC + c;
         double x = 0.0;
-        if (!INV) {
+        if (INV == 0) {
             if (t < T.n) {
                 const double xin = (T.dbg & 64) ? (double)t : from_u64(__ldcs(src + t));
                 x = (T.dbg & 1) ? xin : fmm8(xin, tf[t], q, qi);
             }
-        } else if (t < T.m) {
-            const int ps = T.pos[t];
-            if (ps >= 0) x = fmm8(from_u64(__ldcs(src + ps)), tf[t], q, qi);
+        } else if (INV == 1) {
+            if (t < T.m) {
+                const int ps = T.pos[t];
+                if (ps >= 0) x = fmm8(from_u64(__ldcs(src + ps)), tf[t], q, qi);
+            }
+        } else if (t < T.m - T.n) {
+            x = from_u64(src[INV == 2 ? T.m - 1 - t : T.n + t]);       // canonical, bound q (UQ = UMUL8)
         }
         v[k] = x;
         bd[k] = UMUL8;
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), FNTT_MINB(RB * (1 <
     __syncthreads();
     frt_pass<LOGC, LOGE, true, 0>(v, bd, tau, srow, tw, ptf, q, qi);
     // D^ in the thread-minor layout of this pass (entry of position tau*E + k at k*TPR + tau: coalesced)
-    const double *dh = (INV ? T.fdhi : T.fdhf) + (uint64_t)J.pr * T.M + (uint64_t)row * C + tau;
+    const double *dh = (INV == 0 ? T.fdhf : INV == 1 ? T.fdhi : INV == 2 ? T.fdhb1 : T.fdhb2) + (uint64_t)J.pr * T.M + (uint64_t)row * C + tau;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         need(v, bd, k, LIM_MUL, q, qi);
@@ -346,7 +352,7 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), FNTT_MINB(RB * (1 <
 template <int LOGR, int LOGE, int TC, int INV, int LOGC>
 __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 << (LOGR - LOGE))))
     kf_passC(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride, LimbMap lm, uint64_t job0,
-             double *__restrict__ scratch) {
+             double *__restrict__ scratch, uint64_t *__restrict__ aux) {
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
     constexpr uint32_t CC = 1u << LOGC;
     extern __shared__ double smf[];
@@ -370,16 +376,29 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     }
     __syncthreads();
     fct_pass<LOGR, LOGE, false, TC, 0>(v, bd, tau, col, smf, stw, spt, q, qi);
-    const double *tfo = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
+    const double *tfo = (INV == 1 ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
     uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
     uint64_t *scru = (uint64_t *)scr;
-    if (INV) __syncthreads();   // all columns of this block read before in-place writes of A_t
+    uint64_t *A1 = INV >= 2 ? aux + (uint64_t)blockIdx.y * T.M : nullptr;    // the A_t of this job (Barrett)
+    const uint32_t kq = T.m - T.n;
+    if (INV == 1) __syncthreads();   // all columns of this block read before in-place writes of A_t
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
         const uint32_t t = r * CC + c;
         need(v, bd, k, LIM_MUL, q, qi);
         if (t >= T.m) continue;
+        if (INV == 2) {               // Qr_t (t < m - n) -> Q_{m-n-1-t}, stored over A_{n..m-1}
+            if (t < kq) A1[T.n + (kq - 1 - t)] = to_u64(fred(v[k], q, qi), q);
+            continue;
+        }
+        if (INV == 3) {               // a_t = A_t - (Phi_m Q)_t, t < n
+            if (t < T.n) {
+                const double a = from_u64(A1[t]);
+                __stcs(dst + t, to_u64(fred(__dsub_rn(a, fred(v[k], q, qi)), q, qi), q));
+            }
+            continue;
+        }
         const uint64_t x = to_u64((T.dbg & 16) ? fred(v[k], q, qi) : fmm8(v[k], tfo[t], q, qi), q);
         if (!INV) {
             const int ps = (T.dbg & 32) ? (t < T.n ? (int)t : -1) : T.pos[t];
@@ -403,7 +422,7 @@ struct Shape {
 
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
+                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *scratch2) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
     static bool init = false;
     if (!init) {
@@ -413,6 +432,12 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
         cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 1, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
+        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
+        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         init = true;
     }
     double *scr = (double *)scratch;
@@ -422,11 +447,22 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
     if (!inv) {
         kf_passA<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
-        kf_passC<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr);
+        kf_passC<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
     } else {
         kf_passA<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
-        kf_passC<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr);
+        kf_passC<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
+        if (scratch2) {
+            // composite m: A (length m, in scr) mod Phi_m by Barrett division with two size-M convolutions
+            double *s2 = (double *)scratch2;
+            kf_passA<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scratch, 0, lm, j0, s2);
+            kf_passB<LOGC, LOGEC, S::RB, 2><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
+            kf_passC<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scratch);
+            kf_passA<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scratch, 0, lm, j0, s2);
+            kf_passB<LOGC, LOGEC, S::RB, 3><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
+            kf_passC<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scratch);
+            launch_counter() += 6;
+        }
     }
     launch_counter() += 3;
 }
@@ -446,8 +482,8 @@ bool nttf_supported(const NttTables &T) {
 }
 
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
-#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st)
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *scratch2) {
+#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, scratch2)
     switch (T.logR * 16 + T.logC) {
         case 8 * 16 + 8:
             switch (g_ntt_impl) {

@@ -22,7 +22,7 @@ def pair(oracle_params):
     return get
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2", "c3h", "c3s2"])
 def test_tables_match_oracle(pair, cfg):
     T = pair(cfg)
     q, w = T.ctx.moduli()
@@ -37,9 +37,11 @@ def test_tables_match_oracle(pair, cfg):
         assert sorted(T.ctx.galois()) == galois_for(T.P)
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c3h", "c3s2"])
 def test_ntt_forward_inverse(pair, cfg):
-    """a1/a2: Bluestein forward == naive evaluation; inverse recovers coefficients (all limbs)."""
+    """a1/a2: Bluestein forward == naive evaluation; inverse recovers coefficients (all limbs).
+    c3h / c3s2: composite m (the inverse reduces mod Phi_m: long division on the integer path,
+    Barrett division by two size-M convolutions on the binary64 path)."""
     import torch
     T = pair(cfg)
     P = T.P
@@ -57,9 +59,11 @@ def test_ntt_forward_inverse(pair, cfg):
     torch.cuda.synchronize()
 
 
-def test_ntt_full_size_sampled(pair):
-    """a1/a2 at C2's full ring (n = 30940, M = 65536): two limbs vs naive evaluation."""
-    T = pair("c2")
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_ntt_full_size_sampled(pair, cfg):
+    """a1/a2 at full size (C2: n = 30940, M = 65536; C3: composite m = 52053, n = 34700, M = 131072,
+    Barrett reduction mod Phi_m): two limbs vs naive evaluation, inverse recovers every limb."""
+    T = pair(cfg)
     P = T.P
     rng = np.random.default_rng(12)
     coef = np.stack([rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.moduli])[None]
@@ -93,7 +97,7 @@ def test_ntt_register_passes_match_radix2(pair):
     assert np.array_equal(to_u64(T.ctx.ntt_inv(from_u64(f2, T.ctx.device))), coef)
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c3h", "c3s2"])
 def test_encrypt_decrypt_match_oracle(pair, cfg):
     """R9/R10 + R7 sampler: the product's ciphertexts equal the oracle's bit for bit."""
     T = pair(cfg)
@@ -111,7 +115,7 @@ def test_encrypt_decrypt_match_oracle(pair, cfg):
     assert np.array_equal(dec, words)
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c3s2"])
 def test_ops_match_oracle(pair, cfg):
     """a3 tensor, a4 automorphism, a5 key switching (relin / rotation / Frobenius), a6 modswitch."""
     T = pair(cfg)
@@ -363,8 +367,9 @@ def test_bivariate_compare_matches_oracle(pair):
 
 
 def test_compare_full_c3_decrypts(pair):
-    """C3 stand-in at full size (p = 31 bivariate, m = 17351, (d,l) = (5,3)): compaction of 4
-    sparse ciphertexts (Fig. 7 pattern) to 1, then compare_lt decrypts to [a<b] in every block."""
+    """C3 at full size (Table 3 p10 B: p = 31 bivariate, m = 52053 composite, 3470 x 2 hypercube
+    slots, (d,l) = (5,3), 2312 integers): compaction of 4 sparse ciphertexts (Fig. 7 pattern, every
+    4th block; 289 per row per input) to 1, then compare_lt decrypts to [a<b] in every block."""
     T = pair("c3")
     P = T.P
     ints = T.ctx.ints_per_ct
@@ -435,3 +440,39 @@ def test_binary64_kernels_match_integer_kernels(pair):
     assert np.array_equal(f, g)
     bits = T.ctx.decrypt(T.keys, T.ctx.compare_lt(T.keys, ca, cb), as_bits=True)[0]
     assert list(bits) == [int(x < y) for x, y in zip(a, b)]
+
+
+def test_hypercube_compare_bit_exact(pair):
+    """C3's slot structure on the tiny hypercube ring c3h (p = 31 bivariate, m = 33 = 3 x 11,
+    Z_2 x Z_2 slots, one integer per row): whole compare_lt ciphertext bit-exact vs the oracle."""
+    from oracle import circuits
+    T = pair("c3h")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    a, b = [5, 923520], [7, 923520]
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=910)
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=911)
+    lt = T.ctx.compare_lt(T.keys, ca, cb)
+    assert list(T.ctx.decrypt(T.keys, lt, as_bits=True)[0]) == [int(x < y) for x, y in zip(a, b)]
+    ev = circuits.OracleEval(P, T.okeys)
+    olt, _ = circuits.compare(ev, T.oracle_ct(a, 910), T.oracle_ct(b, 911), P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(lt)[0], T.ct_eval(olt))
+
+
+def test_hypercube_shadow_compare_decrypts(pair):
+    """C3's shadow c3s2 (m = 1851 composite, 56 x 2 hypercube, (d,l) = (5,3), 36 integers): a batch
+    of 3 compares decrypts to [a<b] in every block (row-aligned words, row-local lex rounds)."""
+    T = pair("c3s2")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(44)
+    A, B = [], []
+    for _ in range(3):
+        a, b = mixed_pairs(P, rng, ints)
+        A.append(a)
+        B.append(b)
+    ca = T.ctx.encrypt(T.keys, np.array(A, dtype=np.uint64), SEED_ENC, ct_index0=0)
+    cb = T.ctx.encrypt(T.keys, np.array(B, dtype=np.uint64), SEED_ENC, ct_index0=3)
+    bits = T.ctx.decrypt(T.keys, T.ctx.compare_lt(T.keys, ca, cb), as_bits=True)
+    for i in range(3):
+        assert list(bits[i]) == [int(x < y) for x, y in zip(A[i], B[i])]
