@@ -104,7 +104,9 @@ void bc_keys_destroy(bc_keys *keys);
 /* ---- encode / encrypt / decrypt (R6, R9, R10) -------------------------------- */
 /* words[batch * ints_per_ct] (little-endian digits) -> batch
  * ciphertexts at the top level.  ct_index0 = global index of the first
- * ciphertext (drives the counter-based sampler, R7). */
+ * ciphertext (drives the counter-based sampler, R7).  Word j occupies the l slots
+ * from floor(j / wpr) * S1 + (j mod wpr) * l, wpr = floor(S1 / l) (R6: rows of S1
+ * slots for hypercube slot structures such as p10's 3470 x 2; S1 = S when cyclic). */
 bc_status bc_encrypt(bc_ctx *ctx, const bc_keys *keys, const uint64_t *h_words, uint32_t batch,
                      uint64_t seed, uint64_t ct_index0, bc_ct out, void *d_ws, size_t ws_bytes,
                      void *stream);
