@@ -397,6 +397,8 @@ void ctx_build(bc_ctx *X) {
         for (uint32_t i = 0; i < NP; ++i) f_ok = f_ok && X->moduli[i] < (1ull << 50);
         T.fmods = nullptr;
         T.fdhb1 = T.fdhb2 = nullptr;
+        T.tb = nullptr;
+        T.Mslot = M;
         if (f_ok) {
             auto fd = [&](const std::vector<u64x2> &v, size_t per) {
                 std::vector<double2> o(v.size());
@@ -466,28 +468,68 @@ void ctx_build(bc_ctx *X) {
                     if (mu == 1) { for (uint32_t i = d; i < k; ++i) ir[i] += ir[i - d]; }
                     else if (mu == -1) { for (int64_t i = (int64_t)k - 1; i >= (int64_t)d; --i) ir[i] -= ir[i - d]; }
                 }
-                const uint32_t le = (uint32_t)nttf_row_loge(X->logR, X->logC), E = 1u << le, tpr = X->C >> le;
-                std::vector<u64x2> b1((size_t)NP * M), b2((size_t)NP * M);
+                // the two convolutions run at the smallest power of two Mb >= max(2k - 1, m) (no wrap:
+                // rev(A) Ir needs 2k - 1 < Mb outputs' worth of room, Phi Q has degree m - 1 < Mb), with
+                // their own table set X->Tb (root psi^(M/Mb)); slots of A keep the main stride M
+                uint32_t Mb = 1, lgb = 0;
+                while (Mb < std::max(2 * k - 1, m)) { Mb <<= 1; ++lgb; }
+                NttTables &B = X->Tb;
+                B = NttTables{};
+                B.logR = lgb / 2; B.logC = lgb - B.logR; B.R = 1u << B.logR; B.C = 1u << B.logC;
+                B.M = Mb; B.m = m; B.n = n; B.Mslot = M; B.prime_m = 0; B.mods = X->d_mods;
+                if (ntt2_supported(B)) {
+                const uint32_t le = (uint32_t)nttf_row_loge(B.logR, B.logC), E = 1u << le, tpr = B.C >> le;
+                std::vector<u64x2> b1((size_t)NP * Mb), b2((size_t)NP * Mb), bxa((size_t)NP * Mb), bxb((size_t)NP * Mb);
+                std::vector<u64x2> btR((size_t)NP * (B.R / 2)), btRi((size_t)NP * (B.R / 2)), btC((size_t)NP * (B.C / 2)),
+                    btCi((size_t)NP * (B.C / 2));
                 for (uint32_t i = 0; i < NP; ++i) {
                     const uint64_t q = X->moduli[i];
-                    const uint64_t ps = psi[(size_t)i * M + 1].w, Minv = invmod_h(M % q, q);
-                    std::vector<uint64_t> c1(M, 0), c2(M, 0);
+                    const uint64_t ps = powmod_h(psi[(size_t)i * M + 1].w, M / Mb, q), psinv = invmod_h(ps, q);
+                    const uint64_t Minv = invmod_h(Mb % q, q);
+                    std::vector<uint64_t> pw(Mb);
+                    uint64_t x = 1;
+                    for (uint32_t e = 0; e < Mb; ++e) { pw[e] = x; x = mulmod_h(x, ps, q); }
+                    std::vector<uint64_t> c1(Mb, 0), c2(Mb, 0);
                     for (uint32_t j = 0; j < k; ++j) c1[j] = (uint64_t)(((ir[j] % (int64_t)q) + (int64_t)q) % (int64_t)q);
                     for (uint32_t j = 0; j <= n; ++j) c2[j] = (uint64_t)(((X->phi[j] % (int64_t)q) + (int64_t)q) % (int64_t)q);
                     host_ntt(c1, ps, q);
                     host_ntt(c2, ps, q);
-                    for (uint32_t rp = 0; rp < X->R; ++rp)
+                    for (uint32_t rp = 0; rp < B.R; ++rp)
                         for (uint32_t t = 0; t < tpr; ++t)
                             for (uint32_t e = 0; e < E; ++e) {
                                 const uint32_t cp = t * E + e;     // pass position rp*C + cp, thread-minor order
-                                const uint32_t kk = brev_h(rp, X->logR) + X->R * brev_h(cp, X->logC);
-                                const size_t o = (size_t)i * M + (size_t)rp * X->C + e * tpr + t;
+                                const uint32_t kk = brev_h(rp, B.logR) + B.R * brev_h(cp, B.logC);
+                                const size_t o = (size_t)i * Mb + (size_t)rp * B.C + e * tpr + t;
                                 b1[o] = u64x2{mulmod_h(c1[kk], Minv, q), 0};
                                 b2[o] = u64x2{mulmod_h(c2[kk], Minv, q), 0};
                             }
+                    for (uint32_t r = 0; r < B.R; ++r) {
+                        const uint32_t k1 = brev_h(r, B.logR);
+                        for (uint32_t c = 0; c < B.C; ++c) {
+                            const uint32_t e1 = (c * k1) & (Mb - 1);
+                            bxa[(size_t)i * Mb + (size_t)r * B.C + c] = u64x2{pw[e1], 0};
+                            bxb[(size_t)i * Mb + (size_t)r * B.C + c] = u64x2{pw[(Mb - e1) & (Mb - 1)], 0};
+                        }
+                    }
+                    const uint64_t wR = powmod_h(ps, Mb / B.R, q), wRi = powmod_h(psinv, Mb / B.R, q);
+                    const uint64_t wC = powmod_h(ps, Mb / B.C, q), wCi = powmod_h(psinv, Mb / B.C, q);
+                    std::vector<uint64_t> aR(B.R / 2), aC(B.C / 2);
+                    uint64_t a = 1, bi = 1;
+                    for (uint32_t j = 0; j < B.R / 2; ++j) { aR[j] = a; btRi[(size_t)i * (B.R / 2) + j] = u64x2{bi, 0}; a = mulmod_h(a, wR, q); bi = mulmod_h(bi, wRi, q); }
+                    a = 1; bi = 1;
+                    for (uint32_t j = 0; j < B.C / 2; ++j) { aC[j] = a; btCi[(size_t)i * (B.C / 2) + j] = u64x2{bi, 0}; a = mulmod_h(a, wC, q); bi = mulmod_h(bi, wCi, q); }
+                    for (uint32_t j = 0; j < B.R / 2; ++j) btR[(size_t)i * (B.R / 2) + j] = u64x2{aR[brev_h(j, B.logR - 1)], 0};
+                    for (uint32_t j = 0; j < B.C / 2; ++j) btC[(size_t)i * (B.C / 2) + j] = u64x2{aC[brev_h(j, B.logC - 1)], 0};
                 }
-                T.fdhb1 = fd1(b1, M);
-                T.fdhb2 = fd1(b2, M);
+                B.fdhb1 = fd1(b1, Mb);
+                B.fdhb2 = fd1(b2, Mb);
+                B.fxta = fd1(bxa, Mb);
+                B.fxtb = fd1(bxb, Mb);
+                B.ftwRb = fd(btR, B.R / 2); B.ftwRi = fd(btRi, B.R / 2);
+                B.ftwCb = fd(btC, B.C / 2); B.ftwCi = fd(btCi, B.C / 2);
+                B.fmods = dev_upload(X, fm);
+                T.tb = &X->Tb;
+                }
             }
             bool win = true;
             for (uint32_t i = 0; i < NP; ++i) win = win && X->moduli[i] >= (1ull << 49);

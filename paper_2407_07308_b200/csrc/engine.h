@@ -70,6 +70,7 @@ struct bc_ctx {
     bc::Mod *d_mods = nullptr;
     const double2 *d_fm = nullptr;    // (q, fl(1/q)) per prime when all primes are in [2^49, 2^50) (binary64 kernels)
     bc::NttTables T;
+    bc::NttTables Tb;                   // composite m: size-Mb tables of the two Barrett convolutions (T.tb)
     uint64_t *d_plans = nullptr;
     std::map<std::string, size_t> plan_off;
     std::map<std::string, std::pair<uint32_t, uint32_t>> plan_dims;   // (sources, targets)

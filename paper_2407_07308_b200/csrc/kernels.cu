@@ -314,7 +314,7 @@ uint64_t ntt_group_jobs(const NttTables &T, uint64_t jobs, bool barrett) {
     return std::max<uint64_t>(1, std::min(jobs, g));
 }
 bool ntt_inverse_barrett(const NttTables &T) {
-    return (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T) && !T.prime_m && T.fdhb1 != nullptr;
+    return (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T) && !T.prime_m && T.tb != nullptr;
 }
 
 static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
@@ -339,17 +339,17 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
     const bool vf = (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T);
     // composite m on the binary64 path: Barrett reduction mod Phi_m (needs a second M-word slot per job)
-    const bool barrett = inv && vf && !T.prime_m && T.fdhb1 != nullptr;
+    const bool barrett = inv && vf && !T.prime_m && T.tb != nullptr;
     const uint64_t chunk = ntt_group_jobs(T, jobs, barrett);
     const bool v2 = g_ntt_impl != 1 && ntt2_supported(T);
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
         if (v2) {
-            if (vf)
-                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st,
-                         barrett ? scratch + chunk * T.M : nullptr);
-            else
+            if (vf) {
+                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
+                if (barrett) nttf_barrett(*T.tb, out, lm, out_pstride, scratch, scratch + chunk * T.M, j0, nj, st);
+            } else
                 ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
             if (inv && !barrett) {
                 if (T.prime_m)

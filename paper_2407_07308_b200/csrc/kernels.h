@@ -34,6 +34,8 @@ struct NttTables {
     // composite m (binary64 path): Barrett reduction mod Phi_m by two size-M convolutions with constants, in
     // the D^ layout, M^{-1} folded: NTT(rev(Phi)^{-1} mod x^{m-n}) and NTT(Phi); null -> long division
     const double *fdhb1, *fdhb2;
+    uint32_t Mslot;                // word stride of the per-job A slots read / written by modes 2 and 3
+    const struct NttTables *tb;    // host pointer: the Barrett convolution tables (composite m), or null
     uint32_t m, n, M, R, C, logR, logC;
     int prime_m;
     int dbg;              // ntt3.cu timing experiments only (bc_tune "ntt_dbg"): skip table reads; results invalid          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
@@ -161,7 +163,11 @@ void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
 bool nttf_supported(const NttTables &T);
 int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: position r*C + tau*E + k at r*C + k*(C/E) + tau
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *scratch2 = nullptr);
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
+// composite m: out (poly/limb layout) = A mod Phi_m for the A_t (t < m) the inverse left in the scr1 slots
+// (stride B.Mslot), by the two Barrett convolutions of table set B (scr2: slots of B.M words)
+void nttf_barrett(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,
+                  uint64_t j0, uint32_t nj, cudaStream_t st);
 extern uint64_t g_ntt_group_bytes;
 uint64_t ntt_group_jobs(const NttTables &T, uint64_t jobs, bool barrett);
 bool ntt_inverse_barrett(const NttTables &T);

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     // INV: 0 Bluestein forward, 1 Bluestein inverse, 2/3 the Barrett reduction mod Phi_m of a composite m
     // (2: quotient convolution, input rev(A)_t = A_{m-1-t}, t < m - n; 3: Phi_m * Q, input Q_t = A'_{n+t})
     const double *tf = (INV == 1 ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
-    const uint64_t *src = INV >= 2 ? in + (uint64_t)blockIdx.y * T.M : in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
+    const uint64_t *src = INV >= 2 ? in + (uint64_t)blockIdx.y * T.Mslot : in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
     typedef PtTab<LOGR, LOGE, true> PTT;
     double2 *stw = (double2 *)(smf + (size_t)R * TC), *spt = stw + R / 2;
     const double2 *gtw = T.ftwRb + (uint64_t)J.pr * (R / 2);
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     const double *tfo = (INV == 1 ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
     uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
     uint64_t *scru = (uint64_t *)scr;
-    uint64_t *A1 = INV >= 2 ? aux + (uint64_t)blockIdx.y * T.M : nullptr;    // the A_t of this job (Barrett)
+    uint64_t *A1 = INV >= 2 ? aux + (uint64_t)blockIdx.y * T.Mslot : nullptr;    // the A_t of this job (Barrett)
     const uint32_t kq = T.m - T.n;
     if (INV == 1) __syncthreads();   // all columns of this block read before in-place writes of A_t
 #pragma unroll
@@ -422,7 +422,7 @@ struct Shape {
 
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *scratch2) {
+                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
     static bool init = false;
     if (!init) {
@@ -432,12 +432,6 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
         cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 1, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
-        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
-        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
-        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
-        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
-        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
-        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         init = true;
     }
     double *scr = (double *)scratch;
@@ -452,19 +446,36 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
         kf_passA<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
         kf_passC<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
-        if (scratch2) {
-            // composite m: A (length m, in scr) mod Phi_m by Barrett division with two size-M convolutions
-            double *s2 = (double *)scratch2;
-            kf_passA<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scratch, 0, lm, j0, s2);
-            kf_passB<LOGC, LOGEC, S::RB, 2><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
-            kf_passC<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scratch);
-            kf_passA<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scratch, 0, lm, j0, s2);
-            kf_passB<LOGC, LOGEC, S::RB, 3><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
-            kf_passC<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scratch);
-            launch_counter() += 6;
-        }
     }
     launch_counter() += 3;
+}
+
+// composite m: Barrett division mod Phi_m of the A_t in the scr1 slots (two convolutions with table set B)
+template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
+static void runb(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,
+                 uint64_t j0, uint32_t nj, cudaStream_t st) {
+    typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
+        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
+        cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
+        init = true;
+    }
+    NttTables T = B;
+    T.dbg = 0;
+    double *s2 = (double *)scr2;
+    dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
+    kf_passA<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scr1, 0, lm, j0, s2);
+    kf_passB<LOGC, LOGEC, S::RB, 2><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
+    kf_passC<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scr1);
+    kf_passA<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scr1, 0, lm, j0, s2);
+    kf_passB<LOGC, LOGEC, S::RB, 3><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
+    kf_passC<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scr1);
+    launch_counter() += 6;
 }
 
 }  // namespace f64
@@ -482,8 +493,8 @@ bool nttf_supported(const NttTables &T) {
 }
 
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *scratch2) {
-#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, scratch2)
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
+#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st)
     switch (T.logR * 16 + T.logC) {
         case 8 * 16 + 8:
             switch (g_ntt_impl) {
@@ -509,4 +520,22 @@ void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
 #undef RUNF
 }
 
+}  // namespace bc
+
+namespace bc {
+void nttf_barrett(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,
+                  uint64_t j0, uint32_t nj, cudaStream_t st) {
+#define RUNB(...) f64::runb<__VA_ARGS__>(B, out, lm, out_ps, scr1, scr2, j0, nj, st)
+    switch (B.logR * 16 + B.logC) {
+        case 8 * 16 + 8: RUNB(8, 4, 8, 4, 16, 16); break;
+        case 8 * 16 + 9: RUNB(8, 4, 9, 3, 16); break;
+        case 7 * 16 + 8: RUNB(7, 4, 8, 4, 16); break;
+        case 7 * 16 + 7: RUNB(7, 4, 7, 4, 16); break;
+        case 6 * 16 + 7: RUNB(6, 3, 7, 4, 16); break;
+        case 6 * 16 + 6: RUNB(6, 3, 6, 3, 16); break;
+        case 5 * 16 + 6: RUNB(5, 4, 6, 3, 16); break;
+        default: break;
+    }
+#undef RUNB
+}
 }  // namespace bc
