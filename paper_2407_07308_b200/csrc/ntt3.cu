@@ -223,6 +223,9 @@ __device__ __forceinline__ void fct_pass(double (&v)[1 << LOGE], int (&bd)[1 << 
     if (P + 1 < PS::NP) fct_pass<LOGL, LOGE, FWD, TC, (P + 1 < PS::NP ? P + 1 : P)>(v, bd, tau, col, scol, tw, pt, q, qi);
 }
 
+#ifndef NTTF_LOGE_89
+#define NTTF_LOGE_89 3     // registers per thread 2^LOGE of the 512-point row transforms (M = 131072)
+#endif
 #ifndef NTT_REG_TARGET
 #define NTT_REG_TARGET 64
 #endif
@@ -483,7 +486,8 @@ static void runb(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps,
 // register count E = 2^LOGE of the pass-B row transform of each shape (the D^ table layout depends on it)
 int nttf_row_loge(uint32_t logR, uint32_t logC) {
     switch (logR * 16 + logC) {
-        case 8 * 16 + 9: case 6 * 16 + 6: case 5 * 16 + 6: return 3;
+        case 8 * 16 + 9: return NTTF_LOGE_89;
+        case 6 * 16 + 6: case 5 * 16 + 6: return 3;
         default: return 4;
     }
 }
@@ -507,8 +511,9 @@ void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
             }
             break;
         case 8 * 16 + 9:
-            if (g_ntt_impl == 12) RUNF(8, 4, 9, 3, 8);
-            else RUNF(8, 4, 9, 3, 16);
+            if (g_ntt_impl == 12) RUNF(8, 4, 9, NTTF_LOGE_89, 8);
+            else if (g_ntt_impl == 13) RUNF(8, 4, 9, NTTF_LOGE_89, 16, 8);
+            else RUNF(8, 4, 9, NTTF_LOGE_89, 16);
             break;
         case 7 * 16 + 8: RUNF(7, 4, 8, 4, 16); break;
         case 7 * 16 + 7: RUNF(7, 4, 7, 4, 16); break;
@@ -528,7 +533,7 @@ void nttf_barrett(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps
 #define RUNB(...) f64::runb<__VA_ARGS__>(B, out, lm, out_ps, scr1, scr2, j0, nj, st)
     switch (B.logR * 16 + B.logC) {
         case 8 * 16 + 8: RUNB(8, 4, 8, 4, 16, 16); break;
-        case 8 * 16 + 9: RUNB(8, 4, 9, 3, 16); break;
+        case 8 * 16 + 9: RUNB(8, 4, 9, NTTF_LOGE_89, 16); break;
         case 7 * 16 + 8: RUNB(7, 4, 8, 4, 16); break;
         case 7 * 16 + 7: RUNB(7, 4, 7, 4, 16); break;
         case 6 * 16 + 7: RUNB(6, 3, 7, 4, 16); break;

@@ -1,0 +1,103 @@
+"""Edge cases of the CUDA path (SURVEY §8(b) error mapping, maximum words, degenerate pairs)."""
+import numpy as np
+import pytest
+
+from gpu_util import SEED_ENC, SEED_KEYS, to_u64  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+_CTX = {}
+
+
+def ctx_keys(name):
+    import paper_2407_07308_b200 as bc
+    if name not in _CTX:
+        ctx = bc.Context(bc.load_params(name))
+        _CTX[name] = (ctx, ctx.keygen(SEED_KEYS))
+    return _CTX[name]
+
+
+def boundary_pairs(cap, base, digits, ints):
+    """0, the maximum word, +-1 neighbours, digit-boundary carries, equal pairs"""
+    mx = cap - 1
+    cands = [(0, 0), (mx, mx), (mx - 1, mx), (mx, mx - 1), (0, mx), (mx, 0), (0, 1), (1, 0)]
+    top = base ** (digits - 1)
+    if top < cap:
+        cands += [(top, top - 1), (top - 1, top), (top, top)]
+    cands += [(base, base - 1), (base - 1, base)]
+    while len(cands) < ints:
+        cands.append((mx // 2, mx // 2 + 1))
+    return [a for a, _ in cands[:ints]], [b for _, b in cands[:ints]]
+
+
+@pytest.mark.parametrize("cfg", ["c2s", "c3s2"])
+def test_boundary_words_compare(cfg):
+    """maximum words (2^64 - 1: 7^24 and 31^15 exceed 2^64), zero, +-1 and carry neighbours, equal pairs:
+    compare_lt / compare_eq decrypt to the plaintext answer in every block"""
+    ctx, keys = ctx_keys(cfg)
+    ints = ctx.ints_per_ct
+    cap = min(ctx.base ** (ctx.d * ctx.l), 1 << 64)
+    a, b = boundary_pairs(cap, ctx.base, ctx.d * ctx.l, ints)
+    ca = ctx.encrypt(keys, np.array([a], dtype=np.uint64), SEED_ENC, ct_index0=0)
+    cb = ctx.encrypt(keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=1)
+    assert [int(x) for x in ctx.decrypt(keys, ca)[0]] == a
+    lt = ctx.decrypt(keys, ctx.compare_lt(keys, ca, cb), as_bits=True)[0]
+    eq = ctx.decrypt(keys, ctx.compare_eq(keys, ca, cb), as_bits=True)[0]
+    assert [int(x) for x in lt] == [int(x < y) for x, y in zip(a, b)]
+    assert [int(x) for x in eq] == [int(x == y) for x, y in zip(a, b)]
+
+
+def test_out_of_range_word_is_rejected():
+    """S:333 OutOfRange -> BC_E_RANGE (3): C1 words are 2-bit (base 2, d l = 2)"""
+    import paper_2407_07308_b200 as bc
+    ctx, keys = ctx_keys("c1")
+    words = np.zeros((1, ctx.ints_per_ct), dtype=np.uint64)
+    words[0, 3] = 4
+    with pytest.raises(bc.BoostComError, match=r"status 3"):
+        ctx.encrypt(keys, words, SEED_ENC)
+
+
+def test_empty_batch_is_rejected():
+    """an empty ciphertext view is an argument error (BC_E_ARG = 1), never a silent no-op"""
+    import paper_2407_07308_b200 as bc
+    ctx, keys = ctx_keys("c1")
+    ca = ctx.encrypt(keys, np.zeros((1, ctx.ints_per_ct), dtype=np.uint64), SEED_ENC)
+    with pytest.raises(bc.BoostComError, match=r"status 1"):
+        ctx.compare_lt(keys, ca[0:0], ca[0:0])
+
+
+def test_out_of_levels_is_rejected():
+    """S:427 OutOfLevels -> BC_E_LEVEL (4): a compare of ciphertexts switched down to level 1"""
+    import paper_2407_07308_b200 as bc
+    ctx, keys = ctx_keys("c1")
+    ca = ctx.encrypt(keys, np.zeros((1, ctx.ints_per_ct), dtype=np.uint64), SEED_ENC)
+    while ca.shape[2] > 1:
+        ca = ctx.modswitch(ca)
+    with pytest.raises(bc.BoostComError, match=r"status 4"):
+        ctx.compare_lt(keys, ca, ca)
+
+
+def test_ragged_batch_and_unequal_levels():
+    """an odd batch (3 pairs) on C2's shadow ring; on c1m (spare levels) b one level below a: R12
+    aligns the levels; on C2's exact chain the same misalignment is BC_E_LEVEL (no level to spare)"""
+    import paper_2407_07308_b200 as bc
+    from inputs import word_pairs
+    for name in ("c2s", "c1m"):
+        ctx, keys = ctx_keys(name)
+        ints = ctx.ints_per_ct
+        rng = np.random.default_rng(3)
+        A, B = [], []
+        for _ in range(3):
+            a, b = word_pairs(rng, ints, ctx.base, ctx.d * ctx.l)
+            A.append(a)
+            B.append(b)
+        ca = ctx.encrypt(keys, np.array(A, dtype=np.uint64), SEED_ENC, ct_index0=0)
+        cb = ctx.encrypt(keys, np.array(B, dtype=np.uint64), SEED_ENC, ct_index0=3)
+        if name == "c2s":
+            with pytest.raises(bc.BoostComError, match=r"status 4"):
+                ctx.compare_lt(keys, ca, ctx.modswitch(cb))
+        else:
+            cb = ctx.modswitch(cb)
+        bits = ctx.decrypt(keys, ctx.compare_lt(keys, ca, cb), as_bits=True)
+        for i in range(3):
+            assert [int(x) for x in bits[i]] == [int(x < y) for x, y in zip(A[i], B[i])]
