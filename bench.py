@@ -495,9 +495,11 @@ def run_vector_workload(args, cfg, rank, world, local, workload):
     with ClockSampler(local) as clk:
         barrier()
         e0.record()
+        torch.cuda.nvtx.range_push("step")
         for _ in range(args.steps):
             step()
         e1.record()
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
     live = bc.ntt_timing()
@@ -609,9 +611,11 @@ def run_compact_compare(args, cfg, rank, world, local):
     with ClockSampler(local) as clk:
         barrier()
         e0.record()
+        torch.cuda.nvtx.range_push("step")
         for _ in range(args.steps):
             step()
         e1.record()
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
     live = bc.ntt_timing()
