@@ -744,7 +744,8 @@ CT Eng::sub(const CT &a, uint32_t b0, uint32_t nb) {
 static uint64_t ntt_scratch_words(const bc_ctx *X, uint32_t npoly, uint32_t njl, bool inv = false) {
     const uint64_t jobs = (uint64_t)npoly * njl;
     const bool barrett = inv && ntt_inverse_barrett(X->T);
-    return ntt_group_jobs(X->T, jobs, barrett) * X->M * (barrett ? 2 : 1);
+    const uint64_t g = ntt_group_jobs(X->T, jobs, barrett);
+    return g * X->M * (barrett ? 2 : 1) + (inv ? g : 0);     // + one A_{m-1} word per job (prime m, pass C)
 }
 
 void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {

@@ -346,12 +346,14 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
         if (v2) {
+            const bool direct = vf && inv && T.prime_m;      // pass C writes A_t - A_{m-1} itself
             if (vf) {
-                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
+                nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st,
+                         direct ? scratch + chunk * T.M : nullptr);
                 if (barrett) nttf_barrett(*T.tb, out, lm, out_pstride, scratch, scratch + chunk * T.M, j0, nj, st);
             } else
                 ntt2_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st);
-            if (inv && !barrett) {
+            if (inv && !barrett && !direct) {
                 if (T.prime_m)
                     k_reduce_prime<<<grid_rows(T.n, nj), 256, 0, st>>>(T, out, out_pstride, lm, j0, nj,
                                                                                      scratch);
@@ -678,7 +680,9 @@ __global__ void k_kip(const Mod *__restrict__ mods, const uint64_t *__restrict__
         u[(b * 2 + 1) * ln + rr] = reduce128(h1, l1, M);
     }
 }
-// binary64 variant: sum of 2 * ndig fmulv per output coefficient pair, one reduction each
+// binary64 variant: sum of 2 * ndig fmulv per output coefficient pair, one reduction each.
+// NDIG > 0: the digit count is a compile-time constant (loop unrolled, all loads issued up front)
+template <int NDIG>
 __global__ void k_kip_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ d, uint64_t dps,
                         const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
                         uint64_t *__restrict__ u, uint32_t rows, uint32_t lvl, uint32_t K, uint32_t L1,
@@ -698,7 +702,9 @@ __global__ void k_kip_f(const double2 *__restrict__ fm, const uint64_t *__restri
         const double q = fm[kl].x, qi = fm[kl].y;
         const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
         double s0 = 0.0, s1 = 0.0;      // |s| <= 0.75 q ndig (ndig <= 10: < 8q)
-        for (uint32_t j = 0; j < ndig; ++j) {
+        const uint32_t nd = NDIG > 0 ? (uint32_t)NDIG : ndig;
+#pragma unroll
+        for (uint32_t j = 0; j < nd; ++j) {
             const uint64_t dig = (j == jr) ? d[b * dps + (uint64_t)r * n + x] : ext[((b * ndig + j) * nl + r) * n + x];
             const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
             const double dg = from_u64(dig);
@@ -709,13 +715,27 @@ __global__ void k_kip_f(const double2 *__restrict__ fm, const uint64_t *__restri
         u[(b * 2 + 1) * ln + rr] = to_u64(fred(s1, q, qi), q);
     }
 }
+static void kip_f_dispatch(dim3 g, cudaStream_t st, const double2 *fm, const uint64_t *d, uint64_t dps,
+                           const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t rows, uint32_t lvl,
+                           uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, const int32_t *pos,
+                           const int32_t *zt, uint32_t m, uint32_t perm_t) {
+#define KIPF(N) k_kip_f<N><<<g, 256, 0, st>>>(fm, d, dps, ext, key, u, rows, lvl, K, L1, alpha, ndig, n, pos, zt, m, perm_t)
+    switch (ndig) {
+        case 1: KIPF(1); break;
+        case 2: KIPF(2); break;
+        case 3: KIPF(3); break;
+        case 4: KIPF(4); break;
+        default: KIPF(0); break;
+    }
+#undef KIPF
+}
 void ks_kip(const Mod *mods, const uint64_t *d, uint64_t dps, const uint64_t *ext, const uint64_t *key, uint64_t *u,
             uint32_t B, uint32_t lvl, uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st,
             const double2 *fm) {
     const uint64_t rows = (uint64_t)B * (lvl + K);
     if (fm && ndig <= 10)
-        k_kip_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
-                                                    nullptr, nullptr, 1, 0);
+        kip_f_dispatch(grid_rows(n, rows), st, fm, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
+                       nullptr, nullptr, 1, 0);
     else
         k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
                                                   nullptr, nullptr, 1, 0);
@@ -726,8 +746,8 @@ void ks_kip_perm(const Mod *mods, const NttTables &T, uint32_t perm_t, const uin
                  uint32_t alpha, uint32_t ndig, uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * (lvl + K);
     if (fm && ndig <= 10)
-        k_kip_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
-                                                    T.pos, T.z, T.m, perm_t);
+        kip_f_dispatch(grid_rows(n, rows), st, fm, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
+                       T.pos, T.z, T.m, perm_t);
     else
         k_kip<<<grid_rows(n, rows), 256, 0, st>>>(mods, d, dps, ext, key, u, (uint32_t)rows, lvl, K, L1, alpha, ndig, n,
                                                   T.pos, T.z, T.m, perm_t);

@@ -162,8 +162,9 @@ void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
 // binary64-FMA passes (ntt3.cu)
 bool nttf_supported(const NttTables &T);
 int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: position r*C + tau*E + k at r*C + k*(C/E) + tau
+// corner_buf (prime m, inverse): nj words; pass C then writes the reduction mod Phi_m directly (no k_reduce_prime)
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf = nullptr);
 // composite m: out (poly/limb layout) = A mod Phi_m for the A_t (t < m) the inverse left in the scr1 slots
 // (stride B.Mslot), by the two Barrett convolutions of table set B (scr2: slots of B.M words)
 void nttf_barrett(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,

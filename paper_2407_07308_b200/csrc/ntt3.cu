@@ -384,7 +384,11 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     uint64_t *scru = (uint64_t *)scr;
     uint64_t *A1 = INV >= 2 ? aux + (uint64_t)blockIdx.y * T.Mslot : nullptr;    // the A_t of this job (Barrett)
     const uint32_t kq = T.m - T.n;
-    if (INV == 1) __syncthreads();   // all columns of this block read before in-place writes of A_t
+    // prime m (aux = per-job A_{m-1} from kf_corner): out_t = A_t - A_{m-1} written directly (t < n);
+    // composite m: A_t into the scratch slot in place (read by the Barrett passes)
+    const bool direct = INV == 1 && T.prime_m && aux != nullptr;
+    const uint64_t corner = direct ? aux[blockIdx.y] : 0;
+    if (INV == 1 && !direct) __syncthreads();   // all columns of this block read before in-place writes of A_t
 #pragma unroll
     for (int k = 0; k < E; ++k) {
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
@@ -406,9 +410,39 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         if (!INV) {
             const int ps = (T.dbg & 32) ? (t < T.n ? (int)t : -1) : T.pos[t];
             if (ps >= 0) __stcs(dst + ps, x);
+        } else if (direct) {
+            if (t < T.n) __stcs(dst + t, x >= corner ? x - corner : x + (uint64_t)q - corner);
         } else {
             scru[t] = x;
         }
+    }
+}
+
+// prime m, inverse: A_{m-1} of every job of the group, from the pass-B output column c* = (m-1) mod C:
+// A_{m-1} = tfoi[m-1] * sum_rp x[rp C + c*] omega_R^{-r* brev(rp)}, r* = (m-1) / C (the value pass C computes
+// at t = m-1), so that pass C can write the reduction A_t - A_{m-1} (mod Phi_m, m prime) directly
+template <int LOGR>
+__global__ void __launch_bounds__(32) kf_corner(NttTables T, LimbMap lm, uint64_t job0, const double *__restrict__ scratch,
+                                                 uint64_t *__restrict__ corner) {
+    constexpr int R = 1 << LOGR;
+    const JobF J = job_f(lm, (uint32_t)(job0 + blockIdx.x));
+    const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+    const double *scr = scratch + (uint64_t)blockIdx.x * T.M;
+    const uint32_t cs = (T.m - 1) % T.C, rs = (T.m - 1) / T.C;
+    const double2 *tw = T.ftwRi + (uint64_t)J.pr * (R / 2);
+    double acc = 0.0;                                   // <= (R/32) 0.625 q per lane
+    for (uint32_t rp = threadIdx.x; rp < (uint32_t)R; rp += 32) {
+        const uint32_t e = (rs * (__brev(rp) >> (32 - LOGR))) & (R - 1);
+        double2 w = tw[e & (R / 2 - 1)];
+        if (e >= (uint32_t)(R / 2)) { w.x = -w.x; w.y = -w.y; }      // omega_R^{-R/2} = -1
+        acc = __dadd_rn(acc, fmm(scr[(uint64_t)rp * T.C + cs], w, q));
+    }
+    acc = fred(acc, q, qi);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = fred(__dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o)), q, qi);
+    if (threadIdx.x == 0) {
+        const double *tfo = T.ftfoi + (uint64_t)J.pr * T.m;
+        corner[blockIdx.x] = to_u64(fmm8(acc, tfo[T.m - 1], q, qi), q);
     }
 }
 
@@ -425,7 +459,7 @@ struct Shape {
 
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
+                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
     static bool init = false;
     if (!init) {
@@ -448,7 +482,13 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
     } else {
         kf_passA<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
-        kf_passC<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
+        uint64_t *corner = nullptr;
+        if (T.prime_m && corner_buf) {
+            corner = corner_buf;
+            kf_corner<LOGR><<<nj, 32, 0, st>>>(T, lm, j0, scr, corner);
+            launch_counter() += 1;
+        }
+        kf_passC<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, corner);
     }
     launch_counter() += 3;
 }
@@ -497,8 +537,8 @@ bool nttf_supported(const NttTables &T) {
 }
 
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
-#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st)
+              uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
+#define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf)
     switch (T.logR * 16 + T.logC) {
         case 8 * 16 + 8:
             switch (g_ntt_impl) {
