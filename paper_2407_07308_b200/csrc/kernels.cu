@@ -88,6 +88,14 @@ static inline unsigned grid_for(uint64_t total, unsigned threads, unsigned cap =
     const uint32_t XV_ = blockIdx.x * blockDim.x + threadIdx.x;         \
     if (XV_ >= (N_)) return;                                            \
     for (uint32_t RV_ = blockIdx.y; RV_ < (NROWS_); RV_ += gridDim.y)
+// two coefficients per thread (n = phi(m) is even and every row starts 16-byte aligned): one 128-bit
+// access per operand, x even
+#define ROW_LOOP2(RV_, XV_, NROWS_, N_)                                 \
+    const uint32_t XV_ = 2 * (blockIdx.x * blockDim.x + threadIdx.x);   \
+    if (XV_ >= (N_)) return;                                            \
+    for (uint32_t RV_ = blockIdx.y; RV_ < (NROWS_); RV_ += gridDim.y)
+#define LD2(P_) (*(const ulonglong2 *)(P_))
+#define ST2(P_, A_, B_) (*(ulonglong2 *)(P_) = make_ulonglong2((A_), (B_)))
 static inline dim3 grid_rows(uint32_t n, uint64_t rows, unsigned threads = 256) {
     return dim3((n + threads - 1) / threads, (unsigned)(rows < 65535 ? (rows ? rows : 1) : 65535));
 }
@@ -416,15 +424,17 @@ __device__ __forceinline__ uint64_t small_res(int64_t c, uint64_t q) {
 
 __global__ void k_add(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
                       uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n, int sub) {
-    ROW_LOOP(r, x, rows, n) {
+    ROW_LOOP2(r, x, rows, n) {
         const uint64_t q = mods[r % lvl].q, i = (uint64_t)r * n + x;
-        o[i] = sub ? sub_mod(a[i], b[i], q) : add_mod(a[i], b[i], q);
+        const ulonglong2 av = LD2(a + i), bv = LD2(b + i);
+        if (sub) ST2(o + i, sub_mod(av.x, bv.x, q), sub_mod(av.y, bv.y, q));
+        else ST2(o + i, add_mod(av.x, bv.x, q), add_mod(av.y, bv.y, q));
     }
 }
 void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t parts,
             uint32_t lvl, uint32_t n, int sub, cudaStream_t st) {
     const uint64_t rows = (uint64_t)B * parts * lvl;
-    k_add<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n, sub);
+    k_add<<<grid_rows(n / 2, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n, sub);
     LAUNCHED();
 }
 
@@ -774,19 +784,19 @@ void ew_add_bs(const Mod *mods, const uint64_t *a, uint64_t abs, const uint64_t 
 __global__ void k_scale_sub(const Mod *__restrict__ mods, const uint64_t *__restrict__ u, uint64_t u_pstride,
                             const uint64_t *__restrict__ delta, const u64x2 *__restrict__ inv,
                             uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
-    ROW_LOOP(rw, x, rows, n) {   // rows = npoly * lvl
+    ROW_LOOP2(rw, x, rows, n) {   // rows = npoly * lvl
         const uint32_t pidx = rw / lvl, limb = rw - pidx * lvl;
         const uint64_t rr = (uint64_t)limb * n + x, i = (uint64_t)rw * n + x;
         const uint64_t q = mods[limb].q;
-        const uint64_t v = sub_mod(u[(uint64_t)pidx * u_pstride + rr], delta[i], q);
+        const ulonglong2 uv = LD2(u + (uint64_t)pidx * u_pstride + rr), dv = LD2(delta + i);
         const u64x2 w = inv[limb];
-        o[i] = mul_shoup(v, w.w, w.ws, q);
+        ST2(o + i, mul_shoup(sub_mod(uv.x, dv.x, q), w.w, w.ws, q), mul_shoup(sub_mod(uv.y, dv.y, q), w.w, w.ws, q));
     }
 }
 void ew_scale_sub(const Mod *mods, const uint64_t *u, uint64_t u_pstride, const uint64_t *delta, const u64x2 *inv,
                   uint64_t *o, uint32_t npoly, uint32_t lvl, uint32_t n, cudaStream_t st) {
     const uint64_t rows = (uint64_t)npoly * lvl;
-    k_scale_sub<<<grid_rows(n, rows), 256, 0, st>>>(mods, u, u_pstride, delta, inv, o, (uint32_t)rows, lvl, n);
+    k_scale_sub<<<grid_rows(n / 2, rows), 256, 0, st>>>(mods, u, u_pstride, delta, inv, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 
@@ -809,17 +819,18 @@ __global__ void k_fused_down(const Mod *__restrict__ mods, const uint64_t *__res
                              const uint64_t *__restrict__ delta, const u64x2 *__restrict__ pm,
                              const u64x2 *__restrict__ dinv, uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl,
                              uint32_t n) {
-    ROW_LOOP(rw, x, rows, n) {   // rows = 2B * lvl
+    ROW_LOOP2(rw, x, rows, n) {   // rows = 2B * lvl
         const uint64_t poly = rw / lvl;
         const uint32_t limb = rw - (uint32_t)poly * lvl;
         const uint64_t rr = (uint64_t)limb * n + x, i = (uint64_t)rw * n + x;
         const uint64_t b = poly >> 1, k = poly & 1;
         const uint64_t q = mods[limb].q;
         const u64x2 w = pm[limb], v = dinv[limb];
-        const uint64_t dv = d[b * d_bstride + k * d_kstride + rr];
-        uint64_t x = add_mod(u[poly * u_pstride + rr], mul_shoup(dv, w.w, w.ws, q), q);
-        x = sub_mod(x, delta[i], q);
-        o[i] = mul_shoup(x, v.w, v.ws, q);
+        const ulonglong2 dv = LD2(d + b * d_bstride + k * d_kstride + rr), uv = LD2(u + poly * u_pstride + rr);
+        const ulonglong2 de = LD2(delta + i);
+        const uint64_t x0 = sub_mod(add_mod(uv.x, mul_shoup(dv.x, w.w, w.ws, q), q), de.x, q);
+        const uint64_t x1 = sub_mod(add_mod(uv.y, mul_shoup(dv.y, w.w, w.ws, q), q), de.y, q);
+        ST2(o + i, mul_shoup(x0, v.w, v.ws, q), mul_shoup(x1, v.w, v.ws, q));
     }
 }
 void ew_fused_down(const Mod *mods, uint64_t *u, uint64_t u_pstride, const uint64_t *d, uint64_t d_bstride,
@@ -833,7 +844,7 @@ void ew_fused_down_out(const Mod *mods, const uint64_t *u, uint64_t u_pstride, c
                        uint64_t d_kstride, const uint64_t *delta, const u64x2 *pm, const u64x2 *dinv, uint64_t *o,
                        uint32_t B, uint32_t lvl_out, uint32_t n, cudaStream_t st) {
     const uint64_t rows = (uint64_t)2 * B * lvl_out;
-    k_fused_down<<<grid_rows(n, rows), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, delta, pm, dinv,
+    k_fused_down<<<grid_rows(n / 2, rows), 256, 0, st>>>(mods, u, u_pstride, d, d_bstride, d_kstride, delta, pm, dinv,
                                                      o, (uint32_t)rows, lvl_out, n);
     LAUNCHED();
 }
