@@ -465,17 +465,18 @@ __global__ void k_scalar_f(const double2 *__restrict__ fm, const uint64_t *__res
                            uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
     using namespace f64;
     const double cd = (double)c;
-    ROW_LOOP(r, x, rows, n) {
+    ROW_LOOP2(r, x, rows, n) {
         const double q = fm[r % lvl].x, qi = fm[r % lvl].y;
         const uint64_t i = (uint64_t)r * n + x;
-        o[i] = to_u64(fmulv(from_u64(a[i]), cd, q, qi), q);
+        const ulonglong2 av = LD2(a + i);
+        ST2(o + i, to_u64(fmulv(from_u64(av.x), cd, q, qi), q), to_u64(fmulv(from_u64(av.y), cd, q, qi), q));
     }
 }
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
                uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * parts * lvl;
     if (fm && c > -(1 << 20) && c < (1 << 20))
-        k_scalar_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, a, c, o, (uint32_t)rows, lvl, n);
+        k_scalar_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, c, o, (uint32_t)rows, lvl, n);
     else
         k_scalar<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
@@ -483,16 +484,22 @@ void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint3
 
 __global__ void k_add_const(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, int64_t c,
                             uint64_t *__restrict__ o, uint32_t rows, uint32_t parts, uint32_t lvl, uint32_t n) {
-    ROW_LOOP(r, x, rows, n) {
+    ROW_LOOP2(r, x, rows, n) {
         const uint32_t limb = r % lvl, part = (r / lvl) % parts;
         const uint64_t q = mods[limb].q, i = (uint64_t)r * n + x;
-        o[i] = part == 0 ? add_mod(a[i], small_res(c, q), q) : a[i];
+        const ulonglong2 av = LD2(a + i);
+        if (part == 0) {
+            const uint64_t cr = small_res(c, q);
+            ST2(o + i, add_mod(av.x, cr, q), add_mod(av.y, cr, q));
+        } else {
+            ST2(o + i, av.x, av.y);
+        }
     }
 }
 void ew_add_const(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
                   uint32_t lvl, uint32_t n, cudaStream_t st) {
     const uint64_t rows = (uint64_t)B * parts * lvl;
-    k_add_const<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, parts, lvl, n);
+    k_add_const<<<grid_rows(n / 2, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, parts, lvl, n);
     LAUNCHED();
 }
 
@@ -509,18 +516,20 @@ __global__ void k_ptmul_f(const double2 *__restrict__ fm, const uint64_t *__rest
                           const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint32_t rows,
                           uint32_t lvl, uint32_t n) {
     using namespace f64;
-    ROW_LOOP(r, x, rows, n) {
+    ROW_LOOP2(r, x, rows, n) {
         const uint32_t limb = r % lvl;
         const double q = fm[limb].x, qi = fm[limb].y;
         const uint64_t i = (uint64_t)r * n + x;
-        o[i] = to_u64(fmulv(from_u64(a[i]), from_u64(pt[(uint64_t)limb * n + x]), q, qi), q);
+        const ulonglong2 av = LD2(a + i), pv = LD2(pt + (uint64_t)limb * n + x);
+        ST2(o + i, to_u64(fmulv(from_u64(av.x), from_u64(pv.x), q, qi), q),
+            to_u64(fmulv(from_u64(av.y), from_u64(pv.y), q, qi), q));
     }
 }
 void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *o, uint32_t B, uint32_t parts,
               uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * parts * lvl;
     if (fm)
-        k_ptmul_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, a, pt, o, (uint32_t)rows, lvl, n);
+        k_ptmul_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, pt, o, (uint32_t)rows, lvl, n);
     else
         k_ptmul<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, pt, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
