@@ -35,6 +35,7 @@ int bc_tune(const char *key, int64_t value) {
     if (!strcmp(key, "vec_chunk")) { g_vec_chunk = (uint64_t)std::max<int64_t>(value, 0); return 0; }
     if (!strcmp(key, "ntt_timing")) { g_ntt_timing = value ? 1 : 0; return 0; }
     if (!strcmp(key, "f64_elem")) { g_f64_elem = (int)value; return 0; }
+    if (!strcmp(key, "phi_conv")) { g_phi_conv = (int)value; return 0; }
     if (!strcmp(key, "ntt_dbg")) { g_ntt_dbg = (int)value; return 0; }
     if (!strcmp(key, "ntt_group_bytes")) { g_ntt_group_bytes = (uint64_t)std::max<int64_t>(value, 1 << 20); return 0; }
     return -1;

@@ -528,6 +528,19 @@ void ctx_build(bc_ctx *X) {
                 B.ftwRb = fd(btR, B.R / 2); B.ftwRi = fd(btRi, B.R / 2);
                 B.ftwCb = fd(btC, B.C / 2); B.ftwCi = fd(btCi, B.C / 2);
                 B.fmods = dev_upload(X, fm);
+                {
+                    std::vector<int32_t> off, val;
+                    for (uint32_t j = 0; j < k; ++j)
+                        if (ir[j]) { off.push_back((int32_t)j); val.push_back((int32_t)ir[j]); }
+                    B.ir_nnz = 0;
+                    bool small = off.size() <= 16;
+                    for (int32_t v : val) small = small && v >= -(1 << 20) && v <= (1 << 20);
+                    if (small) {
+                        B.ir_off = dev_upload(X, off);
+                        B.ir_val = dev_upload(X, val);
+                        B.ir_nnz = (int)off.size();
+                    }
+                }
                 T.tb = &X->Tb;
                 }
             }

@@ -20,6 +20,7 @@ namespace bc {
 
 int g_ntt_impl = 0;
 int g_ntt_dbg = 0;
+int g_phi_conv = 0;
 int g_f64_elem = 1;
 uint64_t g_ntt_group_bytes = 1ull << 40;   // one launch group (measured best on B200)
 

@@ -36,6 +36,9 @@ struct NttTables {
     const double *fdhb1, *fdhb2;
     uint32_t Mslot;                // word stride of the per-job A slots read / written by modes 2 and 3
     const struct NttTables *tb;    // host pointer: the Barrett convolution tables (composite m), or null
+    const int32_t *ir_off, *ir_val;   // Barrett set: Phi_m^{-1} mod x^(m-n) when it has <= 16 nonzero terms
+    int ir_nnz;                       //   (the quotient is then a sum of shifted copies, no convolution)
+    int q_in_s2;                      // mode 3 reads Q from the scr2 slot (sparse quotient) instead of A_{n..}
     uint32_t m, n, M, R, C, logR, logC;
     int prime_m;
     int dbg;              // ntt3.cu timing experiments only (bc_tune "ntt_dbg"): skip table reads; results invalid          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
@@ -173,6 +176,7 @@ extern uint64_t g_ntt_group_bytes;
 uint64_t ntt_group_jobs(const NttTables &T, uint64_t jobs, bool barrett);
 bool ntt_inverse_barrett(const NttTables &T);
 extern int g_ntt_dbg;
+extern int g_phi_conv;   // 1: always compute the Barrett quotient by convolution (testing)
 extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when the context allows them   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;
 extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     // INV: 0 Bluestein forward, 1 Bluestein inverse, 2/3 the Barrett reduction mod Phi_m of a composite m
     // (2: quotient convolution, input rev(A)_t = A_{m-1-t}, t < m - n; 3: Phi_m * Q, input Q_t = A'_{n+t})
     const double *tf = (INV == 1 ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m;
-    const uint64_t *src = INV >= 2 ? in + (uint64_t)blockIdx.y * T.Mslot : in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
+    const uint64_t *src = INV >= 2 ? in + (uint64_t)blockIdx.y * (INV == 3 && T.q_in_s2 ? T.M : T.Mslot) : in + (uint64_t)J.poly * in_pstride + (uint64_t)J.lb * T.n;
     typedef PtTab<LOGR, LOGE, true> PTT;
     double2 *stw = (double2 *)(smf + (size_t)R * TC), *spt = stw + R / 2;
     const double2 *gtw = T.ftwRb + (uint64_t)J.pr * (R / 2);
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
                 if (ps >= 0) x = fmm8(from_u64(__ldcs(src + ps)), tf[t], q, qi);
             }
         } else if (t < T.m - T.n) {
-            x = from_u64(src[INV == 2 ? T.m - 1 - t : T.n + t]);       // canonical, bound q (UQ = UMUL8)
+            x = from_u64(src[INV == 2 ? T.m - 1 - t : (T.q_in_s2 ? t : T.n + t)]);   // canonical, bound q (UMUL8)
         }
         v[k] = x;
         bd[k] = UMUL8;
@@ -493,6 +493,27 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
     launch_counter() += 3;
 }
 
+// sparse quotient: Qr_i = sum_j ir_val_j Fr_{i - ir_off_j}, Fr_i = A_{m-1-i}; Q_{k-1-i} = Qr_i -> scr2 slot (stride B.M)
+__global__ void k_ir_sparse(NttTables T, LimbMap lm, uint64_t job0, const uint64_t *__restrict__ scr1,
+                            uint64_t *__restrict__ scr2) {
+    const uint32_t k = T.m - T.n, i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const JobF J = job_f(lm, (uint32_t)(job0 + blockIdx.y));
+    const Mod Md = T.mods[J.pr];
+    const uint64_t q = Md.q;
+    const uint64_t *A = scr1 + (uint64_t)blockIdx.y * T.Mslot;
+    uint64_t acc = 0;
+    for (int j = 0; j < T.ir_nnz; ++j) {
+        const int32_t o = T.ir_off[j], v = T.ir_val[j];
+        if ((int32_t)i < o) continue;
+        const uint64_t f = A[T.m - 1 - (i - o)];
+        if (v == 1) acc = add_mod(acc, f, q);
+        else if (v == -1) acc = sub_mod(acc, f, q);
+        else acc = add_mod(acc, mul_mod(f, from_signed(v, q), Md), q);
+    }
+    scr2[(uint64_t)blockIdx.y * T.M + (k - 1 - i)] = acc;
+}
+
 // composite m: Barrett division mod Phi_m of the A_t in the scr1 slots (two convolutions with table set B)
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runb(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,
@@ -512,6 +533,19 @@ static void runb(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps,
     T.dbg = 0;
     double *s2 = (double *)scr2;
     dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
+    if (T.ir_nnz > 0 && !g_phi_conv) {
+        // Phi_m^{-1} mod x^k is sparse (m = r1 r2 with a small factor: (1 + ... + x^{r1-1})(1 - x^{r2})):
+        // the quotient is a short sum of shifted copies, written as Q into the scr2 slots
+        const uint32_t k = T.m - T.n;
+        k_ir_sparse<<<dim3((k + 255) / 256, nj), 256, 0, st>>>(T, lm, j0, scr1, scr2);
+        T.q_in_s2 = 1;
+        kf_passA<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scr2, 0, lm, j0, s2);
+        kf_passB<LOGC, LOGEC, S::RB, 3><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
+        kf_passC<LOGR, LOGER, S::TC, 3, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scr1);
+        launch_counter() += 4;
+        return;
+    }
+    T.q_in_s2 = 0;
     kf_passA<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, scr1, 0, lm, j0, s2);
     kf_passB<LOGC, LOGEC, S::RB, 2><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, s2);
     kf_passC<LOGR, LOGER, S::TC, 2, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, s2, scr1);

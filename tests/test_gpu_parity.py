@@ -476,3 +476,25 @@ def test_hypercube_shadow_compare_decrypts(pair):
     bits = T.ctx.decrypt(T.keys, T.ctx.compare_lt(T.keys, ca, cb), as_bits=True)
     for i in range(3):
         assert list(bits[i]) == [int(x < y) for x, y in zip(A[i], B[i])]
+
+
+@pytest.mark.parametrize("cfg", ["c3s2", "c3"])
+def test_composite_quotient_sparse_matches_convolution(pair, cfg):
+    """composite m: the Barrett quotient rev(A) Phi_m^{-1} mod x^(m-n) as a sum of shifted copies
+    (Phi_m^{-1} = (1 + x + x^2)(1 - x^r2) mod x^(m-n) for m = 3 r2; default) and as a size-Mb
+    convolution (bc_tune phi_conv) give identical inverse transforms (both exact; the inverse itself
+    is checked against the oracle's schoolbook reduction by the NTT tests)."""
+    import paper_2407_07308_b200 as bc
+    T = pair(cfg)
+    P = T.P
+    rng = np.random.default_rng(17)
+    ev = np.stack([np.stack([rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.moduli]) for _ in range(2)])
+    x = from_u64(ev, T.ctx.device)
+    a = to_u64(T.ctx.ntt_inv(x))
+    try:
+        bc._lib.bc_tune(b"phi_conv", 1)
+        b = to_u64(T.ctx.ntt_inv(x))
+    finally:
+        bc._lib.bc_tune(b"phi_conv", 0)
+    assert np.array_equal(a, b)
+    assert np.array_equal(to_u64(T.ctx.ntt_fwd(from_u64(a, T.ctx.device))), ev)
