@@ -575,23 +575,32 @@ __global__ void k_tensor_f(const double2 *__restrict__ fm, const uint64_t *__res
                            uint32_t lvl, uint32_t n) {
     using namespace f64;
     const uint64_t ln = (uint64_t)lvl * n;
-    ROW_LOOP(rw, x, rows, n) {   // rows = B * lvl
+    ROW_LOOP2(rw, x, rows, n) {   // rows = B * lvl; two coefficients per thread
         const uint32_t bi = rw / lvl, limb = rw - bi * lvl;
         const uint64_t r = (uint64_t)limb * n + x;
         const double q = fm[limb].x, qi = fm[limb].y;
-        const double a0 = from_u64(a[bi * 2 * ln + r]), a1 = from_u64(a[bi * 2 * ln + ln + r]);
-        const double b0 = from_u64(b[bi * 2 * ln + r]), b1 = from_u64(b[bi * 2 * ln + ln + r]);
+        const ulonglong2 A0 = LD2(a + bi * 2 * ln + r), A1 = LD2(a + bi * 2 * ln + ln + r);
+        const ulonglong2 B0 = LD2(b + bi * 2 * ln + r), B1 = LD2(b + bi * 2 * ln + ln + r);
         uint64_t *ob = o + bi * 3 * ln + r;
-        ob[0] = to_u64(fmulv(a0, b0, q, qi), q);
-        ob[ln] = to_u64(fred(__dadd_rn(fmulv(a0, b1, q, qi), fmulv(a1, b0, q, qi)), q, qi), q);
-        ob[2 * ln] = to_u64(fmulv(a1, b1, q, qi), q);
+        uint64_t d0[2], d1[2], d2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const double a0 = from_u64(e ? A0.y : A0.x), a1 = from_u64(e ? A1.y : A1.x);
+            const double b0 = from_u64(e ? B0.y : B0.x), b1 = from_u64(e ? B1.y : B1.x);
+            d0[e] = to_u64(fmulv(a0, b0, q, qi), q);
+            d1[e] = to_u64(fred(__dadd_rn(fmulv(a0, b1, q, qi), fmulv(a1, b0, q, qi)), q, qi), q);
+            d2[e] = to_u64(fmulv(a1, b1, q, qi), q);
+        }
+        ST2(ob, d0[0], d0[1]);
+        ST2(ob + ln, d1[0], d1[1]);
+        ST2(ob + 2 * ln, d2[0], d2[1]);
     }
 }
 void ew_tensor(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, uint32_t B, uint32_t lvl,
                uint32_t n, cudaStream_t st, const double2 *fm) {
     const uint64_t rows = (uint64_t)B * lvl;
     if (fm)
-        k_tensor_f<<<grid_rows(n, rows), 256, 0, st>>>(fm, a, b, o, (uint32_t)rows, lvl, n);
+        k_tensor_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, b, o, (uint32_t)rows, lvl, n);
     else
         k_tensor<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, b, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
