@@ -93,6 +93,11 @@ __device__ __forceinline__ void freg_pass(double (&v)[1 << LOGE], int (&bd)[1 <<
         for (int k = 0; k < E; ++k) {
             if (k & (1 << u)) continue;
             const int k2 = k + (1 << u);
+            if (bd[k2] == 0) {          // y known to be exactly 0 (bound 0): (x + 0, x - 0) = (x, x)
+                v[k2] = v[k];
+                bd[k2] = bd[k];
+                continue;
+            }
             bool trivial;
             uint32_t ti;
             if (FWD) {
@@ -272,6 +277,13 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
         const uint32_t t = r * CC + c;
         double x = 0.0;
+        if (INV <= 1 && k >= E / 2) {
+            // rows >= R/2: t >= M/2 >= m > n, the zero half of the Bluestein input (bound 0 = exactly 0:
+            // the first forward stage copies instead of adding zeros)
+            v[k] = 0.0;
+            bd[k] = 0;
+            continue;
+        }
         if (INV == 0) {
             if (t < T.n) {
                 const double xin = (T.dbg & 64) ? (double)t : from_u64(__ldcs(src + t));
