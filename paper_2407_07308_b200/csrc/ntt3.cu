@@ -403,10 +403,12 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     if (INV == 1 && !direct) __syncthreads();   // all columns of this block read before in-place writes of A_t
 #pragma unroll
     for (int k = 0; k < E; ++k) {
+        if (INV <= 1 && k >= E / 2) continue;   // rows >= R/2: t >= M/2 >= m, never output (the last
+                                                // stage's differences feeding them are dead code)
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
         const uint32_t t = r * CC + c;
-        need(v, bd, k, LIM_MUL, q, qi);
         if (t >= T.m) continue;
+        need(v, bd, k, LIM_MUL, q, qi);
         if (INV == 2) {               // Qr_t (t < m - n) -> Q_{m-n-1-t}, stored over A_{n..m-1}
             if (t < kq) A1[T.n + (kq - 1 - t)] = to_u64(fred(v[k], q, qi), q);
             continue;
