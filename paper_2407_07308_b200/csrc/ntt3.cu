@@ -277,9 +277,9 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
         const uint32_t t = r * CC + c;
         double x = 0.0;
-        if (INV <= 1 && k >= E / 2) {
-            // rows >= R/2: t >= M/2 >= m > n, the zero half of the Bluestein input (bound 0 = exactly 0:
-            // the first forward stage copies instead of adding zeros)
+        if (k >= E / 2) {
+            // rows >= R/2: t >= M/2, the zero half of the input (Bluestein: M/2 >= m > n; Barrett modes:
+            // Mb >= 2k - 1 so k <= Mb/2; bound 0 = exactly 0: the first forward stage copies)
             v[k] = 0.0;
             bd[k] = 0;
             continue;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
     if (INV == 1 && !direct) __syncthreads();   // all columns of this block read before in-place writes of A_t
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-        if (INV <= 1 && k >= E / 2) continue;   // rows >= R/2: t >= M/2 >= m, never output (the last
+        if (INV <= 2 && k >= E / 2) continue;   // rows >= R/2: t >= M/2 >= m (mode 2: >= k), never output (the last
                                                 // stage's differences feeding them are dead code)
         const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
         const uint32_t t = r * CC + c;
