@@ -24,6 +24,18 @@
 // twiddle s = omega_L^{brev(b)} per block b (the CRT splitting X^{2h} - c = (X^h - s)(X^h + s)),
 // whose bounds grow linearly, instead of Gentleman-Sande butterflies whose sums double per stage.
 // The output order (bit-reversed) and therefore every table and the results are unchanged.
+//
+// Further structure used here (all exact, results identical to the integer passes):
+//  - pointwise tables (chirps, D^, cross twiddles) are 8-byte centred residues, fl(w/q) formed in a
+//    register (fmm8, |r| <= q); D^ is stored in pass B's thread-minor order (coalesced);
+//  - passes after the first read their twiddles from per-thread shared-memory tables (conflict-free);
+//  - the upper half of every pass-A input is zero (M/2 >= m > n) and is a compile-time zero (bound 0),
+//    and the rows >= R/2 of pass C are never output (their last-stage differences are dead code);
+//  - prime m, inverse: kf_corner computes A_{m-1} per job after pass B, so pass C writes the reduction
+//    A_t - A_{m-1} mod Phi_m directly (no separate reduction pass);
+//  - composite m, inverse: modes 2 / 3 of the same passes (no chirps, index maps, the constant's
+//    transform in place of D^) run the Barrett division by Phi_m at the smallest sufficient size Mb,
+//    the quotient as a sparse sum of shifted copies (k_ir_sparse) when Phi_m^{-1} mod x^(m-n) is short.
 #include <cuda_runtime.h>
 
 #include "kernels.h"
