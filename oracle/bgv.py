@@ -149,7 +149,7 @@ class Keys:
         self.ksk = {}           # key id -> list over digits of (b_j, a_j) over all QP limbs
 
 
-def keygen(P, seed, galois=()):
+def keygen(P, seed, galois=(), relin=True):
     """R8.  s ternary; pk = (-a s + p e, a) over Q; for key id t (0 = relinearisation with
     s' = s^2, else s' = sigma_t(s)) and digit j: swk_j = (-a_j s + p e_j + P W_j s', a_j) over QP,
     with P W_j = [i in G_j] * (P mod q_i) on cipher limb i and 0 on special limbs."""
@@ -164,7 +164,7 @@ def keygen(P, seed, galois=()):
     pe = int_poly_to_rns(P, P.p * e, qidx)
     b = _sub(pe, _mul(a, s_r, P, qidx), P, qidx)
     K.pk = (b, a)
-    for t in [0] + [int(t) for t in galois]:
+    for t in ([0] if relin else []) + [int(t) for t in galois]:
         gen_switch_key(P, K, seed, t)
     return K
 

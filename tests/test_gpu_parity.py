@@ -498,3 +498,28 @@ def test_composite_quotient_sparse_matches_convolution(pair, cfg):
         bc._lib.bc_tune(b"phi_conv", 0)
     assert np.array_equal(a, b)
     assert np.array_equal(to_u64(T.ctx.ntt_fwd(from_u64(a, T.ctx.device))), ev)
+
+
+@pytest.mark.slow
+def test_full_size_c2_encrypt_modswitch_automorph_bit_exact(pair):
+    """C2 at full size (n = 30940, 11 limbs; BASELINE's mid set): the product's encryptions (R7-R9),
+    modulus switch (a6), automorphism (a4) and tensor (a3) ciphertexts equal the oracle's bit for bit
+    (public key only on the oracle side: a few minutes of schoolbook products)."""
+    T = pair("c2")
+    P, bgv = T.P, T.bgv
+    ints = T.ctx.ints_per_ct
+    K = bgv.keygen(P, SEED_KEYS, (), relin=False)
+    ct_o = bgv.encrypt(P, K, np.zeros(P.n, dtype=np.int64), SEED_ENC, 7)
+    ct_g = T.ctx.encrypt(T.keys, np.zeros((1, ints), dtype=np.uint64), SEED_ENC, ct_index0=7)
+    assert np.array_equal(to_u64(ct_g)[0], np.stack(bgv.ct_to_eval(P, ct_o)))
+    assert np.array_equal(to_u64(T.ctx.modswitch(ct_g))[0], np.stack(bgv.ct_to_eval(P, bgv.modswitch(P, ct_o))))
+    t = pow(P.alg.g, 1, P.m) if P.n < 5000 else 2
+    idx = list(range(P.L1))
+    want = np.stack([bgv.to_eval(P, np.stack([P.ring.automorph_mod(c[r], t, P.moduli[r]) for r in idx]), idx)
+                     for c in ct_o.parts])
+    assert np.array_equal(to_u64(T.ctx.automorph(ct_g, t))[0], want)
+    # a3 tensor of two full-size ciphertexts (a second, independent encryption)
+    ct_o2 = bgv.encrypt(P, K, np.zeros(P.n, dtype=np.int64), SEED_ENC, 8)
+    ct_g2 = T.ctx.encrypt(T.keys, np.zeros((1, ints), dtype=np.uint64), SEED_ENC, ct_index0=8)
+    assert np.array_equal(to_u64(ct_g2)[0], np.stack(bgv.ct_to_eval(P, ct_o2)))
+    assert np.array_equal(to_u64(T.ctx.tensor(ct_g, ct_g2))[0], np.stack(bgv.ct_to_eval(P, bgv.tensor(P, ct_o, ct_o2))))
