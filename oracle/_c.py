@@ -35,7 +35,7 @@ def lib():
             u64p = ctypes.POINTER(ctypes.c_uint64)
             i64p = ctypes.POINTER(ctypes.c_int64)
             i32p = ctypes.POINTER(ctypes.c_int32)
-            L.ring_mul.argtypes = [u64p, u64p, u64p, ctypes.c_int, i64p, ctypes.c_uint64]
+            L.ring_mul.argtypes = [u64p, u64p, u64p, ctypes.c_int, i64p, ctypes.c_uint64, ctypes.c_int]
             L.poly_mod_phi.argtypes = [u64p, ctypes.c_int, i64p, ctypes.c_int, ctypes.c_uint64]
             L.eval_naive.argtypes = [u64p, ctypes.c_int, i32p, ctypes.c_int, ctypes.c_int, u64p,
                                      ctypes.c_uint64, u64p]
@@ -53,7 +53,7 @@ def u64(a):
     return np.ascontiguousarray(a, dtype=np.uint64)
 
 
-def ring_mul(a, b, phi, q):
+def ring_mul(a, b, phi, q, m):
     """Schoolbook a*b mod (q, Phi_m); a, b: uint64[n] residues in [0, q)."""
     a = u64(a)
     b = u64(b)
@@ -61,7 +61,7 @@ def ring_mul(a, b, phi, q):
     out = np.empty(n, dtype=np.uint64)
     ph = np.ascontiguousarray(phi, dtype=np.int64)
     lib().ring_mul(_p(a, ctypes.c_uint64), _p(b, ctypes.c_uint64), _p(out, ctypes.c_uint64), n,
-                   _p(ph, ctypes.c_int64), int(q))
+                   _p(ph, ctypes.c_int64), int(q), int(m))
     return out
 
 

@@ -72,8 +72,8 @@ class Ring:
 
     # --- coefficient-form primitives -------------------------------------------------
     def mul(self, a, b, q):
-        """Schoolbook product mod (q, Phi_m) (C helper)."""
-        return _c.ring_mul(a, b, self.phi, q)
+        """Schoolbook product, folded mod x^m - 1, reduced mod (q, Phi_m) (C helper)."""
+        return _c.ring_mul(a, b, self.phi, q, self.m)
 
     def reduce_int(self, coeffs):
         """Exact reduction of an integer polynomial (any length) modulo Phi_m over Z."""

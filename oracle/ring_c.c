@@ -7,12 +7,12 @@
  * with the CUDA product path (paper_2407_07308_b200/).
  *
  * Everything here is a textbook definition written out:
- *   ring_mul   : schoolbook product in Z_q[x]/(Phi_m(x))            (§2.1)
+ *   ring_mul   : schoolbook product, fold mod x^m - 1, division by Phi_m (§2.1)
  *   poly_mod_phi: long division by the monic integer polynomial Phi_m
  *   eval_naive : E[k] = f(omega^{z_k}) for z_k in Z_m^* ascending     (§2.2)
  *   vec_mulmod : element-wise (a*b) mod q
- * Products use unsigned __int128 and the '%' operator; q < 2^62 so at most
- * 8 products are accumulated before a reduction (8 * 2^124 < 2^128).
+ * Products use unsigned __int128 and the '%' operator; q < 2^62, and a sum is reduced before
+ * it could exceed 2^128 (at most 2^(128 - 2 bits(q)) - 1 products per reduction).
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -43,13 +43,19 @@ void poly_mod_phi(uint64_t *t, int len, const int64_t *phi, int n, uint64_t q)
     }
 }
 
-/* out = a*b mod (q, Phi_m); a, b, out length n; phi length n+1. */
+/* out = a*b mod (q, Phi_m); a, b, out length n; phi length n+1.
+ * Definition: schoolbook product over Z_q, fold mod x^m - 1 (exact:
+ * Phi_m divides x^m - 1), then long division by Phi_m (m - n steps).  The u128 accumulator is
+ * reduced only when the next term could overflow it: with q < 2^b every product is < 2^(2b), so
+ * 2^(128-2b) - 1 terms fit (C2-C5: b = 50, every output coefficient is reduced once). */
 void ring_mul(const uint64_t *a, const uint64_t *b, uint64_t *out, int n,
-              const int64_t *phi, uint64_t q)
+              const int64_t *phi, uint64_t q, int m)
 {
     int len = 2 * n - 1;
-    uint64_t *t = (uint64_t *)calloc((size_t)len, sizeof(uint64_t));
-    #pragma omp parallel for schedule(static)
+    int bits = 64 - __builtin_clzll(q);
+    int lim = 2 * bits >= 127 ? 1 : (2 * bits > 96 ? (int)((((u128)1) << (128 - 2 * bits)) - 1) : 1 << 30);
+    uint64_t *t = (uint64_t *)calloc((size_t)(len > m ? len : m), sizeof(uint64_t));
+    #pragma omp parallel for schedule(dynamic, 64)
     for (int k = 0; k < len; ++k) {
         int lo = k - (n - 1) > 0 ? k - (n - 1) : 0;
         int hi = k < n - 1 ? k : n - 1;
@@ -57,11 +63,17 @@ void ring_mul(const uint64_t *a, const uint64_t *b, uint64_t *out, int n,
         int cnt = 0;
         for (int i = lo; i <= hi; ++i) {
             acc += (u128)a[i] * b[k - i];
-            if (++cnt == 8) { acc %= q; cnt = 0; }
+            if (++cnt == lim) { acc %= q; cnt = 0; }
         }
         t[k] = (uint64_t)(acc % q);
     }
-    poly_mod_phi(t, len, phi, n, q);
+    /* fold mod x^m - 1: x^k = x^(k-m) for k >= m */
+    for (int k = m; k < len; ++k) {
+        uint64_t s = t[k - m] + t[k];
+        t[k - m] = s >= q ? s - q : s;
+        t[k] = 0;
+    }
+    poly_mod_phi(t, m, phi, n, q);
     memcpy(out, t, (size_t)n * sizeof(uint64_t));
     free(t);
 }

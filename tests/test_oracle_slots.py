@@ -19,14 +19,39 @@ def test_table3_closed_forms():
         S = row["N"] // D
         for circ in ("B", "U"):
             d, l = row[circ]["d"], row[circ]["l"]
-            if row["set"] in ("p3", "p10"):
-                # non-cyclic Z_m^*/<p> (hypercube): blocks straddle rows (F7)
-                assert S // l == row[circ]["ints"]
-            else:
-                assert S // l == row[circ]["ints"]
+            # the paper's count is floor(S / l) for every row, hypercube rows included
+            assert S // l == row[circ]["ints"]
             assert d <= D
             base = slots.digit_base(p, circ)
             assert base ** (d * l) >= 2 ** 64
+
+
+def _quotient_orders(p, m):
+    """orders of the elements of Z_m^*/<p> (brute force over divisors of S): -> (S, max order)"""
+    H = {pow(p, k, m) for k in range(nt.mult_order(p, m))}
+    S = nt.euler_phi(m) // len(H)
+    divs = [k for k in range(1, S + 1) if S % k == 0]
+    best = 1
+    for t in range(2, m):
+        if nt.gcd(t, m) == 1:
+            best = max(best, next(k for k in divs if pow(t, k, m) in H))
+    return S, best
+
+
+def test_table3_hypercube_rows():
+    """F7 / S17: Z_m^*/<p> is cyclic for every Table 3 row except p3 and p10, where it is
+    Z_S1 x Z_2; R6's row-aligned layout then holds 2 floor(S1/l) = floor(S/l) - 1 integers."""
+    for row in golden("table3.json")["rows"]:
+        if row["m"] > 60000:
+            continue
+        S, S1 = _quotient_orders(row["p"], row["m"])
+        if row["set"] in ("p3", "p10"):
+            assert S1 * 2 == S
+            for circ in ("B", "U"):
+                l = row[circ]["l"]
+                assert 2 * (S1 // l) == row[circ]["ints"] - 1
+        else:
+            assert S1 == S
 
 
 def test_slot_algebra_spec_pin():
