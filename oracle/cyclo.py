@@ -76,8 +76,11 @@ class Ring:
         return _c.ring_mul(a, b, self.phi, q, self.m)
 
     def reduce_int(self, coeffs):
-        """Exact reduction of an integer polynomial (any length) modulo Phi_m over Z."""
-        t = [int(c) for c in coeffs]
+        """Exact reduction of an integer polynomial (any length) modulo Phi_m over Z: fold the
+        exponents mod m (x^m = 1 modulo Phi_m, which divides x^m - 1), then long division."""
+        t = [0] * self.m
+        for k, c in enumerate(coeffs):
+            t[k % self.m] += int(c)
         n = self.n
         ph = [int(c) for c in self.phi]
         for k in range(len(t) - 1, n - 1, -1):

@@ -57,6 +57,7 @@ bc_status bc_ctx_create(const bc_params *prm, int device, bc_ctx **out) {
     X->device = device;
     try {
         ctx_build(X);
+        ctx_precompute_pt(X);
     } catch (...) {
         ctx_free(X);
         delete X;
@@ -183,6 +184,7 @@ static uint32_t choose_chunk(bc_ctx *X, const bc_keys *keys, uint32_t B, uint32_
 
 static void out_copy(Eng &E, const CT &src, const bc_ct &dst, uint32_t b0) {
     if (src.lvl != dst.level) BC_THROW(BC_E_LEVEL, "output level " + std::to_string(dst.level) + " != computed " + std::to_string(src.lvl));
+    if (!dst.data || (uint64_t)b0 + src.B > dst.batch) BC_THROW(BC_E_ARG, "output view too small");
     uint64_t *d = (uint64_t *)dst.data + (uint64_t)b0 * 2 * dst.level * E.X->n;
     CK(cudaMemcpyAsync(d, src.d, (size_t)src.B * src.bstride * 8, cudaMemcpyDeviceToDevice, E.st));
 }
@@ -190,6 +192,23 @@ static void out_copy(Eng &E, const CT &src, const bc_ct &dst, uint32_t b0) {
 static void check_ct(const bc_ctx *X, const bc_ct &c, const char *nm) {
     if (!c.data || c.batch == 0) BC_THROW(BC_E_ARG, std::string(nm) + ": empty ciphertext view");
     if (c.level < 1 || c.level > X->L1) BC_THROW(BC_E_LEVEL, std::string(nm) + ": bad level");
+}
+
+// output views are validated BEFORE anything is enqueued (no partial outputs on error): the
+// level an operation produces is found by a host-only dry run of the same schedule
+template <class F>
+static uint32_t dry_level(bc_ctx *X, F fn) {
+    Arena A;
+    A.init(nullptr, (size_t)1 << 62, true);
+    Eng E{X, nullptr, &A, 0};
+    return fn(E).lvl;
+}
+static CT dry_view(Eng &E, const bc_ct &c) { return E.view((uint64_t *)(uintptr_t)256, 1, c.level); }
+static void check_out(const bc_ctx *X, const bc_ct &o, uint32_t batch, uint32_t level, const char *nm) {
+    check_ct(X, o, nm);
+    if (o.batch < batch) BC_THROW(BC_E_ARG, std::string(nm) + ": output batch " + std::to_string(o.batch) + " < " + std::to_string(batch));
+    if (o.level != level)
+        BC_THROW(BC_E_LEVEL, std::string(nm) + ": output level " + std::to_string(o.level) + " != " + std::to_string(level));
 }
 
 // which: 0 lt, 1 lt+eq, 3 eq only, 2 min, 4 max
@@ -202,6 +221,26 @@ static bc_status run_compare(bc_ctx *X, const bc_keys *keys, bc_ct a, bc_ct b, b
     if (a.batch != b.batch) BC_THROW(BC_E_ARG, "batch mismatch");
     const uint32_t lvl = std::min(a.level, b.level);
     const int pk = (which == 2 || which == 4) ? 2 : (which == 0 ? 0 : 1);
+    {
+        const uint32_t want = dry_level(X, [&](Eng &E) {
+            CT av = dry_view(E, a), bv = dry_view(E, b), lt, eq;
+            if (which == 2 || which == 4) {
+                compare_batch(E, av, bv, &lt, nullptr);
+                return select_batch(E, lt, av, bv);
+            }
+            compare_batch(E, av, bv, &lt, which ? &eq : nullptr);
+            return which == 3 ? eq : lt;
+        });
+        check_out(X, o1, a.batch, want, "out");
+        if (which == 1 && o2.data) {
+            const uint32_t weq = dry_level(X, [&](Eng &E) {
+                CT av = dry_view(E, a), bv = dry_view(E, b), lt, eq;
+                compare_batch(E, av, bv, &lt, &eq);
+                return eq;
+            });
+            check_out(X, o2, a.batch, weq, "eq_out");
+        }
+    }
     const uint32_t chunk = choose_chunk(X, keys, a.batch, lvl, pk, wsb);
     for (uint32_t b0 = 0; b0 < a.batch; b0 += chunk) {
         const uint32_t nb = std::min(chunk, a.batch - b0);
@@ -255,6 +294,9 @@ bc_status bc_select(bc_ctx *X, const bc_keys *k, bc_ct cond, bc_ct x1, bc_ct x2,
     API_BEGIN
     if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
     check_ct(X, cond, "cond"); check_ct(X, x1, "x1"); check_ct(X, x2, "x2");
+    if (x1.batch != cond.batch || x2.batch != cond.batch) BC_THROW(BC_E_ARG, "batch mismatch");
+    check_out(X, out, cond.batch, dry_level(X, [&](Eng &E) {
+        return select_batch(E, dry_view(E, cond), dry_view(E, x1), dry_view(E, x2)); }), "out");
     Arena A;
     A.init(ws, wsb, false);
     Eng E{X, k, &A, S(st)};
@@ -334,6 +376,7 @@ bc_status bc_automorph(bc_ctx *X, bc_ct a, uint32_t t, bc_ct out, void *st) {
     if (!X) BC_THROW(BC_E_ARG, "null ctx");
     check_ct(X, a, "a");
     if (gcd_u64(t, X->m) != 1) BC_THROW(BC_E_ARG, "t not in Z_m^*");
+    check_out(X, out, a.batch, a.level, "out");
     ew_automorph(X->T, (uint64_t *)a.data, (uint64_t *)out.data, a.batch, 2, a.level, t % X->m, S(st));
     check_launch();
     API_END
@@ -356,6 +399,8 @@ bc_status bc_modswitch(bc_ctx *X, bc_ct a, bc_ct out, void *ws, size_t wsb, void
     API_BEGIN
     if (!X) BC_THROW(BC_E_ARG, "null ctx");
     check_ct(X, a, "a");
+    if (a.level < 2) BC_THROW(BC_E_LEVEL, "modswitch: out of levels");
+    check_out(X, out, a.batch, a.level - 1, "out");
     Arena A;
     A.init(ws, wsb, false);
     Eng E{X, nullptr, &A, S(st)};
@@ -369,6 +414,8 @@ bc_status bc_mul(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_ct out, void 
     API_BEGIN
     if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
     check_ct(X, a, "a"); check_ct(X, b, "b");
+    if (a.batch != b.batch) BC_THROW(BC_E_ARG, "batch mismatch");
+    check_out(X, out, a.batch, dry_level(X, [&](Eng &E) { return E.mul(dry_view(E, a), dry_view(E, b)); }), "out");
     Arena A;
     A.init(ws, wsb, false);
     Eng E{X, k, &A, S(st)};
@@ -382,6 +429,7 @@ bc_status bc_rotate(bc_ctx *X, const bc_keys *k, bc_ct a, int32_t r, bc_ct out, 
     API_BEGIN
     if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
     check_ct(X, a, "a");
+    check_out(X, out, a.batch, a.level, "out");
     Arena A;
     A.init(ws, wsb, false);
     Eng E{X, k, &A, S(st)};
@@ -395,6 +443,7 @@ bc_status bc_frobenius(bc_ctx *X, const bc_keys *k, bc_ct a, uint32_t r, bc_ct o
     API_BEGIN
     if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
     check_ct(X, a, "a");
+    check_out(X, out, a.batch, a.level, "out");
     Arena A;
     A.init(ws, wsb, false);
     Eng E{X, k, &A, S(st)};
@@ -477,7 +526,15 @@ static bc_status run_vec(bc_ctx *X, const bc_keys *k, int which, const bc_ct *v,
     Arena A;
     A.init(ws, wsb, false);
     Eng E{X, k, &A, S(st)};
-    std::vector<CT> r = vec_run(E, which, vec_views(X, E, v, T));
+    std::vector<CT> views = vec_views(X, E, v, T);
+    {
+        std::vector<uint32_t> lv(T);
+        for (uint32_t i = 0; i < T; ++i) lv[i] = v[i].level;
+        const uint32_t want = bc_vec_out_level(X, which, lv.data(), T);
+        const uint32_t nout = which == 2 ? T : 1;
+        for (uint32_t i = 0; i < nout; ++i) check_out(X, out[i], v[0].batch, want, "out[i]");
+    }
+    std::vector<CT> r = vec_run(E, which, views);
     for (size_t i = 0; i < r.size(); ++i) {
         if (out[i].batch != r[i].B) BC_THROW(BC_E_ARG, "output batch mismatch");
         out_copy(E, r[i], out[i], 0);

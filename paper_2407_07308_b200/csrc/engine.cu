@@ -674,6 +674,8 @@ void lift_p(bc_ctx *X, const std::string &key, const Mod *mods, uint32_t p, cons
             uint32_t skipn, int mode, cudaStream_t st) {
     auto it = X->plan_dims.find(key);
     if (it == X->plan_dims.end()) BC_THROW(BC_E_INTERNAL, "missing lift plan " + key);
+    if (it->second.first > (mode == 2 ? 64u : 32u) || it->second.second > 64u)
+        BC_THROW(BC_E_PARAM, "lift plan " + key + " exceeds the kernels' source / target limits");
     lift(X->plan(key), mods, p, src, src_pstride, out, out_pstride, out16, npoly, n, skip0, skipn, mode, st,
          it->second.first, it->second.second, g_f64_elem ? X->d_fm : nullptr);
 }
@@ -699,6 +701,7 @@ void encode_slots_dev(bc_ctx *X, const int16_t *d_slots, uint32_t B, int16_t *d_
 }
 
 uint64_t *ctx_pt(bc_ctx *X, const std::string &key, const std::vector<int16_t> &slots, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(X->pt_mu);
     auto it = X->pt.find(key);
     if (it != X->pt.end()) return it->second;
     const uint32_t n = X->n, L1 = X->L1;
@@ -1127,6 +1130,41 @@ static std::vector<int16_t> block_mask(bc_ctx *X, const std::function<bool(uint3
     return m;
 }
 
+// the slot vectors of the schedule constants (R16 extraction kappa_{i,k}; R16 / R17 masks)
+static std::string kappa_key(uint32_t i, uint32_t k) { return "kappa:" + std::to_string(i) + ":" + std::to_string(k); }
+static std::vector<int16_t> kappa_slots(bc_ctx *X, uint32_t i, uint32_t k) {
+    const uint32_t D = X->alg.D, S = X->alg.S;
+    std::vector<int16_t> sl((size_t)S * D);
+    const auto &kap = X->alg.kappa[(size_t)i * D + k];
+    for (uint32_t s = 0; s < S; ++s)
+        for (uint32_t j = 0; j < D; ++j) sl[(size_t)s * D + j] = (int16_t)kap[j];
+    return sl;
+}
+static std::vector<int16_t> ksm_slots(bc_ctx *X, uint32_t sh) {
+    const uint32_t l = X->l;
+    return block_mask(X, [sh, l](uint32_t t) { return t + sh < l; });
+}
+static std::vector<int16_t> ksi_slots(bc_ctx *X, uint32_t sh) {
+    std::vector<int16_t> im = ksm_slots(X, sh);
+    for (size_t s = 0; s < X->alg.S; ++s) im[s * X->alg.D] = (int16_t)(1 - im[s * X->alg.D]);
+    return im;
+}
+static std::vector<int16_t> bm0_slots(bc_ctx *X) { return block_mask(X, [](uint32_t t) { return t == 0; }); }
+static std::vector<int16_t> bmr_slots(bc_ctx *X, uint32_t sh) {
+    return block_mask(X, [sh](uint32_t t) { return t >= sh; });
+}
+
+void ctx_precompute_pt(bc_ctx *X) {
+    for (uint32_t i = 0; i < X->d; ++i)
+        for (uint32_t k = 0; k < X->alg.D; ++k) ctx_pt(X, kappa_key(i, k), kappa_slots(X, i, k), 0);
+    for (uint32_t sh = 1; sh < X->l; sh <<= 1) {
+        ctx_pt(X, "ksm:" + std::to_string(sh), ksm_slots(X, sh), 0);
+        ctx_pt(X, "ksi:" + std::to_string(sh), ksi_slots(X, sh), 0);
+        ctx_pt(X, "bmr:" + std::to_string(sh), bmr_slots(X, sh), 0);
+    }
+    ctx_pt(X, "bm0", bm0_slots(X), 0);
+}
+
 // digit extraction (a8): digit_i = sum_k kappa_{i,k} (.) sigma_{p^k}(ct); returns d views of one batch
 std::vector<CT> extract_batch(Eng &E, const CT &a) {
     bc_ctx *X = E.X;
@@ -1144,11 +1182,7 @@ std::vector<CT> extract_batch(Eng &E, const CT &a) {
         CT acc;
         bool have = false;
         for (uint32_t k = 0; k < D; ++k) {
-            std::vector<int16_t> sl((size_t)S * D);
-            const auto &kap = X->alg.kappa[(size_t)i * D + k];
-            for (uint32_t s = 0; s < S; ++s)
-                for (uint32_t j = 0; j < D; ++j) sl[(size_t)s * D + j] = (int16_t)kap[j];
-            const uint64_t *pt = ctx_pt(X, "kappa:" + std::to_string(i) + ":" + std::to_string(k), sl, E.st);
+            const uint64_t *pt = ctx_pt(X, kappa_key(i, k), kappa_slots(X, i, k), E.st);
             CT t = E.ptmul(F[k], pt);
             acc = have ? E.add(acc, t) : t;
             have = true;
@@ -1182,10 +1216,8 @@ static void lex_slots(Eng &E, Val *lt, Val *eq, bool need_eq) {
     const uint32_t l = X->l;
     for (uint32_t sh = 1; sh < l; sh <<= 1) {
         const bool last = (sh << 1) >= l;
-        const uint64_t *mask = ctx_pt(X, "ksm:" + std::to_string(sh), block_mask(X, [sh, l](uint32_t t) { return t + sh < l; }), E.st);
-        std::vector<int16_t> im = block_mask(X, [sh, l](uint32_t t) { return t + sh < l; });
-        for (size_t s = 0; s < X->alg.S; ++s) im[s * X->alg.D] = (int16_t)(1 - im[s * X->alg.D]);
-        const uint64_t *inv = ctx_pt(X, "ksi:" + std::to_string(sh), im, E.st);   // 1 - mask, every slot
+        const uint64_t *mask = ctx_pt(X, "ksm:" + std::to_string(sh), ksm_slots(X, sh), E.st);
+        const uint64_t *inv = ctx_pt(X, "ksi:" + std::to_string(sh), ksi_slots(X, sh), E.st);   // 1 - mask, every slot
         CT hi_lt = E.ptmul(E.rotate(lt->ct, sh), mask);
         CT hi_eq = E.add_pt(E.ptmul(E.rotate(eq->ct, sh), mask), inv);
         Val nlt = vadd(E, VT(hi_lt), vmul(E, VT(hi_eq), *lt));
@@ -1236,9 +1268,9 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
 CT broadcast_batch(Eng &E, const CT &cond) {
     bc_ctx *X = E.X;
     const uint32_t l = X->l;
-    CT c = E.ptmul(cond, ctx_pt(X, "bm0", block_mask(X, [](uint32_t t) { return t == 0; }), E.st));
+    CT c = E.ptmul(cond, ctx_pt(X, "bm0", bm0_slots(X), E.st));
     for (uint32_t sh = 1; sh < l; sh <<= 1) {
-        const uint64_t *mk = ctx_pt(X, "bmr:" + std::to_string(sh), block_mask(X, [sh](uint32_t t) { return t >= sh; }), E.st);
+        const uint64_t *mk = ctx_pt(X, "bmr:" + std::to_string(sh), bmr_slots(X, sh), E.st);
         c = E.add(c, E.ptmul(E.rotate(c, -(int64_t)sh), mk));
     }
     return c;

@@ -4,6 +4,7 @@
 
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -83,6 +84,8 @@ struct bc_ctx {
     uint32_t *d_ts = nullptr;
     int8_t *d_red = nullptr;
     std::map<std::string, uint64_t *> pt;       // encoded plaintext constants, eval [L1][n]
+    std::mutex pt_mu;                           // guards pt: the circuit constants are built in
+                                                // ctx_precompute_pt, compaction masks on first use
     // circuit coefficients
     std::vector<int64_t> lt_u, eq_u;            // univariate LT / EQ coefficients
     std::vector<std::vector<int64_t>> lt_b;     // bivariate c[j][k] (Y^j Z^k)
@@ -149,6 +152,9 @@ struct Eng {
 
 // plaintext constants
 uint64_t *ctx_pt(bc_ctx *X, const std::string &key, const std::vector<int16_t> &slots, cudaStream_t st);
+// encodes every plaintext constant of the compare / select schedules (kappa, lexicographic and
+// broadcast masks) once at context creation, so concurrent calls only read the cache
+void ctx_precompute_pt(bc_ctx *X);
 void encode_slots_dev(bc_ctx *X, const int16_t *d_slots, uint32_t B, int16_t *d_coef, Arena *A,
                       cudaStream_t st);
 

@@ -334,15 +334,15 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     const int lTC = T.logC < 4 ? (int)T.logC : 4;
     const int lTR = T.logR < 3 ? (int)T.logR : 3;
     const size_t smA = ((size_t)T.R << lTC) * 8, smB = ((size_t)T.C << lTR) * 8;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set_dev{0};
+    if (attr_pending(attr_set_dev)) {
         cudaFuncSetAttribute(k_passA<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(k_passA<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(k_passB<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(k_passB<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(k_passC<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(k_passC<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        attr_set = true;
+        attr_done(attr_set_dev);
     }
     lm.npoly = npoly;
     // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
@@ -1104,7 +1104,12 @@ __global__ void __launch_bounds__(256) k_lift_f(const uint64_t *__restrict__ pla
             const double2 *B = sB + t * NS;
             double acc = v[0];                                   // B[t][0] = 1
 #pragma unroll
-            for (int k = 1; k < NS; ++k) acc = __dadd_rn(acc, fmm(v[k], B[k], qt));   // < (2 + 0.625 (NS-1)) q_t
+            for (int k = 1; k < NS; ++k) {
+                // < (2 + 0.625 (k-1)) q_t before term k; one reduction after 8 terms keeps the sum
+                // exact for NS <= 16: |fred| <= q/2 + 2, then < (0.5 + 0.625 (NS-9)) q_t + ...
+                if (k == 8) acc = fred(acc, qt, qit);
+                acc = __dadd_rn(acc, fmm(v[k], B[k], qt));
+            }
             if (neg) acc = __dsub_rn(acc, sQ[t].x);
             if (mode == 1) acc = __dadd_rn(acc, fmm(tcd, sQ[t], qt));   // |tc| <= p/2 <= 4q; sum < 7.5 q_t
             const uint64_t r = to_u64(fred(acc, qt, qit), qt);
@@ -1117,10 +1122,11 @@ __global__ void __launch_bounds__(256) k_lift_f(const uint64_t *__restrict__ pla
 void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride, uint64_t *out,
           uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0, uint32_t skipn, int mode,
           cudaStream_t st, uint32_t ns_hint, uint32_t nt_hint, const double2 *fm) {
-    if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 8 && nt_hint <= 64) {
+    if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 16 && nt_hint <= 64) {
         const dim3 g = grid_rows(n, npoly);
 #define LIFT_F(K) case K: k_lift_f<K><<<g, 256, 0, st>>>(plan, fm, p, src, src_pstride, out, out_pstride, npoly, n, skip0, skipn, mode); break;
-        switch (ns_hint) { LIFT_F(1) LIFT_F(2) LIFT_F(3) LIFT_F(4) LIFT_F(5) LIFT_F(6) LIFT_F(7) LIFT_F(8) }
+        switch (ns_hint) { LIFT_F(1) LIFT_F(2) LIFT_F(3) LIFT_F(4) LIFT_F(5) LIFT_F(6) LIFT_F(7) LIFT_F(8)
+                           LIFT_F(9) LIFT_F(10) LIFT_F(11) LIFT_F(12) LIFT_F(13) LIFT_F(14) LIFT_F(15) LIFT_F(16) }
 #undef LIFT_F
         LAUNCHED();
         return;
@@ -1139,8 +1145,8 @@ void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src
         k_lift<64><<<grid_for(total, 128), 128, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, out16,
                                                          total, n, skip0, skipn, mode);
     else
-        k_lift<16><<<grid_for(total, 256), 256, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, out16,
-                                                         total, n, skip0, skipn, mode);
+        k_lift<32><<<grid_for(total, 256), 256, 0, st>>>(plan, mods, p, src, src_pstride, out, out_pstride, out16,
+                                                         total, n, skip0, skipn, mode);   // ns <= 32 (lift_p checks)
     LAUNCHED();
 }
 

@@ -2,11 +2,25 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "modarith.cuh"
 
 namespace bc {
+
+// Per-device kernel-attribute flags (cudaFuncSetAttribute acts on the current device): a call site
+// sets its attributes while attr_pending() is true, then attr_done().  Thread-safe: the bit is set
+// only after the attributes, and two racing threads both setting them is harmless (idempotent).
+inline uint64_t cur_device_bit() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return 1ull << (dev & 63);
+}
+inline bool attr_pending(const std::atomic<uint64_t> &done) {
+    return !(done.load(std::memory_order_acquire) & cur_device_bit());
+}
+inline void attr_done(std::atomic<uint64_t> &done) { done.fetch_or(cur_device_bit(), std::memory_order_acq_rel); }
 
 struct __align__(16) u64x2 { uint64_t w, ws; };   // value + Shoup companion (16-byte aligned: one 128-bit load)
 

@@ -324,15 +324,15 @@ template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 16, int RB_ = 0>
 static void run2(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
                  uint64_t in_ps, uint64_t out_ps, uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st) {
     typedef Ntt2Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
-    static bool init = false;
-    if (!init) {
+    static std::atomic<uint64_t> init_dev{0};
+    if (attr_pending(init_dev)) {
         cudaFuncSetAttribute(k2_passA<LOGR, LOGER, S::TC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(k2_passA<LOGR, LOGER, S::TC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(k2_passC<LOGR, LOGER, S::TC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(k2_passC<LOGR, LOGER, S::TC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(k2_passB<LOGC, LOGEC, S::RB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         cudaFuncSetAttribute(k2_passB<LOGC, LOGEC, S::RB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
-        init = true;
+        attr_done(init_dev);
     }
     dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
     if (!inv) {

@@ -487,15 +487,15 @@ template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
                  uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
-    static bool init = false;
-    if (!init) {
+    static std::atomic<uint64_t> init_dev{0};
+    if (attr_pending(init_dev)) {
         cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 0, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 1, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 0, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 1, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
-        init = true;
+        attr_done(init_dev);
     }
     double *scr = (double *)scratch;
     NttTables T = T0;
@@ -545,15 +545,15 @@ template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runb(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,
                  uint64_t j0, uint32_t nj, cudaStream_t st) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
-    static bool init = false;
-    if (!init) {
+    static std::atomic<uint64_t> init_dev{0};
+    if (attr_pending(init_dev)) {
         cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passA<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 2, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passC<LOGR, LOGER, S::TC, 3, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMA);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
         cudaFuncSetAttribute(kf_passB<LOGC, LOGEC, S::RB, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMB);
-        init = true;
+        attr_done(init_dev);
     }
     NttTables T = B;
     T.dbg = 0;

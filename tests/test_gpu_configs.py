@@ -1,0 +1,178 @@
+"""GPU parity at every BASELINE config (round-2 VERDICT "What's weak" 1): C4 / C5 through their
+shadow rings with the real chains (SURVEY §8(d) shadow table), the full-size C4 / C5 rings (the
+prime-m inverse at M = 2^17, the 16-digit extraction at D = 17, the >8-source lifts), and the
+full-size C2 compare_lt against the digest written by tools/oracle/c2_compare_digest.py (which
+calls only oracle/ and inputs/).
+
+Runs on a B200 (``-m gpu``); the oracle side runs on the host cores.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from gpu_util import SEED_ENC, Pair, from_u64, mixed_pairs, to_u64
+
+pytestmark = pytest.mark.gpu
+
+_PAIRS = {}
+
+
+@pytest.fixture(scope="module")
+def pair(oracle_params):
+    def get(name):
+        if name not in _PAIRS:
+            _PAIRS[name] = Pair(name, oracle_params)
+        return _PAIRS[name]
+    return get
+
+
+def _words(P, rng, ints):
+    return [int(x) for x in rng.integers(0, min(P.base ** (P.d * P.l), 2 ** 62), size=ints)]
+
+
+@pytest.mark.parametrize("cfg", ["c4s", "c5s"])
+def test_shadow_ops_match_oracle(pair, cfg):
+    """a3-a6 on the C4 / C5 chains: tensor, key switch, mul (ModUp digits of alpha = 10 sources and
+    the fused ModDown of K + 1 = 11 sources at c4s: the binary64 9-16-source lift), rotation and
+    Frobenius ciphertexts bit-exact against the oracle."""
+    T = pair(cfg)
+    P, bgv = T.P, T.bgv
+    assert T.ctx.moduli()[0] == P.moduli
+    rng = np.random.default_rng(71)
+    ints = T.ctx.ints_per_ct
+    a, b = mixed_pairs(P, rng, ints)
+    ct = T.ctx.encrypt(T.keys, np.array([a, b], dtype=np.uint64), SEED_ENC, ct_index0=20)
+    oa, ob = T.oracle_ct(a, 20), T.oracle_ct(b, 21)
+    ca, cb = ct[0:1], ct[1:2]
+    assert np.array_equal(to_u64(ca)[0], T.ct_eval(oa))
+    idx = list(range(P.L1))
+    u = to_u64(T.ctx.keyswitch(T.keys, ca[:, 1].contiguous(), 0))[0]
+    u0, u1 = bgv.keyswitch(P, T.okeys, oa.parts[1], P.L1, 0)
+    assert np.array_equal(u, np.stack([bgv.to_eval(P, u0, idx), bgv.to_eval(P, u1, idx)]))
+    m1 = T.ctx.mul(T.keys, ca, cb)
+    om1 = bgv.mul(P, T.okeys, oa, ob)
+    assert np.array_equal(to_u64(m1)[0], T.ct_eval(om1))
+    # a second product one level down (digits of the partial top group)
+    assert np.array_equal(to_u64(T.ctx.mul(T.keys, m1, m1))[0], T.ct_eval(bgv.mul(P, T.okeys, om1, om1)))
+    assert np.array_equal(to_u64(T.ctx.rotate(T.keys, ca, 1))[0], T.ct_eval(bgv.rotate(P, T.okeys, oa, 1)))
+    assert np.array_equal(to_u64(T.ctx.frobenius(T.keys, ca, 1))[0], T.ct_eval(bgv.frobenius(P, T.okeys, oa, 1)))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("op,T", [("min", 4), ("max", 2)])
+def test_shadow_c4_tournament_bit_exact(pair, op, T):
+    """C4's workload (R20 tournament, univariate p = 3, (d,l) = (16,2), 30 + 10 primes, alpha = 10)
+    on its shadow ring m = 1871: every output ciphertext bit-exact vs the oracle's tournament and
+    decrypting to the brute-force min / max."""
+    from oracle import circuits
+    Tp = pair("c4s")
+    P = Tp.P
+    ints = Tp.ctx.ints_per_ct
+    rng = np.random.default_rng(80 + T)
+    W = [_words(P, rng, ints) for _ in range(T)]
+    W[1][0] = W[0][0]                                          # a tie
+    elems = [Tp.ctx.encrypt(Tp.keys, np.array([W[t]], dtype=np.uint64), SEED_ENC, ct_index0=700 + t)
+             for t in range(T)]
+    r = Tp.ctx.max_tree(Tp.keys, elems) if op == "max" else Tp.ctx.min_tree(Tp.keys, elems)
+    f = min if op == "min" else max
+    assert list(Tp.ctx.decrypt(Tp.keys, r)[0]) == [f(W[t][j] for t in range(T)) for j in range(ints)]
+    ev = circuits.OracleEval(P, Tp.okeys)
+    o = circuits.tournament(ev, [Tp.oracle_ct(W[t], 700 + t) for t in range(T)], op, P.circuit, P.d, P.l, ints)
+    assert np.array_equal(to_u64(r)[0], Tp.ct_eval(o))
+
+
+@pytest.mark.slow
+def test_shadow_c5_sort_bit_exact(pair):
+    """C5's workload (R21 rank sort, univariate p = 17, (d,l) = (6,2), 16 + 4 primes) on its shadow
+    ring m = 1423, T = 4 elements with ties: every output ciphertext bit-exact vs the oracle."""
+    from oracle import circuits
+    Tp = pair("c5s")
+    P = Tp.P
+    ints = Tp.ctx.ints_per_ct
+    rng = np.random.default_rng(90)
+    T = 4
+    W = [_words(P, rng, ints) for _ in range(T)]
+    for j in range(0, ints, 7):                                # ties across all elements
+        for t in range(1, T):
+            W[t][j] = W[0][j]
+    elems = [Tp.ctx.encrypt(Tp.keys, np.array([W[t]], dtype=np.uint64), SEED_ENC, ct_index0=800 + t)
+             for t in range(T)]
+    outs = Tp.ctx.sort(Tp.keys, elems)
+    got = [Tp.ctx.decrypt(Tp.keys, o)[0] for o in outs]
+    for j in range(ints):
+        assert [int(got[k][j]) for k in range(T)] == sorted(W[t][j] for t in range(T))
+    ev = circuits.OracleEval(P, Tp.okeys)
+    oo = circuits.sort_rank(ev, [Tp.oracle_ct(W[t], 800 + t) for t in range(T)], P.circuit, P.d, P.l, ints)
+    for k in range(T):
+        assert np.array_equal(to_u64(outs[k])[0], Tp.ct_eval(oo[k]))
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_ntt_c4_c5(pair, cfg):
+    """a1/a2 at M = 2^17 with prime m (C4: m = 34511, C5: m = 41761): two sampled limbs of the
+    forward transform vs naive evaluation; the inverse (reduction mod Phi_m folded into pass C)
+    recovers every limb."""
+    T = pair(cfg)
+    P = T.P
+    rng = np.random.default_rng(72)
+    nl = P.L1 + P.K
+    coef = np.stack([rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.moduli])[None]
+    ev = to_u64(T.ctx.ntt_fwd(from_u64(coef, T.ctx.device)))
+    for i in (0, nl - 1):
+        assert np.array_equal(ev[0, i], P.ring.to_eval(coef[0, i], P.omega[i], P.moduli[i]))
+    assert np.array_equal(to_u64(T.ctx.ntt_inv(from_u64(ev, T.ctx.device))), coef)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_compare_c4_c5_decrypts(pair, cfg):
+    """C4 / C5 rings at full size: one batch of 2 compares (16-digit extraction at D = 17 for C4;
+    lifts of 10 / 11 sources) decrypts to [a < b] in every block."""
+    T = pair(cfg)
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    rng = np.random.default_rng(73)
+    A, B = [], []
+    for _ in range(2):
+        a, b = mixed_pairs(P, rng, ints)
+        A.append(a)
+        B.append(b)
+    ca = T.ctx.encrypt(T.keys, np.array(A, dtype=np.uint64), SEED_ENC, ct_index0=0)
+    cb = T.ctx.encrypt(T.keys, np.array(B, dtype=np.uint64), SEED_ENC, ct_index0=2)
+    bits = T.ctx.decrypt(T.keys, T.ctx.compare_lt(T.keys, ca, cb), as_bits=True)
+    for i in range(2):
+        assert list(bits[i]) == [int(x < y) for x, y in zip(A[i], B[i])]
+
+
+def _digest(E):
+    return hashlib.sha256(np.ascontiguousarray(E, dtype="<u8").tobytes()).hexdigest()
+
+
+@pytest.mark.slow
+def test_full_size_c2_compare_matches_oracle_digest(pair):
+    """The headline workload's compare_lt (C2, n = 30940, 11 + 4 primes) on one pair: the
+    evaluation-form ciphertext's SHA-256 equals the oracle's (tests/golden/c2_compare_digest.json,
+    written by tools/oracle/c2_compare_digest.py from oracle/ and inputs/ only; same seeds, same
+    words).  Exercises data-dependent encode, every key switch and the R16 schedule at
+    full size."""
+    from inputs import word_pairs
+    path = os.path.join(ROOT, "tests", "golden", "c2_compare_digest.json")
+    if not os.path.exists(path):
+        pytest.skip("golden digest not generated yet")
+    g = json.load(open(path))
+    T = pair("c2")
+    P = T.P
+    ints = T.ctx.ints_per_ct
+    a, b = word_pairs(np.random.default_rng(g["seeds"]["words"]), ints, P.base, P.d * P.l)
+    ca = T.ctx.encrypt(T.keys, np.array([a], dtype=np.uint64), g["seeds"]["enc"], ct_index0=g["seeds"]["ct_index"][0])
+    cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), g["seeds"]["enc"], ct_index0=g["seeds"]["ct_index"][1])
+    lt = T.ctx.compare_lt(T.keys, ca, cb)
+    bits = [int(x) for x in T.ctx.decrypt(T.keys, lt, as_bits=True)[0]]
+    assert bits == [int(x < y) for x, y in zip(a, b)]
+    E = to_u64(lt)[0]
+    assert list(E.shape) == g["shape"]
+    assert [int(x) for x in E[:, :, :4].reshape(-1)] == g["first4_per_limb"]
+    assert _digest(E) == g["sha256"]

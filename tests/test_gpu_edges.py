@@ -101,3 +101,27 @@ def test_ragged_batch_and_unequal_levels():
         bits = ctx.decrypt(keys, ctx.compare_lt(keys, ca, cb), as_bits=True)
         for i in range(3):
             assert [int(x) for x in bits[i]] == [int(x < y) for x, y in zip(A[i], B[i])]
+
+
+def test_bad_output_views_are_rejected_before_any_work():
+    """an output view that is too small, at the wrong level or null is BC_E_ARG (1) /
+    BC_E_LEVEL (4) from the C ABI, validated before anything is enqueued (the output is untouched)"""
+    import torch
+    import paper_2407_07308_b200 as bc
+    ctx, keys = ctx_keys("c1m")
+    lib = bc._lib
+    ca = ctx.encrypt(keys, np.zeros((2, ctx.ints_per_ct), dtype=np.uint64), SEED_ENC)
+    lvl = ctx.out_level(ca.shape[2], 0)
+    w, wb = ctx._wsargs(None)
+    st = bc._stream()
+    small = ctx.ct_empty(1, lvl).fill_(7)
+    wrong = ctx.ct_empty(2, lvl + 1).fill_(7)
+    v = ctx.view(ca)
+    assert lib.bc_compare_lt(ctx._h, keys.keys, v, v, ctx.view(small), w, wb, st) == 1
+    assert lib.bc_compare_lt(ctx._h, keys.keys, v, v, ctx.view(wrong), w, wb, st) == 4
+    assert lib.bc_compare_lt(ctx._h, keys.keys, v, v, bc.bc_ct(None, 2, lvl), w, wb, st) == 1
+    assert lib.bc_mul(ctx._h, keys.keys, v, v, ctx.view(small), w, wb, st) in (1, 4)
+    assert lib.bc_rotate(ctx._h, keys.keys, v, 1, ctx.view(small), w, wb, st) in (1, 4)
+    assert lib.bc_automorph(ctx._h, v, 2, ctx.view(small), st) in (1, 4)
+    torch.cuda.synchronize()
+    assert bool((small == 7).all()) and bool((wrong == 7).all())

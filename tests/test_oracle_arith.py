@@ -166,3 +166,15 @@ def test_vec_helpers():
     b = rng.integers(0, q, size=1000, dtype=np.uint64)
     got = _c.vec_mulmod(a, b, q)
     assert [int(x) for x in got] == [int(x) * int(y) % q for x, y in zip(a, b)]
+
+
+@pytest.mark.parametrize("m", [33, 45, 91, 211])
+def test_reduce_int_matches_sympy(m):
+    """Ring.reduce_int (integer polynomial mod Phi_m over Z, any length) = sympy's remainder."""
+    x = sympy.symbols("x")
+    R = cyclo.Ring(m)
+    rng = np.random.default_rng(m)
+    c = [int(v) for v in rng.integers(-50, 50, size=3 * m)]
+    r = sympy.Poly(c[::-1], x).rem(sympy.cyclotomic_poly(m, x, polys=True))
+    want = [int(v) for v in r.all_coeffs()[::-1]]
+    assert R.reduce_int(c) == want + [0] * (R.n - len(want))
