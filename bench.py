@@ -108,35 +108,71 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-# CPU oracle baseline (bounded sample, extrapolated by the oracle's own operation count)
+# CPU oracle baseline: a bounded sample of the SAME workload, timed as it stands
 # ------------------------------------------------------------------------------------------
-def oracle_sample(cfg, budget_s=20.0):
-    """Time the oracle's dominant primitive (schoolbook product mod (q, Phi_m) at the full ring)
-    and extrapolate a compare_lt by counting the oracle's ring products for the schedule."""
-    from oracle import bgv, circuits
-    from oracle.cyclo import Ring
-    import oracle._c as oc
-    P = bgv.Params(cfg)
-    rng = np.random.default_rng(1)
-    q = P.moduli[0]
-    a = rng.integers(0, q, size=P.n, dtype=np.uint64)
-    b = rng.integers(0, q, size=P.n, dtype=np.uint64)
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        P.ring.mul(a, b, q)
-        reps += 1
-        if time.perf_counter() - t0 > budget_s / 2 or reps >= 8:
-            break
-    t_mul = (time.perf_counter() - t0) / reps
-    count = circuits_product_count(P)
-    cores = os.cpu_count()
+def host_info():
+    """CPU model, logical cores, clock and the threads the oracle's OpenMP helper uses."""
+    model, mhz = None, []
     try:
-        import ctypes
-        cores = int(os.environ.get("OMP_NUM_THREADS", cores))
-    except Exception:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and model is None:
+                    model = line.split(":", 1)[1].strip()
+                elif line.startswith("cpu MHz"):
+                    mhz.append(float(line.split(":", 1)[1]))
+    except OSError:
         pass
-    return t_mul, count, reps, cores
+    n = os.cpu_count() or 1
+    threads = int(os.environ.get("OMP_NUM_THREADS", n))
+    return {"cpu_model": model, "nproc": n, "cpu_mhz": float(np.median(mhz)) if mhz else None,
+            "omp_threads": threads}
+
+
+class OracleSample:
+    """One real operation of the compare_lt schedule, at the benchmarked configuration's full size:
+    the oracle's R15 product (tensor, ModUp with exact big-integer CRT lifts, key inner product,
+    fused ModDown + modulus switch) of two full-size ciphertexts at level 2 -- the last product of
+    the schedule.  Ring products dominate the oracle (schoolbook, O(n^2)); the sample's count is
+    checked against the oracle's own call counter, and the compare_lt's count comes from running
+    the R16 schedule on a cost evaluator (circuits_product_count, checked against the counter on
+    C2's shadow ring in tests/test_bench_host.py).  The compare time is extrapolated as
+    (sample time / sample products) x compare products and labelled as such."""
+
+    def __init__(self, cfg, level=2):
+        from oracle import bgv
+        self.bgv = bgv
+        P = bgv.Params(cfg)
+        self.P = P
+        t0 = time.perf_counter()
+        self.K = bgv.keygen(P, SEED_KEYS, (), relin=True)
+        z = np.zeros(P.n, dtype=np.int64)                  # the product's cost does not depend on the message
+        self.a = bgv.modswitch_to(P, bgv.encrypt(P, self.K, z, SEED_ENC, 0), level)
+        self.b = bgv.modswitch_to(P, bgv.encrypt(P, self.K, z, SEED_ENC, 1), level)
+        self.setup_s = time.perf_counter() - t0
+        self.level = level
+        ndig = sum(1 for j in range(P.dnum) if P.digit_group(j, level))
+        self.products = 4 * level + 2 * ndig * (level + P.K)
+        self.compare_products = circuits_product_count(P)
+
+    def run(self):
+        import oracle._c as oc
+        c0 = oc.CALLS["ring_mul"]
+        t0 = time.perf_counter()
+        self.bgv.mul(self.P, self.K, self.a, self.b)
+        dt = time.perf_counter() - t0
+        assert oc.CALLS["ring_mul"] - c0 == self.products, "oracle product count changed"
+        return dt
+
+    def describe(self, t):
+        P = self.P
+        return ("oracle R15 product (tensor + ModUp/KIP + fused ModDown/modswitch, big-integer CRT lifts) of two "
+                "full-size ciphertexts at level %d (n=%d, %d+%d primes): %d schoolbook ring products, %.2f s; "
+                "= %.5f of one compare_lt (%d ring products by the oracle's schedule)"
+                % (self.level, P.n, P.L1, P.K, self.products, t, self.products / self.compare_products,
+                   self.compare_products))
+
+    def extrapolated_compare_s(self, t):
+        return t / self.products * self.compare_products
 
 
 def circuits_product_count(P):
@@ -223,35 +259,56 @@ def circuits_product_count(P):
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only; other ranks exit).
+    Each step runs one real operation of the compare_lt workload at full size (OracleSample); the
+    line reports the measured step time and the fraction of a compare_lt it covers, so
+    value = units_per_step / step time with units = int-compares (fraction x ints per ciphertext)."""
     if rank != 0:
         return
-    steps = []
-    info = None
+    S = OracleSample(cfg)
+    times = []
     for i in range(args.warmup + args.steps):
-        t_mul, count, reps, cores = oracle_sample(cfg, budget_s=6.0)
+        t = S.run()
         if i >= args.warmup:
-            steps.append(t_mul * count)
-        info = (t_mul, count, reps, cores)
-    t_cmp = float(np.mean(steps))
-    from oracle import bgv
-    P = bgv.Params(cfg)
-    ints = P.ints_per_ct if P.n < 5000 else None
-    if ints is None:
-        from oracle.nt import mult_order
-        ints = (P.n // mult_order(P.p, P.m)) // P.l
-    val = ints / t_cmp
+            times.append(t)
+    t_step = float(np.mean(times))
+    ints = compare_ints(cfg, S.P)
+    units = ints * S.products / S.compare_products
+    val = units / t_step
+    hi = host_info()
     line = {"metric": METRIC, "value": val, "unit": "int-compares/s", "impl": "reference",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t_cmp,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic", "config": {"workload": cfg["name"], "pairs_per_step": 1,
-                                           "note": "oracle compare_lt extrapolated from timed primitives"},
-            "cpu_baseline": {"value": val, "unit": "int-compares/s", "cores": info[3], "kind": "oracle",
-                             "sample": "%d schoolbook ring products mod (q, Phi_m) at n=%d timed (%.3f s each) "
-                                       "x %d products per compare_lt (oracle op count)" %
-                                       (info[2], P.n, info[0], info[1])},
+            "data": "synthetic", "config": product_config(args, cfg, ints),
+            "units_per_step": units,
+            "extrapolated_ms_per_ct_compare": 1000 * S.extrapolated_compare_s(t_step),
+            "setup_s": S.setup_s,
+            "cpu_baseline": dict({"value": val, "unit": "int-compares/s", "cores": hi["omp_threads"],
+                                  "kind": "oracle", "sample": S.describe(t_step)}, **hi),
             "e2e": {"value": val, "unit": "int-compares/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def compare_ints(cfg, P):
+    if P.n < 5000:
+        return P.ints_per_ct
+    from oracle.nt import mult_order
+    return (P.n // mult_order(P.p, P.m)) // P.l
+
+
+def product_config(args, cfg, ints, B=None):
+    """the config object of the product arm's line (the reference arm prints the same one)"""
+    B = B if B is not None else (args.pairs or 1000)
+    return {"workload": "C2: Table 3 p5 univariate (p=13, m=30941, (d,l)=(4,6), 64-bit words), "
+                        "%d ciphertext pairs per GPU" % B if args.config == "c2" else args.config,
+            "params": args.config, "pairs_per_gpu": B, "ints_per_ct": ints,
+            "n_cipher": cfg["n_cipher"], "n_special": cfg["n_special"], "alpha": cfg["alpha"],
+            "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (2 * B * 2 * cfg["n_cipher"] * _n_of(cfg) * 8 / 1e9)}
+
+
+def _n_of(cfg):
+    from oracle.nt import euler_phi
+    return euler_phi(int(cfg["m"]))
 
 
 # ------------------------------------------------------------------------------------------
@@ -390,20 +447,17 @@ def main():
     roof = roofline(ctx, bc, live, ms_local * args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        t_mul, count, reps, cores = oracle_sample(cfg)
-        t_cmp = t_mul * count
-        cpu = {"value": ints / t_cmp, "unit": "int-compares/s", "cores": cores, "kind": "oracle",
-               "sample": "%d schoolbook ring products mod (q, Phi_m) at n=%d timed (%.3f s each) x %d products "
-                         "per compare_lt (oracle op count); extrapolated" % (reps, ctx.n, t_mul, count)}
+        S = OracleSample(cfg)
+        t = S.run()
+        units = ints * S.products / S.compare_products
+        cpu = dict({"value": units / t, "unit": "int-compares/s", "cores": host_info()["omp_threads"],
+                    "kind": "oracle", "sample": S.describe(t),
+                    "extrapolated_ms_per_ct_compare": 1000 * S.extrapolated_compare_s(t)}, **host_info())
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "int-compares/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-                "config": {"workload": "C2: Table 3 p5 univariate (p=13, m=30941, (d,l)=(4,6), 64-bit words), "
-                                       "%d ciphertext pairs per GPU" % B if args.config == "c2" else args.config,
-                           "params": args.config, "pairs_per_gpu": B, "ints_per_ct": ints,
-                           "n_cipher": ctx.n_cipher, "n_special": ctx.n_special, "alpha": cfg["alpha"],
-                           "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (2 * ca.numel() * 8 / 1e9)},
+                "config": product_config(args, cfg, ints, B),
                 "ms_per_ct_compare": ms / B, "slot_compares_per_s": total_pairs * ctx.S / (ms / 1000.0),
                 "verified": verified, "gpu_launches": launches, "clocks": clocks,
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu}
