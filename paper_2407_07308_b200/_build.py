@@ -9,7 +9,7 @@ OUT = os.path.join(HERE, "libboostcom.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-O3"]
-SOURCES = ["kernels.cu", "ntt2.cu", "ntt3.cu", "engine.cu", "keys.cu", "capi.cu", "compact.cu", "host_math.cpp"]
+SOURCES = ["kernels.cu", "ntt2.cu", "ntt3.cu", "ntt4.cu", "engine.cu", "keys.cu", "capi.cu", "compact.cu", "host_math.cpp"]
 
 
 def _srcs():

@@ -37,6 +37,8 @@ int bc_tune(const char *key, int64_t value) {
     if (!strcmp(key, "f64_elem")) { g_f64_elem = (int)value; return 0; }
     if (!strcmp(key, "phi_conv")) { g_phi_conv = (int)value; return 0; }
     if (!strcmp(key, "ntt_dbg")) { g_ntt_dbg = (int)value; return 0; }
+    if (!strcmp(key, "nttc_variant")) { g_nttc_variant = (int)value; return 0; }
+    if (!strcmp(key, "nttc_clusters")) { g_nttc_clusters = (int)value; return g_nttc_active; }
     if (!strcmp(key, "ntt_group_bytes")) { g_ntt_group_bytes = (uint64_t)std::max<int64_t>(value, 1 << 20); return 0; }
     return -1;
 }

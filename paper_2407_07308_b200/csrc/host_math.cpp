@@ -243,7 +243,7 @@ std::vector<int64_t> GF::mul(const std::vector<int64_t> &a, const std::vector<in
     r.resize(D);
     return r;
 }
-std::vector<int64_t> GF::pow(std::vector<int64_t> a, uint64_t e) const {
+std::vector<int64_t> GF::pow(std::vector<int64_t> a, unsigned __int128 e) const {
     std::vector<int64_t> r = one();
     while (e) {
         if (e & 1) r = mul(r, a);
@@ -253,7 +253,8 @@ std::vector<int64_t> GF::pow(std::vector<int64_t> a, uint64_t e) const {
     return r;
 }
 
-static uint64_t ipow(uint64_t b, int e) { uint64_t r = 1; while (e--) r *= b; return r; }
+// p^e exactly (p^D reaches 17^18 > 2^64 on the C5 shadow ring: 128-bit)
+static unsigned __int128 ipow(uint64_t b, int e) { unsigned __int128 r = 1; while (e--) r *= b; return r; }
 
 // solve V x = y over F_p (V: D x D, column-major list of columns)
 static std::vector<int64_t> solve_fp(std::vector<std::vector<int64_t>> A, std::vector<int64_t> y, int64_t p) {
@@ -290,9 +291,9 @@ bool SlotAlgebra::build(int64_t p_, uint32_t m_, const std::vector<int64_t> &phi
         if (D == 1 || irreducible(G, p)) { gf.G = G; break; }
     }
     // zeta = beta^((p^D-1)/m) for the first beta (v = 1, 2, ...) giving exact order m
-    uint64_t pD = ipow((uint64_t)p, (int)D);
+    const unsigned __int128 pD = ipow((uint64_t)p, (int)D);
     std::vector<uint64_t> mf = prime_factors(m);
-    for (uint64_t v = 1; v < pD; ++v) {
+    for (uint64_t v = 1; (unsigned __int128)v < pD; ++v) {
         std::vector<int64_t> b(D, 0);
         uint64_t x = v;
         for (uint32_t i = 0; i < D; ++i) { b[i] = (int64_t)(x % p); x /= p; }

@@ -40,7 +40,7 @@ struct GF {
     int D;
     Poly G;  // monic, degree D
     std::vector<int64_t> mul(const std::vector<int64_t> &a, const std::vector<int64_t> &b) const;
-    std::vector<int64_t> pow(std::vector<int64_t> a, uint64_t e) const;
+    std::vector<int64_t> pow(std::vector<int64_t> a, unsigned __int128 e) const;
     std::vector<int64_t> one() const;
     bool is_one(const std::vector<int64_t> &a) const;
 };

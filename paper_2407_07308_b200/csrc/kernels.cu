@@ -346,7 +346,7 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     }
     lm.npoly = npoly;
     // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
-    const bool vf = (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T);
+    const bool vf = (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T);   // 20: fused cluster kernel (below)
     // composite m on the binary64 path: Barrett reduction mod Phi_m (needs a second M-word slot per job)
     const bool barrett = inv && vf && !T.prime_m && T.tb != nullptr;
     const uint64_t chunk = ntt_group_jobs(T, jobs, barrett);
@@ -354,7 +354,9 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);
-        if (v2) {
+        if (g_ntt_impl == 20 && nttf_supported(T) && nttc_supported(T)) {
+            nttc_run(T, in, out, lm, in_pstride, out_pstride, j0, nj, inv, st);
+        } else if (v2) {
             const bool direct = vf && inv && T.prime_m;      // pass C writes A_t - A_{m-1} itself
             if (vf) {
                 nttf_run(T, in, out, lm, in_pstride, out_pstride, scratch, j0, nj, inv, st,

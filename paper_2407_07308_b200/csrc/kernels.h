@@ -182,6 +182,12 @@ int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: pos
 // corner_buf (prime m, inverse): nj words; pass C then writes the reduction mod Phi_m directly (no k_reduce_prime)
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf = nullptr);
+// fused thread-block-cluster transform (ntt4.cu): one kernel per batch, the size-M grid in distributed
+// shared memory, no scratch; prime m only (the inverse writes the reduction mod Phi_m)
+bool nttc_supported(const NttTables &T);
+extern int g_nttc_clusters, g_nttc_active, g_nttc_variant;
+void nttc_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+              uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
 // composite m: out (poly/limb layout) = A mod Phi_m for the A_t (t < m) the inverse left in the scr1 slots
 // (stride B.Mslot), by the two Barrett convolutions of table set B (scr2: slots of B.M words)
 void nttf_barrett(const NttTables &B, uint64_t *out, LimbMap lm, uint64_t out_ps, uint64_t *scr1, uint64_t *scr2,
@@ -195,6 +201,7 @@ extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when t
 extern uint64_t g_vec_chunk;
 extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)
 int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);
-extern int g_ntt_impl;   // 0 = register passes (E=8) when supported, 1 = radix-2 passes, 2 = register passes E=16
+extern int g_ntt_impl;   // 0 = binary64 three-pass kernels (ntt3.cu) where supported; 1 = radix-2 passes;
+                         // 2 = integer register passes; 10-19 = binary64 three-pass shapes; 20 = fused cluster kernel (ntt4.cu)
 
 }  // namespace bc

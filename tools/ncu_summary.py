@@ -36,6 +36,8 @@ def summarise(rep, limb_transforms):
             "duration_us": (f(d.get("gpu__time_duration.sum", "0")) or 0) * U.get("gpu__time_duration.sum", 1e-3),
             "dram_read_MB": rd / 1e6, "dram_write_MB": wr / 1e6,
             "issue_active_pct": f(d.get("sm__inst_issued.avg.pct_of_peak_sustained_active", "")),
+            "pipe_fp64_cycles_pct": f(d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "")),
+            "inst_pipe_fp64_pct": f(d.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "")),
             "pipe_fma_pct": f(d.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "")),
             "pipe_alu_pct": f(d.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "")),
             "warps_active_pct": f(d.get("sm__warps_active.avg.pct_of_peak_sustained_active", "")),

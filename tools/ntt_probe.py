@@ -1,4 +1,5 @@
-"""The bench roofline probe launch (64 polys x 11 limbs forward Bluestein at C2), for ncu."""
+"""The bench roofline probe launch (64 polys x 11 limbs forward Bluestein at C2), for ncu.
+NTT_IMPL selects the kernel family (0 = three binary64 passes, 20 = fused cluster kernel)."""
 import os
 import sys
 
@@ -7,5 +8,6 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2407_07308_b200 as bc  # noqa: E402
 
-ctx = bc.Context(bc.load_params("c2"))
+bc.set_ntt_impl(int(os.environ.get("NTT_IMPL", "0")))
+ctx = bc.Context(bc.load_params(os.environ.get("NTT_CFG", "c2")))
 print(bc.profile_ntt(ctx))
