@@ -28,7 +28,9 @@ class Params:
         self.name = cfg.get("name", "")
         self.p = int(cfg["p"])
         self.m = int(cfg["m"])
-        self.circuit = cfg.get("circuit", "U")
+        self.schedule = cfg.get("schedule", "r16")     # digit-circuit reading: R16 or R23
+        assert self.schedule in ("r16", "r23")
+        self.circuit = cfg.get("circuit", "U") + (":r23" if self.schedule == "r23" else "")
         self.d = int(cfg["d"])
         self.l = int(cfg["l"])
         self.ring = Ring(self.m)

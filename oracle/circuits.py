@@ -210,6 +210,182 @@ def bivariate_lt_eq(ev, x, y, p):
 
 
 # ----------------------------------------------------------------------------------------
+# R23: baby-step / giant-step digit circuits (§8(f) f2; "2p-6 (Bivariate case) and
+# sqrt(p-3) + O(log p) (Univariate case)", the paper's counts are asymptotic: DESIGN.md R23)
+# ----------------------------------------------------------------------------------------
+class CountValue:
+    """stand-in ciphertext for counting products and depth (no arithmetic)"""
+
+    def __init__(self, depth=0):
+        self.depth = depth
+
+
+class CountEval:
+    """evaluator that only counts ct x ct products and tracks the multiplicative depth"""
+
+    def __init__(self, p):
+        self.p = p
+        self.counts = {"mul": 0}
+
+    def mul(self, a, b):
+        self.counts["mul"] += 1
+        return CountValue(max(a.depth, b.depth) + 1)
+
+    def add(self, a, b):
+        return CountValue(max(a.depth, b.depth))
+
+    def scalar(self, a, c):
+        return CountValue(a.depth)
+
+    def add_const(self, a, c):
+        return CountValue(a.depth)
+
+
+def _largest_pow2_below(j):
+    return 1 << ((j - 1).bit_length() - 1)
+
+
+class Giant:
+    """giant powers G_a = B^(a k) of a base power B = x^k (a >= 1): G_1 = B, G_a = G_a' * G_(a - a'),
+    a' = the largest power of two < a (the R16 power rule on multiples of k)"""
+
+    def __init__(self, ev, base):
+        self.ev = ev
+        self.g = {1: base}
+
+    def __call__(self, a):
+        if a not in self.g:
+            a1 = _largest_pow2_below(a)
+            self.g[a] = vmul(self.ev, self(a1), self(a - a1))
+        return self.g[a]
+
+
+def univariate_lt_eq_r23(ev, z, p, k=None):
+    """R23 univariate: W = z^2, e = (p-3)/2, E = e + 1, g(W) = sum_i c_(2i+1) W^i (as R16).
+    Baby powers W^2..W^k (power rule), giant powers G_a = W^(a k), a = 2..A-1, A = ceil((e+1)/k);
+    chunks B_a = sum_(b<k) c_(2(ak+b)+1) W^b; g = B_0 + sum_(a=1)^(A-1) G_a B_a (a ascending);
+    W^E = W^E (E <= k), G_a (E = a k) or G_a W^b (E = a k + b); LT = z g + ((p+1)/2) W^E,
+    EQ = 1 - W^E.  k = r23_univariate_k(p) unless given."""
+    c = lt_univariate_coeffs(p)
+    e = (p - 3) // 2
+    E = e + 1
+    assert all(c[2 * i] == 0 for i in range(1, (p - 1) // 2)) and c[0] == 0
+    g = [c[2 * i + 1] for i in range(e + 1)]
+    top = c[p - 1]
+    if k is None:
+        k = r23_univariate_k(p)
+    W = vmul(ev, z, z)
+    pw = Powers(ev, W)
+    for j in range(2, k + 1):
+        pw(j)
+    A = -(-(e + 1) // k)
+    G = Giant(ev, pw(k))
+    for a in range(2, A):
+        G(a)
+
+    def chunk(a):
+        terms = [(g[a * k + b], pw(b)) for b in range(1, k) if a * k + b <= e]
+        return lincomb(ev, terms, g[a * k])
+
+    gval = chunk(0)
+    for a in range(1, A):
+        B = chunk(a)
+        if is_const(B) and B == 0:
+            continue
+        gval = vadd(ev, gval, vmul(ev, G(a), B))
+    if E <= k:
+        WE = pw(E)
+    else:
+        a, b = divmod(E, k)
+        WE = G(a) if b == 0 else vmul(ev, G(a), pw(b))
+    lt = vadd(ev, vmul(ev, z, gval), vmul(ev, WE, top))
+    eq = vadd(ev, vmul(ev, WE, -1), 1)
+    return lt, eq
+
+
+def bivariate_lt_eq_r23(ev, x, y, p, k=None):
+    """R23 bivariate: Z = x - y, Z^2..Z^(p-1) by the power rule (EQ = 1 - Z^(p-1) is free);
+    LT = sum_(j=1)^(p-1) Y^j R_j(Z) (as R16) evaluated baby-step / giant-step in Y: j = a k + b,
+    baby powers Y^2..Y^k (power rule), giant powers G_a = Y^(a k), a = 2..A-1, A = floor((p-1)/k) + 1;
+    I_a = sum_(b<k, 1<=ak+b<=p-1) Y^b R_(ak+b)(Z) (b ascending; the b = 0 term is R_(ak) itself);
+    LT = I_0 + sum_(a=1)^(A-1) G_a I_a (a ascending).  k = 1 is the R16 tree.  k = r23_bivariate_k(p)
+    unless given."""
+    c = lt_bivariate_coeffs(p)
+    assert all(c[0][i] == 0 for i in range(len(c[0]))), "LT_B has a Y^0 term"
+    if k is None:
+        k = r23_bivariate_k(p)
+    Z = vadd(ev, x, vmul(ev, y, -1))
+    zp = Powers(ev, Z)
+    for j in range(2, p):
+        zp(j)
+    yp = Powers(ev, y)
+    for j in range(2, k + 1):
+        yp(j)
+    A = (p - 1) // k + 1
+    G = Giant(ev, yp(k))
+    for a in range(2, A):
+        G(a)
+
+    def R(j):
+        return lincomb(ev, [(c[j][i], zp(i)) for i in range(1, p)], c[j][0])
+
+    def inner(a):
+        acc = None
+        for b in range(k):
+            j = a * k + b
+            if j < 1 or j > p - 1:
+                continue
+            r = R(j)
+            if is_const(r) and r == 0:
+                continue
+            t = r if b == 0 else vmul(ev, yp(b), r)
+            acc = t if acc is None else vadd(ev, acc, t)
+        return 0 if acc is None else acc
+
+    lt = inner(0)
+    for a in range(1, A):
+        I = inner(a)
+        if is_const(I) and I == 0:
+            continue
+        t = vmul(ev, G(a), I)
+        lt = t if (is_const(lt) and lt == 0) else vadd(ev, lt, t)
+    eq = vadd(ev, vmul(ev, zp(p - 1), -1), 1)
+    return lt, eq
+
+
+def _r23_cost(fn, p, k):
+    ev = CountEval(p)
+    args = (CountValue(),) if fn is univariate_lt_eq_r23 else (CountValue(), CountValue())
+    lt, eq = fn(ev, *args, p, k=k)
+    d = max(getattr(lt, "depth", 0), getattr(eq, "depth", 0))
+    return ev.counts["mul"], d
+
+
+def _r16_depth(kind, p):
+    ev = CountEval(p)
+    if kind == "U":
+        lt, eq = univariate_lt_eq(ev, CountValue(), p)
+    else:
+        lt, eq = bivariate_lt_eq(ev, CountValue(), CountValue(), p)
+    return max(getattr(lt, "depth", 0), getattr(eq, "depth", 0))
+
+
+def r23_univariate_k(p):
+    """R23: among the baby-step sizes k in [1, (p-1)/2] whose circuit is no deeper than R16's (the
+    modulus chains are sized for that depth), the one with the fewest products, then the smallest k"""
+    cap = _r16_depth("U", p)
+    ks = [k for k in range(1, max((p - 1) // 2, 1) + 1) if _r23_cost(univariate_lt_eq_r23, p, k)[1] <= cap]
+    return min(ks, key=lambda k: (_r23_cost(univariate_lt_eq_r23, p, k)[0], k))
+
+
+def r23_bivariate_k(p):
+    """R23: among k in [1, p-1] with depth <= R16's, the fewest products, then the smallest k"""
+    cap = _r16_depth("B", p)
+    ks = [k for k in range(1, p) if _r23_cost(bivariate_lt_eq_r23, p, k)[1] <= cap]
+    return min(ks, key=lambda k: (_r23_cost(bivariate_lt_eq_r23, p, k)[0], k))
+
+
+# ----------------------------------------------------------------------------------------
 # extraction (a8), lexicographic combination (a9), compare
 # ----------------------------------------------------------------------------------------
 def kappa_slots(alg, i, k):
@@ -280,16 +456,20 @@ def lex_slots(ev, lt, eq, l, ints):
 
 
 def compare(ev, a, b, circuit, d, l, ints):
-    """(LT, EQ) of the words packed in a and b (block slot 0 holds the result)."""
+    """(LT, EQ) of the words packed in a and b (block slot 0 holds the result).  circuit: "U" / "B"
+    (R16 digit circuits) or "U:r23" / "B:r23" (R23)."""
     p = ev.p
-    if circuit == "U":
+    r23 = circuit.endswith(":r23")          # R23 digit circuits (params "schedule": "r23"), else R16
+    if circuit[0] == "U":
         z = ev.add(a, ev.scalar(b, -1))
         digs = extract_digits(ev, z, d)
-        res = [univariate_lt_eq(ev, x, p) for x in digs]
+        f = univariate_lt_eq_r23 if r23 else univariate_lt_eq
+        res = [f(ev, x, p) for x in digs]
     else:
         da = extract_digits(ev, a, d)
         db = extract_digits(ev, b, d)
-        res = [bivariate_lt_eq(ev, x, y, p) for x, y in zip(da, db)]
+        f = bivariate_lt_eq_r23 if r23 else bivariate_lt_eq
+        res = [f(ev, x, y, p) for x, y in zip(da, db)]
     lt, eq = lex_tree(ev, [r[0] for r in res], [r[1] for r in res])
     if l > 1:
         lt, eq = lex_slots(ev, lt, eq, l, ints)

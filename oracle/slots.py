@@ -389,7 +389,7 @@ class SlotAlgebra:
 # ----------------------------------------------------------------------------------------
 def digit_base(p, circuit):
     """Bivariate digits in [0, p); univariate digits in [0, (p-1)/2] i.e. base (p+1)/2."""
-    return p if circuit == "B" else (p + 1) // 2
+    return p if circuit[0] == "B" else (p + 1) // 2
 
 
 def int_to_digits(x, base, count):

@@ -64,7 +64,7 @@ class _FpAlg:
         self.gf = slots.GF(p, [0, 1])
 
 
-def _digit_run(p, kind):
+def _digit_run(p, kind, r23=False, k=None):
     """run the schedule on one F_p value per slot covering every digit pair."""
     h = (p - 1) // 2 if kind == "U" else p - 1
     A = _FpAlg(p, (h + 1) ** 2)       # F_p itself (D = 1): one digit pair per slot
@@ -80,13 +80,16 @@ def _digit_run(p, kind):
             X[s, 0], Y[s, 0] = x, y
         ev.counts["mul"] = 0
         if kind == "U":
-            lt, eq = circuits.univariate_lt_eq(ev, circuits.PlainValue((X - Y) % p), p)
+            z = circuits.PlainValue((X - Y) % p)
+            lt, eq = circuits.univariate_lt_eq_r23(ev, z, p, k) if r23 else circuits.univariate_lt_eq(ev, z, p)
+        elif r23:
+            lt, eq = circuits.bivariate_lt_eq_r23(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p, k)
         else:
             lt, eq = circuits.bivariate_lt_eq(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p)
         for s, (x, y) in enumerate(chunk):
             res.append((x, y, int(lt.v[s, 0]), int(eq.v[s, 0])))
             assert not lt.v[s, 1:].any() and not eq.v[s, 1:].any()
-    return res, ev.counts["mul"], lt.depth
+    return res, ev.counts["mul"], max(lt.depth, eq.depth if hasattr(eq, "depth") else 0)
 
 
 @pytest.mark.parametrize("p", PRIMES)
@@ -105,6 +108,46 @@ def test_bivariate_schedule_truth_and_3p_minus_5(p):
     for x, y, lt, eq in res:
         assert (lt, eq) == (int(x < y), int(x == y))
     assert mults == 3 * p - 5      # P:71 [Tan]: 3p-5 non-scalar multiplications (with EQ)
+
+
+@pytest.mark.parametrize("p", PRIMES)
+@pytest.mark.parametrize("kind", ["U", "B"])
+def test_r23_schedule_truth_tables(p, kind):
+    """R23 (f2): the baby-step / giant-step digit circuits give [x < y], [x = y] on every digit
+    pair at every baby-step size k, with no more products and no more depth than R16 at the k the
+    rule selects."""
+    kmax = (p - 1) // 2 if kind == "U" else p - 1
+    ks = sorted({1, 2, max(kmax, 1), (circuits.r23_univariate_k(p) if kind == "U" else circuits.r23_bivariate_k(p))})
+    r16 = _digit_run(p, kind)
+    for k in ks:
+        if k > max(kmax, 1):
+            continue
+        res, mults, depth = _digit_run(p, kind, r23=True, k=k)
+        for x, y, lt, eq in res:
+            assert (lt, eq) == (int(x < y), int(x == y)), (p, kind, k, x, y)
+        if k == (circuits.r23_univariate_k(p) if kind == "U" else circuits.r23_bivariate_k(p)):
+            assert mults <= r16[1] and depth <= r16[2]
+
+
+def test_r23_product_counts_closed_form():
+    """R23 product counts against the hand count of the schedule (R23):
+    U, p = 13, k = 3: W; W^2, W^3; (A = 2: no giant beyond W^3); W^3 B_1; W^6 = W^3 W^3; z g -> 6
+      (R16: 7);
+    B, p = 31, k = 4: Z^2..Z^30 (29); Y^2..Y^4 (3); G_2..G_7 = Y^8..Y^28 (6); I_0..I_6: 3 each (21),
+      I_7 (j = 29, 30): 2; G_a I_a, a = 1..7 (7) -> 68 at depth 7;
+    B, p = 31, k = 14: 29 + Y^2..Y^14 (13) + G_2 (1) + I_0 13 + I_1 13 + I_2 2 + 2 outer -> 73 at
+      depth 6 = R16's depth (88 products, P:71's 3p - 5), the rule's choice."""
+    assert circuits._r23_cost(circuits.univariate_lt_eq_r23, 13, 3) == (6, 5)
+    assert circuits._r23_cost(circuits.bivariate_lt_eq_r23, 31, 4) == (68, 7)
+    assert circuits._r23_cost(circuits.bivariate_lt_eq_r23, 31, 14) == (73, 6)
+    assert circuits.r23_univariate_k(13) == 3 and circuits.r23_bivariate_k(31) == 14
+    # k = 1 is the R16 bivariate tree: 3p - 5 products (P:71)
+    for p in (5, 7, 11, 13):
+        assert circuits._r23_cost(circuits.bivariate_lt_eq_r23, p, 1)[0] == 3 * p - 5
+    # fewer products than 3p - 5 for every bivariate p >= 5 (toward P:77's 2p - 6)
+    for p in PRIMES:
+        if p >= 5:
+            assert circuits._r23_cost(circuits.bivariate_lt_eq_r23, p, circuits.r23_bivariate_k(p))[0] < 3 * p - 5
 
 
 def test_spec_lex_example():
