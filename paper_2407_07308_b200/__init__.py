@@ -21,12 +21,15 @@ if not os.path.exists(_SO):
 _lib = ctypes.CDLL(_SO)
 
 
+_SCHEDULES = {"r16": 16, "r23": 23}    # digit-circuit readings (R16 / R23)
+
+
 class bc_params(ctypes.Structure):
     _fields_ = [("p", ctypes.c_uint32), ("m", ctypes.c_uint32), ("circuit", ctypes.c_char),
                 ("d", ctypes.c_uint32), ("l", ctypes.c_uint32),
                 ("n_cipher", ctypes.c_uint32), ("cipher_bits", ctypes.c_uint32),
                 ("n_special", ctypes.c_uint32), ("special_bits", ctypes.c_uint32),
-                ("alpha", ctypes.c_uint32), ("compact_span", ctypes.c_uint32)]
+                ("alpha", ctypes.c_uint32), ("compact_span", ctypes.c_uint32), ("schedule", ctypes.c_uint32)]
 
 
 class bc_info(ctypes.Structure):
@@ -90,6 +93,7 @@ _sig("bc_rotate", _st, _vp, _vp, bc_ct, ctypes.c_int32, bc_ct, _vp, _sz, _vp)
 _sig("bc_frobenius", _st, _vp, _vp, bc_ct, _u32, bc_ct, _vp, _sz, _vp)
 _sig("bc_extract", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
 _sig("bc_launch_count", _u64, ctypes.c_int)
+_sig("bc_circuit_plan", _st, _u32, ctypes.c_char, _u32, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32))
 _sig("bc_ntt_timing", ctypes.c_int, _vp, _vp, _vp)
 _sig("bc_set_ntt_impl", None, ctypes.c_int)
 _sig("bc_tune", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64)
@@ -134,6 +138,15 @@ def ntt_timing(enable=None):
     return ms.value, j.value, c.value
 
 
+def circuit_plan(p, circuit, schedule="r16"):
+    """host only: (k, products per digit, depth) of the digit circuit (R16: k = 0; R23: the selected
+    baby-step size)"""
+    k, mu, de = _u32(), _u32(), _u32()
+    _check(_lib.bc_circuit_plan(int(p), circuit.encode(), _SCHEDULES[schedule], ctypes.byref(k), ctypes.byref(mu),
+                                ctypes.byref(de)), "bc_circuit_plan")
+    return k.value, mu.value, de.value
+
+
 def launch_count(reset=False):
     return int(_lib.bc_launch_count(1 if reset else 0))
 
@@ -173,7 +186,7 @@ class Context:
         prm = bc_params(int(cfg["p"]), int(cfg["m"]), cfg.get("circuit", "U").encode(), int(cfg["d"]),
                         int(cfg["l"]), int(cfg["n_cipher"]), int(cfg["cipher_bits"]),
                         int(cfg["n_special"]), int(cfg["special_bits"]), int(cfg["alpha"]),
-                        int(cfg.get("compact_span", 3)))
+                        int(cfg.get("compact_span", 3)), _SCHEDULES[cfg.get("schedule", "r16")])
         h = _vp()
         with torch.cuda.device(self.device):
             _check(_lib.bc_ctx_create(ctypes.byref(prm), device, ctypes.byref(h)), "bc_ctx_create")

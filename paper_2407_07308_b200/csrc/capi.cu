@@ -84,6 +84,21 @@ bc_status bc_ctx_info(const bc_ctx *X, bc_info *o) {
     API_END
 }
 
+bc_status bc_circuit_plan(uint32_t p, char circuit, uint32_t schedule, uint32_t *k, uint32_t *products,
+                          uint32_t *depth) {
+    API_BEGIN
+    if (!k || !products || !depth) BC_THROW(BC_E_ARG, "null argument");
+    if (p < 3 || p > 257 || !is_prime_u64(p)) BC_THROW(BC_E_PARAM, "p must be an odd prime <= 257");
+    if (circuit != 'U' && circuit != 'B') BC_THROW(BC_E_PARAM, "circuit must be 'U' or 'B'");
+    if (schedule != 0 && schedule != 16 && schedule != 23) BC_THROW(BC_E_PARAM, "schedule must be 16 or 23");
+    int kk, mu, de;
+    circuit_plan(p, circuit, (int)schedule, &kk, &mu, &de);
+    *k = (uint32_t)kk;
+    *products = (uint32_t)mu;
+    *depth = (uint32_t)de;
+    API_END
+}
+
 bc_status bc_ctx_moduli(const bc_ctx *X, uint64_t *h_out, uint64_t *h_omega) {
     API_BEGIN
     if (!X) BC_THROW(BC_E_ARG, "null ctx");

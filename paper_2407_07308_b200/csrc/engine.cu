@@ -194,6 +194,9 @@ static std::vector<int64_t> interp_fp(int64_t p, const std::function<int64_t(int
 
 // bivariate LT(x,y) = [x<y] = sum_u d_u(x) sum_{v>u} d_v(y), d_u = indicator of u, rewritten in
 // (Y = y, Z = x - y): out[j][k] coefficient of Y^j Z^k.
+int r23_select_k(int64_t p, char circuit, const std::vector<int64_t> &cu, const std::vector<std::vector<int64_t>> &cb,
+                 int *muls, int *depth);
+
 static std::vector<std::vector<int64_t>> lt_bivariate(int64_t p) {
     std::vector<std::vector<int64_t>> dl(p);
     for (int64_t u = 0; u < p; ++u) dl[u] = interp_fp(p, [u](int64_t v) { return v == u ? 1 : 0; });
@@ -276,6 +279,9 @@ void ctx_build(bc_ctx *X) {
         X->lt_u = interp_fp(p, [p, h](int64_t v) { return (v >= p - h && v <= p - 1) ? 1 : 0; });
         X->eq_u = interp_fp(p, [](int64_t v) { return v == 0 ? 1 : 0; });
         if (P.circuit == 'B') X->lt_b = lt_bivariate(p);
+        // R23 (schedule 23): the baby-step size the rule selects; 0 = the R16 circuits
+        if (P.schedule != 0 && P.schedule != 16 && P.schedule != 23) BC_THROW(BC_E_PARAM, "schedule must be 16 or 23");
+        X->r23_k = P.schedule == 23 ? r23_select_k(p, P.circuit, X->lt_u, X->lt_b, nullptr, nullptr) : 0;
     }
     // Galois elements: Frobenius p^k (k < D), rotations g^{+-2^r} (r < ceil log2 l)
     {
@@ -1062,61 +1068,303 @@ struct Powers {
     }
 };
 
-static void univariate(Eng &E, const Val &z, Val *lt, Val *eq) {
-    const int64_t p = E.X->p;
-    const std::vector<int64_t> &c = E.X->lt_u;
+// ---- digit circuits, generic over an evaluator (EngEv: ciphertexts; CntEv: counts products and depth,
+// used to choose the R23 baby-step size).  Ev provides V, cnst(c), isc(v), cval(v), mul(a, b), add(a, b)
+// with the vmul / vadd semantics (constants fold, a constant factor is a scalar product).
+struct EngEv {
+    Eng &E;
+    typedef Val V;
+    V cnst(int64_t c) { return VC(c); }
+    static bool isc(const V &v) { return v.isc; }
+    static int64_t cval(const V &v) { return v.c; }
+    V mul(const V &a, const V &b) { return vmul(E, a, b); }
+    V add(const V &a, const V &b) { return vadd(E, a, b); }
+    int64_t p() const { return E.X->p; }
+};
+struct CntV {
+    bool isc = false;
+    int64_t c = 0;
+    int depth = 0;
+};
+struct CntEv {
+    int64_t pp;
+    int muls = 0;
+    typedef CntV V;
+    V cnst(int64_t c) { V v; v.isc = true; v.c = ((c % pp) + pp) % pp; return v; }
+    static bool isc(const V &v) { return v.isc; }
+    static int64_t cval(const V &v) { return v.c; }
+    V mul(const V &a, const V &b) {
+        if (a.isc && b.isc) return cnst(a.c * b.c);
+        if (a.isc) return b;
+        if (b.isc) return a;
+        ++muls;
+        V r;
+        r.depth = std::max(a.depth, b.depth) + 1;
+        return r;
+    }
+    V add(const V &a, const V &b) {
+        if (a.isc && b.isc) return cnst(a.c + b.c);
+        if (a.isc) return b;
+        if (b.isc) return a;
+        V r;
+        r.depth = std::max(a.depth, b.depth);
+        return r;
+    }
+    int64_t p() const { return pp; }
+};
+
+// R16 power rule: x^j = x^a x^(j-a), a = the largest power of two < j (memoised)
+template <class Ev>
+struct PowersT {
+    Ev &ev;
+    std::map<int, typename Ev::V> pw;
+    PowersT(Ev &e, const typename Ev::V &x) : ev(e) { pw[1] = x; }
+    typename Ev::V get(int j) {
+        auto it = pw.find(j);
+        if (it != pw.end()) return it->second;
+        int a = 1;
+        while (a * 2 < j) a *= 2;
+        typename Ev::V x = get(a), y = get(j - a);
+        typename Ev::V r = ev.mul(x, y);
+        pw[j] = r;
+        return r;
+    }
+};
+// R23 giant powers G_a = B^(a k) of B = x^k: G_1 = B, G_a = G_a' G_(a-a'), a' the largest power of two < a
+template <class Ev>
+struct GiantT {
+    Ev &ev;
+    std::map<int, typename Ev::V> g;
+    GiantT(Ev &e, const typename Ev::V &b) : ev(e) { g[1] = b; }
+    typename Ev::V get(int a) {
+        auto it = g.find(a);
+        if (it != g.end()) return it->second;
+        int a1 = 1;
+        while (a1 * 2 < a) a1 *= 2;
+        typename Ev::V x = get(a1), y = get(a - a1);
+        typename Ev::V r = ev.mul(x, y);
+        g[a] = r;
+        return r;
+    }
+};
+// sum of c x over terms with c != 0 mod p (listed order) plus const (skipped if 0); no ciphertext term -> const
+template <class Ev>
+typename Ev::V lincombT(Ev &ev, const std::vector<std::pair<int64_t, std::function<typename Ev::V()>>> &terms, int64_t cst) {
+    const int64_t p = ev.p();
+    bool have = false;
+    typename Ev::V acc;
+    for (auto &t : terms) {
+        int64_t c = ((t.first % p) + p) % p;
+        if (!c) continue;
+        typename Ev::V v = ev.mul(t.second(), ev.cnst(c));
+        acc = have ? ev.add(acc, v) : v;
+        have = true;
+    }
+    cst = ((cst % p) + p) % p;
+    if (!have) return ev.cnst(cst);
+    if (cst) acc = ev.add(acc, ev.cnst(cst));
+    return acc;
+}
+
+// R16 univariate (mirrors oracle/circuits.py univariate_lt_eq)
+template <class Ev>
+static void univariate_r16(Ev &ev, const typename Ev::V &z, const std::vector<int64_t> &c, typename Ev::V *lt,
+                           typename Ev::V *eq) {
+    typedef typename Ev::V V;
+    const int64_t p = ev.p();
     const int e = (int)(p - 3) / 2;
     std::vector<int64_t> g(e + 1);
     for (int k = 0; k <= e; ++k) g[k] = c[2 * k + 1];
     const int64_t top = c[p - 1];
-    Val W = vmul(E, z, z);
-    Powers pw(E, W);
+    V W = ev.mul(z, z);
+    PowersT<Ev> pw(ev, W);
     int k0 = 1;
     while ((int64_t)k0 * k0 < e + 1) k0 *= 2;   // smallest 2^a with 4^a >= e+1
     for (int j = 2; j <= k0; ++j) pw.get(j);
     const int nch = (e + 1 + k0 - 1) / k0;
     auto chunk = [&](int i) {
-        std::vector<std::pair<int64_t, std::function<Val()>>> terms;
+        std::vector<std::pair<int64_t, std::function<V()>>> terms;
         for (int j = 1; j < k0; ++j)
             if (i * k0 + j <= e) terms.push_back({g[i * k0 + j], [&pw, j]() { return pw.get(j); }});
-        return lincomb(E, terms, g[i * k0]);
+        return lincombT(ev, terms, g[i * k0]);
     };
-    std::function<Val(int, int)> ps = [&](int lo, int hi) -> Val {
+    std::function<V(int, int)> ps = [&](int lo, int hi) -> V {
         if (hi - lo == 1) return chunk(lo);
         int h = 1;
         while (h * 2 < hi - lo) h *= 2;
-        Val low = ps(lo, lo + h);
-        Val high = ps(lo + h, hi);
-        Val gk = pw.get(k0 * h);
-        return vadd(E, low, vmul(E, gk, high));
+        V low = ps(lo, lo + h);
+        V high = ps(lo + h, hi);
+        V gk = pw.get(k0 * h);
+        return ev.add(low, ev.mul(gk, high));
     };
-    Val gval = ps(0, nch);
-    Val We = pw.get(e + 1);
-    *lt = vadd(E, vmul(E, z, gval), vmul(E, We, VC(top)));
-    if (eq) *eq = vadd(E, vmul(E, We, VC(-1)), VC(1));
+    V gval = ps(0, nch);
+    V We = pw.get(e + 1);
+    *lt = ev.add(ev.mul(z, gval), ev.mul(We, ev.cnst(top)));
+    if (eq) *eq = ev.add(ev.mul(We, ev.cnst(-1)), ev.cnst(1));
 }
 
-static void bivariate(Eng &E, const Val &x, const Val &y, Val *lt, Val *eq) {
-    const int64_t p = E.X->p;
-    const auto &c = E.X->lt_b;
-    Val Z = vadd(E, x, vmul(E, y, VC(-1)));
-    Powers zp(E, Z);
+// R16 bivariate (mirrors oracle/circuits.py bivariate_lt_eq)
+template <class Ev>
+static void bivariate_r16(Ev &ev, const typename Ev::V &x, const typename Ev::V &y,
+                          const std::vector<std::vector<int64_t>> &c, typename Ev::V *lt, typename Ev::V *eq) {
+    typedef typename Ev::V V;
+    const int64_t p = ev.p();
+    V Z = ev.add(x, ev.mul(y, ev.cnst(-1)));
+    PowersT<Ev> zp(ev, Z);
     for (int j = 2; j < p; ++j) zp.get(j);
-    Powers yp(E, y);
+    PowersT<Ev> yp(ev, y);
     for (int j = 2; j < p; ++j) yp.get(j);
     bool have = false;
-    Val acc;
+    V acc;
     for (int j = 1; j < p; ++j) {
-        std::vector<std::pair<int64_t, std::function<Val()>>> terms;
+        std::vector<std::pair<int64_t, std::function<V()>>> terms;
         for (int k = 1; k < p; ++k) terms.push_back({c[j][k], [&zp, k]() { return zp.get(k); }});
-        Val R = lincomb(E, terms, c[j][0]);
-        if (R.isc && R.c == 0) continue;
-        Val t = vmul(E, yp.get(j), R);
-        acc = have ? vadd(E, acc, t) : t;
+        V R = lincombT(ev, terms, c[j][0]);
+        if (Ev::isc(R) && Ev::cval(R) == 0) continue;
+        V t = ev.mul(yp.get(j), R);
+        acc = have ? ev.add(acc, t) : t;
         have = true;
     }
     *lt = acc;
-    if (eq) *eq = vadd(E, vmul(E, zp.get((int)p - 1), VC(-1)), VC(1));
+    if (eq) *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
+}
+
+// R23 univariate (§8(f) f2; mirrors oracle/circuits.py univariate_lt_eq_r23): baby powers W^2..W^k,
+// giant G_a = W^(a k), g = B_0 + sum_a G_a B_a, W^E from the baby / giant powers
+template <class Ev>
+static void univariate_r23(Ev &ev, const typename Ev::V &z, const std::vector<int64_t> &c, int k, typename Ev::V *lt,
+                           typename Ev::V *eq) {
+    typedef typename Ev::V V;
+    const int64_t p = ev.p();
+    const int e = (int)(p - 3) / 2, E = e + 1;
+    std::vector<int64_t> g(e + 1);
+    for (int i = 0; i <= e; ++i) g[i] = c[2 * i + 1];
+    const int64_t top = c[p - 1];
+    V W = ev.mul(z, z);
+    PowersT<Ev> pw(ev, W);
+    for (int j = 2; j <= k; ++j) pw.get(j);
+    const int A = (e + 1 + k - 1) / k;
+    GiantT<Ev> G(ev, pw.get(k));
+    for (int a = 2; a < A; ++a) G.get(a);
+    auto chunk = [&](int a) {
+        std::vector<std::pair<int64_t, std::function<V()>>> terms;
+        for (int b = 1; b < k; ++b)
+            if (a * k + b <= e) terms.push_back({g[a * k + b], [&pw, b]() { return pw.get(b); }});
+        return lincombT(ev, terms, g[a * k]);
+    };
+    V gval = chunk(0);
+    for (int a = 1; a < A; ++a) {
+        V B = chunk(a);
+        if (Ev::isc(B) && Ev::cval(B) == 0) continue;
+        gval = ev.add(gval, ev.mul(G.get(a), B));
+    }
+    V WE;
+    if (E <= k) WE = pw.get(E);
+    else {
+        const int a = E / k, b = E % k;
+        WE = b == 0 ? G.get(a) : ev.mul(G.get(a), pw.get(b));
+    }
+    *lt = ev.add(ev.mul(z, gval), ev.mul(WE, ev.cnst(top)));
+    if (eq) *eq = ev.add(ev.mul(WE, ev.cnst(-1)), ev.cnst(1));
+}
+
+// R23 bivariate (mirrors oracle/circuits.py bivariate_lt_eq_r23): all Z powers, baby-step / giant-step in Y
+template <class Ev>
+static void bivariate_r23(Ev &ev, const typename Ev::V &x, const typename Ev::V &y,
+                          const std::vector<std::vector<int64_t>> &c, int k, typename Ev::V *lt, typename Ev::V *eq) {
+    typedef typename Ev::V V;
+    const int64_t p = ev.p();
+    V Z = ev.add(x, ev.mul(y, ev.cnst(-1)));
+    PowersT<Ev> zp(ev, Z);
+    for (int j = 2; j < p; ++j) zp.get(j);
+    PowersT<Ev> yp(ev, y);
+    for (int j = 2; j <= k; ++j) yp.get(j);
+    const int A = (int)(p - 1) / k + 1;
+    GiantT<Ev> G(ev, yp.get(k));
+    for (int a = 2; a < A; ++a) G.get(a);
+    auto R = [&](int j) {
+        std::vector<std::pair<int64_t, std::function<V()>>> terms;
+        for (int i = 1; i < p; ++i) terms.push_back({c[j][i], [&zp, i]() { return zp.get(i); }});
+        return lincombT(ev, terms, c[j][0]);
+    };
+    auto inner = [&](int a) {
+        bool have = false;
+        V acc;
+        for (int b = 0; b < k; ++b) {
+            const int j = a * k + b;
+            if (j < 1 || j > p - 1) continue;
+            V r = R(j);
+            if (Ev::isc(r) && Ev::cval(r) == 0) continue;
+            V t = b == 0 ? r : ev.mul(yp.get(b), r);
+            acc = have ? ev.add(acc, t) : t;
+            have = true;
+        }
+        return have ? acc : ev.cnst(0);
+    };
+    V acc = inner(0);
+    for (int a = 1; a < A; ++a) {
+        V I = inner(a);
+        if (Ev::isc(I) && Ev::cval(I) == 0) continue;
+        V t = ev.mul(G.get(a), I);
+        acc = (Ev::isc(acc) && Ev::cval(acc) == 0) ? t : ev.add(acc, t);
+    }
+    *lt = acc;
+    if (eq) *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
+}
+
+// R23 baby-step size: among k whose circuit is no deeper than R16's, the fewest products, then the smallest k
+static void r23_cost(int64_t p, char circuit, const std::vector<int64_t> &cu, const std::vector<std::vector<int64_t>> &cb,
+                     int k, int *muls, int *depth) {
+    CntEv ev{p};
+    CntV lt, eq;
+    if (circuit == 'U') {
+        if (k <= 0) univariate_r16(ev, CntV(), cu, &lt, &eq);
+        else univariate_r23(ev, CntV(), cu, k, &lt, &eq);
+    } else {
+        if (k <= 0) bivariate_r16(ev, CntV(), CntV(), cb, &lt, &eq);
+        else bivariate_r23(ev, CntV(), CntV(), cb, k, &lt, &eq);
+    }
+    *muls = ev.muls;
+    *depth = std::max(lt.depth, eq.depth);
+}
+int r23_select_k(int64_t p, char circuit, const std::vector<int64_t> &cu, const std::vector<std::vector<int64_t>> &cb,
+                 int *muls, int *depth) {
+    int m16, d16;
+    r23_cost(p, circuit, cu, cb, 0, &m16, &d16);
+    const int kmax = circuit == 'U' ? std::max<int>(1, (int)(p - 1) / 2) : (int)p - 1;
+    int best = -1, bm = 0, bd = 0;
+    for (int k = 1; k <= kmax; ++k) {
+        int mu, de;
+        r23_cost(p, circuit, cu, cb, k, &mu, &de);
+        if (de > d16) continue;
+        if (best < 0 || mu < bm) { best = k; bm = mu; bd = de; }
+    }
+    if (muls) *muls = bm;
+    if (depth) *depth = bd;
+    return best;
+}
+
+// host-only plan query (bc_circuit_plan): the selected k and the products / depth per digit of the
+// schedule (k = 0: R16)
+void circuit_plan(int64_t p, char circuit, int schedule, int *k, int *muls, int *depth) {
+    const int64_t h = (p - 1) / 2;
+    std::vector<int64_t> cu = interp_fp(p, [p, h](int64_t v) { return (v >= p - h && v <= p - 1) ? 1 : 0; });
+    std::vector<std::vector<int64_t>> cb;
+    if (circuit == 'B') cb = lt_bivariate(p);
+    *k = schedule == 23 ? r23_select_k(p, circuit, cu, cb, nullptr, nullptr) : 0;
+    r23_cost(p, circuit, cu, cb, *k, muls, depth);
+}
+
+static void univariate(Eng &E, const Val &z, Val *lt, Val *eq) {
+    EngEv ev{E};
+    if (E.X->r23_k > 0) univariate_r23(ev, z, E.X->lt_u, E.X->r23_k, lt, eq);
+    else univariate_r16(ev, z, E.X->lt_u, lt, eq);
+}
+
+static void bivariate(Eng &E, const Val &x, const Val &y, Val *lt, Val *eq) {
+    EngEv ev{E};
+    if (E.X->r23_k > 0) bivariate_r23(ev, x, y, E.X->lt_b, E.X->r23_k, lt, eq);
+    else bivariate_r16(ev, x, y, E.X->lt_b, lt, eq);
 }
 
 static std::vector<int16_t> block_mask(bc_ctx *X, const std::function<bool(uint32_t)> &pred) {

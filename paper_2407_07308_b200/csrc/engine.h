@@ -89,6 +89,7 @@ struct bc_ctx {
     // circuit coefficients
     std::vector<int64_t> lt_u, eq_u;            // univariate LT / EQ coefficients
     std::vector<std::vector<int64_t>> lt_b;     // bivariate c[j][k] (Y^j Z^k)
+    int r23_k = 0;                              // R23 baby-step size (params schedule 23), 0 = R16 circuits
     const uint64_t *plan(const std::string &k) const;
 };
 
@@ -166,5 +167,7 @@ CT broadcast_batch(Eng &E, const CT &cond);
 CT concat_batch(Eng &E, const std::vector<CT> &parts);
 CT tournament_batch(Eng &E, std::vector<CT> elems, bool is_max);
 std::vector<CT> sort_batch(Eng &E, const std::vector<CT> &x);
+
+void circuit_plan(int64_t p, char circuit, int schedule, int *k, int *muls, int *depth);
 
 }  // namespace bc

@@ -15,8 +15,13 @@ def pytest_configure(config):
 
 
 def load_cfg(name):
-    with open(os.path.join(ROOT, "params", name + ".json")) as f:
-        return json.load(f)
+    """params/<name>.json; "<name>@r16" / "<name>@r23" overrides the digit-circuit schedule (R16 / R23)"""
+    base, _, sched = name.partition("@")
+    with open(os.path.join(ROOT, "params", base + ".json")) as f:
+        cfg = json.load(f)
+    if sched:
+        cfg["schedule"] = sched
+    return cfg
 
 
 def golden(name):

@@ -2,6 +2,7 @@
 import ctypes
 import os
 import re
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -36,3 +37,24 @@ def test_oracle_not_imported_by_product():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_circuit_plan_matches_oracle():
+    """host logic, no device: the digit circuit the library evaluates (bc_circuit_plan: R23 baby-step
+    size, products per digit, depth) equals the oracle's count of its own schedule for every p <= 31,
+    both circuits, R16 and R23 (R16 / R23)"""
+    import paper_2407_07308_b200 as bc
+    from oracle import circuits as c
+    for p in [3, 5, 7, 11, 13, 17, 19, 23, 29, 31]:
+        for kind in "UB":
+            ev = c.CountEval(p)
+            if kind == "U":
+                lt, eq = c.univariate_lt_eq(ev, c.CountValue(), p)
+            else:
+                lt, eq = c.bivariate_lt_eq(ev, c.CountValue(), c.CountValue(), p)
+            assert bc.circuit_plan(p, kind, "r16") == (0, ev.counts["mul"], max(lt.depth, eq.depth))
+            k = c.r23_univariate_k(p) if kind == "U" else c.r23_bivariate_k(p)
+            f = c.univariate_lt_eq_r23 if kind == "U" else c.bivariate_lt_eq_r23
+            assert bc.circuit_plan(p, kind, "r23") == (k,) + c._r23_cost(f, p, k)
+    with pytest.raises(bc.BoostComError):
+        bc.circuit_plan(15, "U", "r23")

@@ -152,18 +152,19 @@ def _digest(E):
 
 
 @pytest.mark.slow
-def test_full_size_c2_compare_matches_oracle_digest(pair):
+@pytest.mark.parametrize("name,golden", [("c2", "c2_compare_digest.json"), ("c2@r16", "c2_compare_digest_r16.json")])
+def test_full_size_c2_compare_matches_oracle_digest(pair, name, golden):
     """The headline workload's compare_lt (C2, n = 30940, 11 + 4 primes) on one pair: the
-    evaluation-form ciphertext's SHA-256 equals the oracle's (tests/golden/c2_compare_digest.json,
+    evaluation-form ciphertext's SHA-256 equals the oracle's (tests/golden/c2_compare_digest*.json,
     written by tools/oracle/c2_compare_digest.py from oracle/ and inputs/ only; same seeds, same
-    words).  Exercises data-dependent encode, every key switch and the R16 schedule at
-    full size."""
+    words).  Exercises data-dependent encode, every key switch and the digit schedule at
+    full size: R23 (C2's schedule) and R16."""
     from inputs import word_pairs
-    path = os.path.join(ROOT, "tests", "golden", "c2_compare_digest.json")
+    path = os.path.join(ROOT, "tests", "golden", golden)
     if not os.path.exists(path):
         pytest.skip("golden digest not generated yet")
     g = json.load(open(path))
-    T = pair("c2")
+    T = pair(name)
     P = T.P
     ints = T.ctx.ints_per_ct
     a, b = word_pairs(np.random.default_rng(g["seeds"]["words"]), ints, P.base, P.d * P.l)

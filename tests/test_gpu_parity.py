@@ -292,11 +292,13 @@ def test_non_blocking_matches_blocking(pair):
 
 
 @pytest.mark.slow
-def test_compare_shadow_c2_bit_exact(pair):
+@pytest.mark.parametrize("name", ["c2s", "c2s@r16"])
+def test_compare_shadow_c2_bit_exact(pair, name):
     """C2's circuit (p=13 univariate, (d,l)=(4,6), 11+3 primes) on its shadow ring m=859:
-    whole compare_lt ciphertext bit-exact vs the oracle (takes ~2 minutes of oracle time)."""
+    whole compare_lt ciphertext bit-exact vs the oracle (takes ~2 minutes of oracle time), with the
+    R23 digit circuit (6 products per digit, C2's schedule) and R16's (7)."""
     from oracle import circuits
-    T = pair("c2s")
+    T = pair(name)
     P = T.P
     ints = T.ctx.ints_per_ct
     rng = np.random.default_rng(20)
@@ -427,12 +429,13 @@ def test_compare_full_c3_decrypts(pair):
 
 
 @pytest.mark.slow
-def test_compare_c3t_bivariate_p31_bit_exact(pair):
-    """C3's p = 31 bivariate digit circuit (88 products, R16) on a small ring (c3t: m = 1129,
-    (d,l) = (1,2), 9 + 4 primes): whole compare_lt ciphertext bit-exact vs the oracle (~4 min of
-    oracle time), decrypted bits = [a<b]."""
+@pytest.mark.parametrize("name", ["c3t", "c3t@r16"])
+def test_compare_c3t_bivariate_p31_bit_exact(pair, name):
+    """C3's p = 31 bivariate digit circuit (R23: 73 products, C3's schedule; R16: 88) on a small
+    ring (c3t: m = 1129, (d,l) = (1,2), 9 + 4 primes): whole compare_lt ciphertext bit-exact vs the
+    oracle (~4 min of oracle time), decrypted bits = [a<b]."""
     from oracle import circuits
-    T = pair("c3t")
+    T = pair(name)
     P = T.P
     ints = T.ctx.ints_per_ct
     rng = np.random.default_rng(43)

@@ -8,7 +8,7 @@ inputs.word_pairs(np.random.default_rng(SEED_WORDS), 1031, base, d*l).  The resu
 SHA-256 over the little-endian u64 array [2][level][n] is stored, with sampled coefficients for
 diagnosis and the decrypted result bits checked against plaintext comparison.
 
-    python tools/oracle/c2_compare_digest.py      # about an hour on 8 host cores
+    python tools/oracle/c2_compare_digest.py [c2|c2@r16] [out.json]   # 20-60 min on 6-8 host cores
 """
 import hashlib
 import json
@@ -30,7 +30,10 @@ OUT = os.path.join(ROOT, "tests", "golden", "c2_compare_digest.json")
 
 def main(cfg_name="c2", out=OUT):
     t0 = time.time()
-    cfg = json.load(open(os.path.join(ROOT, "params", cfg_name + ".json")))
+    base, _, sched = cfg_name.partition("@")        # "c2@r16": C2 with the R16 digit circuits
+    cfg = json.load(open(os.path.join(ROOT, "params", base + ".json")))
+    if sched:
+        cfg["schedule"] = sched
     P = bgv.Params(cfg)
     A = P.alg
     ints = P.ints_per_ct
@@ -54,7 +57,7 @@ def main(cfg_name="c2", out=OUT):
     E = np.stack(bgv.ct_to_eval(P, lt))                     # [2][level][n] u64
     h = hashlib.sha256(np.ascontiguousarray(E, dtype="<u8").tobytes()).hexdigest()
     samp = [int(x) for x in E[:, :, :4].reshape(-1)]
-    rec = {"config": cfg_name, "what": "oracle compare_lt of one C2 pair, evaluation form (R3)",
+    rec = {"config": cfg_name, "schedule": P.schedule, "what": "oracle compare_lt of one C2 pair, evaluation form (R3)",
            "seeds": {"keys": SEED_KEYS, "words": SEED_WORDS, "enc": SEED_ENC, "ct_index": [0, 1]},
            "galois": gal, "level": int(lt.level), "shape": list(E.shape), "sha256": h,
            "first4_per_limb": samp, "lt_bits_sha256": hashlib.sha256(bytes(bits)).hexdigest(),
