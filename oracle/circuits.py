@@ -495,6 +495,37 @@ def select(ev, cond, x1, x2, l, ints):
     return ev.add(x2, ev.mul(bc, diff))
 
 
+def power(ev, x, e):
+    """R24 x^e, e >= 1, left-to-right binary: acc = x; for each bit of e below the top one:
+    acc = acc * acc, then acc = acc * x if the bit is 1 (e = 2^k: k squarings)."""
+    assert e >= 1
+    acc = x
+    for bit in bin(e)[3:]:
+        acc = ev.mul(acc, acc)
+        if bit == "1":
+            acc = ev.mul(acc, x)
+    return acc
+
+
+def private_query(ev, data, q, codes, op1, e, circuit, d, l, ints):
+    """R24 private_q (Listing 4 straightlined, Listing 5 non-blocking -- the same values):
+    c_j = bcast(EQ(q, code_j)), j = 0, 1, 2 (add, mult, power; the query type q and the codes are
+    words in every integer block); for every database ciphertext D_i:
+    out_i = ((D_i + op1) c_0 + (D_i op1) c_1) + D_i^e c_2."""
+    masks = []
+    for code in codes:
+        _, eq = compare(ev, q, code, circuit, d, l, ints)
+        masks.append(broadcast(ev, eq, l, ints))
+    out = []
+    for D in data:
+        d1 = ev.add(D, op1)
+        d2 = ev.mul(D, op1)
+        d3 = power(ev, D, e)
+        acc = ev.add(ev.mul(d1, masks[0]), ev.mul(d2, masks[1]))
+        out.append(ev.add(acc, ev.mul(d3, masks[2])))
+    return out
+
+
 def vmin(ev, a, b, circuit, d, l, ints):
     lt, _ = compare(ev, a, b, circuit, d, l, ints)
     return select(ev, lt, a, b, l, ints)

@@ -297,3 +297,82 @@ def test_spec_min_tournament_example():
     xs = [_plain_words(A, [v] * ints, d, l, base) for v in g["values"]]
     r = circuits.tournament(ev, xs, "min", "U", d, l, ints)
     assert slots.slots_to_words(r.v, d, l, base, ints) == [g["min"]] * ints
+
+
+def _p3s_plain():
+    from oracle import bgv
+    from conftest import load_cfg
+    P = bgv.Params(load_cfg("p3s"))
+    return P, P.alg
+
+
+@pytest.mark.parametrize("e,products", [(1, 0), (2, 1), (5, 3), (8, 3), (1024, 10), (1023, 18)])
+def test_power_product_count(e, products):
+    """R24 left-to-right binary power: one squaring per bit below the top, one product per further 1 bit;
+    every product extends the one chain, so the depth equals the product count"""
+    ev = circuits.CountEval(7)
+    r = circuits.power(ev, circuits.CountValue(), e)
+    assert ev.counts["mul"] == products == (e.bit_length() - 1) + (bin(e).count("1") - 1)
+    assert getattr(r, "depth", 0) == products
+
+
+@pytest.mark.parametrize("qv", [1, 2, 3, 0, 5])
+def test_private_query_semantics(qv):
+    """R24 private_q (Listings 3-4) on plaintext slots of the p3 shadow ring (m = 111, 4 x 2
+    hypercube, (d,l) = (8,4)): query type add (1), mult (2), power (3) or none gives
+    Data + op1, Data * op1, Data^e, 0 in every slot of an integer block (slots outside the row-aligned
+    blocks are 0)"""
+    P, A = _p3s_plain()
+    ev = circuits.PlainEval(A)
+    rng = np.random.default_rng(qv)
+    ints = P.ints_per_ct
+
+    def words(w):
+        return circuits.PlainValue(slots.words_to_slots(w, A, P.d, P.l, P.base))
+
+    def fp_slots():
+        v = np.zeros((A.S, A.D), dtype=np.int64)
+        v[:, 0] = rng.integers(0, P.p, A.S)
+        return v
+    for e in (1, 5):
+        data = [circuits.PlainValue(fp_slots()) for _ in range(2)]
+        op1 = circuits.PlainValue(fp_slots())
+        out = circuits.private_query(ev, data, words([qv] * ints), [words([c] * ints) for c in (1, 2, 3)],
+                                     op1, e, P.circuit, P.d, P.l, ints)
+        covered = np.array([(s % A.S1) < (A.S1 // P.l) * P.l for s in range(A.S)])
+        for D, o in zip(data, out):
+            x, y = D.v[:, 0], op1.v[:, 0]
+            want = {1: (x + y) % P.p, 2: (x * y) % P.p, 3: np.array([pow(int(t), e, P.p) for t in x])}.get(qv, 0 * x)
+            assert np.array_equal(o.v[covered, 0], want[covered])
+            assert not o.v[~covered].any() and not o.v[:, 1:].any()
+
+
+def test_private_query_bgv_decrypts():
+    """R24 on the oracle BGV (p3 shadow ring, 13 + 4 primes): the decrypted result equals the plaintext
+    semantics of a power query (e = 3)"""
+    from oracle import bgv
+    P, A = _p3s_plain()
+    gal = sorted({pow(P.p, k, P.m) for k in range(1, A.D)} | {pow(A.g, s, P.m) for s in (1, 2)}
+                 | {pow(A.g, -s, P.m) for s in (1, 2)})
+    K = bgv.keygen(P, 0xB00C0001, gal)
+    ev = circuits.OracleEval(P, K)
+    ints = P.ints_per_ct
+    rng = np.random.default_rng(7)
+
+    def enc_words(w, idx):
+        return bgv.encrypt(P, K, A.encode(slots.words_to_slots(w, A, P.d, P.l, P.base)), 0xB00C0003, idx)
+
+    def enc_slots(v, idx):
+        return bgv.encrypt(P, K, A.encode(v), 0xB00C0003, idx)
+    x = np.zeros((A.S, A.D), dtype=np.int64)
+    x[:, 0] = rng.integers(0, P.p, A.S)
+    y = np.zeros((A.S, A.D), dtype=np.int64)
+    y[:, 0] = rng.integers(0, P.p, A.S)
+    codes = [enc_words([c] * ints, 10 + c) for c in (1, 2, 3)]
+    covered = np.array([(s % A.S1) < (A.S1 // P.l) * P.l for s in range(A.S)])
+    for qv, want in ((3, np.array([pow(int(t), 3, P.p) for t in x[:, 0]])),):
+        out = circuits.private_query(ev, [enc_slots(x, 1)], enc_words([qv] * ints, 2), codes, enc_slots(y, 3), 3,
+                                     P.circuit, P.d, P.l, ints)
+        dec = A.decode(bgv.decrypt(P, K, out[0]))
+        assert np.array_equal(dec[covered, 0], want[covered])
+        assert not dec[~covered].any()
