@@ -324,11 +324,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verify", type=int, default=1)
-    ap.add_argument("--workload", default=None, choices=[None, "compare", "tournament", "sort", "compact_compare"],
+    ap.add_argument("--workload", default=None,
+                    choices=[None, "compare", "tournament", "sort", "compact_compare", "private_q"],
                     help="compare (default; C2), tournament (C4 min over T vectors), sort (C5 rank sort)")
     ap.add_argument("--T", type=int, default=16, help="tournament / sort: number of elements")
     ap.add_argument("--cts", type=int, default=0, help="ciphertexts per element (tournament: 5 -> 4096 words)")
     ap.add_argument("--vec-chunk", type=int, default=0, help="max ct pairs per batched compare (0 = all)")
+    ap.add_argument("--exps", default="64,128,256,512,1024", help="private_q: exponents op2 swept (Fig. 14)")
     args = ap.parse_args()
     cfg = load_json(os.path.join(ROOT, "params", args.config + ".json"))
     rank, world, local = dist_env()
@@ -336,7 +338,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
-    workload = args.workload or {"c4": "tournament", "c5": "sort", "c3": "compact_compare"}.get(args.config, "compare")
+    workload = args.workload or {"c4": "tournament", "c5": "sort", "c3": "compact_compare",
+                                 "p3q": "private_q"}.get(args.config, "compare")
     if args.pairs is None:
         args.pairs = 16 if workload == "compact_compare" else 1000
     if workload in ("tournament", "sort"):
@@ -344,6 +347,9 @@ def main():
         return
     if workload == "compact_compare":
         run_compact_compare(args, cfg, rank, world, local)
+        return
+    if workload == "private_q":
+        run_private_q(args, cfg, rank, world, local)
         return
 
     import torch
@@ -689,6 +695,147 @@ def run_compact_compare(args, cfg, rank, world, local):
                 "ms_per_dense_compare": ms / Bd, "verified": verified, "gpu_launches": launches,
                 "clocks": clk.summary(), "roofline": roofline(ctx, bc, live, ms_local * args.steps), "e2e": None,
                 "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_private_q(args, cfg, rank, world, local):
+    """f4 private_q (Listings 3-5, R24): a database of --pairs ciphertexts (default 100) on the p3
+    ring; one step = one private query (3 EQs + broadcasts, Data + op1, Data * op1, Data^e, combination),
+    blocking (Listing 4, one stream) and non-blocking (Listing 5: the EQs on a second stream), for every
+    exponent of --exps (Fig. 14).  Both are checked bit-identical and by decryption in warm-up.  Weak
+    scaling over ranks (each rank its own database shard, no collective)."""
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2407_07308_b200 as bc
+    ctx = bc.Context(cfg, device=local)
+    keys = ctx.keygen(SEED_KEYS)
+    N = args.pairs if args.pairs and args.pairs != 1000 else 100
+    ints = ctx.ints_per_ct
+    rng = np.random.default_rng(SEED_INPUT + rank)
+    X = np.zeros((N, ctx.S, ctx.D), dtype=np.int16)
+    X[:, :, 0] = rng.integers(0, ctx.p, (N, ctx.S))
+    Y = np.zeros((1, ctx.S, ctx.D), dtype=np.int16)
+    Y[:, :, 0] = rng.integers(0, ctx.p, (1, ctx.S))
+    base = (N + 8) * rank
+    data = ctx.encrypt_slots(keys, X, SEED_ENC, ct_index0=base)
+    op1 = ctx.encrypt_slots(keys, Y, SEED_ENC, ct_index0=base + N)
+    qv = 3                                   # the power branch (the expensive one, Fig. 14)
+    q = ctx.encrypt(keys, np.array([[qv] * ints], dtype=np.uint64), SEED_ENC, ct_index0=base + N + 1)
+    codes = ctx.encrypt(keys, np.array([[c] * ints for c in (1, 2, 3)], dtype=np.uint64), SEED_ENC,
+                        ct_index0=base + N + 2)
+    side = torch.cuda.Stream(device=dev, priority=-1)   # the branch evaluation first when SMs free up
+    exps = [int(x) for x in args.exps.split(",")]
+    emax = max(exps)
+    wsm = ctx.workspace(int(bc._lib.bc_private_query_workspace_bytes(ctx._h, N, data.shape[2], q.shape[2],
+                                                                     op1.shape[2], emax, 0)))
+    wss = torch.empty(int(bc._lib.bc_private_query_workspace_bytes(ctx._h, N, data.shape[2], q.shape[2],
+                                                                   op1.shape[2], emax, 1)), dtype=torch.uint8,
+                      device=dev)
+    S1 = ctx.S // 2 if cfg["m"] == 20197 else ctx.S
+    rows = []
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            fn()
+        e1.record()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
+
+    verified = True
+    launches = {}
+    q3 = torch.cat([q, q, q])
+    lvl_eq = ctx.out_level(q.shape[2], 1)
+    eq_out = ctx.ct_empty(3, lvl_eq)
+    with ClockSampler(local) as clk:
+        for e in exps:
+            lvl = int(bc._lib.bc_private_query_level(ctx._h, N, data.shape[2], q.shape[2], op1.shape[2], e))
+            out_b, out_n = ctx.ct_empty(N, lvl), ctx.ct_empty(N, lvl)
+            blk = lambda: ctx.private_query(keys, data, q, codes, op1, e, ws=wsm, out=out_b)             # noqa: E731
+            nbl = lambda: ctx.private_query(keys, data, q, codes, op1, e, side_stream=side, ws=wsm,      # noqa: E731
+                                            ws_side=wss, out=out_n)
+            eqo = lambda: bc._check(bc._lib.bc_compare_eq(ctx._h, keys.keys, ctx.view(q3), ctx.view(codes),  # noqa
+                                                          ctx.view(eq_out), bc._ptr(wsm), wsm.numel(), bc._stream()),
+                                    "bc_compare_eq")
+            for w in range(args.warmup):
+                blk()
+                nbl()
+                eqo()
+                if w == 0 and args.verify:
+                    torch.cuda.synchronize()
+                    same = bool(torch.equal(out_b, out_n))
+                    dec = ctx.decrypt_slots(keys, out_n[: min(N, 4)])
+                    want = np.vectorize(lambda t: pow(int(t), e, ctx.p))(X[: min(N, 4), :, 0].astype(np.int64))
+                    cov = np.array([(s % S1) < (S1 // ctx.l) * ctx.l for s in range(ctx.S)])
+                    ok = same and np.array_equal(dec[:, cov, 0], want[:, cov])
+                    verified &= bool(ok)
+                    if not ok:
+                        print("VERIFY FAILED (exponent %d, identical %s)" % (e, same), file=sys.stderr)
+                        sys.exit(3)
+            bc.launch_count(reset=True)
+            tb = timed(blk)
+            launches[e] = bc.launch_count(reset=True) // args.steps
+            tn = timed(nbl)
+            tc = timed(eqo)
+            # the same three calls captured once as CUDA graphs (host planning and launches not repeated)
+            graphs = {}
+            cap = torch.cuda.Stream(device=dev)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(cap):
+                for nm, fn in (("b", blk), ("n", nbl), ("c", eqo)):
+                    g = bc.Graph()
+                    with g:
+                        fn()
+                    graphs[nm] = g
+            torch.cuda.synchronize()
+            with torch.cuda.stream(cap):
+                ref_b = out_b.clone()
+                graphs["n"].launch()
+                cap.synchronize()
+                gsame = bool(torch.equal(out_n, ref_b))
+                graphs["b"].launch()
+                cap.synchronize()
+                gsame &= bool(torch.equal(out_b, ref_b))
+            if not gsame:
+                print("VERIFY FAILED (graph replay, exponent %d)" % e, file=sys.stderr)
+                sys.exit(3)
+            with torch.cuda.stream(cap):
+                tgb = timed(graphs["b"].launch)
+                tgn = timed(graphs["n"].launch)
+                tgc = timed(graphs["c"].launch)
+            rows.append({"exponent": e, "blocking_ms": tb, "nonblocking_ms": tn, "branch_eval_ms": tc,
+                         "hidden_ms": tb - tn, "speedup": tb / tn,
+                         "graph": {"blocking_ms": tgb, "nonblocking_ms": tgn, "branch_eval_ms": tgc,
+                                   "hidden_ms": tgb - tgn, "hidden_frac_of_branch": (tgb - tgn) / tgc if tgc else None,
+                                   "speedup": tgb / tgn}})
+    if rank == 0:
+        last = rows[-1]
+        line = {"metric": "private_q queries/s (database of %d ciphertexts x %d slots, non-blocking comparison, "
+                          "CUDA graph)" % (N, ctx.S),
+                "value": world * 1e3 / last["graph"]["nonblocking_ms"], "unit": "queries/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": last["graph"]["nonblocking_ms"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic",
+                "config": {"workload": "f4 private_q (P:670, Listings 3-5, R24)", "params": args.config,
+                           "m": cfg["m"], "database_cts": N, "slots_per_ct": ctx.S, "query": "power (q = 3)",
+                           "exponent": last["exponent"], "n_cipher": ctx.n_cipher, "l2": "inputs larger than L2"},
+                "sweep": rows, "verified": verified, "gpu_launches_blocking": launches,
+                "clocks": clk.summary(), "roofline": None, "e2e": None, "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -174,10 +174,46 @@ bc_status bc_sort(bc_ctx *ctx, const bc_keys *keys, const bc_ct *v, uint32_t T, 
 uint32_t bc_vec_out_level(bc_ctx *ctx, int which, const uint32_t *levels, uint32_t T);
 size_t bc_vec_workspace_bytes(bc_ctx *ctx, int which, const uint32_t *levels, uint32_t T, uint32_t batch);
 
-/* ---- non-blocking comparison (a11, Listing 5) ------------------------- */
+/* ---- non-blocking comparison (a11, Listing 5) -------------------------
+ * enqueues compare_lt on side_stream (after whatever is already queued there: the caller orders the
+ * inputs' producers before it) and records an event in h; never waits on the device (batches larger
+ * than the workspace run chunk after chunk on side_stream); bc_wait makes joiner_stream wait for it. */
 bc_status bc_compare_lt_async(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out,
                               void *d_ws, size_t ws_bytes, void *side_stream, bc_handle *h);
 bc_status bc_wait(bc_handle *h, void *joiner_stream);   /* BC_E_CONSUMED on 2nd wait */
+
+/* ---- CUDA graphs (launch-bound schedules replayed without host work) ----------
+ * capture_begin starts a thread-local capture on `stream`; every library call then issued on it (and on
+ * the side streams those calls fork to and join back) is recorded instead of executed; capture_end
+ * instantiates the graph.  A replay (bc_graph_launch) re-runs the recorded kernels on the same device
+ * buffers (ciphertexts, workspaces), so their contents are read anew and no host work (schedule
+ * planning, launches) is repeated.  Errors: BC_E_ARG (null), BC_E_CUDA (capture not allowed, e.g. a
+ * call that must synchronise). */
+typedef struct bc_graph bc_graph;
+bc_status bc_graph_capture_begin(void *stream);
+bc_status bc_graph_capture_end(void *stream, bc_graph **out);
+bc_status bc_graph_launch(bc_graph *g, void *stream);
+void bc_graph_destroy(bc_graph *g);
+
+/* ---- private_q (Listings 3-5 at P:511-554, R24) ----------
+ * out[i] = ((data[i] + op1) c_0 + (data[i] op1) c_1) + data[i]^e c_2, c_j = bcast(EQ(q, codes[j]))
+ * (codes: add, mult, power words; q, codes: words in every integer block; op1: one ciphertext;
+ * e >= 1 a plaintext exponent, left-to-right binary powering).  data: batch N; q, op1: batch 1;
+ * codes: batch 3.  side == NULL: blocking (Listing 4), everything on `stream` with ws.  side != NULL:
+ * non-blocking (Listing 5): the EQs and broadcasts run on `side` with ws_side, ordered after the work
+ * already on `stream` and joined by an event before the combination; the host never waits.  ws and
+ * ws_side must stay untouched until `stream` has passed the call.  Bits are identical either way.
+ * out: batch >= N at level bc_private_query_level(...).  Errors: BC_E_ARG (shapes, e = 0, missing
+ * side workspace), BC_E_LEVEL (levels), BC_E_OOM (workspace). */
+uint32_t bc_private_query_level(bc_ctx *ctx, uint32_t n_data, uint32_t data_level, uint32_t q_level,
+                                uint32_t op1_level, uint32_t e);
+/* side = 0: whole query (blocking; also an upper bound for the main stream's share), 1: the side
+ * stream's share (EQs + broadcasts) */
+size_t bc_private_query_workspace_bytes(bc_ctx *ctx, uint32_t n_data, uint32_t data_level, uint32_t q_level,
+                                        uint32_t op1_level, uint32_t e, int side);
+bc_status bc_private_query(bc_ctx *ctx, const bc_keys *keys, bc_ct data, bc_ct q, bc_ct codes, bc_ct op1, uint32_t e,
+                           bc_ct out, void *ws, size_t ws_bytes, void *ws_side, size_t ws_side_bytes, void *stream,
+                           void *side);
 
 /* ---- primitives (each a §8(a) row; used by the parity tests) ---------------------- */
 /* a1/a2: batched Bluestein NTT over `npoly` polynomials of `nlimb` limbs each,

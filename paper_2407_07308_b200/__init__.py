@@ -103,6 +103,13 @@ _sig("bc_max_tree", _st, _vp, _vp, _vp, _u32, bc_ct, _vp, _sz, _vp)
 _sig("bc_sort", _st, _vp, _vp, _vp, _u32, _vp, _vp, _sz, _vp)
 _sig("bc_vec_out_level", _u32, _vp, ctypes.c_int, _vp, _u32)
 _sig("bc_vec_workspace_bytes", _sz, _vp, ctypes.c_int, _vp, _u32, _u32)
+_sig("bc_private_query_level", _u32, _vp, _u32, _u32, _u32, _u32, _u32)
+_sig("bc_private_query_workspace_bytes", _sz, _vp, _u32, _u32, _u32, _u32, _u32, ctypes.c_int)
+_sig("bc_private_query", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, bc_ct, _u32, bc_ct, _vp, _sz, _vp, _sz, _vp, _vp)
+_sig("bc_graph_capture_begin", _st, _vp)
+_sig("bc_graph_capture_end", _st, _vp, ctypes.POINTER(_vp))
+_sig("bc_graph_launch", _st, _vp, _vp)
+_sig("bc_graph_destroy", None, _vp)
 _sig("bc_compact", _st, _vp, _vp, bc_ct, _vp, bc_ct, ctypes.POINTER(_u32), _vp, _vp, _sz, _vp)
 
 EXPORTS = [n for n in dir(_lib) if n.startswith("bc_")]
@@ -145,6 +152,37 @@ def circuit_plan(p, circuit, schedule="r16"):
     _check(_lib.bc_circuit_plan(int(p), circuit.encode(), _SCHEDULES[schedule], ctypes.byref(k), ctypes.byref(mu),
                                 ctypes.byref(de)), "bc_circuit_plan")
     return k.value, mu.value, de.value
+
+
+class Graph:
+    """A CUDA graph of library calls (bc_graph_*): `with Graph() as g: ctx.compare_lt(...)` records the
+    calls issued on the current torch stream (which must not be the default stream); g.launch() replays
+    them on the same buffers."""
+
+    def __init__(self):
+        self._g = None
+        self._st = None
+
+    def __enter__(self):
+        self._st = _stream()
+        _check(_lib.bc_graph_capture_begin(self._st), "bc_graph_capture_begin")
+        return self
+
+    def __exit__(self, et, ev, tb):
+        g = _vp()
+        st = _lib.bc_graph_capture_end(self._st, ctypes.byref(g))
+        if et is None:
+            _check(st, "bc_graph_capture_end")
+            self._g = g
+        return False
+
+    def launch(self, stream=None):
+        _check(_lib.bc_graph_launch(self._g, stream if stream is not None else _stream()), "bc_graph_launch")
+
+    def __del__(self):
+        if self._g is not None and _lib is not None:
+            _lib.bc_graph_destroy(self._g)
+            self._g = None
 
 
 def launch_count(reset=False):
@@ -335,6 +373,30 @@ class Context:
         _check(_lib.bc_compare(self._h, keys.keys, self.view(a), self.view(b), self.view(lt), self.view(eq), w, wb,
                                _stream()), "bc_compare")
         return lt, eq
+
+    def private_query(self, keys, data, q, codes, op1, e, side_stream=None, ws=None, ws_side=None, out=None):
+        """R24 private_q (Listings 3-5): blocking when side_stream is None, else the branch
+        evaluation runs on side_stream (non-blocking).  Returns the result batch (current stream)."""
+        lvl = int(_lib.bc_private_query_level(self._h, data.shape[0], data.shape[2], q.shape[2], op1.shape[2], e))
+        if lvl == 0:
+            raise BoostComError("bc_private_query_level failed")
+        if out is None:
+            out = self.ct_empty(data.shape[0], lvl)
+        if ws is None:
+            ws = self.workspace(int(_lib.bc_private_query_workspace_bytes(self._h, data.shape[0], data.shape[2],
+                                                                          q.shape[2], op1.shape[2], e, 0)))
+        sp, sb, ss = None, 0, None
+        if side_stream is not None:
+            if ws_side is None:
+                torch = _torch()
+                ws_side = torch.empty(int(_lib.bc_private_query_workspace_bytes(
+                    self._h, data.shape[0], data.shape[2], q.shape[2], op1.shape[2], e, 1)), dtype=torch.uint8,
+                    device=self.device)
+            sp, sb, ss = _ptr(ws_side), ws_side.numel(), ctypes.c_void_p(side_stream.cuda_stream)
+        _check(_lib.bc_private_query(self._h, keys.keys, self.view(data), self.view(q), self.view(codes),
+                                     self.view(op1), int(e), self.view(out), _ptr(ws), ws.numel(), sp, sb, _stream(),
+                                     ss), "bc_private_query")
+        return out
 
     def compare_lt_async(self, keys, a, b, out, side_stream, ws):
         h = bc_handle()

@@ -245,7 +245,7 @@ static bc_status run_compare(bc_ctx *X, const bc_keys *keys, bc_ct a, bc_ct b, b
                 compare_batch(E, av, bv, &lt, nullptr);
                 return select_batch(E, lt, av, bv);
             }
-            compare_batch(E, av, bv, &lt, which ? &eq : nullptr);
+            compare_batch(E, av, bv, which == 3 ? nullptr : &lt, which ? &eq : nullptr);
             return which == 3 ? eq : lt;
         });
         check_out(X, o1, a.batch, want, "out");
@@ -272,14 +272,14 @@ static bc_status run_compare(bc_ctx *X, const bc_keys *keys, bc_ct a, bc_ct b, b
             CT r = which == 2 ? select_batch(E, lt, av, bv) : select_batch(E, lt, bv, av);
             out_copy(E, r, o1, b0);
         } else {
-            compare_batch(E, av, bv, &lt, which ? &eq : nullptr);
+            compare_batch(E, av, bv, which == 3 ? nullptr : &lt, which ? &eq : nullptr);   // 3: EQ only
             if (which == 0 || which == 1) out_copy(E, lt, o1, b0);
             if (which == 1 && o2.data) out_copy(E, eq, o2, b0);
             if (which == 3) out_copy(E, eq, o1, b0);
         }
         check_launch();
-        // the arena is reused by the next chunk: make sure the stream has consumed this one
-        if (b0 + nb < a.batch) CK(cudaStreamSynchronize(S(st)));
+        // the next chunk reuses the arena: its kernels are ordered after this chunk's on the same stream,
+        // so no host synchronisation is needed (the compare never blocks the host: a11)
     }
     API_END
 }
@@ -337,6 +337,115 @@ bc_status bc_compare_lt_async(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_
     h->event = ev;
     h->stream = side;
     h->consumed = 0;
+    API_END
+}
+
+// ------------------------------------------------------------------ CUDA graphs
+}  // extern "C"
+struct bc_graph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+};
+extern "C" {
+bc_status bc_graph_capture_begin(void *st) {
+    API_BEGIN
+    if (!st) BC_THROW(BC_E_ARG, "capture needs a non-default stream");
+    CK(cudaStreamBeginCapture(S(st), cudaStreamCaptureModeThreadLocal));
+    API_END
+}
+bc_status bc_graph_capture_end(void *st, bc_graph **out) {
+    API_BEGIN
+    if (!st || !out) BC_THROW(BC_E_ARG, "null argument");
+    bc_graph *G = new bc_graph();
+    cudaError_t e = cudaStreamEndCapture(S(st), &G->g);
+    if (e != cudaSuccess) {
+        delete G;
+        (void)cudaGetLastError();
+        BC_THROW(BC_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+    }
+    e = cudaGraphInstantiateWithFlags(&G->x, G->g, cudaGraphInstantiateFlagUseNodePriority);   // captured stream priorities
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(G->g);
+        delete G;
+        (void)cudaGetLastError();
+        BC_THROW(BC_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    *out = G;
+    API_END
+}
+bc_status bc_graph_launch(bc_graph *g, void *st) {
+    API_BEGIN
+    if (!g || !g->x) BC_THROW(BC_E_ARG, "null graph");
+    CK(cudaGraphLaunch(g->x, S(st)));
+    API_END
+}
+void bc_graph_destroy(bc_graph *g) {
+    if (!g) return;
+    if (g->x) cudaGraphExecDestroy(g->x);
+    if (g->g) cudaGraphDestroy(g->g);
+    delete g;
+}
+
+// R24 private_q (f4): blocking (side == NULL) or with the branch evaluation on `side` (Listing 5)
+static uint32_t pq_level(bc_ctx *X, const bc_keys *k, const bc_ct &data, const bc_ct &q, const bc_ct &codes,
+                         const bc_ct &op1, uint32_t e) {
+    return dry_level(X, [&](Eng &E) {
+        return private_query_batch(E, nullptr, E.view((uint64_t *)(uintptr_t)256, data.batch, data.level),
+                                   E.view((uint64_t *)(uintptr_t)256, 1, q.level),
+                                   E.view((uint64_t *)(uintptr_t)256, 3, codes.level),
+                                   E.view((uint64_t *)(uintptr_t)256, 1, op1.level), e);
+    });
+}
+uint32_t bc_private_query_level(bc_ctx *X, uint32_t n_data, uint32_t data_level, uint32_t q_level,
+                                uint32_t op1_level, uint32_t e) {
+    try {
+        bc_ct d{(void *)256, n_data, data_level}, q{(void *)256, 1, q_level}, c{(void *)256, 3, q_level},
+            o{(void *)256, 1, op1_level};
+        return pq_level(X, nullptr, d, q, c, o, e);
+    } catch (...) {
+        return 0;
+    }
+}
+size_t bc_private_query_workspace_bytes(bc_ctx *X, uint32_t n_data, uint32_t data_level, uint32_t q_level,
+                                        uint32_t op1_level, uint32_t e, int side) {
+    try {
+        size_t pk = dry_peak(X, nullptr, [&](Eng &E) {
+            CT d = E.view((uint64_t *)(uintptr_t)256, n_data, data_level);
+            CT q = E.view((uint64_t *)(uintptr_t)256, 1, q_level), c = E.view((uint64_t *)(uintptr_t)256, 3, q_level);
+            CT o = E.view((uint64_t *)(uintptr_t)256, 1, op1_level);
+            if (side == 1) {        // the side stream's share: the EQs and broadcasts
+                CT qr = concat_batch(E, {q, q, q}), lt, eq;
+                compare_batch(E, qr, c, nullptr, &eq);
+                CT m = broadcast_batch(E, eq);
+            } else {                // the whole query (an upper bound for the main stream's share)
+                CT r = private_query_batch(E, nullptr, d, q, c, o, e);
+            }
+        });
+        return pk + pk / 4 + (64u << 20);
+    } catch (...) {
+        return 0;
+    }
+}
+bc_status bc_private_query(bc_ctx *X, const bc_keys *k, bc_ct data, bc_ct q, bc_ct codes, bc_ct op1, uint32_t e,
+                           bc_ct out, void *ws, size_t wsb, void *ws_side, size_t wsb_side, void *st, void *side) {
+    API_BEGIN
+    if (!X || !k) BC_THROW(BC_E_ARG, "null ctx/keys");
+    check_ct(X, data, "data"); check_ct(X, q, "q"); check_ct(X, codes, "codes"); check_ct(X, op1, "op1");
+    if (q.batch != 1 || op1.batch != 1 || codes.batch != 3) BC_THROW(BC_E_ARG, "q, op1: batch 1; codes: batch 3");
+    if (e < 1) BC_THROW(BC_E_ARG, "exponent must be >= 1");
+    if (side && (!ws_side || !wsb_side)) BC_THROW(BC_E_ARG, "non-blocking query needs a side workspace");
+    check_out(X, out, data.batch, pq_level(X, k, data, q, codes, op1, e), "out");
+    Arena A;
+    A.init(ws, wsb, false);
+    Eng E{X, k, &A, S(st)};
+    Arena A2;
+    if (side) A2.init(ws_side, wsb_side, false);
+    Eng E2{X, k, &A2, S(side)};
+    CT r = private_query_batch(E, side ? &E2 : nullptr, E.view((uint64_t *)data.data, data.batch, data.level),
+                               E.view((uint64_t *)q.data, 1, q.level), E.view((uint64_t *)codes.data, 3, codes.level),
+                               E.view((uint64_t *)op1.data, 1, op1.level), e);
+    out_copy(E, r, out, 0);
+    check_launch();
     API_END
 }
 

@@ -1178,6 +1178,10 @@ static void univariate_r16(Ev &ev, const typename Ev::V &z, const std::vector<in
     const int64_t top = c[p - 1];
     V W = ev.mul(z, z);
     PowersT<Ev> pw(ev, W);
+    if (!lt) {      // EQ only: 1 - W^(e+1) by the power rule (memoised powers are order independent)
+        *eq = ev.add(ev.mul(pw.get(e + 1), ev.cnst(-1)), ev.cnst(1));
+        return;
+    }
     int k0 = 1;
     while ((int64_t)k0 * k0 < e + 1) k0 *= 2;   // smallest 2^a with 4^a >= e+1
     for (int j = 2; j <= k0; ++j) pw.get(j);
@@ -1211,6 +1215,10 @@ static void bivariate_r16(Ev &ev, const typename Ev::V &x, const typename Ev::V 
     const int64_t p = ev.p();
     V Z = ev.add(x, ev.mul(y, ev.cnst(-1)));
     PowersT<Ev> zp(ev, Z);
+    if (!lt) {      // EQ only: 1 - Z^(p-1)
+        *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
+        return;
+    }
     for (int j = 2; j < p; ++j) zp.get(j);
     PowersT<Ev> yp(ev, y);
     for (int j = 2; j < p; ++j) yp.get(j);
@@ -1242,6 +1250,16 @@ static void univariate_r23(Ev &ev, const typename Ev::V &z, const std::vector<in
     const int64_t top = c[p - 1];
     V W = ev.mul(z, z);
     PowersT<Ev> pw(ev, W);
+    if (!lt) {      // EQ only: W^E from the baby / giant powers it needs (memoised, order independent)
+        V WE;
+        if (E <= k) WE = pw.get(E);
+        else {
+            GiantT<Ev> G(ev, pw.get(k));
+            WE = E % k == 0 ? G.get(E / k) : ev.mul(G.get(E / k), pw.get(E % k));
+        }
+        *eq = ev.add(ev.mul(WE, ev.cnst(-1)), ev.cnst(1));
+        return;
+    }
     for (int j = 2; j <= k; ++j) pw.get(j);
     const int A = (e + 1 + k - 1) / k;
     GiantT<Ev> G(ev, pw.get(k));
@@ -1276,6 +1294,10 @@ static void bivariate_r23(Ev &ev, const typename Ev::V &x, const typename Ev::V 
     const int64_t p = ev.p();
     V Z = ev.add(x, ev.mul(y, ev.cnst(-1)));
     PowersT<Ev> zp(ev, Z);
+    if (!lt) {      // EQ only: 1 - Z^(p-1)
+        *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
+        return;
+    }
     for (int j = 2; j < p; ++j) zp.get(j);
     PowersT<Ev> yp(ev, y);
     for (int j = 2; j <= k; ++j) yp.get(j);
@@ -1442,11 +1464,12 @@ std::vector<CT> extract_batch(Eng &E, const CT &a) {
     return out;
 }
 
-static void lex_tree(Eng &E, std::vector<Val> lts, std::vector<Val> eqs, Val *lt, Val *eq, bool need_eq) {
+static void lex_tree(Eng &E, std::vector<Val> lts, std::vector<Val> eqs, Val *lt, Val *eq, bool need_eq,
+                     bool need_lt = true) {
     while (lts.size() > 1) {
         std::vector<Val> nl, ne;
         for (size_t i = 0; i + 1 < lts.size(); i += 2) {
-            nl.push_back(vadd(E, lts[i + 1], vmul(E, eqs[i + 1], lts[i])));
+            nl.push_back(need_lt ? vadd(E, lts[i + 1], vmul(E, eqs[i + 1], lts[i])) : VC(0));
             bool last_round = lts.size() <= 2;
             if (need_eq || !last_round) ne.push_back(vmul(E, eqs[i + 1], eqs[i]));
             else ne.push_back(VC(0));
@@ -1459,18 +1482,19 @@ static void lex_tree(Eng &E, std::vector<Val> lts, std::vector<Val> eqs, Val *lt
     *eq = eqs[0];
 }
 
-static void lex_slots(Eng &E, Val *lt, Val *eq, bool need_eq) {
+static void lex_slots(Eng &E, Val *lt, Val *eq, bool need_eq, bool need_lt = true) {
     bc_ctx *X = E.X;
     const uint32_t l = X->l;
     for (uint32_t sh = 1; sh < l; sh <<= 1) {
         const bool last = (sh << 1) >= l;
         const uint64_t *mask = ctx_pt(X, "ksm:" + std::to_string(sh), ksm_slots(X, sh), E.st);
         const uint64_t *inv = ctx_pt(X, "ksi:" + std::to_string(sh), ksi_slots(X, sh), E.st);   // 1 - mask, every slot
-        CT hi_lt = E.ptmul(E.rotate(lt->ct, sh), mask);
         CT hi_eq = E.add_pt(E.ptmul(E.rotate(eq->ct, sh), mask), inv);
-        Val nlt = vadd(E, VT(hi_lt), vmul(E, VT(hi_eq), *lt));
+        if (need_lt) {
+            CT hi_lt = E.ptmul(E.rotate(lt->ct, sh), mask);
+            *lt = vadd(E, VT(hi_lt), vmul(E, VT(hi_eq), *lt));
+        }
         if (need_eq || !last) *eq = vmul(E, VT(hi_eq), *eq);
-        *lt = nlt;
     }
 }
 
@@ -1478,7 +1502,8 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
     bc_ctx *X = E.X;
     const uint32_t d = X->d, B = a.B;
     std::vector<Val> lts, eqs;
-    const bool need_eq = eq != nullptr;
+    const bool need_eq = eq != nullptr, need_lt = lt != nullptr;   // EQ only: no LT products at all
+    if (!need_lt && !need_eq) BC_THROW(BC_E_INTERNAL, "compare: nothing requested");
     if (X->prm.circuit == 'U') {
         CT z = E.add(a, E.scalar(b, -1));
         std::vector<CT> digs = extract_batch(E, z);
@@ -1486,9 +1511,9 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
         CT all = digs[0];
         all.B = d * B;
         Val L, Q;
-        univariate(E, VT(all), &L, &Q);
+        univariate(E, VT(all), need_lt ? &L : nullptr, &Q);
         for (uint32_t i = 0; i < d; ++i) {
-            lts.push_back(VT(E.sub(L.ct, i * B, B)));
+            lts.push_back(need_lt ? VT(E.sub(L.ct, i * B, B)) : VC(0));
             eqs.push_back(VT(E.sub(Q.ct, i * B, B)));
         }
     } else {
@@ -1498,16 +1523,16 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
         xa.B = d * B;
         xb.B = d * B;
         Val L, Q;
-        bivariate(E, VT(xa), VT(xb), &L, &Q);
+        bivariate(E, VT(xa), VT(xb), need_lt ? &L : nullptr, &Q);
         for (uint32_t i = 0; i < d; ++i) {
-            lts.push_back(VT(E.sub(L.ct, i * B, B)));
+            lts.push_back(need_lt ? VT(E.sub(L.ct, i * B, B)) : VC(0));
             eqs.push_back(VT(E.sub(Q.ct, i * B, B)));
         }
     }
     Val LT, EQ;
-    lex_tree(E, lts, eqs, &LT, &EQ, need_eq || X->l > 1);
-    if (X->l > 1) lex_slots(E, &LT, &EQ, need_eq);
-    *lt = LT.ct;
+    lex_tree(E, lts, eqs, &LT, &EQ, need_eq || X->l > 1, need_lt);
+    if (X->l > 1) lex_slots(E, &LT, &EQ, need_eq, need_lt);
+    if (lt) *lt = LT.ct;
     if (eq) *eq = EQ.ct;
 }
 
@@ -1528,6 +1553,68 @@ CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2) {
     CT c = broadcast_batch(E, cond);
     CT diff = E.add(x1, E.scalar(x2, -1));
     return E.add(x2, E.mul(c, diff));
+}
+
+// R24 x^e (left-to-right binary: per bit below the top, square, then multiply by x if the bit is 1)
+CT power_batch(Eng &E, const CT &x, uint32_t e) {
+    if (e < 1) BC_THROW(BC_E_ARG, "power: exponent must be >= 1");
+    int top = 31;
+    while (!((e >> top) & 1u)) --top;
+    CT acc = x;
+    for (int b = top - 1; b >= 0; --b) {
+        acc = E.mul(acc, acc);
+        if ((e >> b) & 1u) acc = E.mul(acc, x);
+    }
+    return acc;
+}
+
+// N copies of a one-ciphertext batch
+static CT replicate(Eng &E, const CT &one, uint32_t N) {
+    std::vector<CT> parts(N, E.sub(one, 0, 1));
+    if (N == 1) {
+        CT o = E.ct_alloc(1, one.lvl, one.parts);
+        if (!E.dry()) CK(cudaMemcpyAsync(o.d, one.d, (size_t)o.bstride * 8, cudaMemcpyDeviceToDevice, E.st));
+        return o;
+    }
+    return concat_batch(E, parts);
+}
+
+// R24 private_q (Listings 3-5): out_i = ((D_i + op1) c_0 + (D_i op1) c_1) + D_i^e c_2, c_j = bcast(EQ(q,
+// code_j)).  S (optional): the branch evaluation (EQs + broadcasts) runs on S's stream and arena (Listing 5's
+// helper thread, S26), ordered after everything already on E's stream and joined by an event before the
+// combination; the host never waits.  Bits equal the blocking order (every operation is deterministic).
+CT private_query_batch(Eng &E, Eng *S, const CT &data, const CT &q, const CT &codes, const CT &op1, uint32_t e) {
+    if (q.B != 1 || op1.B != 1 || codes.B != 3) BC_THROW(BC_E_ARG, "private_query: q, op1 batch 1, codes batch 3");
+    Eng &C = S ? *S : E;
+    cudaEvent_t ready = nullptr, done = nullptr;
+    if (S && !E.dry()) {
+        CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        CK(cudaEventRecord(ready, E.st));
+        CK(cudaStreamWaitEvent(C.st, ready, 0));
+    }
+    CT masks;
+    {
+        CT qrep = replicate(C, q, 3);
+        CT eq;
+        compare_batch(C, qrep, codes, nullptr, &eq);     // EQ only (R24 reads no LT)
+        masks = broadcast_batch(C, eq);
+    }
+    if (S && !E.dry()) CK(cudaEventRecord(done, C.st));
+    const uint32_t N = data.B;
+    CT op1r = replicate(E, op1, N);
+    CT d1 = E.add(data, op1r);
+    CT d2 = E.mul(data, op1r);
+    CT d3 = power_batch(E, data, e);
+    if (S && !E.dry()) {
+        CK(cudaStreamWaitEvent(E.st, done, 0));
+        CK(cudaEventDestroy(ready));
+        CK(cudaEventDestroy(done));
+    }
+    CT m0 = replicate(E, E.sub(masks, 0, 1), N), m1 = replicate(E, E.sub(masks, 1, 1), N),
+       m2 = replicate(E, E.sub(masks, 2, 1), N);
+    CT acc = E.add(E.mul(d1, m0), E.mul(d2, m1));
+    return E.add(acc, E.mul(d3, m2));
 }
 
 // one contiguous batch from several batches of equal level (a single view is returned as is)

@@ -164,6 +164,8 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq);
 CT select_batch(Eng &E, const CT &cond, const CT &x1, const CT &x2);
 std::vector<CT> extract_batch(Eng &E, const CT &a);
 CT broadcast_batch(Eng &E, const CT &cond);
+CT power_batch(Eng &E, const CT &x, uint32_t e);                       // R24
+CT private_query_batch(Eng &E, Eng *S, const CT &data, const CT &q, const CT &codes, const CT &op1, uint32_t e);
 CT concat_batch(Eng &E, const std::vector<CT> &parts);
 CT tournament_batch(Eng &E, std::vector<CT> elems, bool is_max);
 std::vector<CT> sort_batch(Eng &E, const std::vector<CT> &x);

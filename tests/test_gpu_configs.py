@@ -177,3 +177,85 @@ def test_full_size_c2_compare_matches_oracle_digest(pair, name, golden):
     assert list(E.shape) == g["shape"]
     assert [int(x) for x in E[:, :, :4].reshape(-1)] == g["first4_per_limb"]
     assert _digest(E) == g["sha256"]
+
+
+def _pq_inputs(T, rng, N, qv, idx0):
+    """R24 private_q inputs: N data ciphertexts and op1 (F_p slot values), q and the codes 1, 2, 3 as
+    words in every block; product and oracle encryptions of the same values (same seeds / indices)"""
+    P, A = T.P, T.P.alg
+    ints = T.ctx.ints_per_ct
+    X = np.zeros((N, A.S, A.D), dtype=np.int16)
+    X[:, :, 0] = rng.integers(0, P.p, (N, A.S))
+    Y = np.zeros((1, A.S, A.D), dtype=np.int16)
+    Y[:, :, 0] = rng.integers(0, P.p, (1, A.S))
+    data = T.ctx.encrypt_slots(T.keys, X, SEED_ENC, ct_index0=idx0)
+    op1 = T.ctx.encrypt_slots(T.keys, Y, SEED_ENC, ct_index0=idx0 + N)
+    q = T.ctx.encrypt(T.keys, np.array([[qv] * ints], dtype=np.uint64), SEED_ENC, ct_index0=idx0 + N + 1)
+    codes = T.ctx.encrypt(T.keys, np.array([[c] * ints for c in (1, 2, 3)], dtype=np.uint64), SEED_ENC,
+                          ct_index0=idx0 + N + 2)
+    return X, Y, data, op1, q, codes
+
+
+def _pq_want(P, X, Y, qv, e):
+    x, y = X[..., 0].astype(np.int64), Y[0, :, 0].astype(np.int64)
+    if qv == 1:
+        return (x + y) % P.p
+    if qv == 2:
+        return (x * y) % P.p
+    if qv == 3:
+        return np.vectorize(lambda t: pow(int(t), e, P.p))(x)
+    return 0 * x
+
+
+@pytest.mark.slow
+def test_private_query_shadow_bit_exact(pair):
+    """R24 private_q (f4) on the p3 shadow ring (m = 111, 4 x 2 hypercube, (d,l) = (8,4), 13 + 4 primes):
+    the blocking and the non-blocking (second stream) query give bit-identical ciphertexts, equal to the
+    oracle's, decrypting to Data^e in every integer-block slot"""
+    import torch
+    from oracle import circuits
+    T = pair("p3s")
+    P, A = T.P, T.P.alg
+    rng = np.random.default_rng(61)
+    N, e, qv = 2, 3, 3
+    X, Y, data, op1, q, codes = _pq_inputs(T, rng, N, qv, 700)
+    blk = T.ctx.private_query(T.keys, data, q, codes, op1, e)
+    side = torch.cuda.Stream()
+    nb = T.ctx.private_query(T.keys, data, q, codes, op1, e, side_stream=side)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_u64(blk), to_u64(nb))
+    ev = circuits.OracleEval(P, T.okeys)
+    od = [T.bgv.encrypt(P, T.okeys, A.encode(X[i].astype(np.int64)), SEED_ENC, 700 + i) for i in range(N)]
+    oy = T.bgv.encrypt(P, T.okeys, A.encode(Y[0].astype(np.int64)), SEED_ENC, 700 + N)
+    oq = T.oracle_ct([qv] * P.ints_per_ct, 700 + N + 1)
+    oc = [T.oracle_ct([c] * P.ints_per_ct, 700 + N + 2 + j) for j, c in enumerate((1, 2, 3))]
+    oo = circuits.private_query(ev, od, oq, oc, oy, e, P.circuit, P.d, P.l, P.ints_per_ct)
+    got = to_u64(blk)
+    for i in range(N):
+        assert np.array_equal(got[i], T.ct_eval(oo[i]))
+    dec = T.ctx.decrypt_slots(T.keys, blk)
+    covered = np.array([(s % A.S1) < (A.S1 // P.l) * P.l for s in range(A.S)])
+    want = _pq_want(P, X, Y, qv, e)
+    assert np.array_equal(dec[:, covered, 0], want[:, covered])
+
+
+@pytest.mark.parametrize("qv", [1, 3])
+def test_private_query_p3_full_size(pair, qv):
+    """R24 at the paper's p3 ring (m = 20197, n = 19116, 1062 x 2 hypercube): non-blocking == blocking
+    bit for bit, and the result decrypts to the query's semantics in every integer-block slot"""
+    import torch
+    T = pair("p3q")
+    P, A = T.P, T.P.alg
+    rng = np.random.default_rng(62 + qv)
+    N, e = 3, 64
+    X, Y, data, op1, q, codes = _pq_inputs(T, rng, N, qv, 0)
+    blk = T.ctx.private_query(T.keys, data, q, codes, op1, e)
+    side = torch.cuda.Stream()
+    nb = T.ctx.private_query(T.keys, data, q, codes, op1, e, side_stream=side)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_u64(blk), to_u64(nb))
+    dec = T.ctx.decrypt_slots(T.keys, nb)
+    covered = np.array([(s % A.S1) < (A.S1 // P.l) * P.l for s in range(A.S)])
+    want = _pq_want(P, X, Y, qv, e)
+    assert np.array_equal(dec[:, covered, 0], want[:, covered])
+    assert not dec[:, ~covered].any()

@@ -181,7 +181,8 @@ def test_ops_match_oracle(pair, cfg):
 
 @pytest.mark.parametrize("cfg", ["c1", "c1l2"])
 def test_compare_matches_oracle(pair, cfg):
-    """a7-a9 end to end: compare_lt / compare_eq ciphertexts bit-exact; decrypted bits = [a<b]."""
+    """a7-a9 end to end: compare_lt / compare_eq ciphertexts bit-exact; decrypted bits = [a<b]; the
+    EQ-only call (no LT products) returns the same EQ ciphertext."""
     from oracle import circuits
     T = pair(cfg)
     P = T.P
@@ -201,6 +202,8 @@ def test_compare_matches_oracle(pair, cfg):
     assert np.array_equal(to_u64(eq)[0], T.ct_eval(oeq))
     lt2 = T.ctx.compare_lt(T.keys, ca, cb)
     assert np.array_equal(to_u64(lt2), to_u64(lt))
+    eq2 = T.ctx.compare_eq(T.keys, ca, cb)          # the EQ-only schedule (no LT products)
+    assert np.array_equal(to_u64(eq2), to_u64(eq))
 
 
 def test_extract_matches_oracle(pair):
