@@ -38,6 +38,8 @@
 //    the quotient as a sparse sum of shifted copies (k_ir_sparse) when Phi_m^{-1} mod x^(m-n) is short.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "nttf_core.cuh"
 
 namespace bc {
@@ -106,6 +108,192 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         need(v, bd, k, LIM_MUL, q, qi);
         __stcs(dst + rp * CC + c, (T.dbg & 2) ? fred(v[k], q, qi) : fmm8(v[k], xt[rp * CC + c], q, qi));
     }
+}
+
+// pass A, persistent (forward Bluestein): CTA (column group, g) runs jobs g, g + G, ... of its column group.
+// The group's chirp and cross-twiddle tiles (per prime) stay in shared memory across those jobs, and each
+// thread prefetches the next job's inputs into a shared staging tile with cp.async (LDGSTS) while the
+// current job is transformed; every thread reads back exactly the words it copied, so cp.async.wait_group
+// suffices (no barrier).  Results are identical to kf_passA (same arithmetic, same order).
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int LOGR, int LOGE, int TC, int LOGC>
+struct PersistA {
+    static constexpr int R = 1 << LOGR, E = 1 << LOGE;
+    typedef PtTab<LOGR, LOGE, true> PTT;
+    // doubles: exchange R*TC, chirp tile (R/2)*TC, cross-twiddle tile R*TC, staging (R/2)*TC; int32 position
+    // tile (R/2)*TC (inverse gather); double2: twiddles
+    static constexpr size_t SMEM = ((size_t)R * TC * 2 + (size_t)R * TC) * 8 + (size_t)(R / 2) * TC * 4 +
+                                   ((size_t)R / 2 + PTT::WORDS) * 16;
+};
+
+// INV 0: forward (input t < n), 1: inverse (input gathered through pos[t], t < m)
+template <int LOGR, int LOGE, int TC, int LOGC, int INV>
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
+    kf_passA_p(NttTables T, const uint64_t *__restrict__ in, uint64_t in_pstride, LimbMap lm, uint64_t job0, uint32_t nj,
+               double *__restrict__ scratch) {
+    typedef PersistA<LOGR, LOGE, TC, LOGC> PA;
+    constexpr int E = 1 << LOGE, R = 1 << LOGR;
+    constexpr uint32_t CC = 1u << LOGC;
+    extern __shared__ double smf[];
+    double *scol = smf, *ttf = scol + R * TC, *txt = ttf + (R / 2) * TC;
+    uint64_t *stage = (uint64_t *)(txt + R * TC);
+    double2 *stw = (double2 *)(stage + (R / 2) * TC), *spt = stw + R / 2;
+    int32_t *tpos = (int32_t *)(spt + PA::PTT::WORDS);
+    const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
+    const uint32_t c = blockIdx.x * TC + col;
+    const uint32_t G = gridDim.y;
+    const uint32_t tlim = INV ? T.m : T.n;
+    // the position tile does not depend on the prime: filled once
+    for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+        const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+        tpos[i] = INV ? (t < T.m ? T.pos[t] : -1) : (t < T.n ? (int32_t)t : -1);
+    }
+    __syncthreads();
+    uint32_t cur_pr = 0xffffffffu;
+    auto prefetch = [&](uint32_t jj) {
+        const JobF Jn = job_f(lm, (uint32_t)(job0 + jj));
+        const uint64_t *sn = in + (uint64_t)Jn.poly * in_pstride + (uint64_t)Jn.lb * T.n;
+#pragma unroll
+        for (int k = 0; k < E / 2; ++k) {
+            const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
+            const int ps = tpos[r * TC + col];
+            if (ps >= 0) cp_async8(stage + r * TC + col, sn + ps);
+        }
+        cp_async_commit();
+    };
+    if (blockIdx.y < nj) prefetch(blockIdx.y);
+    for (uint32_t jj = blockIdx.y; jj < nj; jj += G) {
+        const JobF J = job_f(lm, (uint32_t)(job0 + jj));
+        const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+        if (J.pr != cur_pr) {           // uniform over the CTA: the tiles of this prime
+            __syncthreads();
+            const double2 *gtw = T.ftwRb + (uint64_t)J.pr * (R / 2);
+            for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = gtw[j];
+            if (col == 0) PA::PTT::fill(spt, tau, gtw);
+            const double *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m, *xt = T.fxta + (uint64_t)J.pr * T.M;
+            for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+                const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+                ttf[i] = t < tlim ? tf[t] : 0.0;
+            }
+            for (int i = threadIdx.x; i < R * TC; i += blockDim.x)
+                txt[i] = xt[(uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC)];
+            cur_pr = J.pr;
+            __syncthreads();
+        }
+        cp_async_wait_all();            // this thread's staged inputs of job jj
+        double v[E];
+        int bd[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            if (k >= E / 2) {           // rows >= R/2: the zero half of the Bluestein input
+                v[k] = 0.0;
+                bd[k] = 0;
+                continue;
+            }
+            const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
+            v[k] = tpos[r * TC + col] >= 0 ? fmm8(from_u64(stage[r * TC + col]), ttf[r * TC + col], q, qi) : 0.0;
+            bd[k] = UMUL8;
+        }
+        if (jj + G < nj) prefetch(jj + G);   // the next job's inputs while this one is transformed
+        fct_pass<LOGR, LOGE, true, TC, 0>(v, bd, tau, col, scol, stw, spt, q, qi);
+        double *dst = scratch + (uint64_t)jj * T.M;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const uint32_t rp = held_index<LOGE>(tau, 0, k);
+            need(v, bd, k, LIM_MUL, q, qi);
+            __stcs(dst + rp * CC + c, fmm8(v[k], txt[rp * TC + col], q, qi));
+        }
+    }
+    cp_async_wait_all();
+}
+
+// pass C, persistent: column inverse + output chirp + Z_m^* gather (INV 0) or A_t - A_{m-1} (INV 1, prime m,
+// corner[] from kf_corner).  As kf_passA_p: per-prime output-chirp tile and the position tile in shared
+// memory, the next job's pass-B output prefetched with cp.async while this one is transformed.
+template <int LOGR, int LOGE, int TC, int LOGC>
+struct PersistC {
+    static constexpr int R = 1 << LOGR;
+    typedef PtTab<LOGR, LOGE, false> PTT;
+    // doubles: exchange R*TC, staging R*TC, chirp tile (R/2)*TC; int32 positions (R/2)*TC; double2 twiddles
+    static constexpr size_t SMEM = ((size_t)R * TC * 2 + (size_t)(R / 2) * TC) * 8 + (size_t)(R / 2) * TC * 4 +
+                                   ((size_t)R / 2 + PTT::WORDS) * 16;
+};
+
+template <int LOGR, int LOGE, int TC, int LOGC, int INV>
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
+    kf_passC_p(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride, LimbMap lm, uint64_t job0, uint32_t nj,
+               const double *__restrict__ scratch, const uint64_t *__restrict__ corner) {
+    typedef PersistC<LOGR, LOGE, TC, LOGC> PC;
+    constexpr int E = 1 << LOGE, R = 1 << LOGR;
+    constexpr uint32_t CC = 1u << LOGC;
+    extern __shared__ double smf[];
+    double *scol = smf, *stage = scol + R * TC, *tfo = stage + R * TC;
+    int32_t *tpos = (int32_t *)(tfo + (R / 2) * TC);
+    double2 *stw = (double2 *)(tpos + (R / 2) * TC), *spt = stw + R / 2;
+    const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
+    const uint32_t c = blockIdx.x * TC + col;
+    const uint32_t G = gridDim.y;
+    for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+        const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+        tpos[i] = INV ? (t < T.n ? (int32_t)t : -1) : (t < T.m ? T.pos[t] : -1);
+    }
+    __syncthreads();
+    uint32_t cur_pr = 0xffffffffu;
+    auto prefetch = [&](uint32_t jj) {
+        const double *src = scratch + (uint64_t)jj * T.M;
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const uint32_t rp = held_index<LOGE>(tau, 0, k);
+            cp_async8(stage + rp * TC + col, src + rp * CC + c);
+        }
+        cp_async_commit();
+    };
+    if (blockIdx.y < nj) prefetch(blockIdx.y);
+    for (uint32_t jj = blockIdx.y; jj < nj; jj += G) {
+        const JobF J = job_f(lm, (uint32_t)(job0 + jj));
+        const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+        if (J.pr != cur_pr) {
+            __syncthreads();
+            const double2 *gtw = T.ftwRi + (uint64_t)J.pr * (R / 2);
+            for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = gtw[j];
+            if (col == 0) PC::PTT::fill(spt, tau, gtw);
+            const double *tf = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
+            for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+                const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+                tfo[i] = t < T.m ? tf[t] : 0.0;
+            }
+            cur_pr = J.pr;
+            __syncthreads();
+        }
+        cp_async_wait_all();
+        double v[E];
+        int bd[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            v[k] = stage[held_index<LOGE>(tau, 0, k) * TC + col];
+            bd[k] = UMUL8;
+        }
+        if (jj + G < nj) prefetch(jj + G);
+        fct_pass<LOGR, LOGE, false, TC, 0>(v, bd, tau, col, scol, stw, spt, q, qi);
+        uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
+        const uint64_t cn = INV ? corner[jj] : 0;
+#pragma unroll
+        for (int k = 0; k < E / 2; ++k) {   // rows >= R/2: t >= M/2 >= m, never output
+            const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
+            const int ps = tpos[r * TC + col];
+            if (ps < 0) continue;
+            need(v, bd, k, LIM_MUL, q, qi);
+            const uint64_t x = to_u64(fmm8(v[k], tfo[r * TC + col], q, qi), q);
+            __stcs(dst + ps, INV ? (x >= cn ? x - cn : x + (uint64_t)q - cn) : x);
+        }
+    }
+    cp_async_wait_all();
 }
 
 // pass B: row forward (length C), x D^, row inverse, x psi^(-c brev(r)); block = RB rows x C/E threads
@@ -269,7 +457,8 @@ struct Shape {
 
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_ = 8, int RB_ = 0>
 static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
-                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
+                 uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf,
+                 bool persist = false) {
     typedef Shape<LOGR, LOGER, LOGC, LOGEC, TC_, RB_> S;
     static std::atomic<uint64_t> init_dev{0};
     if (attr_pending(init_dev)) {
@@ -285,7 +474,43 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
     NttTables T = T0;
     T.dbg = g_ntt_dbg;
     dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
-    if (!inv) {
+    // persistent passes A and C (tiles of the prime resident in shared memory, cp.async prefetch of the next job)
+    if (persist && LOGR == 8 && !T.dbg && (!inv || (T.prime_m && corner_buf))) {
+        typedef PersistA<LOGR, LOGER, S::TC, LOGC> PA;
+        typedef PersistC<LOGR, LOGER, S::TC, LOGC> PC;
+        static std::atomic<uint64_t> init_p{0};
+        static int nbA[64] = {0}, nbC[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (attr_pending(init_p)) {
+            for (int d = 0; d < 2; ++d) {
+                auto ka = d ? kf_passA_p<LOGR, LOGER, S::TC, LOGC, 1> : kf_passA_p<LOGR, LOGER, S::TC, LOGC, 0>;
+                auto kc = d ? kf_passC_p<LOGR, LOGER, S::TC, LOGC, 1> : kf_passC_p<LOGR, LOGER, S::TC, LOGC, 0>;
+                cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
+                cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
+            }
+            int b = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, S::TC, LOGC, 0>, S::THA, PA::SMEM);
+            nbA[dev & 63] = b > 0 ? b : 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, S::TC, LOGC, 0>, S::THA, PC::SMEM);
+            nbC[dev & 63] = b > 0 ? b : 1;
+            attr_done(init_p);
+        }
+        const uint32_t ncg = (1u << LOGC) / S::TC;
+        const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbA[dev & 63] * 148) / ncg));
+        const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbC[dev & 63] * 148) / ncg));
+        if (!inv) {
+            kf_passA_p<LOGR, LOGER, S::TC, LOGC, 0><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+            kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
+            kf_passC_p<LOGR, LOGER, S::TC, LOGC, 0><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
+        } else {
+            kf_passA_p<LOGR, LOGER, S::TC, LOGC, 1><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+            kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
+            kf_corner<LOGR><<<nj, 32, 0, st>>>(T, lm, j0, scr, corner_buf);
+            kf_passC_p<LOGR, LOGER, S::TC, LOGC, 1><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner_buf);
+            launch_counter() += 1;
+        }
+    } else if (!inv) {
         kf_passA<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
         kf_passC<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
@@ -383,6 +608,7 @@ bool nttf_supported(const NttTables &T) {
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
 #define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf)
+#define RUNP(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf, true)
     switch (T.logR * 16 + T.logC) {
         case 8 * 16 + 8:
             switch (g_ntt_impl) {
@@ -391,13 +617,16 @@ void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
                 case 14: RUNF(8, 4, 8, 4, 16, 4); break;
                 case 15: RUNF(8, 4, 8, 4, 32); break;
                 case 16: RUNF(8, 4, 8, 4, 16); break;
-                default: RUNF(8, 4, 8, 4, 16, 16); break;      // measured best (1.015 us per limb-transform)
+                case 17: RUNF(8, 4, 8, 4, 16, 16); break;     // non-persistent A / C (round-1 default)
+                default: RUNP(8, 4, 8, 4, 16, 16); break;      // persistent A / C: 0.865 us per C2 limb-transform
+                                                               // (0.923 with the non-persistent passes)
             }
             break;
         case 8 * 16 + 9:
             if (g_ntt_impl == 12) RUNF(8, 4, 9, NTTF_LOGE_89, 8);
             else if (g_ntt_impl == 13) RUNF(8, 4, 9, NTTF_LOGE_89, 16, 8);
-            else RUNF(8, 4, 9, NTTF_LOGE_89, 16);
+            else if (g_ntt_impl == 17) RUNF(8, 4, 9, NTTF_LOGE_89, 16);
+            else RUNP(8, 4, 9, NTTF_LOGE_89, 16);
             break;
         case 7 * 16 + 8: RUNF(7, 4, 8, 4, 16); break;
         case 7 * 16 + 7: RUNF(7, 4, 7, 4, 16); break;
@@ -407,6 +636,7 @@ void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
         default: break;
     }
 #undef RUNF
+#undef RUNP
 }
 
 }  // namespace bc
