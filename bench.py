@@ -627,7 +627,7 @@ def run_compact_compare(args, cfg, rank, world, local):
     lvl_c = ctx.n_cipher - 1
     lvl_out = ctx.out_level(lvl_c, 0)
     out = ctx.ct_empty(Bd, lvl_out)
-    da, db = ctx.ct_empty(Bs, lvl_c), ctx.ct_empty(Bs, lvl_c)
+    da, db = ctx.ct_empty(Bd + 2, lvl_c), ctx.ct_empty(Bd + 2, lvl_c)   # Fig. 7 pattern: 4 -> 1
     dest = np.zeros((Bs, ints), dtype=np.int32)
     nout = bc._u32(0)
     uptr = useful.ctypes.data

@@ -253,6 +253,11 @@ bc_status bc_extract(bc_ctx *ctx, const bc_keys *keys, bc_ct a, void *d_out, voi
  * out has capacity n_in cts at level in.level - 1; *n_out is set; h_dest[n_in * ints]
  * receives the destination block (out_ct * ints_per_ct + block) of every useful block,
  * -1 elsewhere. */
+/* host only (no device): the R17 plan bc_compact uses for a usefulness pattern (nin x ints bytes, 1 =
+ * useful): dest[c*ints + b] = c' * ints + b' (its output ciphertext and block) or -1; wpr = blocks per
+ * row (R6).  BC_E_ARG on null pointers, ints = 0, wpr = 0 or wpr > ints. */
+bc_status bc_compact_plan(uint32_t ints, uint32_t span, uint32_t wpr, const uint8_t *h_useful, uint32_t nin,
+                          int32_t *h_dest, uint32_t *n_out);
 bc_status bc_compact(bc_ctx *ctx, const bc_keys *keys, bc_ct in, const uint8_t *h_useful,
                      bc_ct out, uint32_t *n_out, int32_t *h_dest, void *d_ws, size_t ws_bytes,
                      void *stream);

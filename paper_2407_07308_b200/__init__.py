@@ -110,6 +110,7 @@ _sig("bc_graph_capture_begin", _st, _vp)
 _sig("bc_graph_capture_end", _st, _vp, ctypes.POINTER(_vp))
 _sig("bc_graph_launch", _st, _vp, _vp)
 _sig("bc_graph_destroy", None, _vp)
+_sig("bc_compact_plan", _st, _u32, _u32, _u32, _vp, _u32, _vp, ctypes.POINTER(_u32))
 _sig("bc_compact", _st, _vp, _vp, bc_ct, _vp, bc_ct, ctypes.POINTER(_u32), _vp, _vp, _sz, _vp)
 
 EXPORTS = [n for n in dir(_lib) if n.startswith("bc_")]
@@ -183,6 +184,17 @@ class Graph:
         if self._g is not None and _lib is not None:
             _lib.bc_graph_destroy(self._g)
             self._g = None
+
+
+def compact_plan(useful, span=3, wpr=None):
+    """host only: the library's R17 plan of a usefulness matrix [nin][ints] -> (dest [nin][ints], n_out)"""
+    useful = np.ascontiguousarray(useful, dtype=np.uint8)
+    nin, ints = useful.shape
+    dest = np.zeros((nin, ints), dtype=np.int32)
+    n = _u32()
+    _check(_lib.bc_compact_plan(ints, span, wpr or ints, useful.ctypes.data, nin, dest.ctypes.data, ctypes.byref(n)),
+           "bc_compact_plan")
+    return dest, n.value
 
 
 def launch_count(reset=False):

@@ -71,6 +71,7 @@ bc_status bc_ctx_create(const bc_params *prm, int device, bc_ctx **out) {
 
 void bc_ctx_destroy(bc_ctx *ctx) {
     if (!ctx) return;
+    compact_plans_release(ctx);
     ctx_free(ctx);
     delete ctx;
 }

@@ -3,6 +3,8 @@
 // and one rotation; one modulus switch per output at the end.
 #include <algorithm>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <set>
 
 #include "engine.h"
@@ -23,38 +25,62 @@ static std::vector<int32_t> offsets(uint32_t span) {
     return o;
 }
 
-// mirrors oracle/circuits.py plan_compaction (independent implementation of R17)
+// mirrors oracle/circuits.py plan_compaction (independent implementation of R17).  Output occupancy
+// and the candidate targets of each offset are bitmaps over the ints blocks, so one (output, offset)
+// candidate costs ints/64 word operations; full outputs are skipped and a candidate placing every
+// remaining block ends the scan (no later candidate can exceed it: the first maximum wins).
 static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful, uint32_t ints, uint32_t span,
                                uint32_t *n_out, uint32_t wpr) {
-    // a rotation by delta*l moves a block within its row of wpr blocks only (R6 rows, R17)
     auto fits = [&](uint32_t b, int32_t dl) {
         const int64_t t = (int64_t)b - dl, pos = (int64_t)(b % wpr) - dl;
         return t >= 0 && t < (int64_t)ints && pos >= 0 && pos < (int64_t)wpr;
     };
-    std::vector<std::set<int64_t>> occ;
+    const uint32_t W = (ints + 63) / 64;
+    std::vector<std::vector<uint64_t>> occ;     // [output][W]
+    std::vector<uint32_t> freen;                // free blocks per output
     std::vector<Group> groups;
     const std::vector<int32_t> offs = offsets(span);
+    std::vector<std::vector<uint64_t>> cand(offs.size(), std::vector<uint64_t>(W));
     for (uint32_t c = 0; c < useful.size(); ++c) {
         std::vector<uint32_t> rem = useful[c];
         while (!rem.empty()) {
-            int best_cp = -1, best_dl = 0;
-            size_t best_cnt = 0;
-            for (uint32_t cp = 0; cp < occ.size(); ++cp)
-                for (int32_t dl : offs) {
-                    size_t cnt = 0;
-                    for (uint32_t b : rem) {
-                        int64_t t = (int64_t)b - dl;
-                        if (fits(b, dl) && !occ[cp].count(t)) ++cnt;
+            for (size_t o = 0; o < offs.size(); ++o) {
+                std::fill(cand[o].begin(), cand[o].end(), 0);
+                for (uint32_t b : rem)
+                    if (fits(b, offs[o])) {
+                        const uint32_t t = (uint32_t)((int64_t)b - offs[o]);
+                        cand[o][t >> 6] |= 1ull << (t & 63);
                     }
-                    if (cnt > best_cnt) { best_cnt = cnt; best_cp = (int)cp; best_dl = dl; }
+            }
+            int best_cp = -1, best_o = 0;
+            size_t best_cnt = 0;
+            for (uint32_t cp = 0; cp < occ.size() && best_cnt < rem.size(); ++cp) {
+                if (!freen[cp]) continue;
+                for (size_t o = 0; o < offs.size(); ++o) {
+                    size_t cnt = 0;
+                    for (uint32_t w = 0; w < W; ++w) cnt += (size_t)__builtin_popcountll(cand[o][w] & ~occ[cp][w]);
+                    if (cnt > best_cnt) {
+                        best_cnt = cnt;
+                        best_cp = (int)cp;
+                        best_o = (int)o;
+                        if (cnt == rem.size()) break;
+                    }
                 }
-            if (best_cp < 0) { occ.emplace_back(); best_cp = (int)occ.size() - 1; best_dl = 0; }
-            Group g{c, (uint32_t)best_cp, best_dl, {}};
+            }
+            if (best_cp < 0) {
+                occ.emplace_back(W, 0);
+                freen.push_back(ints);
+                best_cp = (int)occ.size() - 1;
+                best_o = 0;             // offset 0
+            }
+            const int32_t dl = offs[best_o];
+            Group g{c, (uint32_t)best_cp, dl, {}};
             std::vector<uint32_t> left;
             for (uint32_t b : rem) {
-                int64_t t = (int64_t)b - best_dl;
-                if (fits(b, best_dl) && !occ[best_cp].count(t)) {
-                    occ[best_cp].insert(t);
+                const int64_t t = (int64_t)b - dl;
+                if (fits(b, dl) && !((occ[best_cp][t >> 6] >> (t & 63)) & 1)) {
+                    occ[best_cp][t >> 6] |= 1ull << (t & 63);
+                    --freen[best_cp];
                     g.blocks.push_back(b);
                 } else {
                     left.push_back(b);
@@ -66,6 +92,46 @@ static std::vector<Group> plan(const std::vector<std::vector<uint32_t>> &useful,
     }
     *n_out = (uint32_t)occ.size();
     return groups;
+}
+
+// plans are cached in the context by their usefulness pattern (the exact bitmap is compared, the hash
+// only indexes): repeated compactions of the same layout (every step of a workload) plan once
+struct CachedPlan {
+    std::vector<uint8_t> mask;
+    uint32_t ints, span, wpr, nout;
+    std::vector<Group> groups;
+};
+static std::mutex g_plan_mu;
+static std::map<std::pair<const bc_ctx *, uint64_t>, std::vector<std::shared_ptr<CachedPlan>>> g_plans;
+
+static std::shared_ptr<CachedPlan> plan_cached(const bc_ctx *X, const uint8_t *h_useful, uint32_t nin, uint32_t ints,
+                                               uint32_t span, uint32_t wpr) {
+    const size_t nb = (size_t)nin * ints;
+    uint64_t h = 1469598103934665603ull ^ ((uint64_t)nin << 32 ^ ints ^ (uint64_t)span << 48 ^ (uint64_t)wpr << 20);
+    for (size_t i = 0; i < nb; ++i) h = (h ^ (h_useful[i] ? 1u : 0u)) * 1099511628211ull;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto &bucket = g_plans[{X, h}];
+    for (auto &p : bucket)
+        if (p->ints == ints && p->span == span && p->wpr == wpr && p->mask.size() == nb) {
+            bool same = true;
+            for (size_t i = 0; i < nb && same; ++i) same = (p->mask[i] != 0) == (h_useful[i] != 0);
+            if (same) return p;
+        }
+    auto p = std::make_shared<CachedPlan>();
+    p->mask.assign(h_useful, h_useful + nb);
+    p->ints = ints; p->span = span; p->wpr = wpr;
+    std::vector<std::vector<uint32_t>> useful(nin);
+    for (uint32_t c = 0; c < nin; ++c)
+        for (uint32_t b = 0; b < ints; ++b)
+            if (h_useful[(size_t)c * ints + b]) useful[c].push_back(b);
+    p->groups = plan(useful, ints, span, &p->nout, wpr);
+    if (bucket.size() < 8) bucket.push_back(p);
+    return p;
+}
+void compact_plans_release(const bc_ctx *X) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (auto it = g_plans.begin(); it != g_plans.end();)
+        it = it->first.first == X ? g_plans.erase(it) : std::next(it);
 }
 
 // 0/1 block mask as an evaluation-form plaintext, cached in the context by its block set
@@ -82,6 +148,31 @@ static const uint64_t *mask_pt(Eng &E, const std::vector<uint32_t> &blocks) {
 
 }  // namespace bc
 
+// host only: the R17 plan of a usefulness pattern (dest[c*ints + b] = c' * ints + b' or -1), for tests
+extern "C" bc_status bc_compact_plan(uint32_t ints, uint32_t span, uint32_t wpr, const uint8_t *h_useful, uint32_t nin,
+                                     int32_t *h_dest, uint32_t *n_out) {
+    try {
+        if (!h_useful || !h_dest || !n_out || !ints || !wpr || wpr > ints) BC_THROW(BC_E_ARG, "bad argument");
+        std::vector<std::vector<uint32_t>> useful(nin);
+        for (uint32_t c = 0; c < nin; ++c)
+            for (uint32_t b = 0; b < ints; ++b)
+                if (h_useful[(size_t)c * ints + b]) useful[c].push_back(b);
+        uint32_t nout = 0;
+        std::vector<Group> groups = plan(useful, ints, span ? span : 3, &nout, wpr);
+        for (size_t i = 0; i < (size_t)nin * ints; ++i) h_dest[i] = -1;
+        for (const Group &g : groups)
+            for (uint32_t b : g.blocks) h_dest[(size_t)g.c * ints + b] = (int32_t)(g.cp * ints + (uint32_t)((int64_t)b - g.dl));
+        *n_out = nout;
+    } catch (BcError &e) {
+        last_error() = e.msg;
+        return e.st;
+    } catch (std::exception &e) {
+        last_error() = e.what();
+        return BC_E_INTERNAL;
+    }
+    return BC_OK;
+}
+
 extern "C" bc_status bc_compact(bc_ctx *X, const bc_keys *keys, bc_ct in, const uint8_t *h_useful, bc_ct out,
                                 uint32_t *n_out, int32_t *h_dest, void *ws, size_t wsb, void *stv) {
     try {
@@ -89,13 +180,10 @@ extern "C" bc_status bc_compact(bc_ctx *X, const bc_keys *keys, bc_ct in, const 
         if (in.level < 2) BC_THROW(BC_E_LEVEL, "compaction needs one level");
         if (out.level != in.level - 1) BC_THROW(BC_E_LEVEL, "output level must be input level - 1");
         const uint32_t ints = X->ints, nin = in.batch;
-        std::vector<std::vector<uint32_t>> useful(nin);
-        for (uint32_t c = 0; c < nin; ++c)
-            for (uint32_t b = 0; b < ints; ++b)
-                if (h_useful[(size_t)c * ints + b]) useful[c].push_back(b);
-        uint32_t nout = 0;
         const uint32_t span = X->prm.compact_span ? X->prm.compact_span : 3;
-        std::vector<Group> groups = plan(useful, ints, span, &nout, X->alg.words_per_row(X->l));
+        std::shared_ptr<CachedPlan> P = plan_cached(X, h_useful, nin, ints, span, X->alg.words_per_row(X->l));
+        const uint32_t nout = P->nout;
+        const std::vector<Group> &groups = P->groups;
         if (nout > out.batch) BC_THROW(BC_E_ARG, "output capacity too small");
         if (h_dest) {
             for (size_t i = 0; i < (size_t)nin * ints; ++i) h_dest[i] = -1;

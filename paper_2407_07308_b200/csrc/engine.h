@@ -172,4 +172,6 @@ std::vector<CT> sort_batch(Eng &E, const std::vector<CT> &x);
 
 void circuit_plan(int64_t p, char circuit, int schedule, int *k, int *muls, int *depth);
 
+void compact_plans_release(const bc_ctx *X);   // compact.cu: drop the context's cached plans
+
 }  // namespace bc

@@ -58,3 +58,25 @@ def test_circuit_plan_matches_oracle():
             assert bc.circuit_plan(p, kind, "r23") == (k,) + c._r23_cost(f, p, k)
     with pytest.raises(bc.BoostComError):
         bc.circuit_plan(15, "U", "r23")
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_compact_plan_matches_oracle(seed):
+    """host logic, no device: bc_compact's R17 plan (bitmap implementation) equals the oracle's
+    plan_compaction on random and Fig. 7 usefulness patterns, with and without row limits"""
+    import numpy as np
+    import paper_2407_07308_b200 as bc
+    from oracle import circuits
+    rng = np.random.default_rng(seed)
+    for nin, ints, wpr, dens in ((9, 40, 40, 0.3), (12, 36, 12, 0.2), (20, 64, 16, 0.25), (6, 30, 10, 0.6)):
+        useful = (rng.random((nin, ints)) < dens).astype(np.uint8)
+        if seed == 2:
+            useful[:] = 0
+            useful[:, 3::4] = 1          # Fig. 7 (P:493-495): every 4th block
+        dest, n = bc.compact_plan(useful, 3, wpr)
+        _, n_o, dest_o = circuits.plan_compaction([list(np.nonzero(u)[0]) for u in useful], ints, 3, wpr)
+        assert n == n_o
+        want = np.full((nin, ints), -1, dtype=np.int32)
+        for (c, b), (cp, bp) in dest_o.items():
+            want[c, b] = cp * ints + bp
+        assert np.array_equal(dest, want)
