@@ -35,7 +35,9 @@ class Params:
         self.l = int(cfg["l"])
         self.ring = Ring(self.m)
         self.n = self.ring.n
-        self.M = bluestein_pad(self.m)
+        self.bluestein = cfg.get("bluestein", "pow2")      # R25: "mixed" -> mixed-radix length
+        assert self.bluestein in ("pow2", "mixed")
+        self.M = bluestein_pad(self.m, self.bluestein == "mixed")
         mod = lcm(self.p, self.m, self.M)
         self.q = prime_chain(mod, int(cfg["cipher_bits"]), int(cfg["n_cipher"]), exclude={self.p})
         self.P = prime_chain(mod, int(cfg["special_bits"]), int(cfg["n_special"]),

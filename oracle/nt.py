@@ -67,11 +67,20 @@ def mult_order(a, m):
     return k
 
 
-def bluestein_pad(m):
-    """M = smallest power of two >= 2m - 1 ("length power of two greater than 2m-1")."""
+def bluestein_pad(m, mixed=False):
+    """M = smallest power of two >= 2m - 1 ("length power of two greater than 2m-1").
+    mixed (R25): the smallest length >= 2m - 1 among the powers of two and
+    256 r N' with r in {3, 5, 7, 9}, N' in {32, 64, 128} (the mixed-radix lengths the transform
+    supports); the convolution is exact at any length >= 2m - 1, so only the primes (R1) depend on it."""
     M = 1
     while M < 2 * m - 1:
         M *= 2
+    if mixed:
+        for r in (3, 5, 7, 9):
+            for nn in (32, 64, 128):
+                L = 256 * r * nn
+                if 2 * m - 1 <= L < M:
+                    M = L
     return M
 
 

@@ -178,3 +178,25 @@ def test_reduce_int_matches_sympy(m):
     r = sympy.Poly(c[::-1], x).rem(sympy.cyclotomic_poly(m, x, polys=True))
     want = [int(v) for v in r.all_coeffs()[::-1]]
     assert R.reduce_int(c) == want + [0] * (R.n - len(want))
+
+
+def test_bluestein_pad_mixed_lengths():
+    """R25 (f3): the mixed-radix Bluestein length of each large ring, by hand from the candidate set
+    {2^k} U {256 r N' : r in {3,5,7,9}, N' in {32,64,128}}: C4 (m = 34511, 2m-1 = 69021) -> 9*8192 =
+    73728; C5 (41761 -> 83521) -> 3*32768 = 98304; C3 (52053 -> 104105) -> 7*16384 = 114688;
+    p3 (20197 -> 40393) -> 5*8192 = 40960; C2 (30941 -> 61881) stays 65536 (P:316's power of two);
+    the minimum over the candidate set by brute force; primes = 1 mod lcm(p, m, M)"""
+    assert nt.bluestein_pad(34511, True) == 73728
+    assert nt.bluestein_pad(41761, True) == 98304
+    assert nt.bluestein_pad(52053, True) == 114688
+    assert nt.bluestein_pad(20197, True) == 40960
+    assert nt.bluestein_pad(30941, True) == 65536
+    cands = sorted({2 ** k for k in range(1, 20)} | {256 * r * nn for r in (3, 5, 7, 9) for nn in (32, 64, 128)})
+    for m in (91, 859, 1423, 1871, 20197, 30941, 34511, 41761, 52053):
+        assert nt.bluestein_pad(m, True) == min(L for L in cands if L >= 2 * m - 1)
+        assert nt.bluestein_pad(m, True) <= nt.bluestein_pad(m)
+    from oracle import bgv
+    from conftest import load_cfg
+    cfg = dict(load_cfg("c4"), bluestein="mixed")
+    P = bgv.Params(cfg)
+    assert P.M == 73728 and all(q % nt.lcm(P.p, P.m, 73728) == 1 for q in P.moduli)
