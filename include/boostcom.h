@@ -69,6 +69,9 @@ typedef struct {
     uint32_t schedule;       /* digit circuits: 0 or 16 = R16, 23 = R23 baby-step / giant-step (SURVEY
                               * §8(f) f2: "2p-6 (Bivariate case) and sqrt(p-3)+O(log p)
                               * (Univariate case)"); anything else -> BC_E_PARAM */
+    uint32_t bluestein;      /* 0: power-of-two Bluestein length; 1: mixed radix (R25, SURVEY §8(f)
+                              * f3: the smallest 256 r N' or 2^k >= 2m - 1; prime m, shapes 9 x 32 and
+                              * 3 x 128 -- others BC_E_PARAM) */
 } bc_params;
 
 typedef struct {

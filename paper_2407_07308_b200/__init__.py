@@ -29,7 +29,8 @@ class bc_params(ctypes.Structure):
                 ("d", ctypes.c_uint32), ("l", ctypes.c_uint32),
                 ("n_cipher", ctypes.c_uint32), ("cipher_bits", ctypes.c_uint32),
                 ("n_special", ctypes.c_uint32), ("special_bits", ctypes.c_uint32),
-                ("alpha", ctypes.c_uint32), ("compact_span", ctypes.c_uint32), ("schedule", ctypes.c_uint32)]
+                ("alpha", ctypes.c_uint32), ("compact_span", ctypes.c_uint32), ("schedule", ctypes.c_uint32),
+                ("bluestein", ctypes.c_uint32)]
 
 
 class bc_info(ctypes.Structure):
@@ -236,7 +237,8 @@ class Context:
         prm = bc_params(int(cfg["p"]), int(cfg["m"]), cfg.get("circuit", "U").encode(), int(cfg["d"]),
                         int(cfg["l"]), int(cfg["n_cipher"]), int(cfg["cipher_bits"]),
                         int(cfg["n_special"]), int(cfg["special_bits"]), int(cfg["alpha"]),
-                        int(cfg.get("compact_span", 3)), _SCHEDULES[cfg.get("schedule", "r16")])
+                        int(cfg.get("compact_span", 3)), _SCHEDULES[cfg.get("schedule", "r16")],
+                        {"pow2": 0, "mixed": 1}[cfg.get("bluestein", "pow2")])
         h = _vp()
         with torch.cuda.device(self.device):
             _check(_lib.bc_ctx_create(ctypes.byref(prm), device, ctypes.byref(h)), "bc_ctx_create")
@@ -558,12 +560,20 @@ class Context:
 
 
 def load_params(name_or_path):
+    """params/<name>.json (or a path); "<name>@pow2" / "@mixed" sets the Bluestein length (R25),
+    "<name>@r16" / "@r23" the digit circuits (R16 / R23)"""
     import json
-    path = name_or_path
+    name, _, opt = name_or_path.partition("@")
+    path = name
     if not os.path.exists(path):
-        path = os.path.join(_HERE, "..", "params", name_or_path + ".json")
+        path = os.path.join(_HERE, "..", "params", name + ".json")
     with open(path) as f:
-        return json.load(f)
+        cfg = json.load(f)
+    if opt in ("pow2", "mixed"):
+        cfg["bluestein"] = opt
+    elif opt:
+        cfg["schedule"] = opt
+    return cfg
 
 
 # ------------------------------------------------------------------------------------------

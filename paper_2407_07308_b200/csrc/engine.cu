@@ -106,6 +106,31 @@ static void host_ntt(std::vector<uint64_t> &a, uint64_t w, uint64_t q) {  // nat
     }
 }
 
+// natural in/out NTT of any length N = r * 2^k (r odd, 3 or 9 here), root w of order N: decimation in time,
+// X[k] = sum_{i < r} w^{i k} Y_i[k mod N/r], Y_i = NTT_{N/r}(a[i::r]) with root w^r (exact)
+static void host_ntt_any(std::vector<uint64_t> &a, uint64_t w, uint64_t q) {
+    const size_t N = a.size();
+    if ((N & (N - 1)) == 0) { host_ntt(a, w, q); return; }
+    size_t r = 3;
+    while (N % r) r += 2;
+    const size_t Nr = N / r;
+    std::vector<std::vector<uint64_t>> Y(r, std::vector<uint64_t>(Nr));
+    for (size_t i = 0; i < r; ++i) {
+        for (size_t j = 0; j < Nr; ++j) Y[i][j] = a[j * r + i];
+        host_ntt_any(Y[i], powmod_h(w, r, q), q);
+    }
+    for (size_t k = 0; k < N; ++k) {
+        uint64_t acc = 0;
+        const uint64_t wk = powmod_h(w, k, q);
+        uint64_t f = 1;
+        for (size_t i = 0; i < r; ++i) {
+            acc = (acc + mulmod_h(f, Y[i][k % Nr], q)) % q;
+            f = mulmod_h(f, wk, q);
+        }
+        a[k] = acc;
+    }
+}
+
 static uint32_t brev_h(uint32_t x, uint32_t bits) {
     uint32_t r = 0;
     for (uint32_t i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
@@ -243,13 +268,32 @@ void ctx_build(bc_ctx *X) {
     X->p = P.p; X->m = P.m; X->d = P.d; X->l = P.l;
     X->M = 1;
     while (X->M < 2 * X->m - 1) X->M <<= 1;
-    uint32_t lg = 0;
-    while ((1u << lg) < X->M) ++lg;
-    X->logR = lg / 2; X->logC = lg - X->logR;
-    X->R = 1u << X->logR; X->C = 1u << X->logC;
     X->phi = cyclotomic(X->m);
     X->n = (uint32_t)X->phi.size() - 1;
     X->prime_m = is_prime_small(X->m);
+    // R25 (f3): the smallest of {2^k} U {256 r N'} (r in 3,5,7,9; N' in 32,64,128) >= 2m - 1
+    X->rad = 1;
+    X->logN = 0;
+    if (P.bluestein > 1) BC_THROW(BC_E_PARAM, "bluestein must be 0 (power of two) or 1 (mixed radix)");
+    if (P.bluestein == 1) {
+        for (uint32_t r : {3u, 5u, 7u, 9u})
+            for (uint32_t lg : {5u, 6u, 7u}) {
+                const uint32_t L = (256u * r) << lg;
+                if (2 * X->m - 1 <= L && L < X->M) { X->M = L; X->rad = r; X->logN = lg; }
+            }
+        if (X->rad > 1 && !X->prime_m) BC_THROW(BC_E_PARAM, "mixed-radix Bluestein lengths need a prime m (R25)");
+        if (X->rad > 1 && !((X->rad == 9 && X->logN == 5) || (X->rad == 3 && X->logN == 7)))
+            BC_THROW(BC_E_PARAM, "mixed-radix shape " + std::to_string(X->rad) + " x 2^" + std::to_string(X->logN) +
+                                     " not implemented (R25: 9 x 32, 3 x 128)");
+    }
+    if (X->rad == 1) {
+        uint32_t lg = 0;
+        while ((1u << lg) < X->M) ++lg;
+        X->logR = lg / 2; X->logC = lg - X->logR;
+        X->R = 1u << X->logR; X->C = 1u << X->logC;
+    } else {
+        X->logR = 8; X->R = 256; X->C = X->M / 256; X->logC = 0;
+    }
     // primes (R1)
     uint64_t L = X->p;
     auto lcm = [](uint64_t a, uint64_t b) { return a / gcd_u64(a, b) * b; };
@@ -340,23 +384,29 @@ void ctx_build(bc_ctx *X) {
             Di[j] = wp[e];
             if (j) { Df[M - j] = wip[e]; Di[M - j] = wp[e]; }
         }
-        host_ntt(Df, ps, q);
-        host_ntt(Di, ps, q);
+        host_ntt_any(Df, ps, q);
+        host_ntt_any(Di, ps, q);
+        const uint32_t NNs = 1u << X->logN;
         for (uint32_t rp = 0; rp < X->R; ++rp)
             for (uint32_t cp = 0; cp < X->C; ++cp) {
-                uint32_t k = brev_h(rp, X->logR) + X->R * brev_h(cp, X->logC);
+                // pass layout: power-of-two rows, bit-reversed column and row frequencies; mixed rows (R25):
+                // sub-row i = cp / N', position pp (bit-reversed sub-row frequency): k2 = i + rad brev(pp)
+                const uint32_t k2 = X->rad == 1 ? brev_h(cp, X->logC)
+                                                : cp / NNs + X->rad * brev_h(cp % NNs, X->logN);
+                const uint32_t k = brev_h(rp, X->logR) + X->R * k2;
                 dhf[(size_t)i * M + (size_t)rp * X->C + cp] = sh2(Df[k], q);
                 dhi[(size_t)i * M + (size_t)rp * X->C + cp] = sh2(Di[k], q);
             }
     }
     // register-pass twiddles omega_L^{+-j} (j < L/2), omega_L = psi^{M/L}
-    std::vector<u64x2> twR((size_t)NP * (X->R / 2)), twRi((size_t)NP * (X->R / 2)), twC((size_t)NP * (X->C / 2)),
-        twCi((size_t)NP * (X->C / 2));
+    const uint32_t CL = X->rad == 1 ? X->C : (1u << X->logN);   // row register transform length (R25: N')
+    std::vector<u64x2> twR((size_t)NP * (X->R / 2)), twRi((size_t)NP * (X->R / 2)), twC((size_t)NP * (CL / 2)),
+        twCi((size_t)NP * (CL / 2));
     for (uint32_t i = 0; i < NP; ++i) {
         const uint64_t q = X->moduli[i];
         const uint64_t ps = psi[(size_t)i * M + 1].w, psinv = invmod_h(ps, q);
         const uint64_t wR = powmod_h(ps, M / X->R, q), wRi = powmod_h(psinv, M / X->R, q);
-        const uint64_t wC = powmod_h(ps, M / X->C, q), wCi = powmod_h(psinv, M / X->C, q);
+        const uint64_t wC = powmod_h(ps, M / CL, q), wCi = powmod_h(psinv, M / CL, q);
         uint64_t a = 1, b = 1;
         for (uint32_t j = 0; j < X->R / 2; ++j) {
             twR[(size_t)i * (X->R / 2) + j] = sh2(a, q);
@@ -364,9 +414,9 @@ void ctx_build(bc_ctx *X) {
             a = mulmod_h(a, wR, q); b = mulmod_h(b, wRi, q);
         }
         a = 1; b = 1;
-        for (uint32_t j = 0; j < X->C / 2; ++j) {
-            twC[(size_t)i * (X->C / 2) + j] = sh2(a, q);
-            twCi[(size_t)i * (X->C / 2) + j] = sh2(b, q);
+        for (uint32_t j = 0; j < CL / 2; ++j) {
+            twC[(size_t)i * (CL / 2) + j] = sh2(a, q);
+            twCi[(size_t)i * (CL / 2) + j] = sh2(b, q);
             a = mulmod_h(a, wC, q); b = mulmod_h(b, wCi, q);
         }
     }
@@ -389,9 +439,9 @@ void ctx_build(bc_ctx *X) {
             for (uint32_t r = 0; r < X->R; ++r) {
                 const uint32_t k1 = brev_h(r, X->logR);
                 for (uint32_t c = 0; c < X->C; ++c) {
-                    const uint32_t e1 = (c * k1) & (M - 1);
+                    const uint32_t e1 = (uint32_t)(((uint64_t)c * k1) % M);
                     xta[(size_t)i * M + (size_t)r * X->C + c] = psi[(size_t)i * M + e1];
-                    xtb[(size_t)i * M + (size_t)r * X->C + c] = psi[(size_t)i * M + ((M - e1) & (M - 1))];
+                    xtb[(size_t)i * M + (size_t)r * X->C + c] = psi[(size_t)i * M + (M - e1) % M];
                 }
             }
             (void)q;
@@ -432,22 +482,47 @@ void ctx_build(bc_ctx *X) {
             std::vector<double2> fm(NP);
             for (uint32_t i = 0; i < NP; ++i) fm[i] = make_double2((double)X->moduli[i], 1.0 / (double)X->moduli[i]);
             T.ftwRb = fd(brv_tab(twR, X->R / 2, X->logR - 1), X->R / 2);
-            T.ftwCb = fd(brv_tab(twC, X->C / 2, X->logC - 1), X->C / 2);
+            const uint32_t logCL = X->rad == 1 ? X->logC : X->logN;
+            T.ftwCb = fd(brv_tab(twC, CL / 2, logCL - 1), CL / 2);
             T.ftwRi = fd(twRi, X->R / 2);
-            T.ftwCi = fd(twCi, X->C / 2);
+            T.ftwCi = fd(twCi, CL / 2);
             T.ftf1 = fd1(tf1, m); T.ftf1i = fd1(tf1i, m); T.ftfo = fd1(tfo, m); T.ftfoi = fd1(tfoi, m);
             {
-                const uint32_t le = (uint32_t)nttf_row_loge(X->logR, X->logC), E = 1u << le, tpr = X->C >> le;
+                // thread-minor order of pass B: position t E + k of a (sub-)row of length L at k (L / E) + t
+                const uint32_t le = X->rad == 1 ? (uint32_t)nttf_row_loge(X->logR, X->logC) : (uint32_t)nttf_mr_loge(X->rad, X->logN);
+                const uint32_t E = 1u << le, L = X->rad == 1 ? X->C : (1u << X->logN), tpr = L >> le;
                 auto perm = [&](const std::vector<u64x2> &v) {
                     std::vector<u64x2> o(v.size());
                     for (size_t i = 0; i < NP; ++i)
                         for (uint32_t r = 0; r < X->R; ++r)
-                            for (uint32_t t = 0; t < tpr; ++t)
-                                for (uint32_t k = 0; k < E; ++k)
-                                    o[i * M + (size_t)r * X->C + k * tpr + t] = v[i * M + (size_t)r * X->C + t * E + k];
+                            for (uint32_t s0 = 0; s0 < X->C; s0 += L)
+                                for (uint32_t t = 0; t < tpr; ++t)
+                                    for (uint32_t k = 0; k < E; ++k)
+                                        o[i * M + (size_t)r * X->C + s0 + k * tpr + t] = v[i * M + (size_t)r * X->C + s0 + t * E + k];
                     return o;
                 };
                 T.fdhf = fd1(perm(dhf), M); T.fdhi = fd1(perm(dhi), M);
+            }
+            if (X->rad > 1) {
+                // R25 row radix tables: omega_C^{+-i j} at i N' + j, omega_rad^{+-j} (j < rad), omega_C = psi^{M/C}
+                const uint32_t NNs = 1u << X->logN, C = X->C;
+                std::vector<u64x2> rtw((size_t)NP * C), rtwi((size_t)NP * C), rc((size_t)NP * 16, u64x2{0, 0}),
+                    rci((size_t)NP * 16, u64x2{0, 0});
+                for (uint32_t i = 0; i < NP; ++i) {
+                    const uint64_t q = X->moduli[i], ps = psi[(size_t)i * M + 1].w, psinv = invmod_h(ps, q);
+                    const uint64_t wc = powmod_h(ps, M / C, q), wci = powmod_h(psinv, M / C, q);
+                    for (uint32_t a = 0; a < X->rad; ++a)
+                        for (uint32_t j = 0; j < NNs; ++j) {
+                            rtw[(size_t)i * C + a * NNs + j] = sh2(powmod_h(wc, (uint64_t)a * j, q), q);
+                            rtwi[(size_t)i * C + a * NNs + j] = sh2(powmod_h(wci, (uint64_t)a * j, q), q);
+                        }
+                    const uint64_t wr = powmod_h(wc, NNs, q), wri = powmod_h(wci, NNs, q);
+                    for (uint32_t j = 0; j < X->rad; ++j) {
+                        rc[(size_t)i * 16 + j] = sh2(powmod_h(wr, j, q), q);
+                        rci[(size_t)i * 16 + j] = sh2(powmod_h(wri, j, q), q);
+                    }
+                }
+                T.frtw = fd1(rtw, C); T.frtwi = fd1(rtwi, C); T.frcon = fd1(rc, 16); T.frconi = fd1(rci, 16);
             }
             T.fxta = fd1(xta, M); T.fxtb = fd1(xtb, M);
             T.fmods = dev_upload(X, fm);
@@ -558,6 +633,7 @@ void ctx_build(bc_ctx *X) {
     T.twR = dev_upload(X, twR); T.twRi = dev_upload(X, twRi); T.twC = dev_upload(X, twC); T.twCi = dev_upload(X, twCi);
     T.pos = dev_upload(X, pos); T.z = dev_upload(X, z); T.phi = dev_upload(X, phi8); T.mods = X->d_mods;
     T.m = m; T.n = n; T.M = M; T.R = X->R; T.C = X->C; T.logR = X->logR; T.logC = X->logC;
+    T.rad = X->rad; T.logN = X->logN;
     T.prime_m = X->prime_m ? 1 : 0;
 
     // ---------------- lift plans ----------------

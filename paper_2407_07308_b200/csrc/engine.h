@@ -61,6 +61,7 @@ struct bc_ctx {
     bc_params prm;
     int device = 0;
     uint32_t p, m, n, M, R, C, logR, logC, L1, K, alpha, dnum, d, l, base, ints;
+    uint32_t rad = 1, logN = 0;       // R25 mixed-radix rows: C = rad 2^logN (rad = 1: C = 2^logC)
     bool prime_m;
     std::vector<uint64_t> moduli, omega;
     std::vector<int64_t> phi;

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <stdexcept>
 #include <vector>
 
 #include "kernels.h"
@@ -345,12 +346,14 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
         attr_done(attr_set_dev);
     }
     lm.npoly = npoly;
+    if (T.rad > 1 && !((g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T)))
+        throw std::runtime_error("mixed-radix Bluestein lengths (R25) run on the binary64 passes only");
     // L2-sized job groups: the scratch of one group (A -> B -> C) stays resident in the 126 MB L2
     const bool vf = (g_ntt_impl == 0 || g_ntt_impl >= 10) && nttf_supported(T);   // 20: fused cluster kernel (below)
     // composite m on the binary64 path: Barrett reduction mod Phi_m (needs a second M-word slot per job)
     const bool barrett = inv && vf && !T.prime_m && T.tb != nullptr;
     const uint64_t chunk = ntt_group_jobs(T, jobs, barrett);
-    const bool v2 = g_ntt_impl != 1 && ntt2_supported(T);
+    const bool v2 = g_ntt_impl != 1 && (ntt2_supported(T) || (T.rad > 1 && vf));   // R25 rows: binary64 only
     for (uint64_t j0 = 0; j0 < jobs; j0 += chunk) {
         const uint32_t nj = (uint32_t)((jobs - j0) < chunk ? (jobs - j0) : chunk);
         dim3 gA(T.C >> lTC, nj), gB(T.R >> lTR, nj);

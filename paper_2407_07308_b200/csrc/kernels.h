@@ -54,6 +54,11 @@ struct NttTables {
     int ir_nnz;                       //   (the quotient is then a sum of shifted copies, no convolution)
     int q_in_s2;                      // mode 3 reads Q from the scr2 slot (sparse quotient) instead of A_{n..}
     uint32_t m, n, M, R, C, logR, logC;
+    // R25 mixed-radix rows (f3): C = rad * 2^logN (rad in {3, 9}); ftwCb / ftwCi then hold the length-2^logN
+    // sub-row twiddles.  rad = 1: power-of-two rows (C = 2^logC)
+    uint32_t rad = 1, logN = 0;
+    const double *frtw = nullptr, *frtwi = nullptr;     // [P][C]: omega_C^{+-i j} at i 2^logN + j
+    const double *frcon = nullptr, *frconi = nullptr;   // [P][16]: omega_rad^{+-j}, j < rad
     int prime_m;
     int dbg;              // ntt3.cu timing experiments only (bc_tune "ntt_dbg"): skip table reads; results invalid          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
 };
@@ -178,6 +183,7 @@ void ntt2_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st);
 // binary64-FMA passes (ntt3.cu)
 bool nttf_supported(const NttTables &T);
+int nttf_mr_loge(uint32_t rad, uint32_t logN);     // registers per thread (log2) of the mixed-radix sub-row transforms
 int nttf_row_loge(uint32_t logR, uint32_t logC);   // D^ (fdhf/fdhi) layout: position r*C + tau*E + k at r*C + k*(C/E) + tau
 // corner_buf (prime m, inverse): nj words; pass C then writes the reduction mod Phi_m directly (no k_reduce_prime)
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,

@@ -122,7 +122,7 @@ __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int LOGR, int LOGE, int TC, int LOGC>
+template <int LOGR, int LOGE, int TC, int CCV>
 struct PersistA {
     static constexpr int R = 1 << LOGR, E = 1 << LOGE;
     typedef PtTab<LOGR, LOGE, true> PTT;
@@ -133,13 +133,13 @@ struct PersistA {
 };
 
 // INV 0: forward (input t < n), 1: inverse (input gathered through pos[t], t < m)
-template <int LOGR, int LOGE, int TC, int LOGC, int INV>
+template <int LOGR, int LOGE, int TC, int CCV, int INV>
 __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
     kf_passA_p(NttTables T, const uint64_t *__restrict__ in, uint64_t in_pstride, LimbMap lm, uint64_t job0, uint32_t nj,
                double *__restrict__ scratch) {
-    typedef PersistA<LOGR, LOGE, TC, LOGC> PA;
+    typedef PersistA<LOGR, LOGE, TC, CCV> PA;
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
-    constexpr uint32_t CC = 1u << LOGC;
+    constexpr uint32_t CC = CCV;          // columns (a power of two, or 256 r N' for the mixed-radix lengths)
     extern __shared__ double smf[];
     double *scol = smf, *ttf = scol + R * TC, *txt = ttf + (R / 2) * TC;
     uint64_t *stage = (uint64_t *)(txt + R * TC);
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
 // pass C, persistent: column inverse + output chirp + Z_m^* gather (INV 0) or A_t - A_{m-1} (INV 1, prime m,
 // corner[] from kf_corner).  As kf_passA_p: per-prime output-chirp tile and the position tile in shared
 // memory, the next job's pass-B output prefetched with cp.async while this one is transformed.
-template <int LOGR, int LOGE, int TC, int LOGC>
+template <int LOGR, int LOGE, int TC, int CCV>
 struct PersistC {
     static constexpr int R = 1 << LOGR;
     typedef PtTab<LOGR, LOGE, false> PTT;
@@ -225,13 +225,13 @@ struct PersistC {
                                    ((size_t)R / 2 + PTT::WORDS) * 16;
 };
 
-template <int LOGR, int LOGE, int TC, int LOGC, int INV>
+template <int LOGR, int LOGE, int TC, int CCV, int INV>
 __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
     kf_passC_p(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride, LimbMap lm, uint64_t job0, uint32_t nj,
                const double *__restrict__ scratch, const uint64_t *__restrict__ corner) {
-    typedef PersistC<LOGR, LOGE, TC, LOGC> PC;
+    typedef PersistC<LOGR, LOGE, TC, CCV> PC;
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
-    constexpr uint32_t CC = 1u << LOGC;
+    constexpr uint32_t CC = CCV;
     extern __shared__ double smf[];
     double *scol = smf, *stage = scol + R * TC, *tfo = stage + R * TC;
     int32_t *tpos = (int32_t *)(tfo + (R / 2) * TC);
@@ -347,6 +347,143 @@ __global__ void __launch_bounds__(RB * (1 << (LOGC - LOGE)), FNTT_MINB(RB * (1 <
     }
 }
 
+// ---- R25 mixed-radix rows (f3): C = RAD * 2^LOGN.  Forward row DFT by decimation in frequency:
+//   u_i[j] = omega_C^{i j} * DFT_RAD(x_j, x_{j+N'}, ..., x_{j+(RAD-1)N'})_i   (j < N' = 2^LOGN, i < RAD),
+//   X[i + RAD k'] = NTT_N'(u_i)[k'] (the power-of-two sub-row transforms of the register passes, output
+//   bit-reversed: sub-row i, position p holds k' = brev(p)); the inverse runs the steps backwards with the
+//   inverse roots (unnormalised, as every inverse here).  Any exact DFT algorithm gives the same residues.
+// small DFTs (fmm8 products; inputs |x| <= q, outputs |y| <= 3q)
+__device__ __forceinline__ void dft3(double &a, double &b, double &c, double w, double q, double qi) {
+    // y0 = a + b + c, y1 = (a - c) + w (b - c), y2 = (a - b) - w (b - c)   (1 + w + w^2 = 0)
+    const double t = fmm8(__dsub_rn(b, c), w, q, qi);
+    const double y0 = __dadd_rn(__dadd_rn(a, b), c);
+    const double y1 = __dadd_rn(__dsub_rn(a, c), t);
+    const double y2 = __dsub_rn(__dsub_rn(a, b), t);
+    a = y0; b = y1; c = y2;
+}
+template <int RAD>
+__device__ __forceinline__ void dft_small(double (&x)[RAD], const double *__restrict__ w, double q, double qi) {
+    static_assert(RAD == 3 || RAD == 9, "radix");
+    if (RAD == 3) {
+        dft3(x[0], x[1], x[2], w[1], q, qi);
+    } else {
+        // 9 = 3 x 3: A[n2][k1] = DFT3_n1(x[3 n1 + n2]); B = A * w9^{n2 k1}; X[k1 + 3 k2] = DFT3_n2(B[n2][k1])
+        const double w3 = w[3];
+        double a[3][3];
+#pragma unroll
+        for (int n2 = 0; n2 < 3; ++n2) {
+            a[n2][0] = x[n2]; a[n2][1] = x[3 + n2]; a[n2][2] = x[6 + n2];
+            dft3(a[n2][0], a[n2][1], a[n2][2], w3, q, qi);
+        }
+#pragma unroll
+        for (int n2 = 0; n2 < 3; ++n2)
+#pragma unroll
+            for (int k1 = 0; k1 < 3; ++k1)
+                a[n2][k1] = (n2 && k1) ? fmm8(a[n2][k1], w[n2 * k1], q, qi) : fred(a[n2][k1], q, qi);
+#pragma unroll
+        for (int k1 = 0; k1 < 3; ++k1) {
+            double b0 = a[0][k1], b1 = a[1][k1], b2 = a[2][k1];
+            dft3(b0, b1, b2, w3, q, qi);
+            x[k1] = b0; x[k1 + 3] = b1; x[k1 + 6] = b2;
+        }
+    }
+}
+
+// pass B, mixed-radix rows: RB rows per block, each split into RAD sub-rows of N' = 2^LOGN (TPS = N'/E threads
+// each).  Radix stage and the sub-row transforms exchange through one shared buffer of RB*RAD padded sub-rows.
+template <int LOGN, int LOGE, int RB, int INV, int RAD>
+__global__ void __launch_bounds__(RB * RAD * (1 << (LOGN - LOGE)))
+    kf_passB_mr(NttTables T, LimbMap lm, uint64_t job0, double *__restrict__ scratch) {
+    constexpr int E = 1 << LOGE, NN = 1 << LOGN, TPS = NN / E, C = RAD * NN;
+    constexpr int ROWW = NN + NN / E;
+    extern __shared__ double smf[];
+    const uint32_t job = (uint32_t)(job0 + blockIdx.y);
+    const JobF J = job_f(lm, job);
+    const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+    const uint32_t sr = threadIdx.x / TPS, tau = threadIdx.x % TPS;   // sub-row sr = rr RAD + i of this block
+    const uint32_t rr = sr / RAD, i = sr % RAD, row = blockIdx.x * RB + rr;
+    double *buf = smf;
+    double *rtw = buf + RB * RAD * ROWW, *rtwi = rtw + C, *rc = rtwi + C, *rci = rc + 16;
+    typedef PtTab<LOGN, LOGE, true> PTF;
+    typedef PtTab<LOGN, LOGE, false> PTI;
+    double2 *tw = (double2 *)(rci + 16), *twi = tw + NN / 2, *ptf = twi + NN / 2, *pti = ptf + PTF::WORDS;
+    const double2 *gtw = T.ftwCb + (uint64_t)J.pr * (NN / 2), *gtwi = T.ftwCi + (uint64_t)J.pr * (NN / 2);
+    for (int j = threadIdx.x; j < NN / 2; j += blockDim.x) {
+        tw[j] = gtw[j];
+        twi[j] = gtwi[j];
+    }
+    for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        rtw[j] = T.frtw[(uint64_t)J.pr * C + j];
+        rtwi[j] = T.frtwi[(uint64_t)J.pr * C + j];
+    }
+    if (threadIdx.x < 16) {
+        rc[threadIdx.x] = T.frcon[(uint64_t)J.pr * 16 + threadIdx.x];
+        rci[threadIdx.x] = T.frconi[(uint64_t)J.pr * 16 + threadIdx.x];
+    }
+    if (sr == 0) PTF::fill(ptf, tau, gtw);
+    if (sr == 1 % (RB * RAD)) PTI::fill(pti, tau, gtwi);
+    __syncthreads();
+    double *grow0 = scratch + (uint64_t)blockIdx.y * T.M + (uint64_t)blockIdx.x * RB * C;
+    // forward radix stage: (row, j) -> u_i[j] into sub-row buffers (natural order, padded)
+    for (int idx = threadIdx.x; idx < RB * NN; idx += blockDim.x) {
+        const int r2 = idx / NN, j = idx % NN;
+        const double *g = grow0 + (uint64_t)r2 * C;
+        double x[RAD];
+#pragma unroll
+        for (int l = 0; l < RAD; ++l) x[l] = __ldcs(g + j + l * NN);   // |x| <= q (pass A output)
+        dft_small<RAD>(x, rc, q, qi);
+#pragma unroll
+        for (int l = 0; l < RAD; ++l) buf[(r2 * RAD + l) * ROWW + j + (j >> LOGE)] = fmm8(x[l], rtw[l * NN + j], q, qi);
+    }
+    __syncthreads();
+    double *srow = buf + sr * ROWW;
+    double v[E];
+    int bd[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        const uint32_t e = held_index<LOGE>(tau, LOGN - LOGE, k);
+        v[k] = srow[e + (e >> LOGE)];
+        bd[k] = UMUL8;
+    }
+    __syncthreads();
+    frt_pass<LOGN, LOGE, true, 0>(v, bd, tau, srow, tw, ptf, q, qi);
+    // D^ in the sub-row thread-minor layout: position tau E + k of sub-row i at row C + i N' + k TPS + tau
+    const double *dh = (INV == 0 ? T.fdhf : T.fdhi) + (uint64_t)J.pr * T.M + (uint64_t)row * C + i * NN + tau;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+        need(v, bd, k, LIM_MUL, q, qi);
+        v[k] = fmm8(v[k], dh[k * TPS], q, qi);
+        bd[k] = UMUL8;
+    }
+    frt_pass<LOGN, LOGE, false, 0>(v, bd, tau, srow, twi, pti, q, qi);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {               // natural positions j; undo the radix twiddle
+        const uint32_t j = held_index<LOGE>(tau, LOGN - LOGE, k);
+        need(v, bd, k, LIM_MUL, q, qi);
+        srow[j + (j >> LOGE)] = fmm8(v[k], rtwi[i * NN + j], q, qi);
+    }
+    __syncthreads();
+    // inverse radix stage, cross twiddle psi^(-c brev(r)), back to the scratch row
+    for (int idx = threadIdx.x; idx < RB * NN; idx += blockDim.x) {
+        const int r2 = idx / NN, j = idx % NN;
+        double x[RAD];
+#pragma unroll
+        for (int l = 0; l < RAD; ++l) x[l] = buf[(r2 * RAD + l) * ROWW + j + (j >> LOGE)];
+        dft_small<RAD>(x, rci, q, qi);
+        double *g = grow0 + (uint64_t)r2 * C;
+        const double *xt = T.fxtb + (uint64_t)J.pr * T.M + (uint64_t)(blockIdx.x * RB + r2) * C;
+#pragma unroll
+        for (int l = 0; l < RAD; ++l) __stcs(g + j + l * NN, fmm8(x[l], xt[j + l * NN], q, qi));
+    }
+}
+
+template <int LOGN, int LOGE, int RB, int RAD>
+struct ShapeMR {
+    static constexpr int NN = 1 << LOGN, C = RAD * NN, THREADS = RB * RAD * (NN >> LOGE);
+    static constexpr size_t SMEM = (size_t)RB * RAD * (NN + NN / (1 << LOGE)) * 8 + (size_t)(2 * C + 32) * 8 +
+                                   (size_t)(NN + PtTab<LOGN, LOGE, true>::WORDS + PtTab<LOGN, LOGE, false>::WORDS) * 16;
+};
+
 // pass C: column inverse (length R) -> natural t, output chirp, canonical u64: Z_m^* gather (fwd) or A_t (inv)
 template <int LOGR, int LOGE, int TC, int INV, int LOGC>
 __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 << (LOGR - LOGE))))
@@ -444,6 +581,56 @@ __global__ void __launch_bounds__(32) kf_corner(NttTables T, LimbMap lm, uint64_
     }
 }
 
+// mixed-radix transform (prime m): persistent passes A / C with C = RAD 2^LOGN columns, mixed row pass B
+template <int RAD, int LOGN, int LOGEB, int RB>
+static void runf_mr(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
+                    uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
+    constexpr int LOGR = 8, LOGER = 4, TC = 16, CCV = RAD << LOGN;
+    typedef PersistA<LOGR, LOGER, TC, CCV> PA;
+    typedef PersistC<LOGR, LOGER, TC, CCV> PC;
+    typedef ShapeMR<LOGN, LOGEB, RB, RAD> SB;
+    constexpr int THA = TC << (LOGR - LOGER);
+    static std::atomic<uint64_t> init_dev{0};
+    static int nbA[64] = {0}, nbC[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_pending(init_dev)) {
+        for (int d = 0; d < 2; ++d) {
+            auto ka = d ? kf_passA_p<LOGR, LOGER, TC, CCV, 1> : kf_passA_p<LOGR, LOGER, TC, CCV, 0>;
+            auto kc = d ? kf_passC_p<LOGR, LOGER, TC, CCV, 1> : kf_passC_p<LOGR, LOGER, TC, CCV, 0>;
+            auto kb = d ? kf_passB_mr<LOGN, LOGEB, RB, 1, RAD> : kf_passB_mr<LOGN, LOGEB, RB, 0, RAD>;
+            cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
+            cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
+            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::SMEM);
+        }
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, TC, CCV, 0>, THA, PA::SMEM);
+        nbA[dev & 63] = b > 0 ? b : 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, TC, CCV, 0>, THA, PC::SMEM);
+        nbC[dev & 63] = b > 0 ? b : 1;
+        attr_done(init_dev);
+    }
+    NttTables T = T0;
+    T.dbg = 0;
+    double *scr = (double *)scratch;
+    const uint32_t ncg = CCV / TC;
+    const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbA[dev & 63] * 148) / ncg));
+    const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbC[dev & 63] * 148) / ncg));
+    dim3 gB((1 << LOGR) / RB, nj);
+    if (!inv) {
+        kf_passA_p<LOGR, LOGER, TC, CCV, 0><<<dim3(ncg, GA), THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+        kf_passB_mr<LOGN, LOGEB, RB, 0, RAD><<<gB, SB::THREADS, SB::SMEM, st>>>(T, lm, j0, scr);
+        kf_passC_p<LOGR, LOGER, TC, CCV, 0><<<dim3(ncg, GC), THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
+    } else {
+        kf_passA_p<LOGR, LOGER, TC, CCV, 1><<<dim3(ncg, GA), THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+        kf_passB_mr<LOGN, LOGEB, RB, 1, RAD><<<gB, SB::THREADS, SB::SMEM, st>>>(T, lm, j0, scr);
+        kf_corner<LOGR><<<nj, 32, 0, st>>>(T, lm, j0, scr, corner_buf);
+        kf_passC_p<LOGR, LOGER, TC, CCV, 1><<<dim3(ncg, GC), THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner_buf);
+        launch_counter() += 1;
+    }
+    launch_counter() += 3;
+}
+
 template <int LOGR, int LOGER, int LOGC, int LOGEC, int TC_, int RB_>
 struct Shape {
     static constexpr int TC = TC_, RB = RB_ ? RB_ : ((LOGC - LOGEC) >= 6 ? 4 : ((LOGC - LOGEC) >= 4 ? 8 : 16));
@@ -476,23 +663,24 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
     dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
     // persistent passes A and C (tiles of the prime resident in shared memory, cp.async prefetch of the next job)
     if (persist && LOGR == 8 && !T.dbg && (!inv || (T.prime_m && corner_buf))) {
-        typedef PersistA<LOGR, LOGER, S::TC, LOGC> PA;
-        typedef PersistC<LOGR, LOGER, S::TC, LOGC> PC;
+        constexpr int CCV = 1 << LOGC;
+        typedef PersistA<LOGR, LOGER, S::TC, CCV> PA;
+        typedef PersistC<LOGR, LOGER, S::TC, CCV> PC;
         static std::atomic<uint64_t> init_p{0};
         static int nbA[64] = {0}, nbC[64] = {0};
         int dev = 0;
         cudaGetDevice(&dev);
         if (attr_pending(init_p)) {
             for (int d = 0; d < 2; ++d) {
-                auto ka = d ? kf_passA_p<LOGR, LOGER, S::TC, LOGC, 1> : kf_passA_p<LOGR, LOGER, S::TC, LOGC, 0>;
-                auto kc = d ? kf_passC_p<LOGR, LOGER, S::TC, LOGC, 1> : kf_passC_p<LOGR, LOGER, S::TC, LOGC, 0>;
+                auto ka = d ? kf_passA_p<LOGR, LOGER, S::TC, CCV, 1> : kf_passA_p<LOGR, LOGER, S::TC, CCV, 0>;
+                auto kc = d ? kf_passC_p<LOGR, LOGER, S::TC, CCV, 1> : kf_passC_p<LOGR, LOGER, S::TC, CCV, 0>;
                 cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
                 cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
             }
             int b = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, S::TC, LOGC, 0>, S::THA, PA::SMEM);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, S::TC, CCV, 0>, S::THA, PA::SMEM);
             nbA[dev & 63] = b > 0 ? b : 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, S::TC, LOGC, 0>, S::THA, PC::SMEM);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, S::TC, CCV, 0>, S::THA, PC::SMEM);
             nbC[dev & 63] = b > 0 ? b : 1;
             attr_done(init_p);
         }
@@ -500,14 +688,14 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
         const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbA[dev & 63] * 148) / ncg));
         const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbC[dev & 63] * 148) / ncg));
         if (!inv) {
-            kf_passA_p<LOGR, LOGER, S::TC, LOGC, 0><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+            kf_passA_p<LOGR, LOGER, S::TC, CCV, 0><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
             kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
-            kf_passC_p<LOGR, LOGER, S::TC, LOGC, 0><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
+            kf_passC_p<LOGR, LOGER, S::TC, CCV, 0><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
         } else {
-            kf_passA_p<LOGR, LOGER, S::TC, LOGC, 1><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+            kf_passA_p<LOGR, LOGER, S::TC, CCV, 1><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
             kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
             kf_corner<LOGR><<<nj, 32, 0, st>>>(T, lm, j0, scr, corner_buf);
-            kf_passC_p<LOGR, LOGER, S::TC, LOGC, 1><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner_buf);
+            kf_passC_p<LOGR, LOGER, S::TC, CCV, 1><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner_buf);
             launch_counter() += 1;
         }
     } else if (!inv) {
@@ -601,12 +789,21 @@ int nttf_row_loge(uint32_t logR, uint32_t logC) {
     }
 }
 
+int nttf_mr_loge(uint32_t rad, uint32_t logN) { return (rad == 9 && logN == 5) ? 3 : 4; }   // runf_mr shapes
+
 bool nttf_supported(const NttTables &T) {
+    if (T.rad > 1) return T.fmods != nullptr && T.prime_m && T.logR == 8 &&
+                          ((T.rad == 9 && T.logN == 5) || (T.rad == 3 && T.logN == 7));
     return T.fmods != nullptr && ntt2_supported(T);
 }
 
 void nttf_run(const NttTables &T, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
               uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
+    if (T.rad > 1) {        // R25 mixed-radix lengths (prime m): C4 9 x 32, C5 3 x 128 row shapes
+        if (T.rad == 9 && T.logN == 5) f64::runf_mr<9, 5, 3, 4>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf);
+        else if (T.rad == 3 && T.logN == 7) f64::runf_mr<3, 7, 4, 4>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf);
+        return;
+    }
 #define RUNF(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf)
 #define RUNP(...) f64::runf<__VA_ARGS__>(T, in, out, lm, in_ps, out_ps, scratch, j0, nj, inv, st, corner_buf, true)
     switch (T.logR * 16 + T.logC) {

@@ -15,11 +15,14 @@ def pytest_configure(config):
 
 
 def load_cfg(name):
-    """params/<name>.json; "<name>@r16" / "<name>@r23" overrides the digit-circuit schedule (R16 / R23)"""
+    """params/<name>.json; "<name>@r16" / "<name>@r23" overrides the digit-circuit schedule (R16 / R23),
+    "<name>@pow2" / "<name>@mixed" the Bluestein length (R25)"""
     base, _, sched = name.partition("@")
     with open(os.path.join(ROOT, "params", base + ".json")) as f:
         cfg = json.load(f)
-    if sched:
+    if sched in ("pow2", "mixed"):         # "<name>@pow2": the power-of-two Bluestein length (R25 off)
+        cfg["bluestein"] = sched
+    elif sched:
         cfg["schedule"] = sched
     return cfg
 

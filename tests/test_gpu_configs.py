@@ -111,13 +111,16 @@ def test_shadow_c5_sort_bit_exact(pair):
         assert np.array_equal(to_u64(outs[k])[0], Tp.ct_eval(oo[k]))
 
 
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
+@pytest.mark.parametrize("cfg", ["c4", "c5", "c4@pow2", "c5@pow2"])
 def test_full_size_ntt_c4_c5(pair, cfg):
-    """a1/a2 at M = 2^17 with prime m (C4: m = 34511, C5: m = 41761): two sampled limbs of the
-    forward transform vs naive evaluation; the inverse (reduction mod Phi_m folded into pass C)
-    recovers every limb."""
+    """a1/a2 with prime m (C4: m = 34511, C5: m = 41761) at the R25 mixed-radix lengths (f3: C4
+    M = 73728 = 256 x 9 x 32, C5 M = 98304 = 256 x 3 x 128; the configs' default) and at the power of two
+    M = 2^17: the moduli equal the oracle's (R1 with the config's M), two sampled limbs of the forward
+    transform vs naive evaluation; the inverse (reduction mod Phi_m folded into pass C) recovers every
+    limb."""
     T = pair(cfg)
     P = T.P
+    assert T.ctx.M == P.M and T.ctx.moduli()[0] == P.moduli
     rng = np.random.default_rng(72)
     nl = P.L1 + P.K
     coef = np.stack([rng.integers(0, q, size=P.n, dtype=np.uint64) for q in P.moduli])[None]
