@@ -34,6 +34,7 @@ int bc_tune(const char *key, int64_t value) {
     if (!key) return -1;
     if (!strcmp(key, "vec_chunk")) { g_vec_chunk = (uint64_t)std::max<int64_t>(value, 0); return 0; }
     if (!strcmp(key, "ntt_timing")) { g_ntt_timing = value ? 1 : 0; return 0; }
+    if (!strcmp(key, "kip_blocked")) { g_kip_blocked = (int)value; return 0; }
     if (!strcmp(key, "f64_elem")) { g_f64_elem = (int)value; return 0; }
     if (!strcmp(key, "phi_conv")) { g_phi_conv = (int)value; return 0; }
     if (!strcmp(key, "ntt_dbg")) { g_ntt_dbg = (int)value; return 0; }

@@ -35,6 +35,7 @@ uint64_t &launch_counter() {
 // ntt_inverse call on the caller's stream, with the number of limb-transforms it ran
 int g_ntt_timing = 0;
 uint64_t g_vec_chunk = 0;   // max ciphertext pairs per batched compare in tournament / sort (0 = all)
+int g_kip_blocked = 1;      // 1: batch-blocked KIP (key words reused over 4 ciphertexts), 0: one ciphertext per thread
 struct NttRec {
     cudaEvent_t a, b;
     uint64_t jobs;
@@ -749,11 +750,72 @@ __global__ void k_kip_f(const double2 *__restrict__ fm, const uint64_t *__restri
         u[(b * 2 + 1) * ln + rr] = to_u64(fred(s1, q, qi), q);
     }
 }
+// batch-blocked variant: a thread keeps the 2 NDIG key words of its (limb, coefficient) in registers and
+// applies them to BB ciphertexts of the batch (the key stream is read once per BB ciphertexts instead of
+// once per ciphertext); sums in the same digit order, so the words are identical to k_kip_f's
+template <int NDIG, int BB>
+__global__ void __launch_bounds__(256) k_kip_fb(const double2 *__restrict__ fm, const uint64_t *__restrict__ d, uint64_t dps,
+                                                const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
+                                                uint64_t *__restrict__ u, uint32_t B, uint32_t lvl, uint32_t K,
+                                                uint32_t L1, uint32_t alpha, uint32_t n, const int32_t *__restrict__ pos,
+                                                const int32_t *__restrict__ zt, uint32_t m, uint32_t perm_t) {
+    using namespace f64;
+    const uint32_t nl = lvl + K;
+    const uint64_t ln = (uint64_t)nl * n;
+    const uint32_t xo = blockIdx.x * blockDim.x + threadIdx.x;
+    if (xo >= n) return;
+    const uint32_t x = perm_t ? (uint32_t)pos[(uint32_t)(((uint64_t)perm_t * (uint32_t)zt[xo]) % m)] : xo;
+    const uint32_t nbc = (B + BB - 1) / BB, rows = nl * nbc;
+    for (uint32_t rw = blockIdx.y; rw < rows; rw += gridDim.y) {
+        const uint32_t r = rw / nbc, b0 = (rw - r * nbc) * BB;
+        const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
+        const double q = fm[kl].x, qi = fm[kl].y;
+        const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
+        double k0[NDIG], k1[NDIG];
+#pragma unroll
+        for (int j = 0; j < NDIG; ++j) {
+            const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
+            k0[j] = from_u64(__ldg(kj + (uint64_t)kl * n + xo));
+            k1[j] = from_u64(__ldg(kj + (uint64_t)(L1 + K + kl) * n + xo));
+        }
+#pragma unroll
+        for (int bb = 0; bb < BB; ++bb) {
+            const uint64_t b = b0 + bb;
+            if (b >= B) break;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < NDIG; ++j) {
+                const uint64_t dig = ((uint32_t)j == jr) ? __ldcs(d + b * dps + (uint64_t)r * n + x)
+                                                         : __ldcs(ext + ((b * NDIG + j) * nl + r) * n + x);
+                const double dg = from_u64(dig);
+                s0 = __dadd_rn(s0, fmulv(dg, k0[j], q, qi));
+                s1 = __dadd_rn(s1, fmulv(dg, k1[j], q, qi));
+            }
+            const uint64_t rr = (uint64_t)r * n + xo;
+            __stcs(u + (b * 2 + 0) * ln + rr, to_u64(fred(s0, q, qi), q));
+            __stcs(u + (b * 2 + 1) * ln + rr, to_u64(fred(s1, q, qi), q));
+        }
+    }
+}
+
 static void kip_f_dispatch(dim3 g, cudaStream_t st, const double2 *fm, const uint64_t *d, uint64_t dps,
                            const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t rows, uint32_t lvl,
                            uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, const int32_t *pos,
                            const int32_t *zt, uint32_t m, uint32_t perm_t) {
 #define KIPF(N) k_kip_f<N><<<g, 256, 0, st>>>(fm, d, dps, ext, key, u, rows, lvl, K, L1, alpha, ndig, n, pos, zt, m, perm_t)
+#define KIPB(N) k_kip_fb<N, 4><<<dim3(g.x, (unsigned)std::min<uint64_t>(65535, (uint64_t)(lvl + K) * ((B + 3) / 4))), 256, 0, st>>>( \
+        fm, d, dps, ext, key, u, B, lvl, K, L1, alpha, n, pos, zt, m, perm_t)
+    const uint32_t B = rows / (lvl + K);
+    if (g_kip_blocked && B >= 4) {
+        switch (ndig) {
+            case 1: KIPB(1); return;
+            case 2: KIPB(2); return;
+            case 3: KIPB(3); return;
+            case 4: KIPB(4); return;
+            default: break;
+        }
+    }
+#undef KIPB
     switch (ndig) {
         case 1: KIPF(1); break;
         case 2: KIPF(2); break;

@@ -205,6 +205,7 @@ extern int g_ntt_dbg;
 extern int g_phi_conv;   // 1: always compute the Barrett quotient by convolution (testing)
 extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when the context allows them   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;
+extern int g_kip_blocked;
 extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)
 int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);
 extern int g_ntt_impl;   // 0 = binary64 three-pass kernels (ntt3.cu) where supported; 1 = radix-2 passes;
