@@ -425,6 +425,18 @@ def main():
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world, dev)
     total_pairs = B * world
+    # per-phase breakdown (Fig. 3 analog): one extra step with phase events (not timed above)
+    phases = None
+    if rank == 0:
+        bc.phase_timing(True)
+        bc.phase_timing()
+        step(ca, cb, out)
+        torch.cuda.synchronize()
+        ph = bc.phase_timing()
+        bc.phase_timing(False)
+        tot = sum(v[0] for v in ph.values())
+        phases = {k: {"ms": round(v[0], 3), "share_of_step": round(v[0] / ms_local, 4)} for k, v in ph.items() if v[1]}
+        phases["unattributed_share"] = round(max(0.0, 1 - tot / ms_local), 4)
     value = total_pairs * ints / (ms / 1000.0)
     clocks = clk.summary()
 
@@ -450,6 +462,29 @@ def main():
                "h2d_bytes_per_step": int(ha.numel() * 8 + hb.numel() * 8),
                "d2h_bytes_per_step": int(ho.numel() * 8), "ms_per_step": ms2}
 
+    # ---- keygen / encrypt / decrypt, timed separately (reported, not counted) ----
+    client = None
+    if not args.no_e2e:
+        barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        _ = ctx.encrypt(keys, A, SEED_ENC, ct_index0=sh["ct_a0"], ws=ws)
+        ev[1].record()
+        _ = ctx.decrypt(keys, out, as_bits=True, ws=ws)
+        ev[2].record()
+        barrier()
+        import time as _time
+        t0 = _time.perf_counter()
+        k2 = ctx.keygen(SEED_KEYS)
+        torch.cuda.synchronize()
+        kg_ms = 1000 * (_time.perf_counter() - t0)
+        del k2
+        client = {"encrypt_ms_per_ct": ev[0].elapsed_time(ev[1]) / B,
+                  "decrypt_bits_ms_per_ct": ev[1].elapsed_time(ev[2]) / B,
+                  "keygen_ms": kg_ms, "n_galois_keys": ctx.n_galois,
+                  "note": "encode (int8 slot-basis GEMM) + public-key encryption of one ct of %d words; decrypt = "
+                          "s-dot-product + exact CRT + decode of the result bits (host wall time for keygen)" % ints}
+
     roof = roofline(ctx, bc, live, ms_local * args.steps)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -466,7 +501,7 @@ def main():
                 "config": product_config(args, cfg, ints, B),
                 "ms_per_ct_compare": ms / B, "slot_compares_per_s": total_pairs * ctx.S / (ms / 1000.0),
                 "verified": verified, "gpu_launches": launches, "clocks": clocks,
-                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu}
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "client_ops": client, "phases": phases}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

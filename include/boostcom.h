@@ -265,19 +265,30 @@ bc_status bc_compact(bc_ctx *ctx, const bc_keys *keys, bc_ct in, const uint8_t *
                      bc_ct out, uint32_t *n_out, int32_t *h_dest, void *d_ws, size_t ws_bytes,
                      void *stream);
 
-/* NTT kernel family: 0 = register-blocked passes, 8 registers per thread (default where the
- * (R, C) shape is supported), 1 = radix-2 shared-memory passes (reference kernels for
- * tests), 2 = register-blocked passes with 16 registers per thread */
+/* NTT kernel family (results identical, a1/a2): 0 = binary64 register-blocked passes (default; the
+ * persistent column passes for R = 256, mixed-radix rows for the R25 lengths), 1 = radix-2 integer
+ * shared-memory passes (reference kernels for tests), 2-7 = 64-bit integer Shoup register passes,
+ * 10-17 = binary64 pass-shape variants (17: non-persistent column passes), 20 = the fused
+ * thread-block-cluster kernel (ntt4.cu; 256 x 256 prime-m shapes, else as 0) */
 void bc_set_ntt_impl(int impl);
-/* tuning knobs (benchmarks / tests): "ntt_timing" (0/1, see bc_ntt_timing),
- * "vec_chunk" = max ciphertext pairs per batched compare inside bc_min_tree/bc_max_tree/bc_sort
- * (0 = one batch per round; bounds the workspace, never changes bits), "ntt_group_bytes" = transform scratch per launch group
- * (default: the whole batch in one group; smaller groups measured slower on B200). Returns 0 if known. */
+/* tuning knobs (benchmarks / tests): "ntt_timing" (0/1, see bc_ntt_timing), "phase_timing" (0/1, see
+ * bc_phase_timing), "vec_chunk" = max ciphertext pairs per batched compare inside bc_min_tree/bc_max_tree/
+ * bc_sort (0 = one batch per round; bounds the workspace, never changes bits), "ntt_group_bytes" = transform
+ * scratch per launch group (default: the whole batch in one group; smaller groups measured slower on B200),
+ * "kip_blocked" (1: batch-blocked key inner product), "f64_elem" (1: binary64 element-wise kernels),
+ * "nttc_variant" / "nttc_clusters" (the fused cluster transform of bc_set_ntt_impl(20); nttc_clusters
+ * returns the occupancy query's cluster count).  None changes a result bit.  Returns 0 if known (-1 if not). */
 int bc_tune(const char *key, int64_t value);
 /* live NTT timing: after bc_tune("ntt_timing", 1) every forward/inverse Bluestein NTT call records
  * a CUDA event pair on its stream.  bc_ntt_timing synchronises those events and returns (then
  * clears) the summed duration in ms, the number of limb-transforms and of calls.  0 on success. */
 int bc_ntt_timing(double *ms, uint64_t *limb_transforms, uint64_t *calls);
+/* with bc_tune("phase_timing", 1): an event pair (and an NVTX range of the same name) around each
+ * leaf phase of the comparison schedule on its stream -- 0 extract (a8), 1 digit_circuit (a7),
+ * 2 lexicographic (a9), 3 broadcast_select (R17), 4 compaction (a10), 5 private_query_main (R24);
+ * bc_phase_timing synchronises them and returns ms[6] and calls[6] since the last call (0, or -1
+ * on a CUDA error).  The NVTX ranges are always emitted. */
+int bc_phase_timing(double *ms, uint64_t *calls);
 /* number of CUDA kernel launches issued by this thread since the last reset */
 uint64_t bc_launch_count(int reset);
 const char *bc_last_error(void);

@@ -96,6 +96,7 @@ _sig("bc_extract", _st, _vp, _vp, bc_ct, _vp, _vp, _sz, _vp)
 _sig("bc_launch_count", _u64, ctypes.c_int)
 _sig("bc_circuit_plan", _st, _u32, ctypes.c_char, _u32, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32))
 _sig("bc_ntt_timing", ctypes.c_int, _vp, _vp, _vp)
+_sig("bc_phase_timing", ctypes.c_int, _vp, _vp)
 _sig("bc_set_ntt_impl", None, ctypes.c_int)
 _sig("bc_tune", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64)
 _sig("bc_last_error", ctypes.c_char_p)
@@ -145,6 +146,21 @@ def ntt_timing(enable=None):
     if _lib.bc_ntt_timing(ctypes.byref(ms), ctypes.byref(j), ctypes.byref(c)) != 0:
         raise BoostComError("bc_ntt_timing failed")
     return ms.value, j.value, c.value
+
+
+PHASES = ("extract", "digit_circuit", "lexicographic", "broadcast_select", "compaction", "private_query_main")
+
+
+def phase_timing(enable=None):
+    """enable/disable per-phase event timing; with enable=None collect -> {phase: (ms, calls)}"""
+    if enable is not None:
+        _lib.bc_tune(b"phase_timing", 1 if enable else 0)
+        return None
+    ms = (ctypes.c_double * 6)()
+    calls = (ctypes.c_uint64 * 6)()
+    if _lib.bc_phase_timing(ms, calls) != 0:
+        raise BoostComError("bc_phase_timing failed")
+    return {k: (ms[i], int(calls[i])) for i, k in enumerate(PHASES)}
 
 
 def circuit_plan(p, circuit, schedule="r16"):

@@ -34,6 +34,7 @@ int bc_tune(const char *key, int64_t value) {
     if (!key) return -1;
     if (!strcmp(key, "vec_chunk")) { g_vec_chunk = (uint64_t)std::max<int64_t>(value, 0); return 0; }
     if (!strcmp(key, "ntt_timing")) { g_ntt_timing = value ? 1 : 0; return 0; }
+    if (!strcmp(key, "phase_timing")) { g_phase_timing = value ? 1 : 0; return 0; }
     if (!strcmp(key, "kip_blocked")) { g_kip_blocked = (int)value; return 0; }
     if (!strcmp(key, "f64_elem")) { g_f64_elem = (int)value; return 0; }
     if (!strcmp(key, "phi_conv")) { g_phi_conv = (int)value; return 0; }
@@ -43,6 +44,7 @@ int bc_tune(const char *key, int64_t value) {
     if (!strcmp(key, "ntt_group_bytes")) { g_ntt_group_bytes = (uint64_t)std::max<int64_t>(value, 1 << 20); return 0; }
     return -1;
 }
+int bc_phase_timing(double *ms, uint64_t *calls) { return phase_timing_collect(ms, calls); }
 int bc_ntt_timing(double *ms, uint64_t *limb_transforms, uint64_t *calls) {
     return ntt_timing_collect(ms, limb_transforms, calls);
 }

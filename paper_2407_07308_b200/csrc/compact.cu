@@ -193,6 +193,7 @@ extern "C" bc_status bc_compact(bc_ctx *X, const bc_keys *keys, bc_ct in, const 
         Arena A;
         A.init(ws, wsb, false);
         Eng E{X, keys, &A, (cudaStream_t)stv};
+        PhaseScope phs(PH_COMPACT, E.st);
         const uint64_t cw = (uint64_t)2 * in.level * X->n;
         // groups with the same (block set, offset) run as one batch: one mask product and one
         // (batched) rotation; every op is per ciphertext, so the bits equal the group-by-group order

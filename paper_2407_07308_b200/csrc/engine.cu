@@ -1581,33 +1581,50 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
     const bool need_eq = eq != nullptr, need_lt = lt != nullptr;   // EQ only: no LT products at all
     if (!need_lt && !need_eq) BC_THROW(BC_E_INTERNAL, "compare: nothing requested");
     if (X->prm.circuit == 'U') {
-        CT z = E.add(a, E.scalar(b, -1));
-        std::vector<CT> digs = extract_batch(E, z);
+        std::vector<CT> digs;
+        {
+            PhaseScope ps(PH_EXTRACT, E.st, !E.dry());
+            CT z = E.add(a, E.scalar(b, -1));
+            digs = extract_batch(E, z);
+        }
         // all d digits form one contiguous batch of d*B ciphertexts
         CT all = digs[0];
         all.B = d * B;
         Val L, Q;
-        univariate(E, VT(all), need_lt ? &L : nullptr, &Q);
+        {
+            PhaseScope ps(PH_DIGIT, E.st, !E.dry());
+            univariate(E, VT(all), need_lt ? &L : nullptr, &Q);
+        }
         for (uint32_t i = 0; i < d; ++i) {
             lts.push_back(need_lt ? VT(E.sub(L.ct, i * B, B)) : VC(0));
             eqs.push_back(VT(E.sub(Q.ct, i * B, B)));
         }
     } else {
-        std::vector<CT> da = extract_batch(E, a);
-        std::vector<CT> db = extract_batch(E, b);
+        std::vector<CT> da, db;
+        {
+            PhaseScope ps(PH_EXTRACT, E.st, !E.dry());
+            da = extract_batch(E, a);
+            db = extract_batch(E, b);
+        }
         CT xa = da[0], xb = db[0];
         xa.B = d * B;
         xb.B = d * B;
         Val L, Q;
-        bivariate(E, VT(xa), VT(xb), need_lt ? &L : nullptr, &Q);
+        {
+            PhaseScope ps(PH_DIGIT, E.st, !E.dry());
+            bivariate(E, VT(xa), VT(xb), need_lt ? &L : nullptr, &Q);
+        }
         for (uint32_t i = 0; i < d; ++i) {
             lts.push_back(need_lt ? VT(E.sub(L.ct, i * B, B)) : VC(0));
             eqs.push_back(VT(E.sub(Q.ct, i * B, B)));
         }
     }
     Val LT, EQ;
-    lex_tree(E, lts, eqs, &LT, &EQ, need_eq || X->l > 1, need_lt);
-    if (X->l > 1) lex_slots(E, &LT, &EQ, need_eq, need_lt);
+    {
+        PhaseScope ps(PH_LEX, E.st, !E.dry());
+        lex_tree(E, lts, eqs, &LT, &EQ, need_eq || X->l > 1, need_lt);
+        if (X->l > 1) lex_slots(E, &LT, &EQ, need_eq, need_lt);
+    }
     if (lt) *lt = LT.ct;
     if (eq) *eq = EQ.ct;
 }
@@ -1615,6 +1632,7 @@ void compare_batch(Eng &E, const CT &a, const CT &b, CT *lt, CT *eq) {
 // R17 broadcast: copy block slot 0 to every slot of its block (mask0, then rotate by -2^r and add
 // under [(s mod l) >= 2^r])
 CT broadcast_batch(Eng &E, const CT &cond) {
+    PhaseScope ps(PH_BCAST, E.st, !E.dry());
     bc_ctx *X = E.X;
     const uint32_t l = X->l;
     CT c = E.ptmul(cond, ctx_pt(X, "bm0", bm0_slots(X), E.st));

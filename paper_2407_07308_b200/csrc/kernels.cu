@@ -14,6 +14,8 @@
 #include <stdexcept>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.h"
 #include "f64arith.cuh"
 
@@ -75,6 +77,53 @@ int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls) {
     if (ms) *ms = t;
     if (jobs) *jobs = j;
     if (calls) *calls = c;
+    return 0;
+}
+
+// per-phase timing of the comparison schedule (bench "phases": the Fig. 3 time breakdown):
+// an event pair on the launching stream around each leaf phase, plus an NVTX range of the same name
+int g_phase_timing = 0;
+static const char *const k_phase_names[NPHASE] = {"extract", "digit_circuit", "lexicographic", "broadcast_select",
+                                                 "compaction", "private_query_main"};
+struct PhaseRec {
+    int ph;
+    cudaEvent_t a, b;
+};
+static std::vector<PhaseRec> &phase_recs() {
+    static std::vector<PhaseRec> r;
+    return r;
+}
+PhaseScope::PhaseScope(int ph, cudaStream_t st, bool on) : ph_(ph), st_(st), on_(on && ph >= 0 && ph < NPHASE) {
+    if (!on_) return;
+    nvtxRangePushA(k_phase_names[ph_]);
+    if (g_phase_timing) {
+        a_ = ev_get();
+        cudaEventRecord((cudaEvent_t)a_, st_);
+    }
+}
+PhaseScope::~PhaseScope() {
+    if (!on_) return;
+    if (g_phase_timing) {
+        cudaEvent_t b = ev_get();
+        cudaEventRecord(b, st_);
+        phase_recs().push_back(PhaseRec{ph_, (cudaEvent_t)a_, b});
+    }
+    nvtxRangePop();
+}
+int phase_timing_collect(double *ms, uint64_t *calls) {
+    for (int i = 0; i < NPHASE; ++i) {
+        if (ms) ms[i] = 0;
+        if (calls) calls[i] = 0;
+    }
+    for (auto &r : phase_recs()) {
+        float x = 0;
+        if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&x, r.a, r.b) != cudaSuccess) return -1;
+        if (ms) ms[r.ph] += x;
+        if (calls) calls[r.ph] += 1;
+        ev_pool().push_back(r.a);
+        ev_pool().push_back(r.b);
+    }
+    phase_recs().clear();
     return 0;
 }
 

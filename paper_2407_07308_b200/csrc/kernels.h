@@ -206,7 +206,19 @@ extern int g_phi_conv;   // 1: always compute the Barrett quotient by convolutio
 extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when the context allows them   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;
 extern int g_kip_blocked;
-extern int g_ntt_timing;  // 1: record an event pair around every NTT call (bench roofline)
+extern int g_ntt_timing;
+// comparison phases (bench "phases"; NVTX ranges of the same names)
+enum { PH_EXTRACT = 0, PH_DIGIT, PH_LEX, PH_BCAST, PH_COMPACT, PH_PQMAIN, NPHASE };
+extern int g_phase_timing;
+struct PhaseScope {      // event pair (when g_phase_timing) + NVTX range around one leaf phase
+    PhaseScope(int ph, cudaStream_t st, bool on = true);
+    ~PhaseScope();
+    int ph_;
+    cudaStream_t st_;
+    bool on_;
+    void *a_ = nullptr;
+};
+int phase_timing_collect(double *ms, uint64_t *calls);   // ms[NPHASE], calls[NPHASE]; clears the records  // 1: record an event pair around every NTT call (bench roofline)
 int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);
 extern int g_ntt_impl;   // 0 = binary64 three-pass kernels (ntt3.cu) where supported; 1 = radix-2 passes;
                          // 2 = integer register passes; 10-19 = binary64 three-pass shapes; 20 = fused cluster kernel (ntt4.cu)
