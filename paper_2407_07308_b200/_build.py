@@ -31,7 +31,8 @@ def build(force=False, verbose=False, out=None, extra=()):
     out = out or OUT
     if not force and out == OUT and up_to_date():
         return OUT
-    objdir = os.path.join(HERE, "build" if out == OUT else "build_" + os.path.basename(out).replace(".so", ""))
+    # object files outside the package (repo-level build/, git-ignored)
+    objdir = os.path.join(HERE, "..", "build", "obj" if out == OUT else "obj_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
 
     def comp(src):
