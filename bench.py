@@ -462,6 +462,32 @@ def main():
                "h2d_bytes_per_step": int(ha.numel() * 8 + hb.numel() * 8),
                "d2h_bytes_per_step": int(ho.numel() * 8), "ms_per_step": ms2}
 
+    # ---- single-pair latency, eager and replayed as a CUDA graph (bc_graph_*) ----
+    latency = None
+    if rank == 0 and not args.no_e2e:
+        a1, b1, o1 = ca[:1].clone(), cb[:1].clone(), out[:1].clone()
+        cap = torch.cuda.Stream(device=dev)
+        res = {}
+        with torch.cuda.stream(cap):
+            for _ in range(2):
+                step(a1, b1, o1)
+            cap.synchronize()
+            g = bc.Graph()
+            with g:
+                step(a1, b1, o1)
+            for nm, fn in (("eager_ms", lambda: step(a1, b1, o1)), ("graph_ms", g.launch)):
+                fn()
+                cap.synchronize()
+                l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                l0.record()
+                for _ in range(5):
+                    fn()
+                l1.record()
+                cap.synchronize()
+                res[nm] = l0.elapsed_time(l1) / 5
+            ok1 = bool(torch.equal(o1[0], out[0]))
+        latency = dict(res, pairs=1, identical_to_batch=ok1, launches_per_compare=int(launches / args.steps))
+
     # ---- keygen / encrypt / decrypt, timed separately (reported, not counted) ----
     client = None
     if not args.no_e2e:
@@ -501,7 +527,8 @@ def main():
                 "config": product_config(args, cfg, ints, B),
                 "ms_per_ct_compare": ms / B, "slot_compares_per_s": total_pairs * ctx.S / (ms / 1000.0),
                 "verified": verified, "gpu_launches": launches, "clocks": clocks,
-                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "client_ops": client, "phases": phases}
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "client_ops": client, "phases": phases,
+                "single_pair_latency": latency}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
