@@ -420,7 +420,7 @@ def main():
         torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
-    live = bc.ntt_timing()
+    live = bc.ntt_timing(split=True)
     bc.ntt_timing(False)
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world, dev)
@@ -624,7 +624,7 @@ def run_vector_workload(args, cfg, rank, world, local, workload):
         torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
-    live = bc.ntt_timing()
+    live = bc.ntt_timing(split=True)
     bc.ntt_timing(False)
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world, dev)
@@ -740,7 +740,7 @@ def run_compact_compare(args, cfg, rank, world, local):
         torch.cuda.nvtx.range_pop()
         barrier()
     launches = bc.launch_count(reset=True)
-    live = bc.ntt_timing()
+    live = bc.ntt_timing(split=True)
     bc.ntt_timing(False)
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world, dev)
@@ -909,11 +909,15 @@ def roofline(ctx, bc, live, step_ms_total):
     region: CUDA event pairs around every NTT call on the launching stream (bc_ntt_timing).
     achieved = limb-transforms x algorithmic 64-bit modular multiplications per limb-transform
      / summed NTT time; peak = FP64-pipe modular-butterfly rate at the max SM clock."""
-    ms, jobs, calls = live
+    if len(live) == 4:
+        ms, jobs, inv_jobs, calls = live
+    else:
+        (ms, jobs, calls), inv_jobs = live, 0
     if not calls or ms <= 0:
         return {"bound": "alu", "error": "no NTT calls timed"}
     work = bc.ntt_work(ctx)
-    achieved = jobs * work / (ms / 1e3) / 1e12
+    bw = bc.barrett_work(ctx)       # composite m: the Barrett division inside every inverse (C3)
+    achieved = (jobs * work + inv_jobs * bw) / (ms / 1e3) / 1e12
     peak = bc.ntt_peak(1965.0)
     traffic = None
     try:
@@ -925,7 +929,8 @@ def roofline(ctx, bc, live, step_ms_total):
     return {"bound": "alu", "kernel": "bluestein_ntt (passA+passB+passC [+reduce]) per ntt_forward/ntt_inverse call",
             "achieved": achieved, "peak": peak, "unit": "T modmul/s", "frac": achieved / peak,
             "traffic": traffic, "per_launch_ms": ms / calls, "limb_transforms_per_launch": jobs / calls,
-            "work_per_limb_transform": work, "launches_timed": calls, "share_of_step": ms / step_ms_total,
+            "work_per_limb_transform": work, "barrett_work_per_inverse": bw, "inverse_limb_transforms": inv_jobs,
+            "launches_timed": calls, "share_of_step": ms / step_ms_total,
             "how": "CUDA events on the launching stream around every NTT call inside the timed region",
             "traffic_note": "ncu --set full dram__bytes_read+write per limb-transform (profiles/ntt_traffic.json) x "
                             "limb-transforms per call",

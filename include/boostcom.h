@@ -283,6 +283,9 @@ int bc_tune(const char *key, int64_t value);
  * a CUDA event pair on its stream.  bc_ntt_timing synchronises those events and returns (then
  * clears) the summed duration in ms, the number of limb-transforms and of calls.  0 on success. */
 int bc_ntt_timing(double *ms, uint64_t *limb_transforms, uint64_t *calls);
+/* the same, also returning how many of the limb-transforms were inverse ones (composite m: those include
+ * the Barrett division by Phi_m, which the roofline counts as extra work) */
+int bc_ntt_timing_split(double *ms, uint64_t *limb_transforms, uint64_t *inverse_limb_transforms, uint64_t *calls);
 /* with bc_tune("phase_timing", 1): an event pair (and an NVTX range of the same name) around each
  * leaf phase of the comparison schedule on its stream -- 0 extract (a8), 1 digit_circuit (a7),
  * 2 lexicographic (a9), 3 broadcast_select (R17), 4 compaction (a10), 5 private_query_main (R24);

@@ -97,6 +97,7 @@ _sig("bc_launch_count", _u64, ctypes.c_int)
 _sig("bc_circuit_plan", _st, _u32, ctypes.c_char, _u32, ctypes.POINTER(_u32), ctypes.POINTER(_u32), ctypes.POINTER(_u32))
 _sig("bc_ntt_timing", ctypes.c_int, _vp, _vp, _vp)
 _sig("bc_phase_timing", ctypes.c_int, _vp, _vp)
+_sig("bc_ntt_timing_split", ctypes.c_int, _vp, _vp, _vp, _vp)
 _sig("bc_set_ntt_impl", None, ctypes.c_int)
 _sig("bc_tune", ctypes.c_int, ctypes.c_char_p, ctypes.c_int64)
 _sig("bc_last_error", ctypes.c_char_p)
@@ -137,8 +138,14 @@ def set_ntt_impl(impl):
     _lib.bc_set_ntt_impl(int(impl))
 
 
-def ntt_timing(enable=None):
-    """enable/disable live NTT event timing; with enable=None collect -> (ms, limb_transforms, calls)."""
+def ntt_timing(enable=None, split=False):
+    """enable/disable live NTT event timing; with enable=None collect -> (ms, limb_transforms, calls)
+    (split=True: (ms, limb_transforms, inverse_limb_transforms, calls))."""
+    if split and enable is None:
+        ms, j, ji, c = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        if _lib.bc_ntt_timing_split(ctypes.byref(ms), ctypes.byref(j), ctypes.byref(ji), ctypes.byref(c)) != 0:
+            raise BoostComError("bc_ntt_timing_split failed")
+        return ms.value, j.value, ji.value, c.value
     if enable is not None:
         _lib.bc_tune(b"ntt_timing", 1 if enable else 0)
         return None
@@ -609,10 +616,26 @@ def ntt_peak(sm_mhz=1965.0):
 
 def ntt_work(ctx):
     """algorithmic 64-bit modular multiplications of one limb-transform (forward Bluestein):
-    two size-M NTTs (M/2 log2 M butterflies each), the pointwise D^ product (M), two chirps (n+m)."""
+    two size-M NTTs (M/2 log2 M butterflies each; log2 of a mixed-radix length M = 256 r N' taken as is),
+    the pointwise D^ product (M), two chirps (n+m)."""
     import math
     M = ctx.M
-    return M * int(math.log2(M)) + M + ctx.n + ctx.m
+    return int(round(M * math.log2(M))) + M + ctx.n + ctx.m
+
+
+def barrett_work(ctx):
+    """extra algorithmic work of an inverse limb-transform at composite m: the Barrett division by Phi_m
+     runs one size-Mb cyclic convolution (Mb log2 Mb butterflies + Mb pointwise products),
+    Mb = the smallest power of two >= max(2(m - n) - 1, m); the sparse quotient (a few shifted adds) is
+    not counted.  0 for prime m."""
+    import math
+    m, n = ctx.m, ctx.n
+    if m - n == 1:
+        return 0
+    Mb = 1
+    while Mb < max(2 * (m - n) - 1, m):
+        Mb *= 2
+    return Mb * int(math.log2(Mb)) + Mb
 
 
 def profile_ntt(ctx, npoly=64, reps=5, sm_mhz=1965.0):

@@ -48,6 +48,9 @@ int bc_phase_timing(double *ms, uint64_t *calls) { return phase_timing_collect(m
 int bc_ntt_timing(double *ms, uint64_t *limb_transforms, uint64_t *calls) {
     return ntt_timing_collect(ms, limb_transforms, calls);
 }
+int bc_ntt_timing_split(double *ms, uint64_t *limb_transforms, uint64_t *inverse_limb_transforms, uint64_t *calls) {
+    return ntt_timing_collect(ms, limb_transforms, calls, inverse_limb_transforms);
+}
 uint64_t bc_launch_count(int reset) {
     uint64_t c = launch_counter();
     if (reset) launch_counter() = 0;

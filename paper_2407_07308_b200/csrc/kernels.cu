@@ -41,6 +41,7 @@ int g_kip_blocked = 1;      // 1: batch-blocked KIP (key words reused over 4 cip
 struct NttRec {
     cudaEvent_t a, b;
     uint64_t jobs;
+    int inv;
 };
 static std::vector<NttRec> &ntt_recs() {
     static std::vector<NttRec> r;
@@ -61,14 +62,15 @@ static cudaEvent_t ev_get() {
     cudaEventCreate(&e);
     return e;
 }
-int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls) {
+int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls, uint64_t *inv_jobs) {
     double t = 0;
-    uint64_t j = 0, c = 0;
+    uint64_t j = 0, c = 0, ji = 0;
     for (auto &r : ntt_recs()) {
         float x = 0;
         if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&x, r.a, r.b) != cudaSuccess) return -1;
         t += x;
         j += r.jobs;
+        if (r.inv) ji += r.jobs;
         ++c;
         ev_pool().push_back(r.a);
         ev_pool().push_back(r.b);
@@ -77,6 +79,7 @@ int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls) {
     if (ms) *ms = t;
     if (jobs) *jobs = j;
     if (calls) *calls = c;
+    if (inv_jobs) *inv_jobs = ji;
     return 0;
 }
 
@@ -450,7 +453,7 @@ static void ntt_timed(const NttTables &T, const uint64_t *in, uint64_t *out, uin
         ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
         return;
     }
-    NttRec r{ev_get(), ev_get(), (uint64_t)npoly * lm.njl};
+    NttRec r{ev_get(), ev_get(), (uint64_t)npoly * lm.njl, inv};
     cudaEventRecord(r.a, st);
     ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
     cudaEventRecord(r.b, st);

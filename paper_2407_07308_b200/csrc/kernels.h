@@ -219,7 +219,7 @@ struct PhaseScope {      // event pair (when g_phase_timing) + NVTX range around
     void *a_ = nullptr;
 };
 int phase_timing_collect(double *ms, uint64_t *calls);   // ms[NPHASE], calls[NPHASE]; clears the records  // 1: record an event pair around every NTT call (bench roofline)
-int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls);
+int ntt_timing_collect(double *ms, uint64_t *jobs, uint64_t *calls, uint64_t *inv_jobs = nullptr);
 extern int g_ntt_impl;   // 0 = binary64 three-pass kernels (ntt3.cu) where supported; 1 = radix-2 passes;
                          // 2 = integer register passes; 10-19 = binary64 three-pass shapes; 20 = fused cluster kernel (ntt4.cu)
 

@@ -239,14 +239,18 @@ def test_select_min_max_match_oracle(pair):
     assert np.array_equal(to_u64(mn)[0], T.ct_eval(omn))
 
 
-def test_compaction_fig7(pair):
-    """a10: 4 ciphertexts at 25% block utilisation (every 4th block, Fig. 7) -> 1 ciphertext."""
+@pytest.mark.parametrize("cfg", ["c1m", "c3s2"])
+def test_compaction_fig7(pair, cfg):
+    """a10: 4 ciphertexts at 25% block utilisation (every 4th block, Fig. 7) -> 1 ciphertext, bit-exact
+    vs the oracle: c1m (59-bit primes, integer kernels) and c3s2 (C3's slot structure: p = 31, composite
+    m = 1851, 56 x 2 hypercube with row-aligned blocks, 50-bit primes, binary64 kernels)."""
     from oracle import circuits
-    T = pair("c1m")
+    T = pair(cfg)
     P = T.P
     ints = T.ctx.ints_per_ct
     rng = np.random.default_rng(18)
-    words = [[int(x) for x in rng.integers(0, P.base ** (P.d * P.l), size=ints)] for _ in range(4)]
+    cap = min(P.base ** (P.d * P.l), 2 ** 63)
+    words = [[int(x) for x in rng.integers(0, cap, size=ints)] for _ in range(4)]
     useful = np.zeros((4, ints), dtype=np.uint8)
     useful[:, 3::4] = 1
     for c in range(4):
@@ -265,6 +269,7 @@ def test_compaction_fig7(pair):
     ev = circuits.OracleEval(P, T.okeys)
     oin = [T.oracle_ct(words[c], 60 + c) for c in range(4)]
     outs, _ = circuits.compact(ev, oin, [list(np.nonzero(useful[c])[0]) for c in range(4)], P.l, ints, 3)
+    assert len(outs) == out.shape[0]
     for k in range(out.shape[0]):
         assert np.array_equal(to_u64(out)[k], T.ct_eval(outs[k]))
 
