@@ -35,6 +35,8 @@ int bc_tune(const char *key, int64_t value) {
     if (!strcmp(key, "vec_chunk")) { g_vec_chunk = (uint64_t)std::max<int64_t>(value, 0); return 0; }
     if (!strcmp(key, "ntt_timing")) { g_ntt_timing = value ? 1 : 0; return 0; }
     if (!strcmp(key, "phase_timing")) { g_phase_timing = value ? 1 : 0; return 0; }
+    if (!strcmp(key, "ntt_split")) { g_ntt_split = (int)value; return 0; }
+    if (!strcmp(key, "ntt_persist_occ")) { g_ntt_persist_occ = (int)value; return 0; }
     if (!strcmp(key, "kip_blocked")) { g_kip_blocked = (int)value; return 0; }
     if (!strcmp(key, "f64_elem")) { g_f64_elem = (int)value; return 0; }
     if (!strcmp(key, "phi_conv")) { g_phi_conv = (int)value; return 0; }
@@ -143,7 +145,7 @@ static size_t dry_peak(bc_ctx *X, const bc_keys *keys, F fn) {
     A.init(nullptr, (size_t)1 << 62, true);
     Eng E{X, keys, &A, 0};
     fn(E);
-    return A.peak;
+    return A.hwm;      // includes fragmentation (same best-fit sequence as the real run)
 }
 
 static size_t compare_peak(bc_ctx *X, const bc_keys *keys, uint32_t B, uint32_t lvl, int which) {

@@ -25,7 +25,7 @@ void Arena::init(void *b, size_t c, bool dry_) {
     base = (char *)b;
     cap = c;
     dry = dry_;
-    used = peak = 0;
+    used = peak = hwm = 0;
     freel.clear();
     if (dry) base = (char *)(uintptr_t)4096;
     freel[0] = cap;
@@ -33,16 +33,24 @@ void Arena::init(void *b, size_t c, bool dry_) {
 char *Arena::alloc(size_t bytes) {
     bytes = (bytes + ALIGN - 1) / ALIGN * ALIGN;
     if (bytes == 0) bytes = ALIGN;
-    // best fit (smallest free block that fits; lowest address on ties) limits fragmentation
+    // best fit among the interior free blocks (smallest that fits; lowest address on ties), the tail block
+    // (the one ending at cap) only when none fits: placements then do not depend on cap, so a dry run's
+    // high-water address is exactly the capacity a real run needs
     auto best = freel.end();
     for (auto it = freel.begin(); it != freel.end(); ++it)
-        if (it->second >= bytes && (best == freel.end() || it->second < best->second)) best = it;
+        if (it->first + it->second != cap && it->second >= bytes && (best == freel.end() || it->second < best->second))
+            best = it;
+    if (best == freel.end()) {
+        auto tail = freel.empty() ? freel.end() : std::prev(freel.end());
+        if (tail != freel.end() && tail->first + tail->second == cap && tail->second >= bytes) best = tail;
+    }
     if (best != freel.end()) {
         size_t off = best->first, sz = best->second;
         freel.erase(best);
         if (sz > bytes) freel[off + bytes] = sz - bytes;
         used += bytes;
         peak = std::max(peak, used);
+        hwm = std::max(hwm, off + bytes);
         return base + off;
     }
     BC_THROW(BC_E_OOM, "workspace exhausted (" + std::to_string(bytes) + " bytes requested, " +

@@ -33,6 +33,8 @@ struct Arena {
     size_t cap = 0;
     bool dry = false;
     size_t used = 0, peak = 0;
+    size_t hwm = 0;                  // high-water address: the capacity this allocation sequence needs
+                                     // (best fit places identically in any arena at least this large)
     std::map<size_t, size_t> freel;  // offset -> size
     void init(void *b, size_t c, bool dry_);
     char *alloc(size_t bytes);

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <stdexcept>
 #include <vector>
 
@@ -447,15 +448,57 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
     }
 }
 
+// two-stream split (bc_tune "ntt_split"): the polys of a call in two halves on the caller's stream and a
+// side stream (fork / join by events, capturable), with the persistent column passes capped at one CTA
+// per SM so that one half's row pass can share the SMs with the other half's column passes.  Disjoint
+// scratch regions; the words are identical (every job is independent).
+int g_ntt_split = 0;
+int g_ntt_persist_occ = 0;
+static cudaStream_t side_stream_for_device() {
+    static std::mutex mu;
+    static cudaStream_t s[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!s[dev & 63]) cudaStreamCreateWithFlags(&s[dev & 63], cudaStreamNonBlocking);
+    return s[dev & 63];
+}
+static void ntt_split_or_common(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                                uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st, int inv) {
+    const uint64_t jobs = (uint64_t)npoly * lm.njl;
+    const bool barrett = inv && nttf_supported(T) && !T.prime_m && T.tb != nullptr;
+    if (!g_ntt_split || npoly < 2 || jobs < 2 * 296 || ntt_group_jobs(T, jobs, barrett) < jobs) {
+        ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
+        return;
+    }
+    const uint32_t p1 = npoly / 2, p2 = npoly - p1;
+    const uint64_t j1 = (uint64_t)p1 * lm.njl;
+    uint64_t *scr2 = scratch + j1 * T.M * (barrett ? 2 : 1) + (inv ? j1 : 0);
+    cudaStream_t side = side_stream_for_device();
+    cudaEvent_t fork = ev_get(), join = ev_get();
+    cudaEventRecord(fork, st);
+    cudaStreamWaitEvent(side, fork, 0);
+    const int occ = g_ntt_persist_occ;
+    g_ntt_persist_occ = 1;
+    ntt_common(T, in, out, p1, lm, in_pstride, out_pstride, scratch, st, inv);
+    ntt_common(T, in + (uint64_t)p1 * in_pstride, out + (uint64_t)p1 * out_pstride, p2, lm, in_pstride, out_pstride,
+               scr2, side, inv);
+    g_ntt_persist_occ = occ;
+    cudaEventRecord(join, side);
+    cudaStreamWaitEvent(st, join, 0);
+    ev_pool().push_back(fork);          // reusable once recorded work completes: re-recording is ordered
+    ev_pool().push_back(join);
+}
+
 static void ntt_timed(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                       uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st, int inv) {
     if (!g_ntt_timing) {
-        ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
+        ntt_split_or_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
         return;
     }
     NttRec r{ev_get(), ev_get(), (uint64_t)npoly * lm.njl, inv};
     cudaEventRecord(r.a, st);
-    ntt_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
+    ntt_split_or_common(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, inv);
     cudaEventRecord(r.b, st);
     ntt_recs().push_back(r);
 }

@@ -614,8 +614,8 @@ static void runf_mr(const NttTables &T0, const uint64_t *in, uint64_t *out, Limb
     T.dbg = 0;
     double *scr = (double *)scratch;
     const uint32_t ncg = CCV / TC;
-    const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbA[dev & 63] * 148) / ncg));
-    const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbC[dev & 63] * 148) / ncg));
+    const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbA[dev & 63]) : nbA[dev & 63]) * 148) / ncg));
+    const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbC[dev & 63]) : nbC[dev & 63]) * 148) / ncg));
     dim3 gB((1 << LOGR) / RB, nj);
     if (!inv) {
         kf_passA_p<LOGR, LOGER, TC, CCV, 0><<<dim3(ncg, GA), THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
@@ -685,8 +685,8 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
             attr_done(init_p);
         }
         const uint32_t ncg = (1u << LOGC) / S::TC;
-        const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbA[dev & 63] * 148) / ncg));
-        const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(nbC[dev & 63] * 148) / ncg));
+        const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbA[dev & 63]) : nbA[dev & 63]) * 148) / ncg));
+        const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbC[dev & 63]) : nbC[dev & 63]) * 148) / ncg));
         if (!inv) {
             kf_passA_p<LOGR, LOGER, S::TC, CCV, 0><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
             kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);

@@ -17,6 +17,7 @@ ws = ctx.workspace(npoly * L * ctx.M * 8 + (64 << 20))
 work = bc.ntt_work(ctx) * npoly * L
 ref = None
 ref_inv = None
+bc._lib.bc_tune(b"ntt_split", int(os.environ.get("SPLIT", "0")))
 for impl, gmb in [(int(a), int(g)) for a in os.environ.get("IMPLS", "7,0").split(",") for g in os.environ.get("GMB", "4096").split(",")]:
     bc.set_ntt_impl(impl)
     bc._lib.bc_tune(b"ntt_group_bytes", gmb << 20)
