@@ -38,7 +38,9 @@ uint64_t &launch_counter() {
 // ntt_inverse call on the caller's stream, with the number of limb-transforms it ran
 int g_ntt_timing = 0;
 uint64_t g_vec_chunk = 0;   // max ciphertext pairs per batched compare in tournament / sort (0 = all)
-int g_kip_blocked = 1;      // 1: batch-blocked KIP (key words reused over 4 ciphertexts), 0: one ciphertext per thread
+int g_kip_blocked = 1;      // 1: batch-blocked KIP (key words reused over 4 ciphertexts; two coefficients per
+                            // thread with 128-bit accesses when no automorphism permutes the digits), 2: blocked
+                            // with one coefficient per thread, 0: one ciphertext per thread
 struct NttRec {
     cudaEvent_t a, b;
     uint64_t jobs;
@@ -893,6 +895,58 @@ __global__ void __launch_bounds__(256) k_kip_fb(const double2 *__restrict__ fm, 
     }
 }
 
+// the same with two coefficients per thread and 128-bit accesses (no automorphism on the digit reads:
+// perm_t == 0, rows 16-byte aligned since n is even)
+template <int NDIG, int BB>
+__global__ void __launch_bounds__(256) k_kip_fb2(const double2 *__restrict__ fm, const uint64_t *__restrict__ d, uint64_t dps,
+                                                 const uint64_t *__restrict__ ext, const uint64_t *__restrict__ key,
+                                                 uint64_t *__restrict__ u, uint32_t B, uint32_t lvl, uint32_t K,
+                                                 uint32_t L1, uint32_t alpha, uint32_t n) {
+    using namespace f64;
+    const uint32_t nl = lvl + K;
+    const uint64_t ln = (uint64_t)nl * n;
+    const uint32_t x = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (x >= n) return;
+    const uint32_t nbc = (B + BB - 1) / BB, rows = nl * nbc;
+    for (uint32_t rw = blockIdx.y; rw < rows; rw += gridDim.y) {
+        const uint32_t r = rw / nbc, b0 = (rw - r * nbc) * BB;
+        const uint32_t kl = r < lvl ? r : L1 + (r - lvl);
+        const double q = fm[kl].x, qi = fm[kl].y;
+        const uint32_t jr = r < lvl ? r / alpha : 0xffffffffu;
+        double k0a[NDIG], k0b[NDIG], k1a[NDIG], k1b[NDIG];
+#pragma unroll
+        for (int j = 0; j < NDIG; ++j) {
+            const uint64_t *kj = key + (uint64_t)j * 2 * (L1 + K) * n;
+            const ulonglong2 w0 = __ldg((const ulonglong2 *)(kj + (uint64_t)kl * n + x));
+            const ulonglong2 w1 = __ldg((const ulonglong2 *)(kj + (uint64_t)(L1 + K + kl) * n + x));
+            k0a[j] = from_u64(w0.x); k0b[j] = from_u64(w0.y);
+            k1a[j] = from_u64(w1.x); k1b[j] = from_u64(w1.y);
+        }
+#pragma unroll
+        for (int bb = 0; bb < BB; ++bb) {
+            const uint64_t b = b0 + bb;
+            if (b >= B) break;
+            double s0a = 0.0, s0b = 0.0, s1a = 0.0, s1b = 0.0;
+#pragma unroll
+            for (int j = 0; j < NDIG; ++j) {
+                const uint64_t *src = ((uint32_t)j == jr) ? d + b * dps + (uint64_t)r * n
+                                                          : ext + ((b * NDIG + j) * nl + r) * n;
+                const ulonglong2 dg = __ldcs((const ulonglong2 *)(src + x));
+                const double ga = from_u64(dg.x), gb = from_u64(dg.y);
+                s0a = __dadd_rn(s0a, fmulv(ga, k0a[j], q, qi));
+                s0b = __dadd_rn(s0b, fmulv(gb, k0b[j], q, qi));
+                s1a = __dadd_rn(s1a, fmulv(ga, k1a[j], q, qi));
+                s1b = __dadd_rn(s1b, fmulv(gb, k1b[j], q, qi));
+            }
+            const uint64_t rr = (uint64_t)r * n + x;
+            __stcs((ulonglong2 *)(u + (b * 2 + 0) * ln + rr),
+                   make_ulonglong2(to_u64(fred(s0a, q, qi), q), to_u64(fred(s0b, q, qi), q)));
+            __stcs((ulonglong2 *)(u + (b * 2 + 1) * ln + rr),
+                   make_ulonglong2(to_u64(fred(s1a, q, qi), q), to_u64(fred(s1b, q, qi), q)));
+        }
+    }
+}
+
 static void kip_f_dispatch(dim3 g, cudaStream_t st, const double2 *fm, const uint64_t *d, uint64_t dps,
                            const uint64_t *ext, const uint64_t *key, uint64_t *u, uint32_t rows, uint32_t lvl,
                            uint32_t K, uint32_t L1, uint32_t alpha, uint32_t ndig, uint32_t n, const int32_t *pos,
@@ -901,6 +955,18 @@ static void kip_f_dispatch(dim3 g, cudaStream_t st, const double2 *fm, const uin
 #define KIPB(N) k_kip_fb<N, 4><<<dim3(g.x, (unsigned)std::min<uint64_t>(65535, (uint64_t)(lvl + K) * ((B + 3) / 4))), 256, 0, st>>>( \
         fm, d, dps, ext, key, u, B, lvl, K, L1, alpha, n, pos, zt, m, perm_t)
     const uint32_t B = rows / (lvl + K);
+#define KIPB2(N) k_kip_fb2<N, 4><<<dim3((n / 2 + 255) / 256, (unsigned)std::min<uint64_t>(65535, (uint64_t)(lvl + K) * ((B + 3) / 4))), 256, 0, st>>>( \
+        fm, d, dps, ext, key, u, B, lvl, K, L1, alpha, n)
+    if (g_kip_blocked == 1 && B >= 4 && perm_t == 0 && (n % 2) == 0 && (dps % 2) == 0) {
+        switch (ndig) {
+            case 1: KIPB2(1); return;
+            case 2: KIPB2(2); return;
+            case 3: KIPB2(3); return;
+            case 4: KIPB2(4); return;
+            default: break;
+        }
+    }
+#undef KIPB2
     if (g_kip_blocked && B >= 4) {
         switch (ndig) {
             case 1: KIPB(1); return;

@@ -19,7 +19,7 @@ ca = ctx.encrypt(keys, np.array(A, dtype=np.uint64).reshape(B, -1), 3, 0)
 cb = ctx.encrypt(keys, np.array(Bw, dtype=np.uint64).reshape(B, -1), 3, B)
 ws = ctx.workspace(max(ctx.workspace_bytes(B), 1 << 30))
 res = {}
-for kb in (0, 1, 0, 1):
+for kb in (0, 2, 1, 0, 2, 1):
     bc._lib.bc_tune(b"kip_blocked", kb)
     r = ctx.compare_lt(keys, ca, cb, ws=ws)
     torch.cuda.synchronize()

@@ -26,8 +26,10 @@ codes = ctx.encrypt(keys, np.array([[c] * ints for c in (1, 2, 3)], dtype=np.uin
 wsm = ctx.workspace(int(bc._lib.bc_private_query_workspace_bytes(ctx._h, N, 13, 13, 13, e, 0)))
 wss = torch.empty(int(bc._lib.bc_private_query_workspace_bytes(ctx._h, N, 13, 13, 13, e, 1)), dtype=torch.uint8,
                   device="cuda")
-for prio in (0, -1):
+for prio, impl in ((-1, 0), (-1, 17)):
+    bc.set_ntt_impl(impl)
     side = torch.cuda.Stream(priority=prio)
+    graphs = {}
     for name, fn in (("blocking", lambda: ctx.private_query(keys, data, q, codes, op1, e, ws=wsm)),
                      ("nonblocking", lambda: ctx.private_query(keys, data, q, codes, op1, e, side_stream=side, ws=wsm,
                                                                ws_side=wss)),
@@ -42,5 +44,6 @@ for prio in (0, -1):
         t1 = time.perf_counter()
         e1.record()
         torch.cuda.synchronize()
-        print(json.dumps({"prio": prio, "what": name, "host_enqueue_ms": round((t1 - t0) * 1e3 / 3, 2),
+        print(json.dumps({"prio": prio, "ntt_impl": impl, "what": name, "host_enqueue_ms": round((t1 - t0) * 1e3 / 3, 2),
                           "device_ms": round(e0.elapsed_time(e1) / 3, 2)}), flush=True)
+bc.set_ntt_impl(0)
