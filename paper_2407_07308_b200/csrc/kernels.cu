@@ -38,6 +38,7 @@ uint64_t &launch_counter() {
 // ntt_inverse call on the caller's stream, with the number of limb-transforms it ran
 int g_ntt_timing = 0;
 uint64_t g_vec_chunk = 0;   // max ciphertext pairs per batched compare in tournament / sort (0 = all)
+int g_lift2 = 1;            // 1: binary64 lift with two coefficients per thread (k_lift_f2), 0: one (k_lift_f)
 int g_kip_blocked = 1;      // 1: batch-blocked KIP (key words reused over 4 ciphertexts; two coefficients per
                             // thread with 128-bit accesses when no automorphism permutes the digits), 2: blocked
                             // with one coefficient per thread, 0: one ciphertext per thread
@@ -1347,9 +1348,118 @@ __global__ void __launch_bounds__(256) k_lift_f(const uint64_t *__restrict__ pla
     }
 }
 
+// the same lift for two adjacent coefficients per thread (128-bit loads / stores; the two Garner chains
+// interleave, which the one-coefficient kernel's dependent chain cannot): identical words
+template <int NS>
+__global__ void __launch_bounds__(256) k_lift_f2(const uint64_t *__restrict__ plan, const double2 *__restrict__ fm,
+                                                 uint32_t p, const uint64_t *__restrict__ src, uint64_t src_pstride,
+                                                 uint64_t *__restrict__ out, uint64_t out_pstride, uint32_t npoly,
+                                                 uint32_t n, uint32_t skip0, uint32_t skipn, int mode) {
+    using namespace f64;
+    __shared__ double2 sB[64 * NS], sQ[64], sT[64], sqm[NS * NS], sinv[NS], ssrc[NS];
+    __shared__ double shalf[NS];
+    __shared__ uint64_t sBp[NS];
+    const uint32_t nt = (uint32_t)plan[1];
+    const uint64_t *P_src = plan + 2, *P_inv = P_src + NS, *P_invs = P_inv + NS, *P_qm = P_invs + NS;
+    const uint64_t *P_qms = P_qm + NS * NS, *P_half = P_qms + NS * NS, *P_tgt = P_half + NS;
+    const uint64_t *P_B = P_tgt + nt, *P_Bs = P_B + (uint64_t)nt * NS, *P_Q = P_Bs + (uint64_t)nt * NS;
+    const uint64_t *P_Qs = P_Q + nt;
+    const uint64_t pmu = P_Qs[nt];
+    const uint32_t ntq = mode == 1 ? nt - 1 : nt;
+    for (uint32_t i = threadIdx.x; i < ntq * NS; i += blockDim.x) {
+        const uint32_t t = i / NS;
+        sB[i] = centred_entry(P_B[i], (uint64_t)fm[P_tgt[t]].x);
+    }
+    for (uint32_t t = threadIdx.x; t < ntq; t += blockDim.x) {
+        sT[t] = fm[P_tgt[t]];
+        sQ[t] = centred_entry(P_Q[t], (uint64_t)sT[t].x);
+    }
+    if (threadIdx.x < NS) {
+        const uint32_t kk = threadIdx.x;
+        ssrc[kk] = fm[P_src[kk]];
+        const uint64_t qk = (uint64_t)ssrc[kk].x;
+        sinv[kk] = centred_entry(P_inv[kk], qk);
+        shalf[kk] = (double)P_half[kk];
+        for (uint32_t j = 0; j < NS; ++j) sqm[kk * NS + j] = centred_entry(P_qm[kk * NS + j], qk);
+        if (mode == 1) sBp[kk] = P_B[(uint64_t)(nt - 1) * NS + kk];
+    }
+    __syncthreads();
+    ROW_LOOP2(poly, x, npoly, n) {
+        const uint64_t *s = src + (uint64_t)poly * src_pstride + x;
+        double v[2][NS];
+#pragma unroll
+        for (int kk = 0; kk < NS; ++kk) {
+            const ulonglong2 w = __ldcs((const ulonglong2 *)(s + (uint64_t)kk * n));
+            v[0][kk] = from_u64(w.x);
+            v[1][kk] = from_u64(w.y);
+        }
+#pragma unroll
+        for (int kk = 1; kk < NS; ++kk) {
+            const double qk = ssrc[kk].x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double acc = v[h][kk - 1];
+#pragma unroll
+                for (int j = kk - 2; j >= 0; --j) acc = __dadd_rn(fmm(acc, sqm[kk * NS + j], qk), v[h][j]);
+                v[h][kk] = canon(fmm(__dsub_rn(v[h][kk], acc), sinv[kk], qk), qk);
+            }
+        }
+        bool neg[2];
+        double tcd[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            neg[h] = false;
+#pragma unroll
+            for (int kk = NS - 1; kk >= 0; --kk) {
+                if (v[h][kk] != shalf[kk]) { neg[h] = v[h][kk] > shalf[kk]; break; }
+            }
+            if (mode == 1) {
+                uint64_t rp = 0;
+#pragma unroll
+                for (int kk = 0; kk < NS; ++kk) rp += mod_small((uint64_t)v[h][kk], p, pmu) * sBp[kk];
+                rp %= p;
+                if (neg[h]) rp = (rp + p - P_Q[nt - 1]) % p;
+                int64_t tc = (int64_t)((p - rp) % p);
+                if (tc > (int64_t)(p / 2)) tc -= p;
+                tcd[h] = (double)tc;
+            }
+        }
+        for (uint32_t t = 0; t < ntq; ++t) {
+            const double qt = sT[t].x, qit = sT[t].y;
+            const double2 *B = sB + t * NS;
+            uint64_t r[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                double acc = v[h][0];
+#pragma unroll
+                for (int kk = 1; kk < NS; ++kk) {
+                    if (kk == 8) acc = fred(acc, qt, qit);
+                    acc = __dadd_rn(acc, fmm(v[h][kk], B[kk], qt));
+                }
+                if (neg[h]) acc = __dsub_rn(acc, sQ[t].x);
+                if (mode == 1) acc = __dadd_rn(acc, fmm(tcd[h], sQ[t], qt));
+                r[h] = to_u64(fred(acc, qt, qit), qt);
+            }
+            const uint32_t lb = (mode == 1 || t < skip0) ? t : t + skipn;
+            ST2(out + (uint64_t)poly * out_pstride + (uint64_t)lb * n + x, r[0], r[1]);
+        }
+    }
+}
+
 void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src, uint64_t src_pstride, uint64_t *out,
           uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0, uint32_t skipn, int mode,
           cudaStream_t st, uint32_t ns_hint, uint32_t nt_hint, const double2 *fm) {
+    const bool two = g_lift2 && (n % 2) == 0 && (src_pstride % 2) == 0 && (out_pstride % 2) == 0 &&
+                     (((uintptr_t)src | (uintptr_t)out) & 15) == 0;
+    if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 16 && nt_hint <= 64 && two) {
+        const dim3 g = grid_rows(n / 2, npoly);
+#define LIFT_F2(K) case K: k_lift_f2<K><<<g, 256, 0, st>>>(plan, fm, p, src, src_pstride, out, out_pstride, npoly, n, skip0, skipn, mode); break;
+        switch (ns_hint) { LIFT_F2(1) LIFT_F2(2) LIFT_F2(3) LIFT_F2(4) LIFT_F2(5) LIFT_F2(6) LIFT_F2(7) LIFT_F2(8)
+                           LIFT_F2(9) LIFT_F2(10) LIFT_F2(11) LIFT_F2(12) LIFT_F2(13) LIFT_F2(14) LIFT_F2(15) LIFT_F2(16) }
+#undef LIFT_F2
+        LAUNCHED();
+        return;
+    }
     if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 16 && nt_hint <= 64) {
         const dim3 g = grid_rows(n, npoly);
 #define LIFT_F(K) case K: k_lift_f<K><<<g, 256, 0, st>>>(plan, fm, p, src, src_pstride, out, out_pstride, npoly, n, skip0, skipn, mode); break;

@@ -206,6 +206,7 @@ extern int g_phi_conv;   // 1: always compute the Barrett quotient by convolutio
 extern int g_f64_elem;   // 1: binary64 element-wise / lift / KIP kernels when the context allows them   // scratch bytes per transform launch group (L2 residency)
 extern uint64_t g_vec_chunk;
 extern int g_kip_blocked;
+extern int g_lift2;
 extern int g_ntt_split;        // 1: transform calls split over two streams (see ntt_split_or_common)
 extern int g_ntt_persist_occ;  // >0: cap of the persistent column passes' CTAs per SM
 extern int g_ntt_timing;

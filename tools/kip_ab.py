@@ -19,8 +19,10 @@ ca = ctx.encrypt(keys, np.array(A, dtype=np.uint64).reshape(B, -1), 3, 0)
 cb = ctx.encrypt(keys, np.array(Bw, dtype=np.uint64).reshape(B, -1), 3, B)
 ws = ctx.workspace(max(ctx.workspace_bytes(B), 1 << 30))
 res = {}
-for kb in (0, 2, 1, 0, 2, 1):
-    bc._lib.bc_tune(b"kip_blocked", kb)
+knob = os.environ.get("KNOB", "kip_blocked").encode()
+vals = [int(v) for v in os.environ.get("VALS", "0,2,1,0,2,1").split(",")]
+for kb in vals:
+    bc._lib.bc_tune(knob, kb)
     r = ctx.compare_lt(keys, ca, cb, ws=ws)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -30,9 +32,9 @@ for kb in (0, 2, 1, 0, 2, 1):
     e1.record()
     torch.cuda.synchronize()
     res.setdefault(kb, []).append(e0.elapsed_time(e1) / 3 / B)
-    if kb == 0:
+    if kb == vals[0]:
         ref = r.clone()
     else:
         assert torch.equal(r, ref), "blocked KIP changed the bits"
 print(json.dumps({"ms_per_compare": res, "identical": True}))
-bc._lib.bc_tune(b"kip_blocked", 1)
+bc._lib.bc_tune(knob, 1)
