@@ -745,6 +745,17 @@ def run_compact_compare(args, cfg, rank, world, local):
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, world, dev)
     useful_ints = int(useful.sum()) * world
+    phases = None
+    if rank == 0:
+        bc.phase_timing(True)
+        bc.phase_timing()
+        step()
+        torch.cuda.synchronize()
+        ph = bc.phase_timing()
+        bc.phase_timing(False)
+        tot = sum(v[0] for v in ph.values())
+        phases = {k: {"ms": round(v[0], 3), "share_of_step": round(v[0] / ms_local, 4)} for k, v in ph.items() if v[1]}
+        phases["unattributed_share"] = round(max(0.0, 1 - tot / ms_local), 4)
     if rank == 0:
         line = {"metric": "encrypted slot-comparisons/s after slot compaction (C3, bivariate p=31)",
                 "value": useful_ints / (ms / 1e3), "unit": "int-compares/s", "n_gpus": world, "steps": args.steps,
@@ -756,7 +767,7 @@ def run_compact_compare(args, cfg, rank, world, local):
                            "l2": "inputs larger than L2"},
                 "ms_per_dense_compare": ms / Bd, "verified": verified, "gpu_launches": launches,
                 "clocks": clk.summary(), "roofline": roofline(ctx, bc, live, ms_local * args.steps), "e2e": None,
-                "cpu_baseline": None}
+                "cpu_baseline": None, "phases": phases}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
