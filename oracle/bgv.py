@@ -28,9 +28,9 @@ class Params:
         self.name = cfg.get("name", "")
         self.p = int(cfg["p"])
         self.m = int(cfg["m"])
-        self.schedule = cfg.get("schedule", "r16")     # digit-circuit reading: R16 or R23
-        assert self.schedule in ("r16", "r23")
-        self.circuit = cfg.get("circuit", "U") + (":r23" if self.schedule == "r23" else "")
+        self.schedule = cfg.get("schedule", "r16")     # digit-circuit reading: R16, R23 or R26
+        assert self.schedule in ("r16", "r23", "r26")
+        self.circuit = cfg.get("circuit", "U") + ("" if self.schedule == "r16" else ":" + self.schedule)
         self.d = int(cfg["d"])
         self.l = int(cfg["l"])
         self.ring = Ring(self.m)

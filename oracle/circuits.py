@@ -12,6 +12,7 @@ Schedules are written once against an evaluator interface and run either on the 
 (OracleEval) or on plaintext slot values (PlainEval, used to pin the schedules).
 Values are either ciphertext objects or python ints (plaintext constants in F_p).
 """
+import functools
 import math
 
 import numpy as np
@@ -53,7 +54,17 @@ def eq_coeffs(p):
     return indicator_poly(p, lambda v: v == 0)
 
 
+@functools.lru_cache(maxsize=None)
+def _lt_bivariate_coeffs_cached(p):
+    return tuple(tuple(r) for r in _lt_bivariate_coeffs(p))
+
+
 def lt_bivariate_coeffs(p):
+    """cached copy of _lt_bivariate_coeffs (pure function of p)"""
+    return [list(r) for r in _lt_bivariate_coeffs_cached(p)]
+
+
+def _lt_bivariate_coeffs(p):
     """LT_B(x, y) = [x < y] on [0,p)^2 by 2-D Lagrange interpolation, rewritten in
     (Y = y, Z = x - y): returns c[j][k] with LT = sum_{j,k} c[j][k] Y^j Z^k."""
     # f(x, y) = sum_{u<v} (1 - (x-u)^{p-1}) (1 - (y-v)^{p-1})
@@ -353,6 +364,68 @@ def bivariate_lt_eq_r23(ev, x, y, p, k=None):
     return lt, eq
 
 
+def bivariate_lt_eq_r26(ev, x, y, p, k1=None, k2=None):
+    """R26 bivariate, two-dimensional Paterson-Stockmeyer: LT = sum_(j,i) c_ji Y^j Z^i (Z = x - y, the R16
+    coefficients) split into blocks j = k1 C + a, i = k2 D + b (a < k1, b < k2):
+    L_CD = sum c Y^a Z^b (baby monomials Y^a Z^b = Y^a * Z^b, created when first needed, a and b ascending),
+    inner_C = L_C0 + sum_(D>=1) Z^(k2 D) L_CD (D ascending), LT = inner_0 + sum_(C>=1) Y^(k1 C) inner_C
+    (C ascending); every power of Y and of Z by the R16 power rule (one memo each, shared with EQ);
+    zero blocks are skipped.  EQ = 1 - Z^(p-1).  (k1, k2) = r26_bivariate_k(p) unless given."""
+    c = lt_bivariate_coeffs(p)
+    if k1 is None:
+        k1, k2 = r26_bivariate_k(p)
+    Z = vadd(ev, x, vmul(ev, y, -1))
+    zp = Powers(ev, Z)
+    yp = Powers(ev, y)
+    mono = {}
+
+    def M(a, b):
+        if (a, b) not in mono:
+            mono[(a, b)] = zp(b) if a == 0 else (yp(a) if b == 0 else vmul(ev, yp(a), zp(b)))
+        return mono[(a, b)]
+
+    terms = {(j, i): c[j][i] % p for j in range(p) for i in range(p) if c[j][i] % p}
+    Cm = max(j for j, _ in terms) // k1
+    Dm = max(i for _, i in terms) // k2
+    lt = 0
+    for C in range(Cm + 1):
+        inner = 0
+        for D in range(Dm + 1):
+            L = lincomb(ev, [(terms[(k1 * C + a, k2 * D + b)], M(a, b)) for a in range(k1) for b in range(k2)
+                             if (a, b) != (0, 0) and (k1 * C + a, k2 * D + b) in terms],
+                        terms.get((k1 * C, k2 * D), 0))
+            if is_const(L) and L == 0:
+                continue
+            t = L if D == 0 else vmul(ev, zp(k2 * D), L)
+            inner = t if (is_const(inner) and inner == 0) else vadd(ev, inner, t)
+        if is_const(inner) and inner == 0:
+            continue
+        t = inner if C == 0 else vmul(ev, yp(k1 * C), inner)
+        lt = t if (is_const(lt) and lt == 0) else vadd(ev, lt, t)
+    eq = vadd(ev, vmul(ev, zp(p - 1), -1), 1)
+    return lt, eq
+
+
+@functools.lru_cache(maxsize=None)
+def r26_bivariate_k(p):
+    """R26: among (k1, k2) in [1, p-1]^2 whose circuit is no deeper than R16's, the fewest products, then
+    the smallest k1, then the smallest k2"""
+    cap = _r16_depth("B", p)
+    best = None
+    for k1 in range(1, p):
+        for k2 in range(1, p):
+            mu, d = _r26_cost(p, k1, k2)
+            if d <= cap and (best is None or mu < best[0]):
+                best = (mu, k1, k2)
+    return best[1], best[2]
+
+
+def _r26_cost(p, k1, k2):
+    ev = CountEval(p)
+    lt, eq = bivariate_lt_eq_r26(ev, CountValue(), CountValue(), p, k1, k2)
+    return ev.counts["mul"], max(getattr(lt, "depth", 0), getattr(eq, "depth", 0))
+
+
 def _r23_cost(fn, p, k):
     ev = CountEval(p)
     args = (CountValue(),) if fn is univariate_lt_eq_r23 else (CountValue(), CountValue())
@@ -457,18 +530,18 @@ def lex_slots(ev, lt, eq, l, ints):
 
 def compare(ev, a, b, circuit, d, l, ints):
     """(LT, EQ) of the words packed in a and b (block slot 0 holds the result).  circuit: "U" / "B"
-    (R16 digit circuits) or "U:r23" / "B:r23" (R23)."""
+    (R16 digit circuits), "U:r23" / "B:r23" (R23) or "U:r26" / "B:r26" (R26 bivariate; univariate = R23)."""
     p = ev.p
-    r23 = circuit.endswith(":r23")          # R23 digit circuits (params "schedule": "r23"), else R16
+    sched = circuit.partition(":")[2] or "r16"   # R16, R23 or R26 digit circuits (params "schedule")
     if circuit[0] == "U":
         z = ev.add(a, ev.scalar(b, -1))
         digs = extract_digits(ev, z, d)
-        f = univariate_lt_eq_r23 if r23 else univariate_lt_eq
+        f = univariate_lt_eq_r23 if sched in ("r23", "r26") else univariate_lt_eq   # R26 univariate = R23
         res = [f(ev, x, p) for x in digs]
     else:
         da = extract_digits(ev, a, d)
         db = extract_digits(ev, b, d)
-        f = bivariate_lt_eq_r23 if r23 else bivariate_lt_eq
+        f = {"r23": bivariate_lt_eq_r23, "r26": bivariate_lt_eq_r26}.get(sched, bivariate_lt_eq)
         res = [f(ev, x, y, p) for x, y in zip(da, db)]
     lt, eq = lex_tree(ev, [r[0] for r in res], [r[1] for r in res])
     if l > 1:

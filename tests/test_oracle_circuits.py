@@ -82,6 +82,8 @@ def _digit_run(p, kind, r23=False, k=None):
         if kind == "U":
             z = circuits.PlainValue((X - Y) % p)
             lt, eq = circuits.univariate_lt_eq_r23(ev, z, p, k) if r23 else circuits.univariate_lt_eq(ev, z, p)
+        elif r23 == "r26":
+            lt, eq = circuits.bivariate_lt_eq_r26(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p, *k)
         elif r23:
             lt, eq = circuits.bivariate_lt_eq_r23(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p, k)
         else:
@@ -376,3 +378,32 @@ def test_private_query_bgv_decrypts():
         dec = A.decode(bgv.decrypt(P, K, out[0]))
         assert np.array_equal(dec[covered, 0], want[covered])
         assert not dec[~covered].any()
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_r26_schedule_truth_tables(p):
+    """R26 (f2): the two-dimensional Paterson-Stockmeyer bivariate circuit gives [x < y], [x = y]
+    on every digit pair at the selected block sizes and at a few others; at the selected ones it uses no
+    more products than R23 for p >= 11 and is no deeper than R16"""
+    sel = circuits.r26_bivariate_k(p)
+    r16 = _digit_run(p, "B")
+    for k in sorted({sel, (1, 1), (2, 3), (min(4, p - 1), min(4, p - 1))}):
+        res, mults, depth = _digit_run(p, "B", r23="r26", k=k)
+        for x, y, lt, eq in res:
+            assert (lt, eq) == (int(x < y), int(x == y)), (p, k, x, y)
+        if k == sel:
+            assert depth <= r16[2] and mults <= r16[1]
+            if p >= 11:
+                assert mults <= circuits._r23_cost(circuits.bivariate_lt_eq_r23, p, circuits.r23_bivariate_k(p))[0]
+
+
+def test_r26_counts():
+    """R26 counts: (k1, k2) = (1, 1) is the R16 tree (3p - 5 products); at p = 31 the rule picks
+    (8, 8) with 59 products at depth 6 (R16: 88, R23: 73 at the same depth); at depth 7, (4, 8) needs 54,
+    below the paper's asymptotic 2p - 6 = 56; at p = 13, 26 (R23: 28)"""
+    for p in (5, 7, 11, 13):
+        assert circuits._r26_cost(p, 1, 1)[0] == 3 * p - 5
+    assert circuits.r26_bivariate_k(31) == (8, 8)
+    assert circuits._r26_cost(31, 8, 8) == (59, 6)
+    assert circuits._r26_cost(31, 4, 8) == (54, 7)
+    assert circuits._r26_cost(13, *circuits.r26_bivariate_k(13)) == (26, 5)

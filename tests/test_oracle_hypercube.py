@@ -101,14 +101,14 @@ def test_hypercube_compaction_stays_in_rows(oracle_params):
     assert n_out == max(-(-k // wpr) for k in per_row) == 2 and len(dest) == 4 * len(useful[0])
 
 
-@pytest.mark.parametrize("sched", ["r16", "r23"])
+@pytest.mark.parametrize("sched", ["r16", "r23", "r26"])
 def test_hypercube_compare_bgv(oracle_params, sched):
     """full BGV compare_lt / compare_eq on the tiny hypercube ring (p = 31 bivariate, m = 33):
     decrypted block slot 0 equals brute force for 2 integers (one per row) per ciphertext, with the
     R16 and the R23 (f2) digit circuits"""
     from oracle import bgv as _bgv
     from conftest import load_cfg
-    P = oracle_params("c3h") if sched == "r16" else _bgv.Params(dict(load_cfg("c3h"), schedule="r23"))
+    P = oracle_params("c3h") if sched == "r16" else _bgv.Params(dict(load_cfg("c3h"), schedule=sched))
     A = P.alg
     gal = [pow(P.p, k, P.m) for k in range(1, A.D)]
     sh = 1
