@@ -66,7 +66,8 @@ typedef struct {
     uint32_t n_special, special_bits;
     uint32_t alpha;
     uint32_t compact_span;   /* slot compaction offsets |delta| <= span blocks (0 -> 3), R17 */
-    uint32_t schedule;       /* digit circuits: 0 or 16 = R16, 23 = R23 baby-step / giant-step (SURVEY
+    uint32_t schedule;       /* digit circuits: 0 or 16 = R16, 23 = R23 baby-step / giant-step, 26 = R26
+                              * (bivariate two-dimensional Paterson-Stockmeyer, univariate as R23) (SURVEY
                               * §8(f) f2: "2p-6 (Bivariate case) and sqrt(p-3)+O(log p)
                               * (Univariate case)"); anything else -> BC_E_PARAM */
     uint32_t bluestein;      /* 0: power-of-two Bluestein length; 1: mixed radix (R25, SURVEY §8(f)
@@ -95,9 +96,9 @@ bc_status bc_ctx_moduli(const bc_ctx *ctx, uint64_t *h_out, uint64_t *h_omega);
 /* slot algebra (R5): h_G[D+1] field polynomial, h_zeta[D], h_t[S] slot exponents */
 bc_status bc_ctx_slots(const bc_ctx *ctx, int64_t *h_G, int64_t *h_zeta, int64_t *h_t);
 /* host only (no device): the digit circuit a context with these (p, circuit, schedule) evaluates --
- * k = the R23 baby-step size (0 for R16), products = ct x ct multiplications per digit (EQ
+ * k = the R23 baby-step size (0 for R16; R26 bivariate: k1 << 8 | k2), products = ct x ct multiplications per digit (EQ
  * included), depth = its multiplicative depth (R16 / R23; P:71's 3p-5 for R16 bivariate).
- * BC_E_PARAM for p not an odd prime <= 257, circuit not 'U'/'B', schedule not 0/16/23. */
+ * BC_E_PARAM for p not an odd prime <= 257, circuit not 'U'/'B', schedule not 0/16/23/26. */
 bc_status bc_circuit_plan(uint32_t p, char circuit, uint32_t schedule, uint32_t *k, uint32_t *products,
                           uint32_t *depth);
 /* Galois elements keygen generates keys for (Frobenius p^k, rotations) */

@@ -229,6 +229,7 @@ static std::vector<int64_t> interp_fp(int64_t p, const std::function<int64_t(int
 // (Y = y, Z = x - y): out[j][k] coefficient of Y^j Z^k.
 int r23_select_k(int64_t p, char circuit, const std::vector<int64_t> &cu, const std::vector<std::vector<int64_t>> &cb,
                  int *muls, int *depth);
+static int r26_select_k(int64_t p, const std::vector<std::vector<int64_t>> &cb);
 
 static std::vector<std::vector<int64_t>> lt_bivariate(int64_t p) {
     std::vector<std::vector<int64_t>> dl(p);
@@ -332,8 +333,11 @@ void ctx_build(bc_ctx *X) {
         X->eq_u = interp_fp(p, [](int64_t v) { return v == 0 ? 1 : 0; });
         if (P.circuit == 'B') X->lt_b = lt_bivariate(p);
         // R23 (schedule 23): the baby-step size the rule selects; 0 = the R16 circuits
-        if (P.schedule != 0 && P.schedule != 16 && P.schedule != 23) BC_THROW(BC_E_PARAM, "schedule must be 16 or 23");
-        X->r23_k = P.schedule == 23 ? r23_select_k(p, P.circuit, X->lt_u, X->lt_b, nullptr, nullptr) : 0;
+        if (P.schedule != 0 && P.schedule != 16 && P.schedule != 23 && P.schedule != 26)
+            BC_THROW(BC_E_PARAM, "schedule must be 16, 23 or 26");
+        // R26 (schedule 26): the bivariate circuit's block sizes; its univariate circuit is R23's
+        X->r23_k = (P.schedule == 23 || P.schedule == 26) ? r23_select_k(p, P.circuit, X->lt_u, X->lt_b, nullptr, nullptr) : 0;
+        X->r26_k = (P.schedule == 26 && P.circuit == 'B') ? r26_select_k(p, X->lt_b) : 0;
     }
     // Galois elements: Frobenius p^k (k < D), rotations g^{+-2^r} (r < ceil log2 l)
     {
@@ -888,7 +892,35 @@ CT Eng::modswitch(const CT &a) {
 
 CT Eng::modswitch_to(const CT &a, uint32_t lvl) {
     CT c = a;
-    while (c.lvl > lvl) c = modswitch(c);
+    while (c.lvl > lvl) {
+        if (!msm || !msm->on || !c.keep) {
+            c = modswitch(c);
+            continue;
+        }
+        const MsMemo::Key k{c.d, c.B, c.lvl, c.bstride};
+        auto it = msm->m.find(k);
+        if (it != msm->m.end()) {
+            BufP sp = it->second.src.lock();
+            if (sp && sp == c.keep) {
+                ++msm->hits;
+                c = it->second.out;
+                continue;
+            }
+            msm->m.erase(it);           // stale: the source buffer is gone (its address may be reused)
+        }
+        ++msm->misses;
+        CT nx = modswitch(c);
+        const uint64_t s = ++msm->seq;
+        msm->m[k] = MsMemo::Ent{c.keep, nx, s};
+        msm->order.push_back({k, s});
+        while (msm->order.size() > MsMemo::N) {
+            auto f = msm->order.front();
+            msm->order.pop_front();
+            auto jt = msm->m.find(f.first);
+            if (jt != msm->m.end() && jt->second.seq == f.second) msm->m.erase(jt);
+        }
+        c = nx;
+    }
     return c;
 }
 
@@ -1418,6 +1450,90 @@ static void bivariate_r23(Ev &ev, const typename Ev::V &x, const typename Ev::V 
     if (eq) *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
 }
 
+// R26 bivariate (mirrors oracle/circuits.py bivariate_lt_eq_r26): two-dimensional Paterson-Stockmeyer over
+// (Y, Z) blocks of k1 x k2 monomials; every power of Y and Z by the power rule (shared memos)
+template <class Ev>
+static void bivariate_r26(Ev &ev, const typename Ev::V &x, const typename Ev::V &y,
+                          const std::vector<std::vector<int64_t>> &c, int k1, int k2, typename Ev::V *lt,
+                          typename Ev::V *eq) {
+    typedef typename Ev::V V;
+    const int64_t p = ev.p();
+    V Z = ev.add(x, ev.mul(y, ev.cnst(-1)));
+    PowersT<Ev> zp(ev, Z);
+    if (!lt) {      // EQ only: 1 - Z^(p-1)
+        *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
+        return;
+    }
+    PowersT<Ev> yp(ev, y);
+    std::map<std::pair<int, int>, V> mono;
+    auto M = [&](int a, int b) -> V {
+        auto it = mono.find({a, b});
+        if (it != mono.end()) return it->second;
+        V v = a == 0 ? zp.get(b) : (b == 0 ? yp.get(a) : ev.mul(yp.get(a), zp.get(b)));
+        mono[{a, b}] = v;
+        return v;
+    };
+    auto coef = [&](int j, int i) -> int64_t {
+        if (j >= (int)c.size() || i >= (int)c[j].size()) return 0;
+        return ((c[j][i] % p) + p) % p;
+    };
+    int jmax = 0, imax = 0;
+    for (int j = 0; j < (int)p; ++j)
+        for (int i = 0; i < (int)p; ++i)
+            if (coef(j, i)) { jmax = std::max(jmax, j); imax = std::max(imax, i); }
+    const int Cm = jmax / k1, Dm = imax / k2;
+    bool have = false;
+    V acc;
+    for (int C = 0; C <= Cm; ++C) {
+        bool hin = false;
+        V inner;
+        for (int D = 0; D <= Dm; ++D) {
+            std::vector<std::pair<int64_t, std::function<V()>>> terms;
+            for (int a = 0; a < k1; ++a)
+                for (int b = 0; b < k2; ++b) {
+                    if (a == 0 && b == 0) continue;
+                    const int64_t cf = coef(k1 * C + a, k2 * D + b);
+                    if (cf) terms.push_back({cf, [&M, a, b]() { return M(a, b); }});
+                }
+            V L = lincombT(ev, terms, coef(k1 * C, k2 * D));
+            if (Ev::isc(L) && Ev::cval(L) == 0) continue;
+            V t = D == 0 ? L : ev.mul(zp.get(k2 * D), L);
+            inner = hin ? ev.add(inner, t) : t;
+            hin = true;
+        }
+        if (!hin) continue;
+        V t = C == 0 ? inner : ev.mul(yp.get(k1 * C), inner);
+        acc = have ? ev.add(acc, t) : t;
+        have = true;
+    }
+    *lt = have ? acc : ev.cnst(0);
+    if (eq) *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
+}
+
+static void r26_cost(int64_t p, const std::vector<std::vector<int64_t>> &cb, int k1, int k2, int *muls, int *depth) {
+    CntEv ev{p};
+    CntV lt, eq;
+    bivariate_r26(ev, CntV(), CntV(), cb, k1, k2, &lt, &eq);
+    *muls = ev.muls;
+    *depth = std::max(lt.depth, eq.depth);
+}
+// R26 block sizes: no deeper than R16, fewest products, then the smallest k1, then k2 (returns k1 << 8 | k2)
+static int r26_select_k(int64_t p, const std::vector<std::vector<int64_t>> &cb) {
+    CntEv e16{p};
+    CntV l16, q16;
+    bivariate_r16(e16, CntV(), CntV(), cb, &l16, &q16);
+    const int cap = std::max(l16.depth, q16.depth);
+    int best = -1, bm = 0;
+    for (int k1 = 1; k1 < (int)p; ++k1)
+        for (int k2 = 1; k2 < (int)p; ++k2) {
+            int mu, de;
+            r26_cost(p, cb, k1, k2, &mu, &de);
+            if (de > cap) continue;
+            if (best < 0 || mu < bm) { best = (k1 << 8) | k2; bm = mu; }
+        }
+    return best;
+}
+
 // R23 baby-step size: among k whose circuit is no deeper than R16's, the fewest products, then the smallest k
 static void r23_cost(int64_t p, char circuit, const std::vector<int64_t> &cu, const std::vector<std::vector<int64_t>> &cb,
                      int k, int *muls, int *depth) {
@@ -1457,19 +1573,38 @@ void circuit_plan(int64_t p, char circuit, int schedule, int *k, int *muls, int 
     std::vector<int64_t> cu = interp_fp(p, [p, h](int64_t v) { return (v >= p - h && v <= p - 1) ? 1 : 0; });
     std::vector<std::vector<int64_t>> cb;
     if (circuit == 'B') cb = lt_bivariate(p);
-    *k = schedule == 23 ? r23_select_k(p, circuit, cu, cb, nullptr, nullptr) : 0;
+    if (schedule == 26 && circuit == 'B') {         // R26: k = k1 << 8 | k2
+        *k = r26_select_k(p, cb);
+        r26_cost(p, cb, *k >> 8, *k & 255, muls, depth);
+        return;
+    }
+    *k = (schedule == 23 || schedule == 26) ? r23_select_k(p, circuit, cu, cb, nullptr, nullptr) : 0;
     r23_cost(p, circuit, cu, cb, *k, muls, depth);
 }
 
+// the modulus-switch memo is on inside a digit circuit (its values are functional) and cleared after it
+struct MemoScope {
+    Eng &E;
+    explicit MemoScope(Eng &e) : E(e) { E.msm->on = true; }
+    ~MemoScope() {
+        E.msm->on = false;
+        E.msm->m.clear();
+        E.msm->order.clear();
+    }
+};
+
 static void univariate(Eng &E, const Val &z, Val *lt, Val *eq) {
+    MemoScope ms(E);
     EngEv ev{E};
     if (E.X->r23_k > 0) univariate_r23(ev, z, E.X->lt_u, E.X->r23_k, lt, eq);
     else univariate_r16(ev, z, E.X->lt_u, lt, eq);
 }
 
 static void bivariate(Eng &E, const Val &x, const Val &y, Val *lt, Val *eq) {
+    MemoScope ms(E);
     EngEv ev{E};
-    if (E.X->r23_k > 0) bivariate_r23(ev, x, y, E.X->lt_b, E.X->r23_k, lt, eq);
+    if (E.X->r26_k > 0) bivariate_r26(ev, x, y, E.X->lt_b, E.X->r26_k >> 8, E.X->r26_k & 255, lt, eq);
+    else if (E.X->r23_k > 0) bivariate_r23(ev, x, y, E.X->lt_b, E.X->r23_k, lt, eq);
     else bivariate_r16(ev, x, y, E.X->lt_b, lt, eq);
 }
 

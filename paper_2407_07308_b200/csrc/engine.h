@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -93,6 +94,7 @@ struct bc_ctx {
     std::vector<int64_t> lt_u, eq_u;            // univariate LT / EQ coefficients
     std::vector<std::vector<int64_t>> lt_b;     // bivariate c[j][k] (Y^j Z^k)
     int r23_k = 0;                              // R23 baby-step size (params schedule 23), 0 = R16 circuits
+    int r26_k = 0;                              // R26 bivariate block sizes k1 << 8 | k2 (schedule 26), 0 = off
     const uint64_t *plan(const std::string &k) const;
 };
 
@@ -115,12 +117,41 @@ void lift_p(bc_ctx *X, const std::string &key, const Mod *mods, uint32_t p, cons
             uint64_t *out, uint64_t out_pstride, int16_t *out16, uint32_t npoly, uint32_t n, uint32_t skip0,
             uint32_t skipn, int mode, cudaStream_t st);
 
+// modulus-switch memo (R12: switching is deterministic, so reusing an earlier switch of the same ciphertext
+// never changes a bit): entries keyed by the source view, valid while the source buffer is the same live
+// object; FIFO-bounded by entry count (so the dry-run sizing sees the same allocations as the real run)
+struct MsMemo {
+    struct Key {
+        const uint64_t *d;
+        uint32_t B, lvl;
+        uint64_t bstride;
+        bool operator<(const Key &o) const {
+            if (d != o.d) return d < o.d;
+            if (B != o.B) return B < o.B;
+            if (lvl != o.lvl) return lvl < o.lvl;
+            return bstride < o.bstride;
+        }
+    };
+    struct Ent {
+        std::weak_ptr<Buf> src;
+        CT out;
+        uint64_t seq;
+    };
+    static constexpr size_t N = 32;
+    std::map<Key, Ent> m;
+    std::deque<std::pair<Key, uint64_t>> order;
+    uint64_t seq = 0;
+    bool on = false;        // enabled inside the digit circuits only (their values are never modified in place)
+    size_t hits = 0, misses = 0;
+};
+
 // engine: batched BGV ops on one stream over a workspace arena
 struct Eng {
     bc_ctx *X;
     const bc_keys *keys;
     Arena *A;
     cudaStream_t st;
+    std::shared_ptr<MsMemo> msm = std::make_shared<MsMemo>();
     bool dry() const { return A->dry; }
 
     BufP alloc_words(uint64_t words);

@@ -56,6 +56,11 @@ def test_circuit_plan_matches_oracle():
             k = c.r23_univariate_k(p) if kind == "U" else c.r23_bivariate_k(p)
             f = c.univariate_lt_eq_r23 if kind == "U" else c.bivariate_lt_eq_r23
             assert bc.circuit_plan(p, kind, "r23") == (k,) + c._r23_cost(f, p, k)
+            if kind == "B":
+                k1, k2 = c.r26_bivariate_k(p)
+                assert bc.circuit_plan(p, kind, "r26") == ((k1 << 8) | k2,) + c._r26_cost(p, k1, k2)
+            else:
+                assert bc.circuit_plan(p, kind, "r26") == bc.circuit_plan(p, kind, "r23")
     with pytest.raises(bc.BoostComError):
         bc.circuit_plan(15, "U", "r23")
 

@@ -440,9 +440,9 @@ def test_compare_full_c3_decrypts(pair):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c3t", "c3t@r16"])
+@pytest.mark.parametrize("name", ["c3t", "c3t@r23", "c3t@r16"])
 def test_compare_c3t_bivariate_p31_bit_exact(pair, name):
-    """C3's p = 31 bivariate digit circuit (R23: 73 products, C3's schedule; R16: 88) on a small
+    """C3's p = 31 bivariate digit circuit (R26: 59 products, C3's schedule; R23: 73; R16: 88) on a small
     ring (c3t: m = 1129, (d,l) = (1,2), 9 + 4 primes): whole compare_lt ciphertext bit-exact vs the
     oracle (~4 min of oracle time), decrypted bits = [a<b]."""
     from oracle import circuits
