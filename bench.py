@@ -578,6 +578,17 @@ def run_vector_workload(args, cfg, rank, world, local, workload):
     if workload == "tournament":
         need = max(need, ctx.workspace_bytes(V))
     free, _ = torch.cuda.mem_get_info(dev)
+    vc = args.vec_chunk
+    while need > free - (1 << 30) and not args.vec_chunk and len(elems) > 1:
+        # the batched pairwise compares do not fit: cap the ciphertext pairs per batched compare (halving)
+        vc = (T * (T - 1) // 2 if vc == 0 else vc) // 2
+        if vc < 1:
+            break
+        bc._lib.bc_tune(b"vec_chunk", vc)
+        need = ctx.vec_workspace_bytes(op, levels, V)
+        if workload == "tournament":
+            need = max(need, ctx.workspace_bytes(V))
+    args.vec_chunk = vc
     if need > free - (1 << 30):
         raise SystemExit("workspace %.1f GB > free %.1f GB: use --vec-chunk" % (need / 1e9, free / 1e9))
     ctx.workspace(need)

@@ -457,6 +457,7 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
 // scratch regions; the words are identical (every job is independent).
 int g_ntt_split = 0;
 int g_ntt_persist_occ = 0;
+int g_ntt_lean = 0;
 static cudaStream_t side_stream_for_device() {
     static std::mutex mu;
     static cudaStream_t s[64] = {nullptr};

@@ -209,6 +209,7 @@ extern int g_kip_blocked;
 extern int g_lift2;
 extern int g_ntt_split;        // 1: transform calls split over two streams (see ntt_split_or_common)
 extern int g_ntt_persist_occ;  // >0: cap of the persistent column passes' CTAs per SM
+extern int g_ntt_lean;         // persistent column passes: table tiles in shared memory (0) or read through L2 (1-3)
 extern int g_ntt_timing;
 // comparison phases (bench "phases"; NVTX ranges of the same names)
 enum { PH_EXTRACT = 0, PH_DIGIT, PH_LEX, PH_BCAST, PH_COMPACT, PH_PQMAIN, NPHASE };

@@ -122,39 +122,58 @@ __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int LOGR, int LOGE, int TC, int CCV>
+template <int LOGR, int LOGE, int TC, int CCV, int LEAN = 0>
 struct PersistA {
     static constexpr int R = 1 << LOGR, E = 1 << LOGE;
     typedef PtTab<LOGR, LOGE, true> PTT;
-    // doubles: exchange R*TC, chirp tile (R/2)*TC, cross-twiddle tile R*TC, staging (R/2)*TC; int32 position
-    // tile (R/2)*TC (inverse gather); double2: twiddles
-    static constexpr size_t SMEM = ((size_t)R * TC * 2 + (size_t)R * TC) * 8 + (size_t)(R / 2) * TC * 4 +
-                                   ((size_t)R / 2 + PTT::WORDS) * 16;
+    // LEAN 0 -- doubles: exchange R*TC, chirp tile (R/2)*TC, cross-twiddle tile R*TC, staging (R/2)*TC; int32
+    // position tile (R/2)*TC (inverse gather); double2: twiddles.  LEAN >= 1 (tables read through L1 / L2, positions
+    // computed or read from T.pos): exchange + staging + twiddles only, 4 CTAs of 256 threads per SM.
+    static constexpr size_t SMEM = LEAN ? ((size_t)R * TC + (size_t)(R / 2) * TC) * 8 + ((size_t)R / 2 + PTT::WORDS) * 16
+                                        : ((size_t)R * TC * 2 + (size_t)R * TC) * 8 + (size_t)(R / 2) * TC * 4 +
+                                              ((size_t)R / 2 + PTT::WORDS) * 16;
 };
 
-// INV 0: forward (input t < n), 1: inverse (input gathered through pos[t], t < m)
-template <int LOGR, int LOGE, int TC, int CCV, int INV>
-__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
+// INV 0: forward (input t < n), 1: inverse (input gathered through pos[t], t < m).  LEAN 0: the group's
+// chirp / cross-twiddle / position tiles resident in shared memory (2 CTAs per SM); LEAN >= 1: the same values
+// read from the global tables (L2-resident) at their point of use, at MINB CTAs per SM.
+template <int LOGR, int LOGE, int TC, int CCV, int INV, int LEAN = 0, int MINB = 2>
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), MINB)
     kf_passA_p(NttTables T, const uint64_t *__restrict__ in, uint64_t in_pstride, LimbMap lm, uint64_t job0, uint32_t nj,
                double *__restrict__ scratch) {
-    typedef PersistA<LOGR, LOGE, TC, CCV> PA;
+    typedef PersistA<LOGR, LOGE, TC, CCV, LEAN> PA;
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
     constexpr uint32_t CC = CCV;          // columns (a power of two, or 256 r N' for the mixed-radix lengths)
     extern __shared__ double smf[];
-    double *scol = smf, *ttf = scol + R * TC, *txt = ttf + (R / 2) * TC;
-    uint64_t *stage = (uint64_t *)(txt + R * TC);
+    double *scol = smf, *ttf = scol + R * TC, *txt = ttf + (LEAN ? 0 : (R / 2) * TC);
+    uint64_t *stage = (uint64_t *)(LEAN ? ttf : txt + R * TC);
     double2 *stw = (double2 *)(stage + (R / 2) * TC), *spt = stw + R / 2;
     int32_t *tpos = (int32_t *)(spt + PA::PTT::WORDS);
     const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
     const uint32_t c = blockIdx.x * TC + col;
     const uint32_t G = gridDim.y;
     const uint32_t tlim = INV ? T.m : T.n;
-    // the position tile does not depend on the prime: filled once
-    for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
-        const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
-        tpos[i] = INV ? (t < T.m ? T.pos[t] : -1) : (t < T.n ? (int32_t)t : -1);
+    // input position of row r of this thread's column (-1: zero)
+    auto posf = [&](uint32_t r) -> int {
+        const uint32_t t = r * CC + c;
+        if (!INV) return t < T.n ? (int)t : -1;
+        if (!LEAN) return tpos[r * TC + col];
+        return t < T.m ? T.pos[t] : -1;
+    };
+    if (!LEAN && INV) {    // the position tile does not depend on the prime: filled once
+        for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+            const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+            tpos[i] = t < T.m ? T.pos[t] : -1;
+        }
+        __syncthreads();
     }
-    __syncthreads();
+    // staging words that no job copies (position -1) hold 0 for the whole kernel: the input products below
+    // are then branch-free (fmm8(0, w) = 0)
+#pragma unroll
+    for (int k = 0; k < E / 2; ++k) {
+        const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
+        if (posf(r) < 0) stage[r * TC + col] = 0;
+    }
     uint32_t cur_pr = 0xffffffffu;
     auto prefetch = [&](uint32_t jj) {
         const JobF Jn = job_f(lm, (uint32_t)(job0 + jj));
@@ -162,7 +181,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
 #pragma unroll
         for (int k = 0; k < E / 2; ++k) {
             const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
-            const int ps = tpos[r * TC + col];
+            const int ps = posf(r);
             if (ps >= 0) cp_async8(stage + r * TC + col, sn + ps);
         }
         cp_async_commit();
@@ -171,18 +190,20 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
     for (uint32_t jj = blockIdx.y; jj < nj; jj += G) {
         const JobF J = job_f(lm, (uint32_t)(job0 + jj));
         const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+        const double *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m, *xt = T.fxta + (uint64_t)J.pr * T.M;
         if (J.pr != cur_pr) {           // uniform over the CTA: the tiles of this prime
             __syncthreads();
             const double2 *gtw = T.ftwRb + (uint64_t)J.pr * (R / 2);
             for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = gtw[j];
             if (col == 0) PA::PTT::fill(spt, tau, gtw);
-            const double *tf = (INV ? T.ftf1i : T.ftf1) + (uint64_t)J.pr * T.m, *xt = T.fxta + (uint64_t)J.pr * T.M;
-            for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
-                const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
-                ttf[i] = t < tlim ? tf[t] : 0.0;
+            if (!LEAN) {
+                for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+                    const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+                    ttf[i] = t < tlim ? tf[t] : 0.0;
+                }
+                for (int i = threadIdx.x; i < R * TC; i += blockDim.x)
+                    txt[i] = xt[(uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC)];
             }
-            for (int i = threadIdx.x; i < R * TC; i += blockDim.x)
-                txt[i] = xt[(uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC)];
             cur_pr = J.pr;
             __syncthreads();
         }
@@ -197,7 +218,8 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
                 continue;
             }
             const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
-            v[k] = tpos[r * TC + col] >= 0 ? fmm8(from_u64(stage[r * TC + col]), ttf[r * TC + col], q, qi) : 0.0;
+            const uint32_t t = r * CC + c;
+            v[k] = fmm8(from_u64(stage[r * TC + col]), LEAN ? __ldg(tf + (t < tlim ? t : tlim - 1)) : ttf[r * TC + col], q, qi);
             bd[k] = UMUL8;
         }
         if (jj + G < nj) prefetch(jj + G);   // the next job's inputs while this one is transformed
@@ -207,7 +229,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
         for (int k = 0; k < E; ++k) {
             const uint32_t rp = held_index<LOGE>(tau, 0, k);
             need(v, bd, k, LIM_MUL, q, qi);
-            __stcs(dst + rp * CC + c, fmm8(v[k], txt[rp * TC + col], q, qi));
+            __stcs(dst + rp * CC + c, fmm8(v[k], LEAN ? __ldg(xt + rp * CC + c) : txt[rp * TC + col], q, qi));
         }
     }
     cp_async_wait_all();
@@ -215,35 +237,51 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
 
 // pass C, persistent: column inverse + output chirp + Z_m^* gather (INV 0) or A_t - A_{m-1} (INV 1, prime m,
 // corner[] from kf_corner).  As kf_passA_p: per-prime output-chirp tile and the position tile in shared
-// memory, the next job's pass-B output prefetched with cp.async while this one is transformed.
-template <int LOGR, int LOGE, int TC, int CCV>
+// memory (LEAN 0), the next job's pass-B output prefetched with cp.async while this one is transformed.
+// LEAN 1: chirp and positions read from the global tables; LEAN 2: in addition the staging tile is the
+// exchange buffer (the next job's prefetch is issued after the exchange, overlapping the second register
+// pass and the epilogue), so 4 CTAs of 256 threads fit an SM; LEAN 4: tiles in shared memory, staging tile
+// as exchange buffer (3 CTAs per SM).
+template <int LOGR, int LOGE, int TC, int CCV, int LEAN = 0>
 struct PersistC {
     static constexpr int R = 1 << LOGR;
     typedef PtTab<LOGR, LOGE, false> PTT;
     // doubles: exchange R*TC, staging R*TC, chirp tile (R/2)*TC; int32 positions (R/2)*TC; double2 twiddles
-    static constexpr size_t SMEM = ((size_t)R * TC * 2 + (size_t)(R / 2) * TC) * 8 + (size_t)(R / 2) * TC * 4 +
+    static constexpr bool GT = LEAN == 1 || LEAN == 2;     // chirp / positions from the global tables
+    static constexpr bool XCH = LEAN == 2 || LEAN == 4;    // the staging tile is the exchange buffer
+    static constexpr size_t SMEM = (size_t)R * TC * 8 * (XCH ? 1 : 2) + (GT ? 0 : (size_t)(R / 2) * TC * 12) +
                                    ((size_t)R / 2 + PTT::WORDS) * 16;
 };
 
-template <int LOGR, int LOGE, int TC, int CCV, int INV>
-__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
+template <int LOGR, int LOGE, int TC, int CCV, int INV, int LEAN = 0, int MINB = 2>
+__global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), MINB)
     kf_passC_p(NttTables T, uint64_t *__restrict__ out, uint64_t out_pstride, LimbMap lm, uint64_t job0, uint32_t nj,
                const double *__restrict__ scratch, const uint64_t *__restrict__ corner) {
-    typedef PersistC<LOGR, LOGE, TC, CCV> PC;
+    typedef PersistC<LOGR, LOGE, TC, CCV, LEAN> PC;
+    typedef Passes<LOGR, LOGE> PS;
+    constexpr bool GT = PC::GT, XCH = PC::XCH;
+    static_assert(!XCH || PS::NP == 2, "staging tile as exchange buffer: two register passes");
     constexpr int E = 1 << LOGE, R = 1 << LOGR;
     constexpr uint32_t CC = CCV;
     extern __shared__ double smf[];
-    double *scol = smf, *stage = scol + R * TC, *tfo = stage + R * TC;
+    double *scol = smf, *stage = XCH ? scol : scol + R * TC, *tfo = stage + R * TC;
     int32_t *tpos = (int32_t *)(tfo + (R / 2) * TC);
-    double2 *stw = (double2 *)(tpos + (R / 2) * TC), *spt = stw + R / 2;
+    double2 *stw = (double2 *)(GT ? tfo : (double *)(tpos + (R / 2) * TC)), *spt = stw + R / 2;
     const uint32_t col = threadIdx.x % TC, tau = threadIdx.x / TC;
     const uint32_t c = blockIdx.x * TC + col;
     const uint32_t G = gridDim.y;
-    for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
-        const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
-        tpos[i] = INV ? (t < T.n ? (int32_t)t : -1) : (t < T.m ? T.pos[t] : -1);
+    auto posf = [&](uint32_t r) -> int {
+        if (!GT) return tpos[r * TC + col];
+        const uint32_t t = r * CC + c;
+        return INV ? (t < T.n ? (int)t : -1) : (t < T.m ? T.pos[t] : -1);
+    };
+    if (!GT) {
+        for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+            const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+            tpos[i] = INV ? (t < T.n ? (int32_t)t : -1) : (t < T.m ? T.pos[t] : -1);
+        }
+        __syncthreads();
     }
-    __syncthreads();
     uint32_t cur_pr = 0xffffffffu;
     auto prefetch = [&](uint32_t jj) {
         const double *src = scratch + (uint64_t)jj * T.M;
@@ -258,15 +296,17 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
     for (uint32_t jj = blockIdx.y; jj < nj; jj += G) {
         const JobF J = job_f(lm, (uint32_t)(job0 + jj));
         const double q = T.fmods[J.pr].x, qi = T.fmods[J.pr].y;
+        const double *tf = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
         if (J.pr != cur_pr) {
             __syncthreads();
             const double2 *gtw = T.ftwRi + (uint64_t)J.pr * (R / 2);
             for (int j = threadIdx.x; j < R / 2; j += blockDim.x) stw[j] = gtw[j];
             if (col == 0) PC::PTT::fill(spt, tau, gtw);
-            const double *tf = (INV ? T.ftfoi : T.ftfo) + (uint64_t)J.pr * T.m;
-            for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
-                const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
-                tfo[i] = t < T.m ? tf[t] : 0.0;
+            if (!GT) {
+                for (int i = threadIdx.x; i < (R / 2) * TC; i += blockDim.x) {
+                    const uint32_t t = (uint32_t)(i / TC) * CC + blockIdx.x * TC + (uint32_t)(i % TC);
+                    tfo[i] = t < T.m ? tf[t] : 0.0;
+                }
             }
             cur_pr = J.pr;
             __syncthreads();
@@ -279,17 +319,34 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), 2)
             v[k] = stage[held_index<LOGE>(tau, 0, k) * TC + col];
             bd[k] = UMUL8;
         }
-        if (jj + G < nj) prefetch(jj + G);
-        fct_pass<LOGR, LOGE, false, TC, 0>(v, bd, tau, col, scol, stw, spt, q, qi);
+        if (!XCH) {
+            if (jj + G < nj) prefetch(jj + G);
+            fct_pass<LOGR, LOGE, false, TC, 0>(v, bd, tau, col, scol, stw, spt, q, qi);
+        } else {
+            // fct_pass<.., 0> written out: register pass 0, exchange through the staging tile (each thread
+            // writes back exactly the words it read), prefetch of the next job once every thread has read its
+            // exchanged values, register pass 1
+            constexpr int TPR = 1 << (LOGR - LOGE);
+            freg_pass<LOGE, PS::dit_ns(0), false, PS::dit_lo(0), false>(v, bd, tau, stw, spt + tau, TPR, LOGR, q, qi);
+#pragma unroll
+            for (int k = 0; k < E; ++k) scol[held_index<LOGE>(tau, PS::dit_lo(0), k) * TC + col] = v[k];
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < E; ++k) v[k] = scol[held_index<LOGE>(tau, PS::dit_lo(1), k) * TC + col];
+            __syncthreads();
+            if (jj + G < nj) prefetch(jj + G);
+            flatten(v, bd, PS::dit_ns(1), q, qi);
+            freg_pass<LOGE, PS::dit_ns(1), false, PS::dit_lo(1), false>(v, bd, tau, stw, spt + tau, TPR, LOGR, q, qi);
+        }
         uint64_t *dst = out + (uint64_t)J.poly * out_pstride + (uint64_t)J.lb * T.n;
         const uint64_t cn = INV ? corner[jj] : 0;
 #pragma unroll
         for (int k = 0; k < E / 2; ++k) {   // rows >= R/2: t >= M/2 >= m, never output
             const uint32_t r = held_index<LOGE>(tau, LOGR - LOGE, k);
-            const int ps = tpos[r * TC + col];
+            const int ps = posf(r);
             if (ps < 0) continue;
             need(v, bd, k, LIM_MUL, q, qi);
-            const uint64_t x = to_u64(fmm8(v[k], tfo[r * TC + col], q, qi), q);
+            const uint64_t x = to_u64(fmm8(v[k], GT ? __ldg(tf + r * CC + c) : tfo[r * TC + col], q, qi), q);
             __stcs(dst + ps, INV ? (x >= cn ? x - cn : x + (uint64_t)q - cn) : x);
         }
     }
@@ -581,53 +638,97 @@ __global__ void __launch_bounds__(32) kf_corner(NttTables T, LimbMap lm, uint64_
     }
 }
 
+// persistent column passes: attributes and occupancy per device (once), CTAs per column group = resident CTAs
+// per SM x 148 / column groups (capped by bc_tune "ntt_persist_occ")
+template <int LOGR, int LOGER, int TC, int CCV, int LEAN, int MINB>
+static void launch_pA(int inv, const NttTables &T, const uint64_t *in, uint64_t in_ps, LimbMap lm, uint64_t j0, uint32_t nj,
+                      double *scr, cudaStream_t st) {
+    typedef PersistA<LOGR, LOGER, TC, CCV, LEAN> PA;
+    constexpr int TH = TC << (LOGR - LOGER);
+    static std::atomic<uint64_t> init_dev{0};
+    static int nb[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_pending(init_dev)) {
+        cudaFuncSetAttribute(kf_passA_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
+        cudaFuncSetAttribute(kf_passA_p<LOGR, LOGER, TC, CCV, 1, LEAN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB>, TH, PA::SMEM);
+        nb[dev & 63] = b > 0 ? b : 1;
+        attr_done(init_dev);
+    }
+    const uint32_t ncg = CCV / TC;
+    const int occ = g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nb[dev & 63]) : nb[dev & 63];
+    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(occ * 148) / ncg));
+    if (inv) kf_passA_p<LOGR, LOGER, TC, CCV, 1, LEAN, MINB><<<dim3(ncg, G), TH, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+    else kf_passA_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB><<<dim3(ncg, G), TH, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
+}
+template <int LOGR, int LOGER, int TC, int CCV, int LEAN, int MINB>
+static void launch_pC(int inv, const NttTables &T, uint64_t *out, uint64_t out_ps, LimbMap lm, uint64_t j0, uint32_t nj,
+                      const double *scr, const uint64_t *corner, cudaStream_t st) {
+    typedef PersistC<LOGR, LOGER, TC, CCV, LEAN> PC;
+    constexpr int TH = TC << (LOGR - LOGER);
+    static std::atomic<uint64_t> init_dev{0};
+    static int nb[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_pending(init_dev)) {
+        cudaFuncSetAttribute(kf_passC_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
+        cudaFuncSetAttribute(kf_passC_p<LOGR, LOGER, TC, CCV, 1, LEAN, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB>, TH, PC::SMEM);
+        nb[dev & 63] = b > 0 ? b : 1;
+        attr_done(init_dev);
+    }
+    const uint32_t ncg = CCV / TC;
+    const int occ = g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nb[dev & 63]) : nb[dev & 63];
+    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)(occ * 148) / ncg));
+    if (inv) kf_passC_p<LOGR, LOGER, TC, CCV, 1, LEAN, MINB><<<dim3(ncg, G), TH, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner);
+    else kf_passC_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB><<<dim3(ncg, G), TH, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
+}
+// g_ntt_lean: 0 -> shared-memory table tiles (2 CTAs per SM); 1 -> lean A (4 per SM) + lean C (3 per SM);
+// 2 -> lean A + C with the staging tile as exchange buffer (4 per SM); 3 -> round-2 A + that C;
+// 4 -> round-2 A + C with shared-memory tiles and the staging tile as exchange buffer (3 per SM)
+template <int LOGR, int LOGER, int TC, int CCV>
+static void persist_A(int inv, const NttTables &T, const uint64_t *in, uint64_t in_ps, LimbMap lm, uint64_t j0, uint32_t nj,
+                      double *scr, cudaStream_t st) {
+    if (g_ntt_lean == 0 || g_ntt_lean >= 3) launch_pA<LOGR, LOGER, TC, CCV, 0, 2>(inv, T, in, in_ps, lm, j0, nj, scr, st);
+    else launch_pA<LOGR, LOGER, TC, CCV, 1, 4>(inv, T, in, in_ps, lm, j0, nj, scr, st);
+}
+template <int LOGR, int LOGER, int TC, int CCV>
+static void persist_C(int inv, const NttTables &T, uint64_t *out, uint64_t out_ps, LimbMap lm, uint64_t j0, uint32_t nj,
+                      const double *scr, const uint64_t *corner, cudaStream_t st) {
+    if (g_ntt_lean == 1) launch_pC<LOGR, LOGER, TC, CCV, 1, 3>(inv, T, out, out_ps, lm, j0, nj, scr, corner, st);
+    else if (g_ntt_lean == 2 || g_ntt_lean == 3) launch_pC<LOGR, LOGER, TC, CCV, 2, 4>(inv, T, out, out_ps, lm, j0, nj, scr, corner, st);
+    else if (g_ntt_lean == 4) launch_pC<LOGR, LOGER, TC, CCV, 4, 3>(inv, T, out, out_ps, lm, j0, nj, scr, corner, st);
+    else launch_pC<LOGR, LOGER, TC, CCV, 0, 2>(inv, T, out, out_ps, lm, j0, nj, scr, corner, st);
+}
+
 // mixed-radix transform (prime m): persistent passes A / C with C = RAD 2^LOGN columns, mixed row pass B
 template <int RAD, int LOGN, int LOGEB, int RB>
 static void runf_mr(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap lm, uint64_t in_ps, uint64_t out_ps,
                     uint64_t *scratch, uint64_t j0, uint32_t nj, int inv, cudaStream_t st, uint64_t *corner_buf) {
     constexpr int LOGR = 8, LOGER = 4, TC = 16, CCV = RAD << LOGN;
-    typedef PersistA<LOGR, LOGER, TC, CCV> PA;
-    typedef PersistC<LOGR, LOGER, TC, CCV> PC;
     typedef ShapeMR<LOGN, LOGEB, RB, RAD> SB;
-    constexpr int THA = TC << (LOGR - LOGER);
     static std::atomic<uint64_t> init_dev{0};
-    static int nbA[64] = {0}, nbC[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (attr_pending(init_dev)) {
-        for (int d = 0; d < 2; ++d) {
-            auto ka = d ? kf_passA_p<LOGR, LOGER, TC, CCV, 1> : kf_passA_p<LOGR, LOGER, TC, CCV, 0>;
-            auto kc = d ? kf_passC_p<LOGR, LOGER, TC, CCV, 1> : kf_passC_p<LOGR, LOGER, TC, CCV, 0>;
-            auto kb = d ? kf_passB_mr<LOGN, LOGEB, RB, 1, RAD> : kf_passB_mr<LOGN, LOGEB, RB, 0, RAD>;
-            cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
-            cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
-            cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::SMEM);
-        }
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, TC, CCV, 0>, THA, PA::SMEM);
-        nbA[dev & 63] = b > 0 ? b : 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, TC, CCV, 0>, THA, PC::SMEM);
-        nbC[dev & 63] = b > 0 ? b : 1;
+        cudaFuncSetAttribute(kf_passB_mr<LOGN, LOGEB, RB, 0, RAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::SMEM);
+        cudaFuncSetAttribute(kf_passB_mr<LOGN, LOGEB, RB, 1, RAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::SMEM);
         attr_done(init_dev);
     }
     NttTables T = T0;
     T.dbg = 0;
     double *scr = (double *)scratch;
-    const uint32_t ncg = CCV / TC;
-    const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbA[dev & 63]) : nbA[dev & 63]) * 148) / ncg));
-    const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbC[dev & 63]) : nbC[dev & 63]) * 148) / ncg));
     dim3 gB((1 << LOGR) / RB, nj);
+    persist_A<LOGR, LOGER, TC, CCV>(inv, T, in, in_ps, lm, j0, nj, scr, st);
     if (!inv) {
-        kf_passA_p<LOGR, LOGER, TC, CCV, 0><<<dim3(ncg, GA), THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
         kf_passB_mr<LOGN, LOGEB, RB, 0, RAD><<<gB, SB::THREADS, SB::SMEM, st>>>(T, lm, j0, scr);
-        kf_passC_p<LOGR, LOGER, TC, CCV, 0><<<dim3(ncg, GC), THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
     } else {
-        kf_passA_p<LOGR, LOGER, TC, CCV, 1><<<dim3(ncg, GA), THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
         kf_passB_mr<LOGN, LOGEB, RB, 1, RAD><<<gB, SB::THREADS, SB::SMEM, st>>>(T, lm, j0, scr);
         kf_corner<LOGR><<<nj, 32, 0, st>>>(T, lm, j0, scr, corner_buf);
-        kf_passC_p<LOGR, LOGER, TC, CCV, 1><<<dim3(ncg, GC), THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner_buf);
         launch_counter() += 1;
     }
+    persist_C<LOGR, LOGER, TC, CCV>(inv, T, out, out_ps, lm, j0, nj, scr, inv ? corner_buf : nullptr, st);
     launch_counter() += 3;
 }
 
@@ -662,43 +763,23 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
     T.dbg = g_ntt_dbg;
     dim3 gA((1 << LOGC) / S::TC, nj), gB((1 << LOGR) / S::RB, nj);
     // persistent passes A and C (tiles of the prime resident in shared memory, cp.async prefetch of the next job)
-    if (persist && LOGR == 8 && !T.dbg && (!inv || (T.prime_m && corner_buf))) {
-        constexpr int CCV = 1 << LOGC;
-        typedef PersistA<LOGR, LOGER, S::TC, CCV> PA;
-        typedef PersistC<LOGR, LOGER, S::TC, CCV> PC;
-        static std::atomic<uint64_t> init_p{0};
-        static int nbA[64] = {0}, nbC[64] = {0};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (attr_pending(init_p)) {
-            for (int d = 0; d < 2; ++d) {
-                auto ka = d ? kf_passA_p<LOGR, LOGER, S::TC, CCV, 1> : kf_passA_p<LOGR, LOGER, S::TC, CCV, 0>;
-                auto kc = d ? kf_passC_p<LOGR, LOGER, S::TC, CCV, 1> : kf_passC_p<LOGR, LOGER, S::TC, CCV, 0>;
-                cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PA::SMEM);
-                cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC::SMEM);
-            }
-            int b = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passA_p<LOGR, LOGER, S::TC, CCV, 0>, S::THA, PA::SMEM);
-            nbA[dev & 63] = b > 0 ? b : 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kf_passC_p<LOGR, LOGER, S::TC, CCV, 0>, S::THA, PC::SMEM);
-            nbC[dev & 63] = b > 0 ? b : 1;
-            attr_done(init_p);
-        }
-        const uint32_t ncg = (1u << LOGC) / S::TC;
-        const uint32_t GA = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbA[dev & 63]) : nbA[dev & 63]) * 148) / ncg));
-        const uint32_t GC = std::max<uint32_t>(1, std::min<uint32_t>(nj, (uint32_t)((g_ntt_persist_occ > 0 ? std::min(g_ntt_persist_occ, nbC[dev & 63]) : nbC[dev & 63]) * 148) / ncg));
+    if constexpr (LOGR == 8) {
+        if (persist && !T.dbg && (!inv || (T.prime_m && corner_buf))) {
+            constexpr int CCV = 1 << LOGC;
+        persist_A<LOGR, LOGER, S::TC, CCV>(inv, T, in, in_ps, lm, j0, nj, scr, st);
         if (!inv) {
-            kf_passA_p<LOGR, LOGER, S::TC, CCV, 0><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
             kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
-            kf_passC_p<LOGR, LOGER, S::TC, CCV, 0><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
         } else {
-            kf_passA_p<LOGR, LOGER, S::TC, CCV, 1><<<dim3(ncg, GA), S::THA, PA::SMEM, st>>>(T, in, in_ps, lm, j0, nj, scr);
             kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
             kf_corner<LOGR><<<nj, 32, 0, st>>>(T, lm, j0, scr, corner_buf);
-            kf_passC_p<LOGR, LOGER, S::TC, CCV, 1><<<dim3(ncg, GC), S::THA, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner_buf);
             launch_counter() += 1;
         }
-    } else if (!inv) {
+        persist_C<LOGR, LOGER, S::TC, CCV>(inv, T, out, out_ps, lm, j0, nj, scr, inv ? corner_buf : nullptr, st);
+            launch_counter() += 3;
+            return;
+        }
+    }
+    if (!inv) {
         kf_passA<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
         kf_passC<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
