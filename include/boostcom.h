@@ -278,7 +278,11 @@ void bc_set_ntt_impl(int impl);
  * scratch per launch group (default: the whole batch in one group; smaller groups measured slower on B200),
  * "kip_blocked" (1: batch-blocked key inner product), "f64_elem" (1: binary64 element-wise kernels),
  * "nttc_variant" / "nttc_clusters" (the fused cluster transform of bc_set_ntt_impl(20); nttc_clusters
- * returns the occupancy query's cluster count).  None changes a result bit.  Returns 0 if known (-1 if not). */
+ * returns the occupancy query's cluster count), "ntt_epi" (1: the modulus-switch / ModDown scale-sub
+ * and the fused ModDown epilogue run inside pass C of the forward transform of delta; 0, default: separate
+ * kernels -- measured faster on B200), "ntt_lean" (4 default: pass-C staging tile as exchange buffer, 3 CTAs per SM; 0: round-2 passes; 1-3:
+ * tables read through L2 and / or the staging tile as exchange buffer), "ntt_persist_occ" (cap of the persistent passes' CTAs per SM),
+ * "ntt_split" (two-stream transform calls).  None changes a result bit.  Returns 0 if known (-1 if not). */
 int bc_tune(const char *key, int64_t value);
 /* live NTT timing: after bc_tune("ntt_timing", 1) every forward/inverse Bluestein NTT call records
  * a CUDA event pair on its stream.  bc_ntt_timing synchronises those events and returns (then

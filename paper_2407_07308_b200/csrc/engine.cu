@@ -863,6 +863,14 @@ void Eng::ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
     if (dry()) return;
     ntt_forward(X->T, in, out, npoly, lm, ips, ops, (uint64_t *)scr->p, st);
 }
+bool Eng::ntt_fwd_epi(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops,
+                      const NttEpi &e) {
+    if (!g_ntt_epi || !ntt_epi_supported(X->T)) return false;    // same decision in the dry run (sizing)
+    BufP scr = alloc_words(ntt_scratch_words(X, npoly, lm.njl));
+    if (dry()) return true;
+    ntt_forward_epi(X->T, e, in, out, npoly, lm, ips, ops, (uint64_t *)scr->p, st);
+    return true;
+}
 void Eng::ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops) {
     BufP scr = alloc_words(ntt_scratch_words(X, npoly, lm.njl, true));
     if (dry()) return;
@@ -882,6 +890,15 @@ CT Eng::modswitch(const CT &a) {
     if (!dry())
         lift_p(X, ("ms:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)last->p, n, (uint64_t *)delta->p,
              (uint64_t)(lv - 1) * n, nullptr, np, n, 0, 0, 1, st);
+    NttEpi e;                           // (c - delta) q^{-1} in pass C of the forward transform of delta
+    e.mode = 1;
+    e.mods = X->d_mods;
+    e.u = a.d;
+    e.ups = (uint64_t)lv * n;
+    e.w = X->d_invq + (size_t)lv * X->L1;
+    if (ntt_fwd_epi((uint64_t *)delta->p, out.d, np, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
+                    (uint64_t)(lv - 1) * n, e))
+        return out;
     ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, np, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
             (uint64_t)(lv - 1) * n);
     if (!dry())
@@ -1028,6 +1045,17 @@ CT Eng::ks_moddown(const BufP &u, uint32_t B, uint32_t lvl) {
         lift_p(X, ("down:" + std::to_string(lvl)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)K * n,
              (uint64_t *)delta->p, (uint64_t)lvl * n, nullptr, 2 * B, n, 0, 0, 1, st);
     sp.reset();
+    if (g_ntt_epi && ntt_epi_supported(X->T)) {   // (u - delta) P^{-1} in pass C of the forward transform of delta
+        CT o = ct_alloc(B, lvl, 2);
+        NttEpi e;
+        e.mode = 1;
+        e.mods = X->d_mods;
+        e.u = (uint64_t *)u->p;
+        e.ups = (uint64_t)nl * n;
+        e.w = X->d_invP;
+        ntt_fwd_epi((uint64_t *)delta->p, o.d, 2 * B, limbmap_plain(lvl, 0), (uint64_t)lvl * n, (uint64_t)lvl * n, e);
+        return o;
+    }
     ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lvl, 0), (uint64_t)lvl * n, (uint64_t)lvl * n);
     CT o = ct_alloc(B, lvl, 2);
     if (!dry())
@@ -1090,6 +1118,22 @@ CT Eng::mul(const CT &a0, const CT &b0) {
         lift_p(X, ("fd:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)(K + 1) * n,
              (uint64_t *)delta->p, (uint64_t)(lv - 1) * n, nullptr, 2 * B, n, 0, 0, 1, st);
     sp.reset();
+    if (g_ntt_epi && ntt_epi_supported(X->T)) {   // (w - delta) D^{-1} in pass C of the forward transform of delta
+        CT o = ct_alloc(B, lv - 1, 2);
+        NttEpi e;
+        e.mode = 2;
+        e.mods = X->d_mods;
+        e.u = U;
+        e.ups = ups;
+        e.d = Tt;
+        e.dbs = tw;
+        e.dks = (uint64_t)lv * n;
+        e.pm = X->d_Pm;
+        e.w = X->d_invD + (size_t)lv * L1;
+        ntt_fwd_epi((uint64_t *)delta->p, o.d, 2 * B, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
+                    (uint64_t)(lv - 1) * n, e);
+        return o;
+    }
     ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
             (uint64_t)(lv - 1) * n);
     CT o = ct_alloc(B, lv - 1, 2);

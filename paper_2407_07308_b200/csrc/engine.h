@@ -162,6 +162,9 @@ struct Eng {
     // transforms / element-wise
     void ntt_fwd(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops);
     void ntt_inv(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops);
+    // forward transform with the scale-sub / fused-ModDown epilogue in pass C (false: not available, nothing done)
+    bool ntt_fwd_epi(const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm, uint64_t ips, uint64_t ops,
+                     const NttEpi &e);
 
     CT modswitch(const CT &a);
     CT modswitch_to(const CT &a, uint32_t lvl);

@@ -457,7 +457,9 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
 // scratch regions; the words are identical (every job is independent).
 int g_ntt_split = 0;
 int g_ntt_persist_occ = 0;
-int g_ntt_lean = 0;
+int g_ntt_lean = 4;
+int g_ntt_epi = 0;      // measured: C2 compare 3.53 -> 3.55 ms with the fused epilogue (pass C's scattered
+                        // u / d loads cost more than the separate 128-bit streaming kernel), so off
 static cudaStream_t side_stream_for_device() {
     static std::mutex mu;
     static cudaStream_t s[64] = {nullptr};
@@ -513,6 +515,16 @@ void ntt_forward(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t
 void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                  uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st) {
     ntt_timed(T, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 1);
+}
+bool ntt_epi_supported(const NttTables &T) {
+    return (g_ntt_impl == 0 || (g_ntt_impl >= 10 && g_ntt_impl != 20)) && nttf_supported(T) && !g_ntt_split;
+}
+void ntt_forward_epi(const NttTables &T, const NttEpi &e, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                     uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st) {
+    if (!ntt_epi_supported(T)) throw std::runtime_error("ntt_forward_epi: fused epilogue needs the binary64 passes");
+    NttTables Te = T;
+    Te.epi = e;
+    ntt_timed(Te, in, out, npoly, lm, in_pstride, out_pstride, scratch, st, 0);
 }
 
 // =====================================================================================

@@ -24,6 +24,22 @@ inline void attr_done(std::atomic<uint64_t> &done) { done.fetch_or(cur_device_bi
 
 struct __align__(16) u64x2 { uint64_t w, ws; };   // value + Shoup companion (16-byte aligned: one 128-bit load)
 
+// Fused epilogue of a forward transform (binary64 pass C): the word x = NTT(in) at output position i of
+// poly p, limb lb becomes
+//   mode 1: (u - x) w_lb                  -- modulus switch (R13) / ModDown scale-sub (R14)
+//   mode 2: (u + pm_lb d - x) w_lb        -- fused ModDown + modulus switch of a product (R15), p = 2 b + k
+// with u = u[p ups + lb n + i], d = d[b dbs + k dks + lb n + i]; results identical to the separate kernels
+// (ew_scale_sub / ew_fused_down_out) -- the delta words are never written to memory.
+struct NttEpi {
+    int mode = 0;
+    const Mod *mods = nullptr;
+    const uint64_t *u = nullptr;
+    uint64_t ups = 0;
+    const uint64_t *d = nullptr;
+    uint64_t dbs = 0, dks = 0;
+    const u64x2 *pm = nullptr, *w = nullptr;
+};
+
 // Device tables of the Bluestein transforms (§8(a) a1/a2), one slice per prime.
 struct NttTables {
     const u64x2 *psi;     // [P][M]  psi^e (size-M root, free internal choice)
@@ -60,6 +76,7 @@ struct NttTables {
     const double *frtw = nullptr, *frtwi = nullptr;     // [P][C]: omega_C^{+-i j} at i 2^logN + j
     const double *frcon = nullptr, *frconi = nullptr;   // [P][16]: omega_rad^{+-j}, j < rad
     int prime_m;
+    NttEpi epi;           // forward transforms only (ntt_forward_epi); mode 0 elsewhere
     int dbg;              // ntt3.cu timing experiments only (bc_tune "ntt_dbg"): skip table reads; results invalid          // 1 if m is prime (reduction mod Phi_m is a single subtraction)
 };
 
@@ -79,6 +96,10 @@ void ntt_forward(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t
                  uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st);
 void ntt_inverse(const NttTables &T, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
                  uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st);
+// forward transform with a fused epilogue (NttEpi); only where ntt_epi_supported(T) (binary64 passes)
+bool ntt_epi_supported(const NttTables &T);
+void ntt_forward_epi(const NttTables &T, const NttEpi &e, const uint64_t *in, uint64_t *out, uint32_t npoly, LimbMap lm,
+                     uint64_t in_pstride, uint64_t out_pstride, uint64_t *scratch, cudaStream_t st);
 
 // ---- fused ModDown + modulus switch of a product (R15) ----
 // step 1: u[b][k][level-1] += (P mod q) d_k[level-1]   (u: [B][2] polys of stride u_pstride)
@@ -209,6 +230,7 @@ extern int g_kip_blocked;
 extern int g_lift2;
 extern int g_ntt_split;        // 1: transform calls split over two streams (see ntt_split_or_common)
 extern int g_ntt_persist_occ;  // >0: cap of the persistent column passes' CTAs per SM
+extern int g_ntt_epi;          // 1: scale-sub / fused-ModDown epilogues inside pass C of the forward transform
 extern int g_ntt_lean;         // persistent column passes: table tiles in shared memory (0) or read through L2 (1-3)
 extern int g_ntt_timing;
 // comparison phases (bench "phases"; NVTX ranges of the same names)

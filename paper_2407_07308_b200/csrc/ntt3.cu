@@ -115,6 +115,22 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
 // thread prefetches the next job's inputs into a shared staging tile with cp.async (LDGSTS) while the
 // current job is transformed; every thread reads back exactly the words it copied, so cp.async.wait_group
 // suffices (no barrier).  Results are identical to kf_passA (same arithmetic, same order).
+// fused forward epilogue (NttEpi, kernels.h): x = the transform's canonical output word at position i of poly
+// `poly`, limb lb -> (u - x) w_lb or (u + pm_lb d - x) w_lb, the values ew_scale_sub / ew_fused_down_out compute
+__device__ __forceinline__ uint64_t epi_apply(const NttEpi &e, uint32_t poly, uint32_t lb, uint32_t n, uint32_t i,
+                                              uint64_t x) {
+    const uint64_t q = e.mods[lb].q;
+    const uint64_t off = (uint64_t)lb * n + i;
+    uint64_t u = __ldcs(e.u + (uint64_t)poly * e.ups + off);
+    if (e.mode == 2) {
+        const u64x2 pm = e.pm[lb];
+        const uint64_t d = __ldcs(e.d + (uint64_t)(poly >> 1) * e.dbs + (uint64_t)(poly & 1) * e.dks + off);
+        u = add_mod(u, mul_shoup(d, pm.w, pm.ws, q), q);
+    }
+    const u64x2 w = e.w[lb];
+    return mul_shoup(sub_mod(u, x, q), w.w, w.ws, q);
+}
+
 __device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)), "l"(gsrc)
                  : "memory");
@@ -347,7 +363,8 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), MINB)
             if (ps < 0) continue;
             need(v, bd, k, LIM_MUL, q, qi);
             const uint64_t x = to_u64(fmm8(v[k], GT ? __ldg(tf + r * CC + c) : tfo[r * TC + col], q, qi), q);
-            __stcs(dst + ps, INV ? (x >= cn ? x - cn : x + (uint64_t)q - cn) : x);
+            __stcs(dst + ps, INV ? (x >= cn ? x - cn : x + (uint64_t)q - cn)
+                                 : (T.epi.mode ? epi_apply(T.epi, J.poly, J.lb, T.n, (uint32_t)ps, x) : x));
         }
     }
     cp_async_wait_all();
@@ -601,7 +618,7 @@ __global__ void __launch_bounds__(TC * (1 << (LOGR - LOGE)), FNTT_MINB(TC * (1 <
         const uint64_t x = to_u64((T.dbg & 16) ? fred(v[k], q, qi) : fmm8(v[k], tfo[t], q, qi), q);
         if (!INV) {
             const int ps = (T.dbg & 32) ? (t < T.n ? (int)t : -1) : T.pos[t];
-            if (ps >= 0) __stcs(dst + ps, x);
+            if (ps >= 0) __stcs(dst + ps, T.epi.mode ? epi_apply(T.epi, J.poly, J.lb, T.n, (uint32_t)ps, x) : x);
         } else if (direct) {
             if (t < T.n) __stcs(dst + t, x >= corner ? x - corner : x + (uint64_t)q - corner);
         } else {
@@ -686,9 +703,10 @@ static void launch_pC(int inv, const NttTables &T, uint64_t *out, uint64_t out_p
     if (inv) kf_passC_p<LOGR, LOGER, TC, CCV, 1, LEAN, MINB><<<dim3(ncg, G), TH, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, corner);
     else kf_passC_p<LOGR, LOGER, TC, CCV, 0, LEAN, MINB><<<dim3(ncg, G), TH, PC::SMEM, st>>>(T, out, out_ps, lm, j0, nj, scr, nullptr);
 }
-// g_ntt_lean: 0 -> shared-memory table tiles (2 CTAs per SM); 1 -> lean A (4 per SM) + lean C (3 per SM);
-// 2 -> lean A + C with the staging tile as exchange buffer (4 per SM); 3 -> round-2 A + that C;
-// 4 -> round-2 A + C with shared-memory tiles and the staging tile as exchange buffer (3 per SM)
+// g_ntt_lean (measured, C2 / C4 / C5 limb-transforms): 4 (default, 1-2% faster than 0) -> round-2 A + C with
+// shared-memory tiles and the staging tile as exchange buffer (3 per SM); 0 -> shared-memory table tiles
+// (2 CTAs per SM); 1 -> lean A (4 per SM) + lean C (3 per SM);
+// 2 -> lean A + C with the staging tile as exchange buffer (4 per SM); 3 -> round-2 A + that C
 template <int LOGR, int LOGER, int TC, int CCV>
 static void persist_A(int inv, const NttTables &T, const uint64_t *in, uint64_t in_ps, LimbMap lm, uint64_t j0, uint32_t nj,
                       double *scr, cudaStream_t st) {
