@@ -21,7 +21,7 @@ bc._lib.bc_tune(b"ntt_split", int(os.environ.get("SPLIT", "0")))
 for impl, gmb, lean in [(int(a), int(g), int(ln)) for a in os.environ.get("IMPLS", "7,0").split(",")
                         for g in os.environ.get("GMB", "4096").split(",") for ln in os.environ.get("LEAN", "0").split(",")]:
     bc.set_ntt_impl(impl)
-    bc._lib.bc_tune(b"ntt_lean", lean)
+    bc._lib.bc_tune(os.environ.get("KNOB", "ntt_lean").encode(), lean)
     bc._lib.bc_tune(b"ntt_group_bytes", gmb << 20)
     for _ in range(2):
         y = ctx.ntt_fwd(x, ws=ws)
@@ -44,9 +44,8 @@ for impl, gmb, lean in [(int(a), int(g), int(ln)) for a in os.environ.get("IMPLS
     if ref_inv is None:
         ref_inv = z.clone()
     ok = bool(torch.equal(y, ref)) and bool(torch.equal(z, ref_inv))
-    print(json.dumps({"limbs": npoly * L, "impl": impl, "group_mb": gmb, "lean": lean, "fwd_ms": round(f, 3), "inv_ms": round(i, 3),
+    print(json.dumps({"limbs": npoly * L, "impl": impl, "group_mb": gmb, "knob": os.environ.get("KNOB", "ntt_lean"), "value": lean, "fwd_ms": round(f, 3), "inv_ms": round(i, 3),
                       "us_per_limb_fwd": round(1000 * f / (npoly * L), 3),
                       "Tmulmod_s": round(work / (f / 1e3) / 1e12, 3), "matches_radix2": ok, "roundtrip": bool(torch.equal(ctx.ntt_inv(y, ws=ws), x))}), flush=True)
 bc.set_ntt_impl(0)
-bc._lib.bc_tune(b"ntt_lean", 0)
 bc._lib.bc_tune(b"ntt_group_bytes", 48 << 20)

@@ -15,6 +15,6 @@ if "NTT_LEAN" in os.environ:
 ctx = bc.Context(bc.load_params(os.environ.get("NTT_CFG", "c2")))
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("probe")      # ncu --nvtx --nvtx-include probe/ (context creation runs small NTTs)
-r = bc.profile_ntt(ctx)
+r = bc.profile_ntt(ctx, npoly=int(os.environ.get("NPOLY", "64")))
 torch.cuda.nvtx.range_pop()
 print(r)
