@@ -154,6 +154,18 @@ bc_status bc_max(bc_ctx *ctx, const bc_keys *keys, bc_ct a, bc_ct b, bc_ct out, 
                  size_t ws_bytes, void *stream);
 /* output level of compare_lt / select for an input level (for sizing outputs) */
 uint32_t bc_compare_out_level(bc_ctx *ctx, uint32_t level, int which /*0 lt, 1 eq, 2 min*/);
+/* compare_lt on HOST buffers (the end-to-end call; P:440's host<->device staging, pipelined): h_a, h_b =
+ * batch ciphertexts [batch][2][level][n] u64 in host memory (pinned for the copies to overlap), h_out =
+ * [batch][2][bc_compare_out_level(level, 0)][n].  The batch runs in chunks of `chunk` pairs (0: batch / 4):
+ * the host->device copy of chunk i+1 and the device->host copy of chunk i-1 run on a library copy stream
+ * while chunk i is compared on `stream` (events only, the host is never blocked).  d_stage: device buffer of
+ * bc_host_stage_bytes(ctx, chunk, level) bytes (two slots of inputs + output), d_ws as bc_compare_lt (per
+ * chunk).  `stream` completes after the last output word has reached h_out.  Words identical to
+ * bc_compare_lt.  BC_E_ARG for a short staging buffer or null pointers. */
+size_t bc_host_stage_bytes(bc_ctx *ctx, uint32_t chunk, uint32_t level);
+bc_status bc_compare_lt_host(bc_ctx *ctx, const bc_keys *keys, const uint64_t *h_a, const uint64_t *h_b,
+                             uint32_t batch, uint32_t level, uint64_t *h_out, uint32_t chunk, void *d_stage,
+                             size_t stage_bytes, void *d_ws, size_t ws_bytes, void *stream);
 
 /* ---- vectors of ciphertexts: min/max tournament, rank sort -------------- */
 /* Each element v[i] is a batch of `batch` ciphertexts (the same batch for all i); the operation

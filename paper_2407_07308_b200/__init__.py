@@ -81,6 +81,8 @@ _sig("bc_select", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
 _sig("bc_min", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
 _sig("bc_max", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp)
 _sig("bc_compare_out_level", _u32, _vp, _u32, ctypes.c_int)
+_sig("bc_host_stage_bytes", _sz, _vp, _u32, _u32)
+_sig("bc_compare_lt_host", _st, _vp, _vp, _vp, _vp, _u32, _u32, _vp, _u32, _vp, _sz, _vp, _sz, _vp)
 _sig("bc_compare_lt_async", _st, _vp, _vp, bc_ct, bc_ct, bc_ct, _vp, _sz, _vp, ctypes.POINTER(bc_handle))
 _sig("bc_wait", _st, ctypes.POINTER(bc_handle), _vp)
 _sig("bc_ntt_fwd", _st, _vp, _vp, _vp, _u32, _u32, _u32, _vp, _sz, _vp)
@@ -392,6 +394,20 @@ class Context:
 
     def compare_lt(self, keys, a, b, ws=None):
         return self._cmp(_lib.bc_compare_lt, keys, a, b, 0, ws)
+
+    def compare_lt_host(self, keys, h_a, h_b, h_out, chunk=0, ws=None, stage=None):
+        """bc_compare_lt_host: compare_lt of host (pinned) ciphertext tensors into the host tensor h_out,
+        host<->device copies pipelined with the compare on a library copy stream (end-to-end path)."""
+        B, lvl = h_a.shape[0], h_a.shape[2]
+        ch = chunk or max(1, (B + 3) // 4)
+        need = int(_lib.bc_host_stage_bytes(self._h, ch, lvl))
+        if stage is None:                # its own buffer: the compare workspace must not alias it
+            stage = _torch().empty(need, dtype=_torch().uint8, device=self.device)
+        w, wb = self._wsargs(ws)
+        _check(_lib.bc_compare_lt_host(self._h, keys.keys, h_a.data_ptr(), h_b.data_ptr(), B, lvl, h_out.data_ptr(), ch,
+                                       stage.data_ptr(), stage.numel() * stage.element_size(), w, wb, _stream()),
+               "bc_compare_lt_host")
+        return h_out
 
     def compare_eq(self, keys, a, b, ws=None):
         return self._cmp(_lib.bc_compare_eq, keys, a, b, 1, ws)

@@ -1,6 +1,7 @@
 // capi.cu -- extern "C" boundary of libboostcom.so (include/boostcom.h).
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 
 #include "engine.h"
 
@@ -38,6 +39,7 @@ int bc_tune(const char *key, int64_t value) {
     if (!strcmp(key, "ntt_split")) { g_ntt_split = (int)value; return 0; }
     if (!strcmp(key, "ntt_persist_occ")) { g_ntt_persist_occ = (int)value; return 0; }
     if (!strcmp(key, "ntt_lean")) { g_ntt_lean = (int)value; return 0; }
+    if (!strcmp(key, "axpy")) { g_axpy = (int)value; return 0; }
     if (!strcmp(key, "ntt_epi")) { g_ntt_epi = (int)value; return 0; }
     if (!strcmp(key, "lift2")) { g_lift2 = (int)value; return 0; }
     if (!strcmp(key, "kip_blocked")) { g_kip_blocked = (int)value; return 0; }
@@ -350,6 +352,86 @@ bc_status bc_compare_lt_async(bc_ctx *X, const bc_keys *k, bc_ct a, bc_ct b, bc_
     h->event = ev;
     h->stream = side;
     h->consumed = 0;
+    API_END
+}
+
+// ------------------------------------------------------------------ host buffers, pipelined (e2e)
+}  // extern "C"
+static cudaStream_t copy_stream_for_device() {
+    static std::mutex mu;
+    static cudaStream_t s[64] = {nullptr};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!s[dev & 63]) CK(cudaStreamCreateWithFlags(&s[dev & 63], cudaStreamNonBlocking));
+    return s[dev & 63];
+}
+extern "C" {
+
+size_t bc_host_stage_bytes(bc_ctx *X, uint32_t chunk, uint32_t level) {
+    if (!X || !chunk || level < 1 || level > X->L1) return 0;
+    const uint32_t lo = bc_compare_out_level(X, level, 0);
+    return (size_t)2 * chunk * (2ull * 2 * level + 2ull * lo) * X->n * 8;
+}
+
+bc_status bc_compare_lt_host(bc_ctx *X, const bc_keys *keys, const uint64_t *h_a, const uint64_t *h_b, uint32_t batch,
+                             uint32_t level, uint64_t *h_out, uint32_t chunk, void *d_stage, size_t stage_bytes,
+                             void *ws, size_t wsb, void *st) {
+    API_BEGIN
+    if (!X || !keys || !h_a || !h_b || !h_out || !d_stage) BC_THROW(BC_E_ARG, "null argument");
+    if (!batch) return BC_OK;
+    if (level < 1 || level > X->L1) BC_THROW(BC_E_LEVEL, "bad level");
+    if (!chunk) chunk = std::max<uint32_t>(1, (batch + 3) / 4);
+    chunk = std::min(chunk, batch);
+    if (bc_host_stage_bytes(X, chunk, level) > stage_bytes) BC_THROW(BC_E_ARG, "staging buffer smaller than bc_host_stage_bytes");
+    const uint32_t lo = bc_compare_out_level(X, level, 0);
+    const uint64_t cw = 2ull * level * X->n, ow = 2ull * lo * X->n;     // words per input / output ciphertext
+    const uint64_t slot = (uint64_t)chunk * (2 * cw + ow);
+    cudaStream_t cs = copy_stream_for_device(), ms = S(st);
+    cudaEvent_t h2d[2], done[2], d2h = nullptr;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&h2d[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&d2h, cudaEventDisableTiming));
+    // the copy stream starts after the work already queued on the caller's stream (e.g. a previous call's reads)
+    CK(cudaEventRecord(d2h, ms));
+    CK(cudaStreamWaitEvent(cs, d2h, 0));
+    bc_status rc = BC_OK;
+    const uint32_t nch = (batch + chunk - 1) / chunk;
+    auto slot_ptr = [&](uint32_t i) { return (uint64_t *)d_stage + (i & 1) * slot; };
+    // host->device copy of chunk i into slot i & 1 (copy stream).  Queue order on the copy stream:
+    // H2D(0), H2D(1), D2H(0), H2D(2), D2H(1), ... -- H2D(i+1) follows D2H(i-1), which waits for compare(i-1), so
+    // it overlaps compare(i) and never overwrites a slot that compare(i-1) or D2H(i-1) still reads
+    auto h2d_chunk = [&](uint32_t i) {
+        const uint32_t b0 = i * chunk, nb = std::min(chunk, batch - b0);
+        uint64_t *da = slot_ptr(i), *db = da + (uint64_t)chunk * cw;
+        CK(cudaMemcpyAsync(da, h_a + (uint64_t)b0 * cw, (size_t)nb * cw * 8, cudaMemcpyHostToDevice, cs));
+        CK(cudaMemcpyAsync(db, h_b + (uint64_t)b0 * cw, (size_t)nb * cw * 8, cudaMemcpyHostToDevice, cs));
+        CK(cudaEventRecord(h2d[i & 1], cs));
+    };
+    h2d_chunk(0);
+    for (uint32_t i = 0; i < nch; ++i) {
+        const uint32_t b0 = i * chunk, nb = std::min(chunk, batch - b0);
+        if (i + 1 < nch) h2d_chunk(i + 1);
+        uint64_t *da = slot_ptr(i), *db = da + (uint64_t)chunk * cw, *dout = db + (uint64_t)chunk * cw;
+        CK(cudaStreamWaitEvent(ms, h2d[i & 1], 0));
+        bc_ct av{da, nb, level}, bv{db, nb, level}, ov{dout, nb, lo}, none{nullptr, 0, 0};
+        rc = run_compare(X, keys, av, bv, ov, none, ws, wsb, st, 0);
+        if (rc != BC_OK) break;
+        CK(cudaEventRecord(done[i & 1], ms));
+        CK(cudaStreamWaitEvent(cs, done[i & 1], 0));
+        CK(cudaMemcpyAsync(h_out + (uint64_t)b0 * ow, dout, (size_t)nb * ow * 8, cudaMemcpyDeviceToHost, cs));
+    }
+    // the caller's stream completes only after every output word has reached the host
+    CK(cudaEventRecord(d2h, cs));
+    CK(cudaStreamWaitEvent(ms, d2h, 0));
+    for (int j = 0; j < 2; ++j) {
+        cudaEventDestroy(h2d[j]);
+        cudaEventDestroy(done[j]);
+    }
+    cudaEventDestroy(d2h);
+    if (rc != BC_OK) return rc;
     API_END
 }
 

@@ -969,6 +969,18 @@ CT Eng::scalar(const CT &a, int64_t c) {
     if (!dry()) ew_scalar(X->d_mods, a.d, centered_p(c, X->p), o.d, a.B, a.parts, a.lvl, X->n, st, g_f64_elem ? X->d_fm : nullptr);
     return o;
 }
+// acc + c x in one pass; the same words as add(acc, scalar(x, c)): modular arithmetic is exact, and where x sits
+// above acc's level the scalar product stays at x's level before the switch (the unfused order)
+CT Eng::axpy(const CT &acc0, const CT &x, int64_t c) {
+    if (!g_axpy || x.lvl > acc0.lvl || x.parts != acc0.parts || x.B != acc0.B) return add(acc0, scalar(x, c));
+    CT a = modswitch_to(acc0, x.lvl);
+    const uint64_t bs = (uint64_t)a.parts * x.lvl * X->n;
+    if (a.bstride != bs || x.bstride != bs) return add(a, scalar(x, c));
+    CT o = ct_alloc(a.B, x.lvl, a.parts);
+    if (!dry())
+        ew_axpy(X->d_mods, a.d, x.d, centered_p(c, X->p), o.d, a.B, a.parts, x.lvl, X->n, st, g_f64_elem ? X->d_fm : nullptr);
+    return o;
+}
 CT Eng::add_const(const CT &a, int64_t c) {
     CT o = ct_alloc(a.B, a.lvl, a.parts);
     if (!dry()) ew_add_const(X->d_mods, a.d, centered_p(c, X->p), o.d, a.B, a.parts, a.lvl, X->n, st);
@@ -1195,23 +1207,6 @@ static Val vadd(Eng &E, const Val &a, const Val &b) {
     if (b.isc) return VT(E.add_const(a.ct, b.c));
     return VT(E.add(a.ct, b.ct));
 }
-static Val lincomb(Eng &E, const std::vector<std::pair<int64_t, std::function<Val()>>> &terms, int64_t cst) {
-    const int64_t p = E.X->p;
-    bool have = false;
-    Val acc;
-    for (auto &t : terms) {
-        int64_t c = ((t.first % p) + p) % p;
-        if (!c) continue;
-        Val v = vmul(E, t.second(), VC(c));
-        acc = have ? vadd(E, acc, v) : v;
-        have = true;
-    }
-    cst = ((cst % p) + p) % p;
-    if (!have) return VC(cst);
-    if (cst) acc = vadd(E, acc, VC(cst));
-    return acc;
-}
-
 struct Powers {
     Eng &E;
     std::map<int, Val> pw;
@@ -1239,6 +1234,10 @@ struct EngEv {
     static int64_t cval(const V &v) { return v.c; }
     V mul(const V &a, const V &b) { return vmul(E, a, b); }
     V add(const V &a, const V &b) { return vadd(E, a, b); }
+    V axpy(const V &acc, const V &x, int64_t c) {          // add(acc, mul(x, cnst(c)))
+        if (acc.isc || x.isc) return vadd(E, acc, vmul(E, x, VC(c)));
+        return VT(E.axpy(acc.ct, x.ct, c));
+    }
     int64_t p() const { return E.X->p; }
 };
 struct CntV {
@@ -1270,6 +1269,7 @@ struct CntEv {
         r.depth = std::max(a.depth, b.depth);
         return r;
     }
+    V axpy(const V &acc, const V &x, int64_t c) { return add(acc, mul(x, cnst(c))); }
     int64_t p() const { return pp; }
 };
 
@@ -1316,8 +1316,7 @@ typename Ev::V lincombT(Ev &ev, const std::vector<std::pair<int64_t, std::functi
     for (auto &t : terms) {
         int64_t c = ((t.first % p) + p) % p;
         if (!c) continue;
-        typename Ev::V v = ev.mul(t.second(), ev.cnst(c));
-        acc = have ? ev.add(acc, v) : v;
+        acc = have ? ev.axpy(acc, t.second(), c) : ev.mul(t.second(), ev.cnst(c));
         have = true;
     }
     cst = ((cst % p) + p) % p;

@@ -169,6 +169,7 @@ struct Eng {
     CT modswitch(const CT &a);
     CT modswitch_to(const CT &a, uint32_t lvl);
     CT add(const CT &a, const CT &b);
+    CT axpy(const CT &acc, const CT &x, int64_t c);   // acc + c x (= add(acc, scalar(x, c)), one kernel)
     CT scalar(const CT &a, int64_t c);       // c in F_p (centered)
     CT add_const(const CT &a, int64_t c);
     CT ptmul(const CT &a, const uint64_t *pt);

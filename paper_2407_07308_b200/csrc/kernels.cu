@@ -458,6 +458,7 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
 int g_ntt_split = 0;
 int g_ntt_persist_occ = 0;
 int g_ntt_lean = 4;
+int g_axpy = 1;
 int g_ntt_epi = 0;      // measured: C2 compare 3.53 -> 3.55 ms with the fused epilogue (pass C's scattered
                         // u / d loads cost more than the separate 128-bit streaming kernel), so off
 static cudaStream_t side_stream_for_device() {
@@ -597,6 +598,37 @@ void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint3
         k_scalar_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, c, o, (uint32_t)rows, lvl, n);
     else
         k_scalar<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, c, o, (uint32_t)rows, lvl, n);
+    LAUNCHED();
+}
+
+// o = a + c x (the linear-combination step of the digit circuits: one pass instead of ew_scalar + ew_add)
+__global__ void k_axpy(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, const uint64_t *__restrict__ xs,
+                       int64_t c, uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
+    ROW_LOOP(r, x, rows, n) {
+        const Mod M = mods[r % lvl];
+        const uint64_t i = (uint64_t)r * n + x;
+        o[i] = add_mod(a[i], mul_mod(xs[i], small_res(c, M.q), M), M.q);
+    }
+}
+__global__ void k_axpy_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ a, const uint64_t *__restrict__ xs,
+                         int64_t c, uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {
+    using namespace f64;
+    const double cd = (double)c;
+    ROW_LOOP2(r, x, rows, n) {
+        const double q = fm[r % lvl].x, qi = fm[r % lvl].y;
+        const uint64_t qq = (uint64_t)q, i = (uint64_t)r * n + x;
+        const ulonglong2 av = LD2(a + i), xv = LD2(xs + i);
+        ST2(o + i, add_mod(av.x, to_u64(fmulv(from_u64(xv.x), cd, q, qi), q), qq),
+            add_mod(av.y, to_u64(fmulv(from_u64(xv.y), cd, q, qi), q), qq));
+    }
+}
+void ew_axpy(const Mod *mods, const uint64_t *a, const uint64_t *x, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
+             uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm) {
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    if (fm && c > -(1 << 20) && c < (1 << 20))
+        k_axpy_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, x, c, o, (uint32_t)rows, lvl, n);
+    else
+        k_axpy<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, x, c, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 

@@ -117,6 +117,8 @@ void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, 
 // o = a (parts pa) + b (parts pb) where the extra parts are copied (3-part + 2-part etc.)
 void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
             uint32_t n, cudaStream_t st);
+void ew_axpy(const Mod *mods, const uint64_t *a, const uint64_t *x, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
+             uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm);   // o = a + c x
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
                uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm = nullptr);
 // part 0 += c (constant polynomial: every evaluation point)
@@ -231,7 +233,8 @@ extern int g_lift2;
 extern int g_ntt_split;        // 1: transform calls split over two streams (see ntt_split_or_common)
 extern int g_ntt_persist_occ;  // >0: cap of the persistent column passes' CTAs per SM
 extern int g_ntt_epi;          // 1: scale-sub / fused-ModDown epilogues inside pass C of the forward transform
-extern int g_ntt_lean;         // persistent column passes: table tiles in shared memory (0) or read through L2 (1-3)
+extern int g_ntt_lean;
+extern int g_axpy;             // 1: fused a + c x in the digit circuits' linear combinations (default)         // persistent column passes: table tiles in shared memory (0) or read through L2 (1-3)
 extern int g_ntt_timing;
 // comparison phases (bench "phases"; NVTX ranges of the same names)
 enum { PH_EXTRACT = 0, PH_DIGIT, PH_LEX, PH_BCAST, PH_COMPACT, PH_PQMAIN, NPHASE };

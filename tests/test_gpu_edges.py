@@ -125,3 +125,28 @@ def test_bad_output_views_are_rejected_before_any_work():
     assert lib.bc_automorph(ctx._h, v, 2, ctx.view(small), st) in (1, 4)
     torch.cuda.synchronize()
     assert bool((small == 7).all()) and bool((wrong == 7).all())
+
+
+@pytest.mark.parametrize("batch,chunk", [(5, 2), (3, 0), (1, 4)])
+def test_compare_lt_host_pipelined(batch, chunk):
+    """bc_compare_lt_host (host buffers, H2D / compare / D2H pipelined over chunks with a ragged tail) gives
+    the words of bc_compare_lt on device buffers; a short staging buffer is BC_E_ARG"""
+    import torch
+    import paper_2407_07308_b200 as bc
+    ctx, keys = ctx_keys("c2s")
+    rng = np.random.default_rng(71)
+    cap = min(ctx.base ** (ctx.d * ctx.l), 1 << 64)
+    w = rng.integers(0, cap, size=(2, batch, ctx.ints_per_ct), dtype=np.uint64)
+    ca = ctx.encrypt(keys, w[0], SEED_ENC, ct_index0=0)
+    cb = ctx.encrypt(keys, w[1], SEED_ENC, ct_index0=batch)
+    ref = ctx.compare_lt(keys, ca, cb)
+    ha, hb = ca.cpu().pin_memory(), cb.cpu().pin_memory()
+    ho = torch.zeros(ref.shape, dtype=ref.dtype).pin_memory()
+    ctx.compare_lt_host(keys, ha, hb, ho, chunk=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(ho, ref.cpu())
+    bits = ctx.decrypt(keys, ho.cuda(), as_bits=True)
+    assert np.array_equal(bits, (w[0] < w[1]).astype(np.uint64))
+    small = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(bc.BoostComError):
+        ctx.compare_lt_host(keys, ha, hb, ho, chunk=chunk, stage=small)
