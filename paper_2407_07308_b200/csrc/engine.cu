@@ -8,6 +8,9 @@
 #include <cstring>
 #include <functional>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "engine.h"
 
 namespace bc {
@@ -265,6 +268,32 @@ static bool is_prime_small(uint32_t m) {
     if (m < 2) return false;
     for (uint32_t d = 2; d * d <= m; ++d) if (m % d == 0) return false;
     return true;
+}
+
+// SURVEY §5 failure detection: BC_FAULT_INJECT="<prime>:<word>" (or any other non-empty value: 0:0) adds 1 to
+// one word of the forward Bluestein kernel transform D^ (the binary64 table where it exists, else the 64-bit
+// one) when a context is created -- every later forward transform of that prime is wrong, so the parity tests
+// and the bench's decrypt-and-verify warm-up must fail (tests/test_gpu_edges.py checks they notice)
+static void fault_inject(bc_ctx *X) {
+    const char *e = getenv("BC_FAULT_INJECT");
+    if (!e || !*e) return;
+    unsigned pr = 0, w = 0;
+    if (sscanf(e, "%u:%u", &pr, &w) != 2) pr = w = 0;
+    const size_t NP = X->moduli.size();
+    if (pr >= NP || w >= X->M) BC_THROW(BC_E_PARAM, "BC_FAULT_INJECT: word out of range");
+    const size_t at = (size_t)pr * X->M + w;
+    if (X->T.fdhf) {
+        double v = 0;
+        CK(cudaMemcpy(&v, X->T.fdhf + at, 8, cudaMemcpyDeviceToHost));
+        v += 1.0;
+        CK(cudaMemcpy((double *)X->T.fdhf + at, &v, 8, cudaMemcpyHostToDevice));
+    }
+    if (X->T.dhf) {
+        u64x2 v{0, 0};
+        CK(cudaMemcpy(&v, X->T.dhf + at, 16, cudaMemcpyDeviceToHost));
+        v.w = (v.w + 1) % X->moduli[pr];
+        CK(cudaMemcpy((u64x2 *)X->T.dhf + at, &v, 16, cudaMemcpyHostToDevice));
+    }
 }
 
 void ctx_build(bc_ctx *X) {
@@ -760,6 +789,7 @@ void ctx_build(bc_ctx *X) {
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
     }
+    fault_inject(X);
 }
 
 // lift with the plan's (sources, targets) known on the host: selects the register-resident kernel

@@ -150,3 +150,23 @@ def test_compare_lt_host_pipelined(batch, chunk):
     small = torch.empty(16, dtype=torch.uint8, device="cuda")
     with pytest.raises(bc.BoostComError):
         ctx.compare_lt_host(keys, ha, hb, ho, chunk=chunk, stage=small)
+
+
+def test_fault_injection_is_detected(monkeypatch):
+    """SURVEY §5 failure detection: BC_FAULT_INJECT=<prime>:<word> corrupts one word of the forward D^ table
+    at context creation; the same seeded compare then no longer decrypts to the plaintext answer and its words
+    differ from the clean context's (what the parity tests and the bench's verify-in-warm-up rely on)"""
+    import paper_2407_07308_b200 as bc
+    ctx, keys = ctx_keys("c2s")
+    rng = np.random.default_rng(72)
+    cap = min(ctx.base ** (ctx.d * ctx.l), 1 << 64)
+    w = rng.integers(0, cap, size=(2, 2, ctx.ints_per_ct), dtype=np.uint64)
+    clean = to_u64(ctx.compare_lt(keys, ctx.encrypt(keys, w[0], SEED_ENC, 0), ctx.encrypt(keys, w[1], SEED_ENC, 2)))
+    monkeypatch.setenv("BC_FAULT_INJECT", "1:17")
+    bad_ctx = bc.Context(bc.load_params("c2s"))
+    monkeypatch.delenv("BC_FAULT_INJECT")
+    bad_keys = bad_ctx.keygen(SEED_KEYS)
+    lt = bad_ctx.compare_lt(bad_keys, bad_ctx.encrypt(bad_keys, w[0], SEED_ENC, 0), bad_ctx.encrypt(bad_keys, w[1], SEED_ENC, 2))
+    assert not np.array_equal(to_u64(lt), clean)
+    bits = bad_ctx.decrypt(bad_keys, lt, as_bits=True)
+    assert not np.array_equal(bits, (w[0] < w[1]).astype(np.uint64))
