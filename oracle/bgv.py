@@ -28,8 +28,8 @@ class Params:
         self.name = cfg.get("name", "")
         self.p = int(cfg["p"])
         self.m = int(cfg["m"])
-        self.schedule = cfg.get("schedule", "r16")     # digit-circuit reading: R16, R23 or R26
-        assert self.schedule in ("r16", "r23", "r26")
+        self.schedule = cfg.get("schedule", "r16")     # digit-circuit reading: R16, R23, R26 or R27
+        assert self.schedule in ("r16", "r23", "r26", "r27")
         self.circuit = cfg.get("circuit", "U") + ("" if self.schedule == "r16" else ":" + self.schedule)
         self.d = int(cfg["d"])
         self.l = int(cfg["l"])
@@ -441,6 +441,38 @@ def mul(P, K, a, b):
     for dk, u in ((d0, u0), (d1, u1)):
         w = u.copy()
         w[:lv] = _add(_scal(dk, Pprod, P, cidx), u[:lv], P, cidx)
+        r, _ = lift_centered(P, w[drop_rows], drop_idx)
+        parts.append(_scale_down(P, w[:lv - 1], list(range(lv - 1)), None, r, D))
+    return Ciphertext(parts, lv - 1)
+
+
+def mul_sum(P, K, pairs):
+    """R27 (lazy ModDown of a sum of products): sum_i a_i b_i with ONE scale-down.  Every
+    operand is switched to lv = the lowest level of all of them (R12); per pair the w_k = P d_k + u_k of mul()
+    (R15: tensor, ModUp + KIP of d2, over the cipher limbs of lv and the special limbs) are summed limb-wise;
+    the sum takes mul()'s single scale-down by D = P q_{lv-1}.  One pair: exactly mul() (a test pin); more
+    pairs: decrypts to the sum of the products, different bits from summing mul() results (one rounding)."""
+    lv = min(min(a.level, b.level) for a, b in pairs)
+    assert lv >= 2, "OutOfLevels"
+    Pprod = 1
+    for q in P.P:
+        Pprod *= q
+    D = Pprod * P.moduli[lv - 1]
+    cidx = list(range(lv))
+    rows = cidx + P.special
+    W = [None, None]
+    for a, b in pairs:
+        a, b = modswitch_to(P, a, lv), modswitch_to(P, b, lv)
+        d0, d1, d2 = tensor(P, a, b).parts
+        u0, u1 = keyswitch_up(P, K, d2, lv, 0)
+        for k, (dk, u) in enumerate(((d0, u0), (d1, u1))):
+            w = u.copy()
+            w[:lv] = _add(_scal(dk, Pprod, P, cidx), u[:lv], P, cidx)
+            W[k] = w if W[k] is None else _add(W[k], w, P, rows)
+    drop_rows = list(range(lv, lv + P.K)) + [lv - 1]
+    drop_idx = P.special + [lv - 1]
+    parts = []
+    for w in W:
         r, _ = lift_centered(P, w[drop_rows], drop_idx)
         parts.append(_scale_down(P, w[:lv - 1], list(range(lv - 1)), None, r, D))
     return Ciphertext(parts, lv - 1)

@@ -140,6 +140,13 @@ def lincomb(ev, terms, const):
     return acc
 
 
+def vmul_sum(ev, pairs):
+    """R27: sum of the ct x ct products of pairs with one scale-down (ev.mul_sum); one pair is ev.mul"""
+    if len(pairs) == 1:
+        return ev.mul(*pairs[0])
+    return ev.mul_sum(pairs)
+
+
 class Powers:
     """R16 power rule: x^1 given; x^j (j >= 2) = x^a * x^(j-a), a = largest power of two < j."""
 
@@ -244,6 +251,10 @@ class CountEval:
 
     def add(self, a, b):
         return CountValue(max(a.depth, b.depth))
+
+    def mul_sum(self, pairs):
+        self.counts["mul"] += len(pairs)
+        return CountValue(max(max(a.depth, b.depth) for a, b in pairs) + 1)
 
     def scalar(self, a, c):
         return CountValue(a.depth)
@@ -364,13 +375,16 @@ def bivariate_lt_eq_r23(ev, x, y, p, k=None):
     return lt, eq
 
 
-def bivariate_lt_eq_r26(ev, x, y, p, k1=None, k2=None):
+def bivariate_lt_eq_r26(ev, x, y, p, k1=None, k2=None, lazy=False):
     """R26 bivariate, two-dimensional Paterson-Stockmeyer: LT = sum_(j,i) c_ji Y^j Z^i (Z = x - y, the R16
     coefficients) split into blocks j = k1 C + a, i = k2 D + b (a < k1, b < k2):
     L_CD = sum c Y^a Z^b (baby monomials Y^a Z^b = Y^a * Z^b, created when first needed, a and b ascending),
     inner_C = L_C0 + sum_(D>=1) Z^(k2 D) L_CD (D ascending), LT = inner_0 + sum_(C>=1) Y^(k1 C) inner_C
     (C ascending); every power of Y and of Z by the R16 power rule (one memo each, shared with EQ);
-    zero blocks are skipped.  EQ = 1 - Z^(p-1).  (k1, k2) = r26_bivariate_k(p) unless given."""
+    zero blocks are skipped.  EQ = 1 - Z^(p-1).  (k1, k2) = r26_bivariate_k(p) unless given.
+    lazy (R27): the products of each sum take one scale-down -- inner_C = L_C0, then the
+    scalar terms c Z^(k2 D) of constant blocks (D ascending), then vmul_sum([(Z^(k2 D), L_CD) : D >= 1, L_CD
+    a ciphertext]); LT likewise from inner_0 and the (Y^(k1 C), inner_C), C >= 1.  Same products and depth."""
     c = lt_bivariate_coeffs(p)
     if k1 is None:
         k1, k2 = r26_bivariate_k(p)
@@ -387,21 +401,48 @@ def bivariate_lt_eq_r26(ev, x, y, p, k1=None, k2=None):
     terms = {(j, i): c[j][i] % p for j in range(p) for i in range(p) if c[j][i] % p}
     Cm = max(j for j, _ in terms) // k1
     Dm = max(i for _, i in terms) // k2
+    def acc(s, t):
+        return t if (is_const(s) and s == 0) else vadd(ev, s, t)
+
+    def lazy_sum(s, prs):
+        """s, then the scalar terms, then one vmul_sum of the ciphertext pairs (R27)"""
+        cts = []
+        for g, v in prs:
+            if is_const(v):
+                s = acc(s, vmul(ev, g, v))
+            else:
+                cts.append((g, v))
+        return acc(s, vmul_sum(ev, cts)) if cts else s
+
     lt = 0
+    outer = []
     for C in range(Cm + 1):
         inner = 0
+        prs = []
         for D in range(Dm + 1):
             L = lincomb(ev, [(terms[(k1 * C + a, k2 * D + b)], M(a, b)) for a in range(k1) for b in range(k2)
                              if (a, b) != (0, 0) and (k1 * C + a, k2 * D + b) in terms],
                         terms.get((k1 * C, k2 * D), 0))
             if is_const(L) and L == 0:
                 continue
-            t = L if D == 0 else vmul(ev, zp(k2 * D), L)
-            inner = t if (is_const(inner) and inner == 0) else vadd(ev, inner, t)
+            if D == 0:
+                inner = L
+            elif lazy:
+                prs.append((zp(k2 * D), L))
+            else:
+                inner = acc(inner, vmul(ev, zp(k2 * D), L))
+        if lazy:
+            inner = lazy_sum(inner, prs)
         if is_const(inner) and inner == 0:
             continue
-        t = inner if C == 0 else vmul(ev, yp(k1 * C), inner)
-        lt = t if (is_const(lt) and lt == 0) else vadd(ev, lt, t)
+        if C == 0:
+            lt = inner
+        elif lazy:
+            outer.append((yp(k1 * C), inner))
+        else:
+            lt = acc(lt, vmul(ev, yp(k1 * C), inner))
+    if lazy:
+        lt = lazy_sum(lt, outer)
     eq = vadd(ev, vmul(ev, zp(p - 1), -1), 1)
     return lt, eq
 
@@ -530,18 +571,20 @@ def lex_slots(ev, lt, eq, l, ints):
 
 def compare(ev, a, b, circuit, d, l, ints):
     """(LT, EQ) of the words packed in a and b (block slot 0 holds the result).  circuit: "U" / "B"
-    (R16 digit circuits), "U:r23" / "B:r23" (R23) or "U:r26" / "B:r26" (R26 bivariate; univariate = R23)."""
+    (R16 digit circuits), "U:r23" / "B:r23" (R23), "U:r26" / "B:r26" (R26 bivariate; univariate = R23) or
+    "U:r27" / "B:r27" (R26 with R27's lazy scale-down of its sums)."""
     p = ev.p
     sched = circuit.partition(":")[2] or "r16"   # R16, R23 or R26 digit circuits (params "schedule")
     if circuit[0] == "U":
         z = ev.add(a, ev.scalar(b, -1))
         digs = extract_digits(ev, z, d)
-        f = univariate_lt_eq_r23 if sched in ("r23", "r26") else univariate_lt_eq   # R26 univariate = R23
+        f = univariate_lt_eq_r23 if sched in ("r23", "r26", "r27") else univariate_lt_eq   # R26 / R27 univariate = R23
         res = [f(ev, x, p) for x in digs]
     else:
         da = extract_digits(ev, a, d)
         db = extract_digits(ev, b, d)
-        f = {"r23": bivariate_lt_eq_r23, "r26": bivariate_lt_eq_r26}.get(sched, bivariate_lt_eq)
+        f = {"r23": bivariate_lt_eq_r23, "r26": bivariate_lt_eq_r26,
+             "r27": functools.partial(bivariate_lt_eq_r26, lazy=True)}.get(sched, bivariate_lt_eq)
         res = [f(ev, x, y, p) for x, y in zip(da, db)]
     lt, eq = lex_tree(ev, [r[0] for r in res], [r[1] for r in res])
     if l > 1:
@@ -698,6 +741,11 @@ class OracleEval:
     def add(self, a, b):
         return bgv.add(self.P, a, b)
 
+    def mul_sum(self, pairs):
+        self.counts["mul"] += len(pairs)
+        self.counts["ks"] += len(pairs)
+        return bgv.mul_sum(self.P, self.K, pairs)
+
     def scalar(self, a, c):
         return bgv.mul_scalar(self.P, a, c)
 
@@ -748,6 +796,11 @@ class PlainEval:
 
     def add(self, a, b):
         return PlainValue((a.v + b.v) % self.p, max(a.depth, b.depth))
+
+    def mul_sum(self, pairs):
+        self.counts["mul"] += len(pairs)
+        v = sum(self.gf.mul(a.v, b.v) for a, b in pairs) % self.p
+        return PlainValue(v, max(max(a.depth, b.depth) for a, b in pairs) + 1)
 
     def scalar(self, a, c):
         return PlainValue(a.v * int(c) % self.p, a.depth)

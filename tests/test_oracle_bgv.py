@@ -198,6 +198,29 @@ def test_fused_mul_decrypts_like_two_step(c1):
         assert bgv.noise_bits(P, K, f)[0] <= bgv.noise_bits(P, K, u)[0] + 2
 
 
+def test_mul_sum_lazy_scale_down(c1):
+    """R27 (lazy ModDown): mul_sum of one pair IS mul (every word); of three pairs at two
+    levels it decrypts to sum b1_i * b2_i at the level mul would give the lowest pair, with noise within 2 bits
+    of the sum of separate products, and its words differ from that sum (one rounding instead of three)."""
+    P, K = c1
+    A = P.alg
+    rng = np.random.default_rng(9)
+    bs = [(rng.integers(0, P.p, size=(A.S, A.D)), rng.integers(0, P.p, size=(A.S, A.D))) for _ in range(3)]
+    cs = [(_enc_slots(P, K, x, 60 + 2 * i), _enc_slots(P, K, y, 61 + 2 * i)) for i, (x, y) in enumerate(bs)]
+    one = bgv.mul_sum(P, K, [cs[0]])
+    ref = bgv.mul(P, K, *cs[0])
+    assert one.level == ref.level and all(np.array_equal(u, v) for u, v in zip(one.parts, ref.parts))
+    pairs = [cs[0], (bgv.modswitch(P, cs[1][0]), cs[1][1]), cs[2]]      # one operand a level lower
+    lz = bgv.mul_sum(P, K, pairs)
+    sep = bgv.add(P, bgv.add(P, bgv.mul(P, K, *pairs[0]), bgv.mul(P, K, *pairs[1])), bgv.mul(P, K, *pairs[2]))
+    assert lz.level == sep.level == P.L1 - 2
+    want = sum(A.gf.mul(x, y) for x, y in bs) % P.p
+    assert np.array_equal(A.decode(bgv.decrypt(P, K, lz)), want)
+    assert np.array_equal(A.decode(bgv.decrypt(P, K, sep)), want)
+    assert bgv.noise_bits(P, K, lz)[0] <= bgv.noise_bits(P, K, sep)[0] + 2
+    assert not np.array_equal(lz.parts[0], sep.parts[0])
+
+
 def test_hoisted_automorphisms_decrypt_like_plain(c1):
     """R22 hoisted key switching: every sigma_t of one ciphertext decrypts exactly like the
     non-hoisted automorphism (Frobenius: slot-wise p^k power; rotations: slot

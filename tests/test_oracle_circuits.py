@@ -82,8 +82,9 @@ def _digit_run(p, kind, r23=False, k=None):
         if kind == "U":
             z = circuits.PlainValue((X - Y) % p)
             lt, eq = circuits.univariate_lt_eq_r23(ev, z, p, k) if r23 else circuits.univariate_lt_eq(ev, z, p)
-        elif r23 == "r26":
-            lt, eq = circuits.bivariate_lt_eq_r26(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p, *k)
+        elif r23 in ("r26", "r27"):
+            lt, eq = circuits.bivariate_lt_eq_r26(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p, *k,
+                                                  lazy=r23 == "r27")
         elif r23:
             lt, eq = circuits.bivariate_lt_eq_r23(ev, circuits.PlainValue(X), circuits.PlainValue(Y), p, k)
         else:
@@ -395,6 +396,20 @@ def test_r26_schedule_truth_tables(p):
             assert depth <= r16[2] and mults <= r16[1]
             if p >= 11:
                 assert mults <= circuits._r23_cost(circuits.bivariate_lt_eq_r23, p, circuits.r23_bivariate_k(p))[0]
+
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_r27_lazy_schedule_truth_tables(p):
+    """R27 (R26 with one scale-down per sum of products, f1): [x < y], [x = y] on every digit pair at the
+    selected and at other block sizes, with exactly R26's product count and depth (the lazy sums regroup
+    the same products)"""
+    sel = circuits.r26_bivariate_k(p)
+    for k in sorted({sel, (1, 1), (2, 3), (min(4, p - 1), min(4, p - 1))}):
+        res, mults, depth = _digit_run(p, "B", r23="r27", k=k)
+        for x, y, lt, eq in res:
+            assert (lt, eq) == (int(x < y), int(x == y)), (p, k, x, y)
+        _, m26, d26 = _digit_run(p, "B", r23="r26", k=k)
+        assert (mults, depth) == (m26, d26)
 
 
 def test_r26_counts():

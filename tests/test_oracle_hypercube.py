@@ -101,7 +101,7 @@ def test_hypercube_compaction_stays_in_rows(oracle_params):
     assert n_out == max(-(-k // wpr) for k in per_row) == 2 and len(dest) == 4 * len(useful[0])
 
 
-@pytest.mark.parametrize("sched", ["r16", "r23", "r26"])
+@pytest.mark.parametrize("sched", ["r16", "r23", "r26", "r27"])
 def test_hypercube_compare_bgv(oracle_params, sched):
     """full BGV compare_lt / compare_eq on the tiny hypercube ring (p = 31 bivariate, m = 33):
     decrypted block slot 0 equals brute force for 2 integers (one per row) per ciphertext, with the
