@@ -303,6 +303,7 @@ def product_config(args, cfg, ints, B=None):
                         "%d ciphertext pairs per GPU" % B if args.config == "c2" else args.config,
             "params": args.config, "pairs_per_gpu": B, "ints_per_ct": ints,
             "n_cipher": cfg["n_cipher"], "n_special": cfg["n_special"], "alpha": cfg["alpha"],
+            "schedule": cfg.get("schedule", "r16"),
             "l2": "inputs (%.1f GB) larger than L2 (126 MB)" % (2 * B * 2 * cfg["n_cipher"] * _n_of(cfg) * 8 / 1e9)}
 
 
@@ -323,6 +324,7 @@ def main():
                     help="ciphertext pairs per GPU (default: 1000 for compare (C2), 16 dense pairs for c3 compact_compare)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="chunks of the pipelined host-buffer compare (e2e)")
+    ap.add_argument("--schedule", default=None, help="override the config's digit-circuit schedule (r16/r23/r26/r27)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verify", type=int, default=1)
     ap.add_argument("--workload", default=None,
@@ -334,6 +336,8 @@ def main():
     ap.add_argument("--exps", default="64,128,256,512,1024", help="private_q: exponents op2 swept (Fig. 14)")
     args = ap.parse_args()
     cfg = load_json(os.path.join(ROOT, "params", args.config + ".json"))
+    if args.schedule:
+        cfg["schedule"] = args.schedule          # digit-circuit reading override (r16 / r23 / r26 / r27)
     rank, world, local = dist_env()
 
     if args.impl == "reference":

@@ -69,7 +69,8 @@ typedef struct {
     uint32_t schedule;       /* digit circuits: 0 or 16 = R16, 23 = R23 baby-step / giant-step, 26 = R26
                               * (bivariate two-dimensional Paterson-Stockmeyer, univariate as R23) (SURVEY
                               * §8(f) f2: "2p-6 (Bivariate case) and sqrt(p-3)+O(log p)
-                              * (Univariate case)"); anything else -> BC_E_PARAM */
+                              * (Univariate case)"), 27 = R27 (R26 with one scale-down per sum of
+                              * products: §8(f) f1 lazy ModDown); anything else -> BC_E_PARAM */
     uint32_t bluestein;      /* 0: power-of-two Bluestein length; 1: mixed radix (R25, SURVEY §8(f)
                               * f3: the smallest 256 r N' or 2^k >= 2m - 1; prime m, shapes 9 x 32 and
                               * 3 x 128 -- others BC_E_PARAM) */
@@ -98,7 +99,7 @@ bc_status bc_ctx_slots(const bc_ctx *ctx, int64_t *h_G, int64_t *h_zeta, int64_t
 /* host only (no device): the digit circuit a context with these (p, circuit, schedule) evaluates --
  * k = the R23 baby-step size (0 for R16; R26 bivariate: k1 << 8 | k2), products = ct x ct multiplications per digit (EQ
  * included), depth = its multiplicative depth (R16 / R23; P:71's 3p-5 for R16 bivariate).
- * BC_E_PARAM for p not an odd prime <= 257, circuit not 'U'/'B', schedule not 0/16/23/26. */
+ * BC_E_PARAM for p not an odd prime <= 257, circuit not 'U'/'B', schedule not 0/16/23/26/27. */
 bc_status bc_circuit_plan(uint32_t p, char circuit, uint32_t schedule, uint32_t *k, uint32_t *products,
                           uint32_t *depth);
 /* Galois elements keygen generates keys for (Frobenius p^k, rotations) */

@@ -21,7 +21,7 @@ if not os.path.exists(_SO):
 _lib = ctypes.CDLL(_SO)
 
 
-_SCHEDULES = {"r16": 16, "r23": 23, "r26": 26}    # digit-circuit readings (R16 / R23 / R26)
+_SCHEDULES = {"r16": 16, "r23": 23, "r26": 26, "r27": 27}    # digit-circuit readings (R16 / R23 / R26 / R27)
 
 
 class bc_params(ctypes.Structure):

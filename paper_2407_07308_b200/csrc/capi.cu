@@ -104,8 +104,8 @@ bc_status bc_circuit_plan(uint32_t p, char circuit, uint32_t schedule, uint32_t 
     if (!k || !products || !depth) BC_THROW(BC_E_ARG, "null argument");
     if (p < 3 || p > 257 || !is_prime_u64(p)) BC_THROW(BC_E_PARAM, "p must be an odd prime <= 257");
     if (circuit != 'U' && circuit != 'B') BC_THROW(BC_E_PARAM, "circuit must be 'U' or 'B'");
-    if (schedule != 0 && schedule != 16 && schedule != 23 && schedule != 26)
-        BC_THROW(BC_E_PARAM, "schedule must be 16, 23 or 26");
+    if (schedule != 0 && schedule != 16 && schedule != 23 && schedule != 26 && schedule != 27)
+        BC_THROW(BC_E_PARAM, "schedule must be 16, 23, 26 or 27");
     int kk, mu, de;
     circuit_plan(p, circuit, (int)schedule, &kk, &mu, &de);
     *k = (uint32_t)kk;

@@ -362,11 +362,14 @@ void ctx_build(bc_ctx *X) {
         X->eq_u = interp_fp(p, [](int64_t v) { return v == 0 ? 1 : 0; });
         if (P.circuit == 'B') X->lt_b = lt_bivariate(p);
         // R23 (schedule 23): the baby-step size the rule selects; 0 = the R16 circuits
-        if (P.schedule != 0 && P.schedule != 16 && P.schedule != 23 && P.schedule != 26)
-            BC_THROW(BC_E_PARAM, "schedule must be 16, 23 or 26");
-        // R26 (schedule 26): the bivariate circuit's block sizes; its univariate circuit is R23's
-        X->r23_k = (P.schedule == 23 || P.schedule == 26) ? r23_select_k(p, P.circuit, X->lt_u, X->lt_b, nullptr, nullptr) : 0;
-        X->r26_k = (P.schedule == 26 && P.circuit == 'B') ? r26_select_k(p, X->lt_b) : 0;
+        if (P.schedule != 0 && P.schedule != 16 && P.schedule != 23 && P.schedule != 26 && P.schedule != 27)
+            BC_THROW(BC_E_PARAM, "schedule must be 16, 23, 26 or 27");
+        // R26 (schedule 26): the bivariate circuit's block sizes; its univariate circuit is R23's.  R27 (27): R26
+        // with one scale-down per sum of products
+        const bool r2x = P.schedule == 26 || P.schedule == 27;
+        X->r23_k = (P.schedule == 23 || r2x) ? r23_select_k(p, P.circuit, X->lt_u, X->lt_b, nullptr, nullptr) : 0;
+        X->r26_k = (r2x && P.circuit == 'B') ? r26_select_k(p, X->lt_b) : 0;
+        X->r27 = P.schedule == 27;
     }
     // Galois elements: Frobenius p^k (k < D), rotations g^{+-2^r} (r < ceil log2 l)
     {
@@ -1185,6 +1188,49 @@ CT Eng::mul(const CT &a0, const CT &b0) {
     return o;
 }
 
+// R27: sum of products with ONE scale-down (oracle bgv.mul_sum): operands switched to the lowest level lv,
+// per pair tensor -> ModUp + KIP of d2 -> w_k = P d_k + u_k summed into W (extended basis), then R15's
+// scale-down of W by D = P q_{lv-1}.  One pair: mul() itself.
+CT Eng::mul_sum(const std::vector<std::pair<CT, CT>> &prs) {
+    if (prs.empty()) BC_THROW(BC_E_INTERNAL, "mul_sum: no pairs");
+    if (prs.size() == 1) return mul(prs[0].first, prs[0].second);
+    uint32_t lv = 0xffffffffu;
+    for (auto &pr : prs) lv = std::min(lv, std::min(pr.first.lvl, pr.second.lvl));
+    if (lv < 2) BC_THROW(BC_E_LEVEL, "mul_sum: out of levels");
+    const uint32_t n = X->n, B = prs[0].first.B, K = X->K, L1 = X->L1, nl = lv + K;
+    const uint64_t tw = (uint64_t)3 * lv * n, ups = (uint64_t)nl * n;
+    BufP W = alloc_words((uint64_t)B * 2 * nl * n);
+    uint64_t *Wp = (uint64_t *)W->p;
+    bool first = true;
+    for (auto &pr : prs) {
+        CT a = modswitch_to(pr.first, lv), b = modswitch_to(pr.second, lv);
+        if (a.B != B || b.B != B) BC_THROW(BC_E_INTERNAL, "mul_sum: batch mismatch");
+        if (a.bstride != (uint64_t)2 * lv * n || b.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "mul_sum: strided");
+        BufP t = alloc_words((uint64_t)B * tw);
+        if (!dry()) ew_tensor(X->d_mods, a.d, b.d, (uint64_t *)t->p, B, lv, n, st, g_f64_elem ? X->d_fm : nullptr);
+        BufP u = ks_up((uint64_t *)t->p + (uint64_t)2 * lv * n, tw, B, lv, 0);
+        if (!dry())
+            ew_ext_acc(X->d_mods, Wp, (uint64_t *)u->p, (uint64_t *)t->p, tw, (uint64_t)lv * n, X->d_Pm, B, lv, K, L1, n,
+                       first ? 1 : 0, st);
+        first = false;
+    }
+    // R15's scale-down by D = P q_{lv-1}: INTT of rows lv-1 .. lv+K-1, exact lift, NTT, (W - delta) D^{-1}
+    BufP sp = alloc_words((uint64_t)2 * B * (K + 1) * n);
+    ntt_inv(Wp + (uint64_t)(lv - 1) * n, (uint64_t *)sp->p, 2 * B, LimbMap{K + 1, K + 1, 0, 1, lv - 1, L1}, ups,
+            (uint64_t)(K + 1) * n);
+    BufP delta = alloc_words((uint64_t)2 * B * (lv - 1) * n);
+    if (!dry())
+        lift_p(X, ("fd:" + std::to_string(lv)), X->d_mods, X->p, (uint64_t *)sp->p, (uint64_t)(K + 1) * n,
+             (uint64_t *)delta->p, (uint64_t)(lv - 1) * n, nullptr, 2 * B, n, 0, 0, 1, st);
+    sp.reset();
+    ntt_fwd((uint64_t *)delta->p, (uint64_t *)delta->p, 2 * B, limbmap_plain(lv - 1, 0), (uint64_t)(lv - 1) * n,
+            (uint64_t)(lv - 1) * n);
+    CT o = ct_alloc(B, lv - 1, 2);
+    if (!dry())
+        ew_scale_sub(X->d_mods, Wp, ups, (uint64_t *)delta->p, X->d_invD + (size_t)lv * L1, o.d, 2 * B, lv - 1, n, st);
+    return o;
+}
+
 CT Eng::automorph(const CT &a, uint32_t t) {
     const uint32_t n = X->n, lv = a.lvl, B = a.B;
     if (a.bstride != (uint64_t)2 * lv * n) BC_THROW(BC_E_INTERNAL, "automorph: strided");
@@ -1268,6 +1314,11 @@ struct EngEv {
         if (acc.isc || x.isc) return vadd(E, acc, vmul(E, x, VC(c)));
         return VT(E.axpy(acc.ct, x.ct, c));
     }
+    V mul_sum(const std::vector<std::pair<V, V>> &prs) {   // R27, ciphertext pairs only
+        std::vector<std::pair<CT, CT>> c;
+        for (auto &pr : prs) c.push_back({pr.first.ct, pr.second.ct});
+        return VT(E.mul_sum(c));
+    }
     int64_t p() const { return E.X->p; }
 };
 struct CntV {
@@ -1300,6 +1351,12 @@ struct CntEv {
         return r;
     }
     V axpy(const V &acc, const V &x, int64_t c) { return add(acc, mul(x, cnst(c))); }
+    V mul_sum(const std::vector<std::pair<V, V>> &prs) {
+        muls += (int)prs.size();
+        V r;
+        for (auto &pr : prs) r.depth = std::max(r.depth, std::max(pr.first.depth, pr.second.depth) + 1);
+        return r;
+    }
     int64_t p() const { return pp; }
 };
 
@@ -1528,7 +1585,7 @@ static void bivariate_r23(Ev &ev, const typename Ev::V &x, const typename Ev::V 
 template <class Ev>
 static void bivariate_r26(Ev &ev, const typename Ev::V &x, const typename Ev::V &y,
                           const std::vector<std::vector<int64_t>> &c, int k1, int k2, typename Ev::V *lt,
-                          typename Ev::V *eq) {
+                          typename Ev::V *eq, bool lazy = false) {
     typedef typename Ev::V V;
     const int64_t p = ev.p();
     V Z = ev.add(x, ev.mul(y, ev.cnst(-1)));
@@ -1555,11 +1612,23 @@ static void bivariate_r26(Ev &ev, const typename Ev::V &x, const typename Ev::V 
         for (int i = 0; i < (int)p; ++i)
             if (coef(j, i)) { jmax = std::max(jmax, j); imax = std::max(imax, i); }
     const int Cm = jmax / k1, Dm = imax / k2;
-    bool have = false;
-    V acc;
+    auto is0 = [](const V &v) { return Ev::isc(v) && Ev::cval(v) == 0; };
+    auto accf = [&](const V &sum, const V &t) { return is0(sum) ? t : ev.add(sum, t); };
+    // R27 (lazy): sum, then the scalar terms of constant blocks, then ONE scale-down for the ciphertext products
+    auto lazy_sum = [&](V sum, const std::vector<std::pair<V, V>> &prs) {
+        std::vector<std::pair<V, V>> cts;
+        for (auto &pr : prs) {
+            if (Ev::isc(pr.second)) sum = accf(sum, ev.mul(pr.first, pr.second));
+            else cts.push_back(pr);
+        }
+        if (cts.empty()) return sum;
+        return accf(sum, cts.size() == 1 ? ev.mul(cts[0].first, cts[0].second) : ev.mul_sum(cts));
+    };
+    V acc = ev.cnst(0);
+    std::vector<std::pair<V, V>> outer;
     for (int C = 0; C <= Cm; ++C) {
-        bool hin = false;
-        V inner;
+        V inner = ev.cnst(0);
+        std::vector<std::pair<V, V>> prs;
         for (int D = 0; D <= Dm; ++D) {
             std::vector<std::pair<int64_t, std::function<V()>>> terms;
             for (int a = 0; a < k1; ++a)
@@ -1569,17 +1638,19 @@ static void bivariate_r26(Ev &ev, const typename Ev::V &x, const typename Ev::V 
                     if (cf) terms.push_back({cf, [&M, a, b]() { return M(a, b); }});
                 }
             V L = lincombT(ev, terms, coef(k1 * C, k2 * D));
-            if (Ev::isc(L) && Ev::cval(L) == 0) continue;
-            V t = D == 0 ? L : ev.mul(zp.get(k2 * D), L);
-            inner = hin ? ev.add(inner, t) : t;
-            hin = true;
+            if (is0(L)) continue;
+            if (D == 0) inner = L;
+            else if (lazy) prs.push_back({zp.get(k2 * D), L});
+            else inner = accf(inner, ev.mul(zp.get(k2 * D), L));
         }
-        if (!hin) continue;
-        V t = C == 0 ? inner : ev.mul(yp.get(k1 * C), inner);
-        acc = have ? ev.add(acc, t) : t;
-        have = true;
+        if (lazy) inner = lazy_sum(inner, prs);
+        if (is0(inner)) continue;
+        if (C == 0) acc = inner;
+        else if (lazy) outer.push_back({yp.get(k1 * C), inner});
+        else acc = accf(acc, ev.mul(yp.get(k1 * C), inner));
     }
-    *lt = have ? acc : ev.cnst(0);
+    if (lazy) acc = lazy_sum(acc, outer);
+    *lt = acc;
     if (eq) *eq = ev.add(ev.mul(zp.get((int)p - 1), ev.cnst(-1)), ev.cnst(1));
 }
 
@@ -1646,12 +1717,12 @@ void circuit_plan(int64_t p, char circuit, int schedule, int *k, int *muls, int 
     std::vector<int64_t> cu = interp_fp(p, [p, h](int64_t v) { return (v >= p - h && v <= p - 1) ? 1 : 0; });
     std::vector<std::vector<int64_t>> cb;
     if (circuit == 'B') cb = lt_bivariate(p);
-    if (schedule == 26 && circuit == 'B') {         // R26: k = k1 << 8 | k2
+    if ((schedule == 26 || schedule == 27) && circuit == 'B') {         // R26 / R27: k = k1 << 8 | k2
         *k = r26_select_k(p, cb);
         r26_cost(p, cb, *k >> 8, *k & 255, muls, depth);
         return;
     }
-    *k = (schedule == 23 || schedule == 26) ? r23_select_k(p, circuit, cu, cb, nullptr, nullptr) : 0;
+    *k = (schedule == 23 || schedule == 26 || schedule == 27) ? r23_select_k(p, circuit, cu, cb, nullptr, nullptr) : 0;
     r23_cost(p, circuit, cu, cb, *k, muls, depth);
 }
 
@@ -1676,7 +1747,7 @@ static void univariate(Eng &E, const Val &z, Val *lt, Val *eq) {
 static void bivariate(Eng &E, const Val &x, const Val &y, Val *lt, Val *eq) {
     MemoScope ms(E);
     EngEv ev{E};
-    if (E.X->r26_k > 0) bivariate_r26(ev, x, y, E.X->lt_b, E.X->r26_k >> 8, E.X->r26_k & 255, lt, eq);
+    if (E.X->r26_k > 0) bivariate_r26(ev, x, y, E.X->lt_b, E.X->r26_k >> 8, E.X->r26_k & 255, lt, eq, E.X->r27);
     else if (E.X->r23_k > 0) bivariate_r23(ev, x, y, E.X->lt_b, E.X->r23_k, lt, eq);
     else bivariate_r16(ev, x, y, E.X->lt_b, lt, eq);
 }

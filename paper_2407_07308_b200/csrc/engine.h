@@ -95,6 +95,7 @@ struct bc_ctx {
     std::vector<std::vector<int64_t>> lt_b;     // bivariate c[j][k] (Y^j Z^k)
     int r23_k = 0;                              // R23 baby-step size (params schedule 23), 0 = R16 circuits
     int r26_k = 0;                              // R26 bivariate block sizes k1 << 8 | k2 (schedule 26), 0 = off
+    bool r27 = false;                           // R27 (schedule 27): R26 with one scale-down per sum of products
     const uint64_t *plan(const std::string &k) const;
 };
 
@@ -169,6 +170,7 @@ struct Eng {
     CT modswitch(const CT &a);
     CT modswitch_to(const CT &a, uint32_t lvl);
     CT add(const CT &a, const CT &b);
+    CT mul_sum(const std::vector<std::pair<CT, CT>> &prs);   // R27: sum of products, one scale-down
     CT axpy(const CT &acc, const CT &x, int64_t c);   // acc + c x (= add(acc, scalar(x, c)), one kernel)
     CT scalar(const CT &a, int64_t c);       // c in F_p (centered)
     CT add_const(const CT &a, int64_t c);

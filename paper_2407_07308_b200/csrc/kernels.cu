@@ -601,6 +601,33 @@ void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint3
     LAUNCHED();
 }
 
+// R27: W[b][k][r] (+)= u[b][k][r] + (r < lv ? (P mod q_r) d_k[b][r] : 0) over the lv cipher rows and the K
+// special rows (prime L1 + r - lv) of the extended basis -- R15's w_k of one product, summed (first: W = w)
+__global__ void k_ext_acc(const Mod *__restrict__ mods, uint64_t *__restrict__ W, const uint64_t *__restrict__ u,
+                          const uint64_t *__restrict__ d, uint64_t d_bstride, uint64_t d_kstride,
+                          const u64x2 *__restrict__ pm, uint32_t rows, uint32_t lv, uint32_t nl, uint32_t L1,
+                          uint32_t n, int first) {
+    ROW_LOOP(rw, x, rows, n) {   // rows = 2B * nl
+        const uint64_t poly = rw / nl;
+        const uint32_t r = rw - (uint32_t)poly * nl;
+        const uint64_t q = mods[r < lv ? r : L1 + (r - lv)].q, i = (uint64_t)rw * n + x;
+        uint64_t w = u[i];
+        if (r < lv) {
+            const u64x2 c = pm[r];
+            w = add_mod(w, mul_shoup(d[(poly >> 1) * d_bstride + (poly & 1) * d_kstride + (uint64_t)r * n + x], c.w, c.ws, q), q);
+        }
+        W[i] = first ? w : add_mod(W[i], w, q);
+    }
+}
+void ew_ext_acc(const Mod *mods, uint64_t *W, const uint64_t *u, const uint64_t *d, uint64_t d_bstride,
+                uint64_t d_kstride, const u64x2 *pm, uint32_t B, uint32_t lv, uint32_t K, uint32_t L1, uint32_t n,
+                int first, cudaStream_t st) {
+    const uint64_t rows = (uint64_t)2 * B * (lv + K);
+    k_ext_acc<<<grid_rows(n, rows), 256, 0, st>>>(mods, W, u, d, d_bstride, d_kstride, pm, (uint32_t)rows, lv, lv + K,
+                                                  L1, n, first);
+    LAUNCHED();
+}
+
 // o = a + c x (the linear-combination step of the digit circuits: one pass instead of ew_scalar + ew_add)
 __global__ void k_axpy(const Mod *__restrict__ mods, const uint64_t *__restrict__ a, const uint64_t *__restrict__ xs,
                        int64_t c, uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl, uint32_t n) {

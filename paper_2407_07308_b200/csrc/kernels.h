@@ -117,6 +117,9 @@ void ew_add(const Mod *mods, const uint64_t *a, const uint64_t *b, uint64_t *o, 
 // o = a (parts pa) + b (parts pb) where the extra parts are copied (3-part + 2-part etc.)
 void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl,
             uint32_t n, cudaStream_t st);
+void ew_ext_acc(const Mod *mods, uint64_t *W, const uint64_t *u, const uint64_t *d, uint64_t d_bstride,
+                uint64_t d_kstride, const u64x2 *pm, uint32_t B, uint32_t lv, uint32_t K, uint32_t L1, uint32_t n,
+                int first, cudaStream_t st);   // R27: W (+)= u + P d (extended basis)
 void ew_axpy(const Mod *mods, const uint64_t *a, const uint64_t *x, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
              uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm);   // o = a + c x
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,

@@ -61,6 +61,7 @@ def test_circuit_plan_matches_oracle():
                 assert bc.circuit_plan(p, kind, "r26") == ((k1 << 8) | k2,) + c._r26_cost(p, k1, k2)
             else:
                 assert bc.circuit_plan(p, kind, "r26") == bc.circuit_plan(p, kind, "r23")
+            assert bc.circuit_plan(p, kind, "r27") == bc.circuit_plan(p, kind, "r26")   # R27 regroups R26's products
     with pytest.raises(bc.BoostComError):
         bc.circuit_plan(15, "U", "r23")
 

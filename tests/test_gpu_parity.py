@@ -440,7 +440,7 @@ def test_compare_full_c3_decrypts(pair):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c3t", "c3t@r23", "c3t@r16"])
+@pytest.mark.parametrize("name", ["c3t", "c3t@r27", "c3t@r23", "c3t@r16"])
 def test_compare_c3t_bivariate_p31_bit_exact(pair, name):
     """C3's p = 31 bivariate digit circuit (R26: 59 products, C3's schedule; R23: 73; R16: 88) on a small
     ring (c3t: m = 1129, (d,l) = (1,2), 9 + 4 primes): whole compare_lt ciphertext bit-exact vs the
@@ -485,11 +485,13 @@ def test_binary64_kernels_match_integer_kernels(pair):
     assert list(bits) == [int(x < y) for x, y in zip(a, b)]
 
 
-def test_hypercube_compare_bit_exact(pair):
+@pytest.mark.parametrize("name", ["c3h", "c3h@r27"])
+def test_hypercube_compare_bit_exact(pair, name):
     """C3's slot structure on the tiny hypercube ring c3h (p = 31 bivariate, m = 33 = 3 x 11,
-    Z_2 x Z_2 slots, one integer per row): whole compare_lt ciphertext bit-exact vs the oracle."""
+    Z_2 x Z_2 slots, one integer per row): whole compare_lt ciphertext bit-exact vs the oracle (C3's R26
+    circuit, and R27: R26 with one scale-down per sum of products)."""
     from oracle import circuits
-    T = pair("c3h")
+    T = pair(name)
     P = T.P
     ints = T.ctx.ints_per_ct
     a, b = [5, 923520], [7, 923520]
