@@ -123,6 +123,10 @@ if os.environ.get("BC_NTT_GROUP_MB"):
     _lib.bc_tune(b"ntt_group_bytes", int(os.environ["BC_NTT_GROUP_MB"]) << 20)
 if os.environ.get("BC_NTT_IMPL"):
     _lib.bc_set_ntt_impl(int(os.environ["BC_NTT_IMPL"]))
+for _kv in filter(None, os.environ.get("BC_TUNE", "").split(",")):   # "key=value,..." -> bc_tune (A/B runs)
+    _k, _, _v = _kv.partition("=")
+    if _lib.bc_tune(_k.strip().encode(), int(_v)) != 0:
+        raise ValueError("BC_TUNE: unknown knob " + _k)
 
 
 class BoostComError(RuntimeError):

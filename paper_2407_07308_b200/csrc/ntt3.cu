@@ -802,7 +802,14 @@ static void runf(const NttTables &T0, const uint64_t *in, uint64_t *out, LimbMap
         kf_passB<LOGC, LOGEC, S::RB, 0><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
         kf_passC<LOGR, LOGER, S::TC, 0, LOGC><<<gA, S::THA, S::SMA, st>>>(T, out, out_ps, lm, j0, scr, nullptr);
     } else {
-        kf_passA<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
+        bool pa = false;
+        if constexpr (LOGR == 8) {      // composite m: the persistent pass A (identical scratch), pass C below
+            if (persist && !T.dbg && g_ntt_lean != 0) {   // (ntt_lean 0: the round-2 passes)
+                persist_A<LOGR, LOGER, S::TC, (1 << LOGC)>(1, T, in, in_ps, lm, j0, nj, scr, st);
+                pa = true;
+            }
+        }
+        if (!pa) kf_passA<LOGR, LOGER, S::TC, 1, LOGC><<<gA, S::THA, S::SMA, st>>>(T, in, in_ps, lm, j0, scr);
         kf_passB<LOGC, LOGEC, S::RB, 1><<<gB, S::THB, S::SMB, st>>>(T, lm, j0, scr);
         uint64_t *corner = nullptr;
         if (T.prime_m && corner_buf) {

@@ -13,7 +13,7 @@ ctx = bc.Context(cfg)
 L = ctx.n_cipher
 npoly = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 x = torch.randint(0, 1 << 40, (npoly, L, ctx.n), dtype=torch.int64, device="cuda")
-ws = ctx.workspace(npoly * L * ctx.M * 8 + (64 << 20))
+ws = ctx.workspace(2 * npoly * L * ctx.M * 8 + (64 << 20))   # composite m: two slots per job
 work = bc.ntt_work(ctx) * npoly * L
 ref = None
 ref_inv = None
