@@ -388,12 +388,15 @@ bc_status bc_compare_lt_host(bc_ctx *X, const bc_keys *keys, const uint64_t *h_a
     const uint64_t cw = 2ull * level * X->n, ow = 2ull * lo * X->n;     // words per input / output ciphertext
     const uint64_t slot = (uint64_t)chunk * (2 * cw + ow);
     cudaStream_t cs = copy_stream_for_device(), ms = S(st);
-    cudaEvent_t h2d[2], done[2], d2h = nullptr;
-    for (int i = 0; i < 2; ++i) {
-        CK(cudaEventCreateWithFlags(&h2d[i], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
-    }
-    CK(cudaEventCreateWithFlags(&d2h, cudaEventDisableTiming));
+    struct Events {                     // destroyed on every exit (pending ones are released once complete)
+        cudaEvent_t e[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+        ~Events() {
+            for (cudaEvent_t x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } evs;
+    for (int i = 0; i < 5; ++i) CK(cudaEventCreateWithFlags(&evs.e[i], cudaEventDisableTiming));
+    cudaEvent_t *h2d = evs.e, *done = evs.e + 2, d2h = evs.e[4];
     // the copy stream starts after the work already queued on the caller's stream (e.g. a previous call's reads)
     CK(cudaEventRecord(d2h, ms));
     CK(cudaStreamWaitEvent(cs, d2h, 0));
@@ -426,11 +429,6 @@ bc_status bc_compare_lt_host(bc_ctx *X, const bc_keys *keys, const uint64_t *h_a
     // the caller's stream completes only after every output word has reached the host
     CK(cudaEventRecord(d2h, cs));
     CK(cudaStreamWaitEvent(ms, d2h, 0));
-    for (int j = 0; j < 2; ++j) {
-        cudaEventDestroy(h2d[j]);
-        cudaEventDestroy(done[j]);
-    }
-    cudaEventDestroy(d2h);
     if (rc != BC_OK) return rc;
     API_END
 }
