@@ -1811,6 +1811,20 @@ std::vector<CT> extract_batch(Eng &E, const CT &a) {
     }
     CT all = E.ct_alloc(a.B * d, a.lvl, 2);
     std::vector<CT> out;
+    bool fuse = g_ptsum && D <= 32;     // one kappa-weighted sum per digit (ew_ptsum) over contiguous images
+    for (const CT &f : F) fuse = fuse && f.bstride == (uint64_t)2 * a.lvl * X->n && f.lvl == a.lvl;
+    for (uint32_t i = 0; i < d && fuse; ++i) {
+        PtSumArgs A;
+        A.D = D;
+        for (uint32_t k = 0; k < D; ++k) {
+            A.F[k] = F[k].d;
+            A.pt[k] = ctx_pt(X, kappa_key(i, k), kappa_slots(X, i, k), E.st);
+        }
+        CT dst = E.sub(all, i * a.B, a.B);
+        if (!E.dry()) ew_ptsum(X->d_mods, A, dst.d, a.B, 2, a.lvl, X->n, E.st, g_f64_elem ? X->d_fm : nullptr);
+        out.push_back(dst);
+    }
+    if (fuse) return out;
     for (uint32_t i = 0; i < d; ++i) {
         CT acc;
         bool have = false;

@@ -458,6 +458,7 @@ static void ntt_common(const NttTables &T, const uint64_t *in, uint64_t *out, ui
 int g_ntt_split = 0;
 int g_ntt_persist_occ = 0;
 int g_ntt_lean = 4;
+int g_ptsum = 1;
 int g_axpy = 1;
 int g_ntt_epi = 0;      // measured: C2 compare 3.53 -> 3.55 ms with the fused epilogue (pass C's scattered
                         // u / d loads cost more than the separate 128-bit streaming kernel), so off
@@ -709,6 +710,45 @@ void ew_ptmul(const Mod *mods, const uint64_t *a, const uint64_t *pt, uint64_t *
         k_ptmul_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, pt, o, (uint32_t)rows, lvl, n);
     else
         k_ptmul<<<grid_rows(n, rows), 256, 0, st>>>(mods, a, pt, o, (uint32_t)rows, lvl, n);
+    LAUNCHED();
+}
+
+// a8 digit extraction: o = sum_k pt_k (.) F_k (the kappa-weighted sum of the Frobenius images) in one
+// pass instead of D plaintext products and D - 1 additions (modular sums are exact: the same words)
+__global__ void k_ptsum(const Mod *__restrict__ mods, PtSumArgs A, uint64_t *__restrict__ o, uint32_t rows, uint32_t lvl,
+                        uint32_t n) {
+    ROW_LOOP(r, x, rows, n) {
+        const uint32_t limb = r % lvl;
+        const Mod M = mods[limb];
+        const uint64_t i = (uint64_t)r * n + x, j = (uint64_t)limb * n + x;
+        uint64_t acc = 0;
+        for (uint32_t k = 0; k < A.D; ++k) acc = add_mod(acc, mul_mod(A.F[k][i], A.pt[k][j], M), M.q);
+        o[i] = acc;
+    }
+}
+__global__ void k_ptsum_f(const double2 *__restrict__ fm, PtSumArgs A, uint64_t *__restrict__ o, uint32_t rows,
+                          uint32_t lvl, uint32_t n) {
+    using namespace f64;
+    ROW_LOOP2(r, x, rows, n) {
+        const uint32_t limb = r % lvl;
+        const double q = fm[limb].x, qi = fm[limb].y;
+        const uint64_t i = (uint64_t)r * n + x, j = (uint64_t)limb * n + x;
+        double a0 = 0.0, a1 = 0.0;      // |a| <= q/2 + 2 after each fred, + a product |r| <= 0.75 q
+        for (uint32_t k = 0; k < A.D; ++k) {
+            const ulonglong2 fv = LD2(A.F[k] + i), pv = LD2(A.pt[k] + j);
+            a0 = fred(__dadd_rn(a0, fmulv(from_u64(fv.x), from_u64(pv.x), q, qi)), q, qi);
+            a1 = fred(__dadd_rn(a1, fmulv(from_u64(fv.y), from_u64(pv.y), q, qi)), q, qi);
+        }
+        ST2(o + i, to_u64(a0, q), to_u64(a1, q));
+    }
+}
+void ew_ptsum(const Mod *mods, const PtSumArgs &A, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n,
+              cudaStream_t st, const double2 *fm) {
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    if (fm)
+        k_ptsum_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, A, o, (uint32_t)rows, lvl, n);
+    else
+        k_ptsum<<<grid_rows(n, rows), 256, 0, st>>>(mods, A, o, (uint32_t)rows, lvl, n);
     LAUNCHED();
 }
 

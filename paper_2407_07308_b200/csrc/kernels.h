@@ -120,6 +120,13 @@ void ew_neg(const Mod *mods, const uint64_t *a, uint64_t *o, uint32_t B, uint32_
 void ew_ext_acc(const Mod *mods, uint64_t *W, const uint64_t *u, const uint64_t *d, uint64_t d_bstride,
                 uint64_t d_kstride, const u64x2 *pm, uint32_t B, uint32_t lv, uint32_t K, uint32_t L1, uint32_t n,
                 int first, cudaStream_t st);   // R27: W (+)= u + P d (extended basis)
+struct PtSumArgs {       // up to 32 Frobenius images and their kappa plaintexts (contiguous [B][parts][lvl][n])
+    const uint64_t *F[32];
+    const uint64_t *pt[32];
+    uint32_t D;
+};
+void ew_ptsum(const Mod *mods, const PtSumArgs &A, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n,
+              cudaStream_t st, const double2 *fm);   // o = sum_k pt_k (.) F_k
 void ew_axpy(const Mod *mods, const uint64_t *a, const uint64_t *x, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
              uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm);   // o = a + c x
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
@@ -237,6 +244,7 @@ extern int g_ntt_split;        // 1: transform calls split over two streams (see
 extern int g_ntt_persist_occ;  // >0: cap of the persistent column passes' CTAs per SM
 extern int g_ntt_epi;          // 1: scale-sub / fused-ModDown epilogues inside pass C of the forward transform
 extern int g_ntt_lean;
+extern int g_ptsum;            // 1: digit extraction as one kappa-weighted sum kernel per digit (default)
 extern int g_axpy;             // 1: fused a + c x in the digit circuits' linear combinations (default)         // persistent column passes: table tiles in shared memory (0) or read through L2 (1-3)
 extern int g_ntt_timing;
 // comparison phases (bench "phases"; NVTX ranges of the same names)

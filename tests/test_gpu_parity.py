@@ -573,9 +573,10 @@ def test_full_size_c2_encrypt_modswitch_automorph_bit_exact(pair):
 @pytest.mark.parametrize("name", ["c2s", "c4s", "c2"])
 def test_fused_epilogue_and_column_pass_variants_identical(pair, name):
     """The scale-sub / fused-ModDown epilogues inside pass C (bc_tune ntt_epi 1, opt-in), the pass-C
-    staging-tile-as-exchange variant (ntt_lean 4, default) and the fused a + c x of the digit circuits'
-    linear combinations (axpy 1, default) give the same compare_lt words as the separate kernels and the
-    round-2 passes (ntt_epi 0, ntt_lean 0, axpy 0); the default words are the ones the oracle parity tests
+    staging-tile-as-exchange variant (ntt_lean 4, default), the fused a + c x of the digit circuits'
+    linear combinations (axpy 1, default) and the one-kernel kappa-weighted extraction sums (ptsum 1, default)
+    give the same compare_lt words as the separate kernels and the round-2 passes (ntt_epi 0, ntt_lean 0,
+    axpy 0, ptsum 0); the default words are the ones the oracle parity tests
     pin (c2s) -- here on the C2 shadow, the C4 shadow and full-size C2."""
     import paper_2407_07308_b200 as bc
     T = pair(name)
@@ -587,13 +588,15 @@ def test_fused_epilogue_and_column_pass_variants_identical(pair, name):
     cb = T.ctx.encrypt(T.keys, np.array([b], dtype=np.uint64), SEED_ENC, ct_index0=41)
     ref = to_u64(T.ctx.compare_lt(T.keys, ca, cb))
     try:
-        for epi, lean, axpy in [(0, 0, 0), (1, 4, 1), (1, 0, 0), (1, 2, 1)]:
+        for epi, lean, axpy, ptsum in [(0, 0, 0, 0), (1, 4, 1, 0), (1, 0, 0, 1), (1, 2, 1, 0)]:
             bc._lib.bc_tune(b"ntt_epi", epi)
             bc._lib.bc_tune(b"ntt_lean", lean)
             bc._lib.bc_tune(b"axpy", axpy)
-            assert np.array_equal(to_u64(T.ctx.compare_lt(T.keys, ca, cb)), ref), (epi, lean, axpy)
+            bc._lib.bc_tune(b"ptsum", ptsum)
+            assert np.array_equal(to_u64(T.ctx.compare_lt(T.keys, ca, cb)), ref), (epi, lean, axpy, ptsum)
     finally:
         bc._lib.bc_tune(b"ntt_epi", 0)
         bc._lib.bc_tune(b"ntt_lean", 4)
         bc._lib.bc_tune(b"axpy", 1)
+        bc._lib.bc_tune(b"ptsum", 1)
     assert list(T.ctx.decrypt(T.keys, T.ctx.compare_lt(T.keys, ca, cb), as_bits=True)[0]) == [int(x < y) for x, y in zip(a, b)]
