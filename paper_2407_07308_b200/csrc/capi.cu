@@ -40,6 +40,7 @@ int bc_tune(const char *key, int64_t value) {
     if (!strcmp(key, "ntt_persist_occ")) { g_ntt_persist_occ = (int)value; return 0; }
     if (!strcmp(key, "ntt_lean")) { g_ntt_lean = (int)value; return 0; }
     if (!strcmp(key, "axpy")) { g_axpy = (int)value; return 0; }
+    if (!strcmp(key, "lift_blocks")) { g_lift_blocks = (int)value; return 0; }
     if (!strcmp(key, "ptsum")) { g_ptsum = (int)value; return 0; }
     if (!strcmp(key, "ntt_epi")) { g_ntt_epi = (int)value; return 0; }
     if (!strcmp(key, "lift2")) { g_lift2 = (int)value; return 0; }

@@ -459,6 +459,7 @@ int g_ntt_split = 0;
 int g_ntt_persist_occ = 0;
 int g_ntt_lean = 4;
 int g_ptsum = 1;
+int g_lift_blocks = 16;
 int g_axpy = 1;
 int g_ntt_epi = 0;      // measured: C2 compare 3.53 -> 3.55 ms with the fused epilogue (pass C's scattered
                         // u / d loads cost more than the separate 128-bit streaming kernel), so off
@@ -1564,7 +1565,10 @@ void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src
     const bool two = g_lift2 && (n % 2) == 0 && (src_pstride % 2) == 0 && (out_pstride % 2) == 0 &&
                      (((uintptr_t)src | (uintptr_t)out) & 15) == 0;
     if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 16 && nt_hint <= 64 && two) {
-        const dim3 g = grid_rows(n / 2, npoly);
+        dim3 g = grid_rows(n / 2, npoly);
+        // each block sets up its constant tables (a barrier) before its rows: cap the row blocks so a block
+        // loops over several polys (ROW_LOOP2 strides by gridDim.y) and the setup is amortised
+        if (g_lift_blocks > 0) g.y = std::max<unsigned>(1, std::min<unsigned>(g.y, (unsigned)(148u * g_lift_blocks / g.x)));
 #define LIFT_F2(K) case K: k_lift_f2<K><<<g, 256, 0, st>>>(plan, fm, p, src, src_pstride, out, out_pstride, npoly, n, skip0, skipn, mode); break;
         switch (ns_hint) { LIFT_F2(1) LIFT_F2(2) LIFT_F2(3) LIFT_F2(4) LIFT_F2(5) LIFT_F2(6) LIFT_F2(7) LIFT_F2(8)
                            LIFT_F2(9) LIFT_F2(10) LIFT_F2(11) LIFT_F2(12) LIFT_F2(13) LIFT_F2(14) LIFT_F2(15) LIFT_F2(16) }
@@ -1573,7 +1577,8 @@ void lift(const uint64_t *plan, const Mod *mods, uint32_t p, const uint64_t *src
         return;
     }
     if (fm && mode != 2 && ns_hint >= 1 && ns_hint <= 16 && nt_hint <= 64) {
-        const dim3 g = grid_rows(n, npoly);
+        dim3 g = grid_rows(n, npoly);
+        if (g_lift_blocks > 0) g.y = std::max<unsigned>(1, std::min<unsigned>(g.y, (unsigned)(148u * g_lift_blocks / g.x)));
 #define LIFT_F(K) case K: k_lift_f<K><<<g, 256, 0, st>>>(plan, fm, p, src, src_pstride, out, out_pstride, npoly, n, skip0, skipn, mode); break;
         switch (ns_hint) { LIFT_F(1) LIFT_F(2) LIFT_F(3) LIFT_F(4) LIFT_F(5) LIFT_F(6) LIFT_F(7) LIFT_F(8)
                            LIFT_F(9) LIFT_F(10) LIFT_F(11) LIFT_F(12) LIFT_F(13) LIFT_F(14) LIFT_F(15) LIFT_F(16) }

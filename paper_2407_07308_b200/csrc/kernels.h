@@ -244,6 +244,7 @@ extern int g_ntt_split;        // 1: transform calls split over two streams (see
 extern int g_ntt_persist_occ;  // >0: cap of the persistent column passes' CTAs per SM
 extern int g_ntt_epi;          // 1: scale-sub / fused-ModDown epilogues inside pass C of the forward transform
 extern int g_ntt_lean;
+extern int g_lift_blocks;      // binary64 lifts: row blocks capped at 148 x this / column blocks (0: one per poly)
 extern int g_ptsum;            // 1: digit extraction as one kappa-weighted sum kernel per digit (default)
 extern int g_axpy;             // 1: fused a + c x in the digit circuits' linear combinations (default)         // persistent column passes: table tiles in shared memory (0) or read through L2 (1-3)
 extern int g_ntt_timing;
