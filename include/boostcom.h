@@ -295,7 +295,10 @@ void bc_set_ntt_impl(int impl);
  * and the fused ModDown epilogue run inside pass C of the forward transform of delta; 0, default: separate
  * kernels -- measured faster on B200), "ntt_lean" (4 default: pass-C staging tile as exchange buffer, 3 CTAs per SM; 0: round-2 passes; 1-3:
  * tables read through L2 and / or the staging tile as exchange buffer), "ntt_persist_occ" (cap of the persistent passes' CTAs per SM),
- * "ntt_split" (two-stream transform calls).  None changes a result bit.  Returns 0 if known (-1 if not). */
+ * "ntt_split" (two-stream transform calls), "axpy" (1, default: a + c x of the digit circuits' linear
+ * combinations in one kernel), "ptsum" (1, default: each extracted digit's kappa-weighted sum in one kernel),
+ * "lift_blocks" (row-block cap of the binary64 lifts, default 16).  None changes a result bit.  Returns 0 if
+ * known (-1 if not). */
 int bc_tune(const char *key, int64_t value);
 /* live NTT timing: after bc_tune("ntt_timing", 1) every forward/inverse Bluestein NTT call records
  * a CUDA event pair on its stream.  bc_ntt_timing synchronises those events and returns (then
