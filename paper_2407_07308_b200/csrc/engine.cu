@@ -1024,6 +1024,12 @@ CT Eng::ptmul(const CT &a, const uint64_t *pt) {
     if (!dry()) ew_ptmul(X->d_mods, a.d, pt, o.d, a.B, a.parts, a.lvl, X->n, st, g_f64_elem ? X->d_fm : nullptr);
     return o;
 }
+CT Eng::ptmul_add_pt(const CT &a, const uint64_t *pm, const uint64_t *pa) {
+    if (!g_f64_elem || !X->d_fm || a.bstride != (uint64_t)a.parts * a.lvl * X->n) return add_pt(ptmul(a, pm), pa);
+    CT o = ct_alloc(a.B, a.lvl, a.parts);
+    if (!dry()) ew_ptmul_addpt(X->d_fm, a.d, pm, pa, o.d, a.B, a.parts, a.lvl, X->n, st);
+    return o;
+}
 CT Eng::add_pt(const CT &a, const uint64_t *pt) {
     CT o = ct_alloc(a.B, a.lvl, a.parts);
     if (!dry()) ew_add_pt(X->d_mods, a.d, pt, o.d, a.B, a.parts, a.lvl, X->n, st);
@@ -1866,7 +1872,7 @@ static void lex_slots(Eng &E, Val *lt, Val *eq, bool need_eq, bool need_lt = tru
         const bool last = (sh << 1) >= l;
         const uint64_t *mask = ctx_pt(X, "ksm:" + std::to_string(sh), ksm_slots(X, sh), E.st);
         const uint64_t *inv = ctx_pt(X, "ksi:" + std::to_string(sh), ksi_slots(X, sh), E.st);   // 1 - mask, every slot
-        CT hi_eq = E.add_pt(E.ptmul(E.rotate(eq->ct, sh), mask), inv);
+        CT hi_eq = E.ptmul_add_pt(E.rotate(eq->ct, sh), mask, inv);
         if (need_lt) {
             CT hi_lt = E.ptmul(E.rotate(lt->ct, sh), mask);
             *lt = vadd(E, VT(hi_lt), vmul(E, VT(hi_eq), *lt));

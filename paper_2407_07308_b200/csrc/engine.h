@@ -176,6 +176,7 @@ struct Eng {
     CT add_const(const CT &a, int64_t c);
     CT ptmul(const CT &a, const uint64_t *pt);
     CT add_pt(const CT &a, const uint64_t *pt);
+    CT ptmul_add_pt(const CT &a, const uint64_t *pm, const uint64_t *pa);   // add_pt(ptmul(a, pm), pa), one pass
     // key switch of polys d (ct b at d + b*dps, lvl limbs, eval) -> [B][2][lvl][n]
     CT keyswitch(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);
     BufP ks_up(const uint64_t *d, uint64_t dps, uint32_t B, uint32_t lvl, uint32_t key_id);  // ModUp + KIP

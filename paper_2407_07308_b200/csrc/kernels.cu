@@ -753,6 +753,33 @@ void ew_ptsum(const Mod *mods, const PtSumArgs &A, uint64_t *o, uint32_t B, uint
     LAUNCHED();
 }
 
+// o = a (.) pm, + pa on part 0 (ShiftMul's masked rotation plus 1 - mask, a9: one pass for ptmul + add_pt)
+__global__ void k_ptmul_addpt_f(const double2 *__restrict__ fm, const uint64_t *__restrict__ a,
+                                const uint64_t *__restrict__ pm, const uint64_t *__restrict__ pa, uint64_t *__restrict__ o,
+                                uint32_t rows, uint32_t parts, uint32_t lvl, uint32_t n) {
+    using namespace f64;
+    ROW_LOOP2(r, x, rows, n) {
+        const uint32_t limb = r % lvl, part = (r / lvl) % parts;
+        const double q = fm[limb].x, qi = fm[limb].y;
+        const uint64_t qq = (uint64_t)q, i = (uint64_t)r * n + x, j = (uint64_t)limb * n + x;
+        const ulonglong2 av = LD2(a + i), mv = LD2(pm + j);
+        uint64_t r0 = to_u64(fmulv(from_u64(av.x), from_u64(mv.x), q, qi), q);
+        uint64_t r1 = to_u64(fmulv(from_u64(av.y), from_u64(mv.y), q, qi), q);
+        if (part == 0) {
+            const ulonglong2 cv = LD2(pa + j);
+            r0 = add_mod(r0, cv.x, qq);
+            r1 = add_mod(r1, cv.y, qq);
+        }
+        ST2(o + i, r0, r1);
+    }
+}
+void ew_ptmul_addpt(const double2 *fm, const uint64_t *a, const uint64_t *pm, const uint64_t *pa, uint64_t *o,
+                    uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st) {
+    const uint64_t rows = (uint64_t)B * parts * lvl;
+    k_ptmul_addpt_f<<<grid_rows(n / 2, rows), 256, 0, st>>>(fm, a, pm, pa, o, (uint32_t)rows, parts, lvl, n);
+    LAUNCHED();
+}
+
 __global__ void k_add_pt(const Mod *__restrict__ mods, const uint64_t *__restrict__ a,
                          const uint64_t *__restrict__ pt, uint64_t *__restrict__ o, uint32_t rows,
                          uint32_t parts, uint32_t lvl, uint32_t n) {

@@ -127,6 +127,8 @@ struct PtSumArgs {       // up to 32 Frobenius images and their kappa plaintexts
 };
 void ew_ptsum(const Mod *mods, const PtSumArgs &A, uint64_t *o, uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n,
               cudaStream_t st, const double2 *fm);   // o = sum_k pt_k (.) F_k
+void ew_ptmul_addpt(const double2 *fm, const uint64_t *a, const uint64_t *pm, const uint64_t *pa, uint64_t *o,
+                    uint32_t B, uint32_t parts, uint32_t lvl, uint32_t n, cudaStream_t st);   // a (.) pm (+ pa on part 0)
 void ew_axpy(const Mod *mods, const uint64_t *a, const uint64_t *x, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
              uint32_t lvl, uint32_t n, cudaStream_t st, const double2 *fm);   // o = a + c x
 void ew_scalar(const Mod *mods, const uint64_t *a, int64_t c, uint64_t *o, uint32_t B, uint32_t parts,
